@@ -1,0 +1,331 @@
+// K4: encoder self-attention (non-causal, 1500 x 1500 x 64 per head) on
+// tcgen05. One CTA per (128-query tile, segment*head). Warp roles:
+//   w0: TMA producer (Q once, then K / V^T tiles through a 2-stage ring)
+//   w1: MMA issuer (S_j = Q K_j^T into a double-buffered TMEM tile,
+//       PV_j = P_j V_j into a double-buffered 64-column TMEM tile)
+//   w2..5: softmax, one query row per thread (TMEM lane = row): row max /
+//       exp2 / row sum entirely in registers (no shuffles), P_j written as
+//       bf16 straight into the 128B-swizzled K-major smem layout the next MMA
+//       reads, PV_j folded into a register accumulator with the online-softmax
+//       rescale.
+// Q arrives pre-scaled by head_dim^-0.5 (modeling_whisper.py:310) from the
+// QKV GEMM epilogue; V arrives transposed ([dims, positions]) so both MMAs
+// are K-major. Keys >= 1500 (the 1536-padded tail) are masked to -inf.
+
+#include "common.cuh"
+
+namespace dm {
+
+constexpr int kAttnThreads = 192;
+constexpr int kAttnKS = 2;           // K/V ring depth
+constexpr int kQBytes = 128 * 128;   // 128 rows x 64 bf16
+constexpr int kKBytes = 128 * 128;
+constexpr int kVBytes = 2 * 64 * 128;  // two 64-key boxes of [64 dims x 64 keys]
+constexpr int kPBytes = 2 * 128 * 128; // two 64-key column blocks of [128 rows x 64 keys]
+
+struct AttnSmemLayout {
+  static constexpr int q = 0;
+  static constexpr int k = q + kQBytes;
+  static constexpr int v = k + kAttnKS * kKBytes;
+  static constexpr int p = v + kAttnKS * kVBytes;
+  static constexpr int bars = p + 2 * kPBytes;
+  static constexpr int total = bars + 256 + 1024;
+};
+
+__global__ void __launch_bounds__(kAttnThreads, 1)
+attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
+                    const __grid_constant__ CUtensorMap tm_k,
+                    const __grid_constant__ CUtensorMap tm_vt, int T, int t_pad,
+                    int heads, uint16_t* __restrict__ out, int ldo) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AttnSmemLayout::bars);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;            // [KS]
+  uint64_t* kv_empty = kv_full + kAttnKS;  // [KS]
+  uint64_t* s_full = kv_empty + kAttnKS;   // [2]
+  uint64_t* s_empty = s_full + 2;          // [2]
+  uint64_t* p_full = s_empty + 2;          // [2]
+  uint64_t* o_full = p_full + 2;           // [2]
+  uint64_t* o_empty = o_full + 2;          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int qt = blockIdx.x, bh = blockIdx.y;
+  const int nb = ceil_div(T, 128);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_q);
+    tma_prefetch_desc(&tm_k);
+    tma_prefetch_desc(&tm_vt);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < kAttnKS; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_empty[i], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (elect_one()) {
+      mbar_arrive_expect_tx(q_full, kQBytes);
+      tma_load_2d(smem + AttnSmemLayout::q, &tm_q, q_full, 0, bh * t_pad + qt * 128);
+      for (int j = 0; j < nb; ++j) {
+        const int st = j % kAttnKS;
+        mbar_wait(&kv_empty[st], ((j / kAttnKS) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[st], kKBytes + kVBytes);
+        tma_load_2d(smem + AttnSmemLayout::k + st * kKBytes, &tm_k, &kv_full[st], 0,
+                    bh * t_pad + j * 128);
+        uint8_t* sv = smem + AttnSmemLayout::v + st * kVBytes;
+        tma_load_2d(sv, &tm_vt, &kv_full[st], j * 128, bh * 64);
+        tma_load_2d(sv + 64 * 128, &tm_vt, &kv_full[st], j * 128 + 64, bh * 64);
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128);
+    constexpr uint32_t idesc_o = umma_idesc_bf16(128, 64);
+    const uint32_t sq = smem_u32(smem + AttnSmemLayout::q);
+    mbar_wait(q_full, 0);
+    auto issue_pv = [&](int j) {
+      const int pb = j & 1, st = j % kAttnKS;
+      mbar_wait(&p_full[pb], (j >> 1) & 1);
+      mbar_wait(&o_empty[pb], ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sp = smem_u32(smem + AttnSmemLayout::p + pb * kPBytes);
+        const uint32_t sv = smem_u32(smem + AttnSmemLayout::v + st * kVBytes);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t a = sp + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+          const uint32_t bb = sv + (kk >> 2) * (64 * 128) + (kk & 3) * 32;
+          umma_bf16_ss(tmem + 256 + pb * 64, umma_desc_sw128(a), umma_desc_sw128(bb), idesc_o,
+                       kk != 0);
+        }
+        umma_commit(&o_full[pb]);
+        umma_commit(&kv_empty[st]);
+      }
+      __syncwarp();
+    };
+    for (int j = 0; j < nb; ++j) {
+      const int st = j % kAttnKS, sb = j & 1;
+      mbar_wait(&kv_full[st], (j / kAttnKS) & 1);
+      mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sk = smem_u32(smem + AttnSmemLayout::k + st * kKBytes);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16_ss(tmem + sb * 128, umma_desc_sw128(sq + kk * 32),
+                       umma_desc_sw128(sk + kk * 32), idesc_s, kk != 0);
+        umma_commit(&s_full[sb]);
+      }
+      __syncwarp();
+      if (j >= 1) issue_pv(j - 1);
+    }
+    issue_pv(nb - 1);
+  } else {
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;                       // query row in tile
+    const uint32_t lane_off = uint32_t(quad * 32) << 16;
+    constexpr float kLog2e = 1.4426950408889634f;
+    float m_run = -INFINITY, l_run = 0.f, alpha_prev = 0.f;
+    float o[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) o[i] = 0.f;
+    auto fold_pv = [&](int j) {
+      const int ob = j & 1;
+      mbar_wait(&o_full[ob], (j >> 1) & 1);
+      tc_fence_after();
+      uint32_t pv[32];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        tmem_ld32(tmem + lane_off + 256 + ob * 64 + c * 32, pv);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          o[c * 32 + i] = fmaf(o[c * 32 + i], alpha_prev, __uint_as_float(pv[i]));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&o_empty[ob]);
+    };
+    for (int j = 0; j < nb; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      const int kvalid = T - j * 128;                    // keys valid in this block
+      // pass 1: row max
+      float mx = m_run;
+      uint32_t sr[32];
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        tmem_ld32(tmem + lane_off + sb * 128 + c * 32, sr);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c * 32 + i < kvalid) mx = fmaxf(mx, __uint_as_float(sr[i]));
+      }
+      const float alpha = exp2f((m_run - mx) * kLog2e);
+      const float mscaled = mx * kLog2e;
+      // pass 2: p = exp(s - m), row sum, bf16 P into swizzled smem
+      float rs = 0.f;
+      uint8_t* prow = smem + AttnSmemLayout::p + sb * kPBytes + r * 128;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        tmem_ld32(tmem + lane_off + sb * 128 + c * 32, sr);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          float p0 = (c * 32 + 2 * i < kvalid)
+                         ? exp2f(fmaf(__uint_as_float(sr[2 * i]), kLog2e, -mscaled)) : 0.f;
+          float p1 = (c * 32 + 2 * i + 1 < kvalid)
+                         ? exp2f(fmaf(__uint_as_float(sr[2 * i + 1]), kLog2e, -mscaled)) : 0.f;
+          rs += p0 + p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+        // 32 keys = 4 chunks of 16 B; block = c / 2, chunk-in-row = (c % 2) * 4 + u
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int chunk = (c & 1) * 4 + u;
+          uint4* dst = reinterpret_cast<uint4*>(prow + (c >> 1) * (128 * 128) +
+                                                ((chunk ^ (r & 7)) << 4));
+          *dst = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+      }
+      tc_fence_before();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&s_empty[sb]);
+        mbar_arrive(&p_full[sb]);
+      }
+      l_run = l_run * alpha + rs;
+      m_run = mx;
+      if (j >= 1) fold_pv(j - 1);
+      alpha_prev = alpha;
+    }
+    fold_pv(nb - 1);
+    // normalise and store this query row
+    const int t = qt * 128 + r;
+    if (t < T) {
+      const float inv = 1.0f / l_run;
+      const int b = bh / heads, h = bh % heads;
+      uint4* dst = reinterpret_cast<uint4*>(out + (size_t(b) * T + t) * ldo + h * 64);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        dst[i] = make_uint4(pack_bf16x2(o[8 * i] * inv, o[8 * i + 1] * inv),
+                            pack_bf16x2(o[8 * i + 2] * inv, o[8 * i + 3] * inv),
+                            pack_bf16x2(o[8 * i + 4] * inv, o[8 * i + 5] * inv),
+                            pack_bf16x2(o[8 * i + 6] * inv, o[8 * i + 7] * inv));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------ LayerNorm
+// fp32 rows -> bf16 rows (encoder pre-LN and final LN). One warp per row,
+// two-pass mean/variance in registers, eps 1e-5.
+template <int V4>  // float4 per lane
+__global__ void __launch_bounds__(256)
+layernorm_bf16_kernel(const float* __restrict__ x, const uint16_t* __restrict__ g,
+                      const uint16_t* __restrict__ bta, uint16_t* __restrict__ y, int rows,
+                      int d) {
+  const int row = blockIdx.x * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= rows) return;
+  const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * d);
+  const int n4 = d / 4;
+  float4 v[V4];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    int c = lane + 32 * i;
+    v[i] = c < n4 ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    int c = lane + 32 * i;
+    if (c < n4) {
+      float a = v[i].x - mean, b = v[i].y - mean, cc = v[i].z - mean, e = v[i].w - mean;
+      q += (a * a + b * b) + (cc * cc + e * e);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = rsqrtf(q / d + 1e-5f);
+  uint2* yr = reinterpret_cast<uint2*>(y + size_t(row) * d);
+#pragma unroll
+  for (int i = 0; i < V4; ++i) {
+    int c = lane + 32 * i;
+    if (c < n4) {
+      float o0 = (v[i].x - mean) * rstd * bf16_to_f32(g[4 * c]) + bf16_to_f32(bta[4 * c]);
+      float o1 = (v[i].y - mean) * rstd * bf16_to_f32(g[4 * c + 1]) + bf16_to_f32(bta[4 * c + 1]);
+      float o2 = (v[i].z - mean) * rstd * bf16_to_f32(g[4 * c + 2]) + bf16_to_f32(bta[4 * c + 2]);
+      float o3 = (v[i].w - mean) * rstd * bf16_to_f32(g[4 * c + 3]) + bf16_to_f32(bta[4 * c + 3]);
+      yr[c] = make_uint2(pack_bf16x2(o0, o1), pack_bf16x2(o2, o3));
+    }
+  }
+}
+
+int launch_layernorm_bf16(const float* x, const uint16_t* g, const uint16_t* b, uint16_t* y,
+                          int rows, int d, cudaStream_t stream) {
+  DM_REQUIRE(d % 128 == 0 && d <= 1280, "layernorm d must be a multiple of 128, <= 1280");
+  dim3 grid(ceil_div(rows, 8));
+  const int v4 = d / 128;
+  switch (v4) {
+#define DM_LN_CASE(n) \
+  case n: layernorm_bf16_kernel<n><<<grid, 256, 0, stream>>>(x, g, b, y, rows, d); break;
+    DM_LN_CASE(1) DM_LN_CASE(2) DM_LN_CASE(3) DM_LN_CASE(4) DM_LN_CASE(5)
+    DM_LN_CASE(6) DM_LN_CASE(7) DM_LN_CASE(8) DM_LN_CASE(9) DM_LN_CASE(10)
+#undef DM_LN_CASE
+    default: DM_REQUIRE(false, "unsupported d");
+  }
+  DM_CHECK_LAUNCH();
+  return 0;
+}
+
+// host: tensor maps for Q/K ([BH*Tp, 64]) and V^T ([BH*64, Tp])
+int make_attn_maps(const uint16_t* q, const uint16_t* k, const uint16_t* vt, int bh, int t_pad,
+                   CUtensorMap* mq, CUtensorMap* mk, CUtensorMap* mv);
+
+int launch_attention(const uint16_t* q, const uint16_t* k, const uint16_t* vt, int n_seg,
+                     int heads, int T, int t_pad, uint16_t* out, int ldo, cudaStream_t stream) {
+  DM_REQUIRE(t_pad % 128 == 0 && t_pad >= T, "t_pad must be a multiple of 128 >= T");
+  CUtensorMap mq, mk, mv;
+  if (make_attn_maps(q, k, vt, n_seg * heads, t_pad, &mq, &mk, &mv)) return 2;
+  static bool attr = false;
+  if (!attr) {
+    DM_CHECK_CUDA(cudaFuncSetAttribute(attn_tcgen05_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       AttnSmemLayout::total));
+    attr = true;
+  }
+  dim3 grid(ceil_div(T, 128), n_seg * heads);
+  attn_tcgen05_kernel<<<grid, kAttnThreads, AttnSmemLayout::total, stream>>>(
+      mq, mk, mv, T, t_pad, heads, out, ldo);
+  DM_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // namespace dm

@@ -1,0 +1,678 @@
+// C-ABI entry points and the Whisper engine: owns device buffers, runs the
+// encoder (log-mel -> conv stem -> L layers -> LN -> cross-KV into slots) and
+// the decode step (captured once as a CUDA graph, replayed per step), and the
+// K7 slot / self-KV page allocator.
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dictamux_b200.h"
+#include "common.cuh"
+#include "decode.cuh"
+#include "gemm.cuh"
+
+namespace dm {
+
+// ------------------------------------------------------------ error state
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+const char* last_error() { return g_err.c_str(); }
+
+// forward decls (logmel.cu / attention.cu)
+struct LogmelTables;
+int launch_logmel(const int16_t*, const int64_t*, const int32_t*, int, int,
+                  const LogmelTables*, float*, uint16_t*, uint32_t*, cudaStream_t);
+int launch_layernorm_bf16(const float*, const uint16_t*, const uint16_t*, uint16_t*, int, int,
+                          cudaStream_t);
+int launch_attention(const uint16_t*, const uint16_t*, const uint16_t*, int, int, int, int,
+                     uint16_t*, int, cudaStream_t);
+
+// ------------------------------------------------------------ log-mel tables
+struct LogmelTablesHost {
+  float2 tw200[25 * 8];
+  float2 tw25[25];
+  float2 tw400[201];
+  float window[400];
+  int mel_start[128];
+  int mel_count[128];
+  int mel_woff[128];
+  float mel_w[1024];
+};
+
+static double hz_to_mel(double f) {
+  if (f >= 1000.0) return 15.0 + std::log(f / 1000.0) * (27.0 / std::log(6.4));
+  return 3.0 * f / 200.0;
+}
+static double mel_to_hz(double m) {
+  if (m >= 15.0) return 1000.0 * std::exp(std::log(6.4) / 27.0 * (m - 15.0));
+  return 200.0 * m / 3.0;
+}
+
+// Restates mel_filter_bank(201, n_mels, 0, 8000, 16000, "slaney", "slaney")
+// (transformers audio_utils.py:453-545) in double precision.
+static int build_logmel_tables(int n_mels, LogmelTablesHost* t) {
+  const double PI = 3.14159265358979323846;
+  for (int q = 0; q < 25; ++q)
+    for (int k1 = 0; k1 < 8; ++k1) {
+      double a = -2.0 * PI * q * k1 / 200.0;
+      t->tw200[q * 8 + k1] = make_float2(float(std::cos(a)), float(std::sin(a)));
+    }
+  for (int j = 0; j < 25; ++j) {
+    double a = -2.0 * PI * j / 25.0;
+    t->tw25[j] = make_float2(float(std::cos(a)), float(std::sin(a)));
+  }
+  for (int k = 0; k < 201; ++k) {
+    double a = -2.0 * PI * k / 400.0;
+    t->tw400[k] = make_float2(float(std::cos(a)), float(std::sin(a)));
+  }
+  for (int n = 0; n < 400; ++n) t->window[n] = float(0.5 - 0.5 * std::cos(2.0 * PI * n / 400.0));
+  std::vector<double> filt(n_mels + 2);
+  const double m0 = hz_to_mel(0.0), m1 = hz_to_mel(8000.0);
+  for (int i = 0; i < n_mels + 2; ++i) filt[i] = mel_to_hz(m0 + (m1 - m0) * i / (n_mels + 1));
+  int woff = 0;
+  for (int m = 0; m < n_mels; ++m) {
+    const double enorm = 2.0 / (filt[m + 2] - filt[m]);
+    int start = -1, count = 0;
+    for (int k = 0; k < 201; ++k) {
+      const double f = 8000.0 * k / 200.0;
+      const double down = (f - filt[m]) / (filt[m + 1] - filt[m]);
+      const double up = (filt[m + 2] - f) / (filt[m + 2] - filt[m + 1]);
+      const double w = std::max(0.0, std::min(down, up)) * enorm;
+      if (w > 0.0) {
+        if (start < 0) start = k;
+        if (woff + (k - start) >= 1024) return 1;
+        t->mel_w[woff + (k - start)] = float(w);
+        count = k - start + 1;
+      }
+    }
+    if (start < 0) start = 0;
+    t->mel_start[m] = start;
+    t->mel_count[m] = count;
+    t->mel_woff[m] = woff;
+    woff += count;
+  }
+  return 0;
+}
+
+static std::mutex g_tab_mu;
+static std::map<std::pair<int, int>, void*> g_tables;   // (device, n_mels) -> device ptr
+
+static int get_logmel_tables(int n_mels, const LogmelTables** out) {
+  int dev = 0;
+  DM_CHECK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_tab_mu);
+  auto key = std::make_pair(dev, n_mels);
+  auto it = g_tables.find(key);
+  if (it == g_tables.end()) {
+    LogmelTablesHost h;
+    std::memset(&h, 0, sizeof(h));
+    DM_REQUIRE(build_logmel_tables(n_mels, &h) == 0, "mel table overflow");
+    void* d = nullptr;
+    DM_CHECK_CUDA(cudaMalloc(&d, sizeof(h)));
+    DM_CHECK_CUDA(cudaMemcpy(d, &h, sizeof(h), cudaMemcpyHostToDevice));
+    it = g_tables.emplace(key, d).first;
+  }
+  *out = static_cast<const LogmelTables*>(it->second);
+  return 0;
+}
+
+// ------------------------------------------------------------ weight fill
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void fill_normal_kernel(uint16_t* dst, uint64_t n, uint64_t key, float scale,
+                                   float mean) {
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t h = splitmix64(key + i);
+    const int64_t s = int64_t(h & 0xFFFF) + int64_t((h >> 16) & 0xFFFF) +
+                      int64_t((h >> 32) & 0xFFFF) + int64_t(h >> 48);
+    const float z = float(s - 131070);                    // exact (< 2^24)
+    const float v = __fadd_rn(__fmul_rn(z, scale), mean);
+    dst[i] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+  }
+}
+
+// ------------------------------------------------------------ Whisper engine
+struct WhisperEngine {
+  dm_whisper_config cfg;
+  int d, H, L, Ld, F, nm, Cp;
+  // weights
+  const uint16_t* w = nullptr;
+  std::vector<int64_t> off;
+  const uint16_t* W(int i) const { return w + off[i]; }
+  int enc_layer_base(int l) const { return 5 + 12 * l; }
+  int after_enc() const { return 5 + 12 * L; }          // enc.ln.g
+  int dec_layer_base(int l) const { return after_enc() + 4 + 18 * l; }
+  int after_dec() const { return after_enc() + 4 + 18 * Ld; }
+  uint16_t* conv1_w_pad = nullptr;   // [d, 3, Cp]
+  // encoder workspace
+  int E = 0;
+  float* mel = nullptr;          // [E, nm, 3000]
+  uint16_t* mel_t = nullptr;     // [E, 3002, Cp]
+  uint32_t* segmax = nullptr;
+  uint16_t* conv1_out = nullptr; // [E, 3002, d]
+  float* resid = nullptr;        // [E*1500, d]
+  uint16_t* lnb = nullptr;       // [E*1500, d]
+  uint16_t *qb = nullptr, *kb = nullptr, *vtb = nullptr;  // [E*H, 1536, 64] / [E*H*64, 1536]
+  uint16_t* attn_out = nullptr;  // [E*1500, d]
+  uint16_t* fc1_out = nullptr;   // [E*1500, F]
+  uint16_t* enc_out = nullptr;   // [E*1500, d]
+  int32_t* slot_dev = nullptr;   // [E]
+  int32_t* slot_host = nullptr;  // pinned [E]
+  int last_n = 0;
+  // decode
+  DecodeState st{};
+  int32_t* prompt_dev = nullptr;
+  int32_t* active_dev = nullptr;
+  int32_t* n_active_dev = nullptr;
+  int32_t* page_table_dev = nullptr;
+  std::vector<int32_t> page_table_host;
+  std::vector<int> free_pages;
+  std::vector<int> slot_pages;       // pages held per slot
+  int32_t* staging = nullptr;        // pinned scratch for uploads
+  std::vector<void*> allocs;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t step_exec = nullptr;
+  cudaGraph_t step_graph = nullptr;
+  int gemv_counter_base = 0, xattn_counter_base = 0;
+
+  int alloc(void** p, size_t bytes, bool zero = true) {
+    DM_CHECK_CUDA(cudaMalloc(p, bytes));
+    allocs.push_back(*p);
+    if (zero) DM_CHECK_CUDA(cudaMemset(*p, 0, bytes));
+    return 0;
+  }
+  template <class T>
+  int alloc_t(T** p, size_t count, bool zero = true) {
+    return alloc(reinterpret_cast<void**>(p), count * sizeof(T), zero);
+  }
+
+  ~WhisperEngine() {
+    if (step_exec) cudaGraphExecDestroy(step_exec);
+    if (step_graph) cudaGraphDestroy(step_graph);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+    for (void* p : allocs) cudaFree(p);
+    if (slot_host) cudaFreeHost(slot_host);
+    if (staging) cudaFreeHost(staging);
+  }
+};
+
+__global__ void repack_conv1_kernel(const uint16_t* __restrict__ w, uint16_t* __restrict__ out,
+                                    int d, int nm, int Cp) {
+  // w [d, 3, nm] -> out [d, 3, Cp] (zero channels >= nm)
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d * 3 * Cp) return;
+  const int c = i % Cp, tap = (i / Cp) % 3, o = i / (3 * Cp);
+  out[i] = c < nm ? w[(size_t(o) * 3 + tap) * nm + c] : uint16_t(0);
+}
+
+static int engine_init(WhisperEngine* e) {
+  const dm_whisper_config& c = e->cfg;
+  e->d = c.d_model; e->H = c.heads; e->L = c.enc_layers; e->Ld = c.dec_layers;
+  e->F = c.ffn; e->nm = c.n_mels; e->Cp = c.n_mels <= 64 ? 64 : 128;
+  DM_REQUIRE(e->d % 128 == 0 && e->d / e->H == 64, "d must be a multiple of 128 with head_dim 64");
+  DM_REQUIRE(c.n_mels == 80 || c.n_mels == 128, "n_mels must be 80 or 128");
+  DM_REQUIRE(c.max_slots >= 1 && c.max_slots <= 64, "max_slots must be in [1, 64]");
+  DM_REQUIRE(c.max_encode_batch >= 1, "max_encode_batch >= 1");
+  DM_REQUIRE(c.prompt_len >= 1 && c.prompt_len <= 8, "prompt_len in [1, 8]");
+  DM_REQUIRE(c.num_pages >= c.max_slots, "num_pages >= max_slots");
+  const int d = e->d, E = c.max_encode_batch, S = c.max_slots;
+  e->E = E;
+  const size_t rows = size_t(E) * 1500;
+  if (e->alloc_t(&e->conv1_w_pad, size_t(d) * 3 * e->Cp)) return 2;
+  {
+    const int n = d * 3 * e->Cp;
+    repack_conv1_kernel<<<ceil_div(n, 256), 256>>>(e->W(0), e->conv1_w_pad, d, e->nm, e->Cp);
+    DM_CHECK_LAUNCH();
+  }
+  if (e->alloc_t(&e->mel, size_t(E) * e->nm * 3000, false)) return 2;
+  if (e->alloc_t(&e->mel_t, size_t(E) * 3002 * e->Cp)) return 2;
+  if (e->alloc_t(&e->segmax, E)) return 2;
+  if (e->alloc_t(&e->conv1_out, size_t(E) * 3002 * d)) return 2;
+  if (e->alloc_t(&e->resid, rows * d, false)) return 2;
+  if (e->alloc_t(&e->lnb, rows * d, false)) return 2;
+  if (e->alloc_t(&e->qb, size_t(E) * e->H * 1536 * 64)) return 2;
+  if (e->alloc_t(&e->kb, size_t(E) * e->H * 1536 * 64)) return 2;
+  if (e->alloc_t(&e->vtb, size_t(E) * e->H * 64 * 1536)) return 2;
+  if (e->alloc_t(&e->attn_out, rows * d, false)) return 2;
+  if (e->alloc_t(&e->fc1_out, rows * e->F, false)) return 2;
+  if (e->alloc_t(&e->enc_out, rows * d, false)) return 2;
+  if (e->alloc_t(&e->slot_dev, E)) return 2;
+  DM_CHECK_CUDA(cudaMallocHost(&e->slot_host, sizeof(int32_t) * E));
+  DM_CHECK_CUDA(cudaMallocHost(&e->staging, sizeof(int32_t) * (4 * 64 * 8 + 4096)));
+
+  // decode state
+  DecodeState& st = e->st;
+  st.max_slots = S; st.d = d; st.heads = e->H; st.layers = e->Ld; st.ffn = e->F;
+  st.vocab = c.vocab; st.page_tokens = 64; st.pages_per_slot = 7; st.eot = c.eot;
+  st.prompt_len = c.prompt_len;
+  if (e->alloc_t(&e->prompt_dev, 8)) return 2;
+  DM_CHECK_CUDA(cudaMemcpy(e->prompt_dev, c.prompt, sizeof(int32_t) * 8, cudaMemcpyHostToDevice));
+  st.prompt = e->prompt_dev;
+  if (e->alloc_t(&e->active_dev, S)) return 2;
+  if (e->alloc_t(&e->n_active_dev, 1)) return 2;
+  st.active = e->active_dev; st.n_active = e->n_active_dev;
+  if (e->alloc_t(&st.pos, S)) return 2;
+  if (e->alloc_t(&st.cur_tok, S)) return 2;
+  if (e->alloc_t(&st.n_gen, S)) return 2;
+  if (e->alloc_t(&st.cap, S)) return 2;
+  if (e->alloc_t(&st.done, S)) return 2;
+  {
+    std::vector<int32_t> ones(S, 1);
+    DM_CHECK_CUDA(cudaMemcpy(st.done, ones.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice));
+  }
+  if (e->alloc_t(&st.out_tokens, size_t(S) * 448)) return 2;
+  if (e->alloc_t(&e->page_table_dev, size_t(S) * 7)) return 2;
+  st.page_table = e->page_table_dev;
+  e->page_table_host.assign(size_t(S) * 7, 0);
+  e->slot_pages.assign(S, 0);
+  for (int p = c.num_pages - 1; p >= 0; --p) e->free_pages.push_back(p);
+  const size_t page_elems = size_t(e->Ld) * 2 * e->H * 64 * 64;
+  if (e->alloc_t(&st.kv_pool, page_elems * c.num_pages)) return 2;
+  uint16_t* xkv = nullptr;
+  if (e->alloc_t(&xkv, size_t(e->Ld) * S * 2 * e->H * 1500 * 64)) return 2;
+  st.xkv = xkv;
+  if (e->alloc_t(&st.x, size_t(S) * d)) return 2;
+  if (e->alloc_t(&st.xn, size_t(S) * d)) return 2;
+  if (e->alloc_t(&st.q, size_t(S) * d)) return 2;
+  if (e->alloc_t(&st.attn, size_t(S) * d)) return 2;
+  if (e->alloc_t(&st.h1, size_t(S) * e->F)) return 2;
+  // cross-attention key splits: enough CTAs to cover the chip at full batch
+  st.xsplits = 1;
+  while (S * e->H * st.xsplits < 2 * kNumSMs && st.xsplits < 8) st.xsplits *= 2;
+  // split-K partial scratch: max over GEMV shapes and cross-attn partials
+  size_t part = 0;
+  const int shapes[5][2] = {{3 * d, d}, {d, d}, {e->F, d}, {d, e->F}, {d, d}};
+  for (auto& sh : shapes) part = std::max(part, size_t(gemv_splits(sh[0], sh[1])) * 64 * sh[0]);
+  part = std::max(part, size_t(S) * e->H * st.xsplits * 66);
+  if (e->alloc_t(&st.part, part)) return 2;
+  e->gemv_counter_base = 0;
+  e->xattn_counter_base = 4096;
+  if (e->alloc_t(&st.counters, 4096 + size_t(S) * e->H)) return 2;
+  const int tiles = ceil_div(c.vocab, 64);
+  if (e->alloc_t(&st.amax_val, size_t(tiles) * S)) return 2;
+  if (e->alloc_t(&st.amax_idx, size_t(tiles) * S)) return 2;
+  st.logits_dbg = nullptr;
+  DM_CHECK_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+  DM_CHECK_CUDA(cudaDeviceSynchronize());
+  return 0;
+}
+
+static int encoder_forward(WhisperEngine* e, const int16_t* pcm, const int64_t* offsets,
+                           const int32_t* lengths, int n, cudaStream_t s) {
+  const int d = e->d, H = e->H;
+  const LogmelTables* tab = nullptr;
+  if (int rc = get_logmel_tables(e->nm, &tab)) return rc;
+  if (int rc = launch_logmel(pcm, offsets, lengths, n, e->nm, tab, e->mel, e->mel_t, e->segmax, s))
+    return rc;
+  // conv1 (implicit GEMM over the padded time-major mel), GELU
+  {
+    GemmArgs g;
+    g.A = e->mel_t; g.a_mode = A_CONV_S1; g.C = e->Cp; g.K = 3 * e->Cp; g.T = 3000; g.Bt = n;
+    g.W = e->conv1_w_pad; g.N = d;
+    g.epi.mode = EPI_CONV1; g.epi.bias = e->W(1); g.epi.out = e->conv1_out; g.epi.ldo = d;
+    if (int rc = launch_gemm(g, s)) return rc;
+  }
+  // conv2 (stride 2), GELU, + sinusoid positions -> fp32 residual stream
+  {
+    GemmArgs g;
+    g.A = e->conv1_out; g.a_mode = A_CONV_S2; g.C = d; g.K = 3 * d; g.T = 1500; g.Bt = n;
+    g.W = e->W(2); g.N = d;
+    g.epi.mode = EPI_CONV2_POS; g.epi.bias = e->W(3); g.epi.out = e->resid; g.epi.ldo = d;
+    g.epi.pos = e->W(4);
+    if (int rc = launch_gemm(g, s)) return rc;
+  }
+  const int M = n * 1500;
+  auto flat = [&](const uint16_t* A, int K, const uint16_t* Wt, int N) {
+    GemmArgs g;
+    g.A = A; g.a_mode = A_FLAT; g.K = K; g.T = M; g.Bt = 1; g.lda = K; g.a_bstride = 0;
+    g.W = Wt; g.N = N;
+    return g;
+  };
+  for (int l = 0; l < e->L; ++l) {
+    const int b0 = e->enc_layer_base(l);
+    if (int rc = launch_layernorm_bf16(e->resid, e->W(b0 + 0), e->W(b0 + 1), e->lnb, M, d, s))
+      return rc;
+    {
+      GemmArgs g = flat(e->lnb, d, e->W(b0 + 2), 3 * d);
+      g.epi.mode = EPI_QKV; g.epi.bias = e->W(b0 + 3);
+      g.epi.q = e->qb; g.epi.k = e->kb; g.epi.vt = e->vtb; g.epi.heads = H; g.epi.t_pad = 1536;
+      g.epi.q_scale = 0.125f;
+      if (int rc = launch_gemm(g, s)) return rc;
+    }
+    if (int rc = launch_attention(e->qb, e->kb, e->vtb, n, H, 1500, 1536, e->attn_out, d, s))
+      return rc;
+    {
+      GemmArgs g = flat(e->attn_out, d, e->W(b0 + 4), d);
+      g.epi.mode = EPI_RESID_F32; g.epi.bias = e->W(b0 + 5); g.epi.out = e->resid; g.epi.ldo = d;
+      if (int rc = launch_gemm(g, s)) return rc;
+    }
+    if (int rc = launch_layernorm_bf16(e->resid, e->W(b0 + 6), e->W(b0 + 7), e->lnb, M, d, s))
+      return rc;
+    {
+      GemmArgs g = flat(e->lnb, d, e->W(b0 + 8), e->F);
+      g.epi.mode = EPI_GELU_BF16; g.epi.bias = e->W(b0 + 9); g.epi.out = e->fc1_out;
+      g.epi.ldo = e->F;
+      if (int rc = launch_gemm(g, s)) return rc;
+    }
+    {
+      GemmArgs g = flat(e->fc1_out, e->F, e->W(b0 + 10), d);
+      g.epi.mode = EPI_RESID_F32; g.epi.bias = e->W(b0 + 11); g.epi.out = e->resid; g.epi.ldo = d;
+      if (int rc = launch_gemm(g, s)) return rc;
+    }
+  }
+  const int a = e->after_enc();
+  if (int rc = launch_layernorm_bf16(e->resid, e->W(a), e->W(a + 1), e->enc_out, M, d, s))
+    return rc;
+  // cross-KV precompute for every decoder layer, scattered into the slots
+  {
+    const int x = e->after_dec();
+    GemmArgs g = flat(e->enc_out, d, e->W(x), 2 * d * e->Ld);
+    g.epi.mode = EPI_XKV; g.epi.bias = e->W(x + 1); g.epi.out = const_cast<uint16_t*>(e->st.xkv);
+    g.epi.slot_ids = e->slot_dev; g.epi.n_slots = e->cfg.max_slots; g.epi.layers = e->Ld;
+    g.epi.heads = H;
+    if (int rc = launch_gemm(g, s)) return rc;
+  }
+  return 0;
+}
+
+static int record_step(WhisperEngine* e, cudaStream_t s) {
+  DecodeState& st = e->st;
+  const int d = e->d;
+  const int a = e->after_enc();
+  const uint16_t* embed = e->W(a + 2);
+  const uint16_t* pos_emb = e->W(a + 3);
+  if (int rc = launch_embed(st, embed, pos_emb, s)) return rc;
+  for (int l = 0; l < e->Ld; ++l) {
+    const int b0 = e->dec_layer_base(l);
+    auto gv = [&](const float* X, int wi, float* Y, int N, int K, int epi, float scale) {
+      GemvArgs g;
+      g.X = X; g.W = e->W(wi); g.bias = e->W(wi + 1); g.Y = Y; g.N = N; g.K = K; g.epi = epi;
+      g.scale = scale; g.layer = l; g.splits = gemv_splits(N, K);
+      g.counter_base = e->gemv_counter_base;
+      return launch_gemv(st, g, s);
+    };
+    if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 0), e->W(b0 + 1), st.xn, s)) return rc;
+    if (int rc = gv(st.xn, b0 + 2, nullptr, 3 * d, d, GV_QKV, 0.125f)) return rc;
+    if (int rc = launch_self_attn(st, l, s)) return rc;
+    if (int rc = gv(st.attn, b0 + 4, st.x, d, d, GV_RESID, 1.f)) return rc;
+    if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 6), e->W(b0 + 7), st.xn, s)) return rc;
+    if (int rc = gv(st.xn, b0 + 8, st.q, d, d, GV_SCALE, 0.125f)) return rc;
+    if (int rc = launch_cross_attn(st, l, e->xattn_counter_base, s)) return rc;
+    if (int rc = gv(st.attn, b0 + 10, st.x, d, d, GV_RESID, 1.f)) return rc;
+    if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 12), e->W(b0 + 13), st.xn, s)) return rc;
+    if (int rc = gv(st.xn, b0 + 14, st.h1, e->F, d, GV_GELU, 1.f)) return rc;
+    if (int rc = gv(st.h1, b0 + 16, st.x, d, e->F, GV_RESID, 1.f)) return rc;
+  }
+  const int x = e->after_dec();
+  if (int rc = launch_decode_ln(st, st.x, e->W(x + 2), e->W(x + 3), st.xn, s)) return rc;
+  if (int rc = launch_lm_head(st, embed, s)) return rc;
+  if (int rc = launch_finalize(st, s)) return rc;
+  return 0;
+}
+
+static int build_step_graph(WhisperEngine* e) {
+  if (e->step_exec) {
+    cudaGraphExecDestroy(e->step_exec);
+    e->step_exec = nullptr;
+  }
+  if (e->step_graph) {
+    cudaGraphDestroy(e->step_graph);
+    e->step_graph = nullptr;
+  }
+  DM_CHECK_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+  int rc = record_step(e, e->cap_stream);
+  cudaGraph_t g = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &g);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  DM_CHECK_CUDA(ce);
+  e->step_graph = g;
+  DM_CHECK_CUDA(cudaGraphInstantiate(&e->step_exec, g, 0));
+  return 0;
+}
+
+}  // namespace dm
+
+using namespace dm;
+
+// ================================================================ C ABI
+extern "C" {
+
+const char* dm_last_error(void) { return dm::last_error(); }
+int dm_version(void) { return 1; }
+
+int dm_fill_normal_bf16(uint16_t* dst, uint64_t numel, uint64_t key, float scale, float mean,
+                        void* stream) {
+  DM_REQUIRE(dst != nullptr || numel == 0, "null destination");
+  if (numel == 0) return 0;
+  uint64_t blocks = (numel + 255) / 256;
+  if (blocks > 148ull * 64) blocks = 148ull * 64;
+  fill_normal_kernel<<<unsigned(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      dst, numel, key, scale, mean);
+  DM_CHECK_LAUNCH();
+  return 0;
+}
+
+int dm_logmel(const int16_t* pcm, const int64_t* offsets, const int32_t* lengths, int n,
+              int n_mels, float* out, void* stream) {
+  DM_REQUIRE(n >= 0, "n < 0");
+  if (n == 0) return 0;
+  const LogmelTables* tab = nullptr;
+  if (int rc = get_logmel_tables(n_mels, &tab)) return rc;
+  uint32_t* segmax = nullptr;
+  DM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&segmax), sizeof(uint32_t) * n,
+                                static_cast<cudaStream_t>(stream)));
+  int rc = launch_logmel(pcm, offsets, lengths, n, n_mels, tab, out, nullptr, segmax,
+                         static_cast<cudaStream_t>(stream));
+  cudaFreeAsync(segmax, static_cast<cudaStream_t>(stream));
+  return rc;
+}
+
+int dm_gemm_bf16_f32(const uint16_t* A, const uint16_t* Wt, const uint16_t* bias, float* out,
+                     int M, int N, int K, void* stream) {
+  GemmArgs g;
+  g.A = A; g.a_mode = A_FLAT; g.K = K; g.T = M; g.Bt = 1; g.lda = K; g.W = Wt; g.N = N;
+  g.epi.mode = EPI_STORE_F32; g.epi.bias = bias; g.epi.out = out; g.epi.ldo = N;
+  return launch_gemm(g, static_cast<cudaStream_t>(stream));
+}
+
+int dm_whisper_create(const dm_whisper_config* cfg, const uint16_t* weights,
+                      const int64_t* offsets, int n_offsets, void** handle) {
+  DM_REQUIRE(cfg && weights && offsets && handle, "null argument");
+  const int expect = 5 + 12 * cfg->enc_layers + 4 + 18 * cfg->dec_layers + 4;
+  DM_REQUIRE(n_offsets == expect, "offset table has " + std::to_string(n_offsets) +
+                                      " entries, expected " + std::to_string(expect));
+  auto* e = new WhisperEngine();
+  e->cfg = *cfg;
+  e->w = weights;
+  e->off.assign(offsets, offsets + n_offsets);
+  for (int64_t o : e->off)
+    if (o % 8 != 0) {
+      delete e;
+      DM_REQUIRE(false, "weight offsets must be 16-byte aligned");
+    }
+  if (int rc = engine_init(e)) {
+    delete e;
+    return rc;
+  }
+  *handle = e;
+  return 0;
+}
+
+int dm_whisper_destroy(void* handle) {
+  delete static_cast<WhisperEngine*>(handle);
+  return 0;
+}
+
+int dm_whisper_encode(void* handle, const int16_t* pcm, const int64_t* offsets,
+                      const int32_t* lengths, int n, const int32_t* slot_ids, void* stream) {
+  auto* e = static_cast<WhisperEngine*>(handle);
+  DM_REQUIRE(e != nullptr, "null handle");
+  DM_REQUIRE(n >= 1 && n <= e->E, "n must be in [1, max_encode_batch]");
+  for (int i = 0; i < n; ++i)
+    DM_REQUIRE(slot_ids[i] >= 0 && slot_ids[i] < e->cfg.max_slots, "slot id out of range");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DM_CHECK_CUDA(cudaStreamSynchronize(s));   // slot_host staging reuse
+  std::memcpy(e->slot_host, slot_ids, sizeof(int32_t) * n);
+  DM_CHECK_CUDA(cudaMemcpyAsync(e->slot_dev, e->slot_host, sizeof(int32_t) * n,
+                                cudaMemcpyHostToDevice, s));
+  e->last_n = n;
+  return encoder_forward(e, pcm, offsets, lengths, n, s);
+}
+
+__global__ void admit_kernel(DecodeState st, const int32_t* args, int n) {
+  // args: [slot, cap] * n
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int slot = args[2 * i], cap = args[2 * i + 1];
+  st.pos[slot] = 0;
+  st.cur_tok[slot] = st.prompt[0];
+  st.n_gen[slot] = 0;
+  st.cap[slot] = cap;
+  st.done[slot] = 0;
+}
+
+int dm_whisper_admit(void* handle, const int32_t* slot_ids, const int32_t* caps, int n,
+                     void* stream) {
+  auto* e = static_cast<WhisperEngine*>(handle);
+  DM_REQUIRE(e != nullptr, "null handle");
+  DM_REQUIRE(n >= 0 && n <= e->cfg.max_slots, "bad n");
+  if (n == 0) return 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // allocate pages (host side), then upload table rows + slot resets
+  int need = 0;
+  for (int i = 0; i < n; ++i) {
+    DM_REQUIRE(slot_ids[i] >= 0 && slot_ids[i] < e->cfg.max_slots, "slot id out of range");
+    DM_REQUIRE(caps[i] >= 1 && caps[i] <= 448 - e->cfg.prompt_len, "cap out of range");
+    DM_REQUIRE(e->slot_pages[slot_ids[i]] == 0, "slot already holds pages (release it first)");
+    need += ceil_div(e->cfg.prompt_len + caps[i], 64);
+  }
+  if (need > int(e->free_pages.size())) {
+    set_error("self-KV page pool exhausted");
+    return 3;
+  }
+  DM_CHECK_CUDA(cudaStreamSynchronize(s));   // staging reuse
+  for (int i = 0; i < n; ++i) {
+    const int slot = slot_ids[i];
+    const int np = ceil_div(e->cfg.prompt_len + caps[i], 64);
+    for (int p = 0; p < 7; ++p) {
+      int page = 0;
+      if (p < np) {
+        page = e->free_pages.back();
+        e->free_pages.pop_back();
+      }
+      e->page_table_host[size_t(slot) * 7 + p] = page;
+    }
+    e->slot_pages[slot] = np;
+    e->staging[2 * i] = slot;
+    e->staging[2 * i + 1] = caps[i];
+  }
+  DM_CHECK_CUDA(cudaMemcpyAsync(e->page_table_dev, e->page_table_host.data(),
+                                sizeof(int32_t) * e->page_table_host.size(),
+                                cudaMemcpyHostToDevice, s));
+  int32_t* args = e->staging + 4096;
+  std::memcpy(args, e->staging, sizeof(int32_t) * 2 * n);
+  admit_kernel<<<ceil_div(n, 64), 64, 0, s>>>(e->st, args, n);
+  DM_CHECK_LAUNCH();
+  DM_CHECK_CUDA(cudaStreamSynchronize(s));   // host table / staging consumed
+  return 0;
+}
+
+int dm_whisper_release(void* handle, const int32_t* slot_ids, int n) {
+  auto* e = static_cast<WhisperEngine*>(handle);
+  DM_REQUIRE(e != nullptr, "null handle");
+  for (int i = 0; i < n; ++i) {
+    const int slot = slot_ids[i];
+    DM_REQUIRE(slot >= 0 && slot < e->cfg.max_slots, "slot id out of range");
+    for (int p = 0; p < e->slot_pages[slot]; ++p)
+      e->free_pages.push_back(e->page_table_host[size_t(slot) * 7 + p]);
+    e->slot_pages[slot] = 0;
+  }
+  return 0;
+}
+
+int dm_whisper_set_active(void* handle, const int32_t* slot_ids, int n, void* stream) {
+  auto* e = static_cast<WhisperEngine*>(handle);
+  DM_REQUIRE(e != nullptr, "null handle");
+  DM_REQUIRE(n >= 0 && n <= e->cfg.max_slots, "bad n");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DM_CHECK_CUDA(cudaStreamSynchronize(s));
+  e->staging[0] = n;
+  for (int i = 0; i < n; ++i) {
+    DM_REQUIRE(slot_ids[i] >= 0 && slot_ids[i] < e->cfg.max_slots, "slot id out of range");
+    e->staging[1 + i] = slot_ids[i];
+  }
+  DM_CHECK_CUDA(cudaMemcpyAsync(e->n_active_dev, e->staging, sizeof(int32_t),
+                                cudaMemcpyHostToDevice, s));
+  if (n)
+    DM_CHECK_CUDA(cudaMemcpyAsync(e->active_dev, e->staging + 1, sizeof(int32_t) * n,
+                                  cudaMemcpyHostToDevice, s));
+  DM_CHECK_CUDA(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int dm_whisper_step(void* handle, int n_steps, void* stream) {
+  auto* e = static_cast<WhisperEngine*>(handle);
+  DM_REQUIRE(e != nullptr, "null handle");
+  if (!e->step_exec)
+    if (int rc = build_step_graph(e)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(e->step_exec, s));
+  return 0;
+}
+
+int dm_whisper_read(void* handle, int32_t* done, int32_t* n_gen, int32_t* tokens, void* stream) {
+  auto* e = static_cast<WhisperEngine*>(handle);
+  DM_REQUIRE(e != nullptr, "null handle");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int S = e->cfg.max_slots;
+  if (done) DM_CHECK_CUDA(cudaMemcpyAsync(done, e->st.done, sizeof(int32_t) * S, cudaMemcpyDeviceToHost, s));
+  if (n_gen) DM_CHECK_CUDA(cudaMemcpyAsync(n_gen, e->st.n_gen, sizeof(int32_t) * S, cudaMemcpyDeviceToHost, s));
+  if (tokens)
+    DM_CHECK_CUDA(cudaMemcpyAsync(tokens, e->st.out_tokens, sizeof(int32_t) * S * 448,
+                                  cudaMemcpyDeviceToHost, s));
+  DM_CHECK_CUDA(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void* stream) {
+  auto* e = static_cast<WhisperEngine*>(handle);
+  DM_REQUIRE(e != nullptr, "null handle");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const void* src = nullptr;
+  size_t avail = 0;
+  switch (which) {
+    case 0: src = e->enc_out; avail = size_t(e->last_n) * 1500 * e->d * 2; break;
+    case 1: src = e->mel; avail = size_t(e->last_n) * e->nm * 3000 * 4; break;
+    case 2:
+      DM_REQUIRE(e->st.logits_dbg != nullptr, "logits tap not enabled");
+      src = e->st.logits_dbg; avail = size_t(e->cfg.max_slots) * e->cfg.vocab * 4;
+      break;
+    case 3: {
+      if (!e->st.logits_dbg) {
+        if (e->alloc_t(&e->st.logits_dbg, size_t(e->cfg.max_slots) * e->cfg.vocab)) return 2;
+        if (int rc = build_step_graph(e)) return rc;   // re-capture with the tap
+      }
+      return 0;
+    }
+    default: DM_REQUIRE(false, "unknown debug tap");
+  }
+  DM_REQUIRE(bytes <= avail, "debug copy larger than the tapped buffer");
+  DM_CHECK_CUDA(cudaMemcpyAsync(host_dst, src, bytes, cudaMemcpyDeviceToHost, s));
+  DM_CHECK_CUDA(cudaStreamSynchronize(s));
+  return 0;
+}
+
+}  // extern "C"

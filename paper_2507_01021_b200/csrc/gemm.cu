@@ -1,0 +1,411 @@
+// tcgen05 GEMM: persistent, warp-specialised, TMA -> 128B-swizzled smem ring
+// -> tcgen05.mma (M=128, N=BN, K=16 per instruction, fp32 accumulators in
+// TMEM, double-buffered) -> 4 epilogue warps (tcgen05.ld -> fused epilogue ->
+// global). Implements the encoder's conv stem (implicit im2col: each conv tap
+// is a separate K range read through its own TMA coordinates), the layer GEMMs
+// and the cross-KV precompute.
+//
+// Batch invariance: the reduction order of every output element depends only
+// on K (fixed BLOCK_K = 64, no split-K), never on M or on batch composition.
+
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "gemm.cuh"
+
+namespace dm {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;
+constexpr int kGemmThreads = 192;   // w0 TMA, w1 MMA + TMEM alloc, w2..5 epilogue
+
+__device__ __forceinline__ void tma_load_4d(void* smem_dst, const CUtensorMap* m,
+                                            uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::"
+      "bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1),
+      "r"(c2), "r"(c3)
+      : "memory");
+}
+
+struct TileGeom {
+  int MT, NT, tiles, KB, cpb;   // cpb = channel blocks per conv tap
+};
+
+template <int BN>
+__device__ __forceinline__ void epilogue_chunk(const Epilogue& e, const GemmArgs& g,
+                                               int b, int t, int row_valid, int n0,
+                                               uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  if (e.bias != nullptr) {
+    const uint4* bp = reinterpret_cast<const uint4*>(e.bias + n0);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      uint4 w = __ldg(bp + i);
+      uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        v[i * 8 + 2 * j] += __uint_as_float(ws[j] << 16);
+        v[i * 8 + 2 * j + 1] += __uint_as_float(ws[j] & 0xFFFF0000u);
+      }
+    }
+  }
+  if (!row_valid) return;
+  const int N = g.N;
+  switch (e.mode) {
+    case EPI_GELU_BF16:
+    case EPI_CONV1:
+    case EPI_CONV2_POS:
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = gelu_erf(v[i]);
+      break;
+    default:
+      break;
+  }
+  switch (e.mode) {
+    case EPI_STORE_BF16:
+    case EPI_GELU_BF16:
+    case EPI_CONV1: {
+      size_t row = (e.mode == EPI_CONV1) ? size_t(b) * (g.T + 2) + t + 1
+                                         : size_t(b) * g.T + t;
+      uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(e.out) +
+                                            row * e.ldo + n0);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        dst[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]),
+                            pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                            pack_bf16x2(v[8 * i + 4], v[8 * i + 5]),
+                            pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+      break;
+    }
+    case EPI_CONV2_POS: {
+      const uint4* pp = reinterpret_cast<const uint4*>(e.pos + size_t(t) * N + n0);
+      float4* dst = reinterpret_cast<float4*>(static_cast<float*>(e.out) +
+                                              (size_t(b) * g.T + t) * e.ldo + n0);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint4 w = __ldg(pp + i);
+        uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          o[2 * j] = v[i * 8 + 2 * j] + __uint_as_float(ws[j] << 16);
+          o[2 * j + 1] = v[i * 8 + 2 * j + 1] + __uint_as_float(ws[j] & 0xFFFF0000u);
+        }
+        dst[2 * i] = make_float4(o[0], o[1], o[2], o[3]);
+        dst[2 * i + 1] = make_float4(o[4], o[5], o[6], o[7]);
+      }
+      break;
+    }
+    case EPI_RESID_F32:
+    case EPI_STORE_F32: {
+      float4* dst = reinterpret_cast<float4*>(static_cast<float*>(e.out) +
+                                              (size_t(b) * g.T + t) * e.ldo + n0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 o = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        if (e.mode == EPI_RESID_F32) {
+          float4 rr = dst[i];
+          o.x += rr.x; o.y += rr.y; o.z += rr.z; o.w += rr.w;
+        }
+        dst[i] = o;
+      }
+      break;
+    }
+    case EPI_QKV: {
+      // global row -> (segment, position)
+      const int d = N / 3;
+      const int row = b * g.T + t;
+      const int seg = row / 1500, pos = row % 1500;
+      const int region = n0 / d, h = (n0 % d) / 64, j0 = n0 % 64;
+      const size_t head = size_t(seg) * e.heads + h;
+      if (region < 2) {
+        uint16_t* base = region == 0 ? e.q : e.k;
+        const float sc = region == 0 ? e.q_scale : 1.0f;
+        uint4* dst = reinterpret_cast<uint4*>(base + (head * e.t_pad + pos) * 64 + j0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(pack_bf16x2(v[8 * i] * sc, v[8 * i + 1] * sc),
+                              pack_bf16x2(v[8 * i + 2] * sc, v[8 * i + 3] * sc),
+                              pack_bf16x2(v[8 * i + 4] * sc, v[8 * i + 5] * sc),
+                              pack_bf16x2(v[8 * i + 6] * sc, v[8 * i + 7] * sc));
+      } else {
+        uint16_t* base = e.vt + (head * 64 + j0) * e.t_pad + pos;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) base[size_t(i) * e.t_pad] = f32_to_bf16(v[i]);
+      }
+      break;
+    }
+    case EPI_XKV: {
+      const int d = N / (2 * e.layers);
+      const int row = b * g.T + t;
+      const int seg = row / 1500, pos = row % 1500;
+      const int slot = e.slot_ids[seg];
+      const int l = n0 / (2 * d), kv = (n0 / d) % 2, h = (n0 % d) / 64, j0 = n0 % 64;
+      size_t idx = ((((size_t(l) * e.n_slots + slot) * 2 + kv) * e.heads + h) * 1500 + pos) * 64 + j0;
+      uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(e.out) + idx);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        dst[i] = make_uint4(pack_bf16x2(v[8 * i], v[8 * i + 1]),
+                            pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
+                            pack_bf16x2(v[8 * i + 4], v[8 * i + 5]),
+                            pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBytes = STAGES * kStageBytes + 1024 /*align*/ + 256 /*bars*/;
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                    const __grid_constant__ CUtensorMap tmap_b, const GemmArgs g,
+                    const TileGeom geo) {
+  using S = GemmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStageBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;      // [2]
+  uint64_t* tmem_empty = tmem_full + 2;      // [2]
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tmem_full[s], 1);
+      mbar_init(&tmem_empty[s], 4);      // one arrive per epilogue warp
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_base_slot, 2 * BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < geo.tiles; tile += gridDim.x) {
+        const int nt = tile % geo.NT;
+        const int mb = tile / geo.NT;
+        const int b = mb / geo.MT, mt = mb % geo.MT;
+        for (int kb = 0; kb < geo.KB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStageBytes;
+          uint8_t* sb = sa + S::kABytes;
+          mbar_arrive_expect_tx(&full[stage], S::kStageBytes);
+          if (g.a_mode == A_FLAT) {
+            tma_load_3d(sa, &tmap_a, &full[stage], kb * kBK, mt * kBM, b);
+          } else {
+            const int tap = kb / geo.cpb, c0 = (kb % geo.cpb) * kBK;
+            if (g.a_mode == A_CONV_S1)
+              tma_load_3d(sa, &tmap_a, &full[stage], c0, mt * kBM + tap, b);
+            else
+              tma_load_4d(sa, &tmap_a, &full[stage], c0, tap & 1, mt * kBM + (tap >> 1), b);
+          }
+          tma_load_2d(sb, &tmap_b, &full[stage], kb * kBK, nt * BN);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = umma_idesc_bf16(kBM, BN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < geo.tiles; tile += gridDim.x, ++it) {
+      const int as = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tmem_empty[as], aphase ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + as * BN;
+      for (int kb = 0; kb < geo.KB; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
+          const uint32_t sb = sa + S::kABytes;
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            umma_bf16_ss(d_tmem, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32),
+                         idesc, (kb | k) != 0);
+          }
+          umma_commit(&empty[stage]);
+          if (kb == geo.KB - 1) umma_commit(&tmem_full[as]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    // ---------------- epilogue warps (2..5): TMEM lane quadrant = warp % 4
+    const int quad = warp & 3;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < geo.tiles; tile += gridDim.x, ++it) {
+      const int nt = tile % geo.NT;
+      const int mb = tile / geo.NT;
+      const int b = mb / geo.MT, mt = mb % geo.MT;
+      const int as = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      mbar_wait(&tmem_full[as], aphase);
+      tc_fence_after();
+      const int t = mt * kBM + quad * 32 + lane;
+      const int row_valid = t < g.T;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        const int n0 = nt * BN + c;
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (uint32_t(quad * 32) << 16) + as * BN + c, r);
+        tmem_wait_ld();
+        if (n0 < g.N) epilogue_chunk<BN>(g.epi, g, b, t, row_valid, n0, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[as]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 2 * BN);
+  }
+}
+
+// ------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+bool tma_available() {
+  std::call_once(g_encode_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+static int make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims,
+                    const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims,
+                        strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed with CUresult " + std::to_string(int(r)));
+    return 2;
+  }
+  return 0;
+}
+
+template <int BN, int STAGES>
+static int launch_bn(const GemmArgs& g, cudaStream_t stream) {
+  CUtensorMap ma, mb;
+  if (g.a_mode == A_FLAT) {
+    cuuint64_t dims[3] = {cuuint64_t(g.K), cuuint64_t(g.T), cuuint64_t(g.Bt)};
+    cuuint64_t str[2] = {cuuint64_t(g.lda) * 2, cuuint64_t(g.a_bstride) * 2};
+    cuuint32_t box[3] = {kBK, kBM, 1};
+    if (make_map(&ma, g.A, 3, dims, str, box)) return 2;
+  } else if (g.a_mode == A_CONV_S1) {
+    cuuint64_t dims[3] = {cuuint64_t(g.C), cuuint64_t(g.T + 2), cuuint64_t(g.Bt)};
+    cuuint64_t str[2] = {cuuint64_t(g.C) * 2, cuuint64_t(g.C) * 2 * (g.T + 2)};
+    cuuint32_t box[3] = {kBK, kBM, 1};
+    if (make_map(&ma, g.A, 3, dims, str, box)) return 2;
+  } else {
+    cuuint64_t dims[4] = {cuuint64_t(g.C), 2, cuuint64_t(g.T + 1), cuuint64_t(g.Bt)};
+    cuuint64_t str[3] = {cuuint64_t(g.C) * 2, cuuint64_t(g.C) * 4,
+                         cuuint64_t(g.C) * 2 * (2 * g.T + 2)};
+    cuuint32_t box[4] = {kBK, 1, kBM, 1};
+    if (make_map(&ma, g.A, 4, dims, str, box)) return 2;
+  }
+  {
+    cuuint64_t dims[2] = {cuuint64_t(g.K), cuuint64_t(g.N)};
+    cuuint64_t str[1] = {cuuint64_t(g.K) * 2};
+    cuuint32_t box[2] = {kBK, BN};
+    if (make_map(&mb, g.W, 2, dims, str, box)) return 2;
+  }
+  TileGeom geo;
+  geo.MT = ceil_div(g.T, kBM);
+  geo.NT = ceil_div(g.N, BN);
+  geo.tiles = g.Bt * geo.MT * geo.NT;
+  geo.KB = ceil_div(g.K, kBK);
+  geo.cpb = g.C > 0 ? g.C / kBK : 1;
+  const int smem = GemmSmem<BN, STAGES>::kBytes;
+  static bool attr = false;
+  if (!attr) {
+    DM_CHECK_CUDA(cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, STAGES>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  int grid = geo.tiles < kNumSMs ? geo.tiles : kNumSMs;
+  gemm_tcgen05_kernel<BN, STAGES><<<grid, kGemmThreads, smem, stream>>>(ma, mb, g, geo);
+  DM_CHECK_LAUNCH();
+  return 0;
+}
+
+int make_attn_maps(const uint16_t* q, const uint16_t* k, const uint16_t* vt, int bh, int t_pad,
+                   CUtensorMap* mq, CUtensorMap* mk, CUtensorMap* mv) {
+  DM_REQUIRE(tma_available(), "cuTensorMapEncodeTiled entry point unavailable");
+  {
+    cuuint64_t dims[2] = {64, cuuint64_t(bh) * t_pad};
+    cuuint64_t str[1] = {128};
+    cuuint32_t box[2] = {64, 128};
+    if (make_map(mq, q, 2, dims, str, box)) return 2;
+    if (make_map(mk, k, 2, dims, str, box)) return 2;
+  }
+  {
+    cuuint64_t dims[2] = {cuuint64_t(t_pad), cuuint64_t(bh) * 64};
+    cuuint64_t str[1] = {cuuint64_t(t_pad) * 2};
+    cuuint32_t box[2] = {64, 64};
+    if (make_map(mv, vt, 2, dims, str, box)) return 2;
+  }
+  return 0;
+}
+
+int launch_gemm(const GemmArgs& g, cudaStream_t stream) {
+  DM_REQUIRE(tma_available(), "cuTensorMapEncodeTiled entry point unavailable");
+  DM_REQUIRE(g.K > 0 && g.N > 0 && g.T > 0 && g.Bt > 0, "empty GEMM");
+  DM_REQUIRE(g.N % 32 == 0, "N must be a multiple of 32");
+  DM_REQUIRE(g.K % 8 == 0, "K must be a multiple of 8 (16-byte rows)");
+  DM_REQUIRE(g.a_mode == A_FLAT || (g.C % kBK == 0 && g.K == 3 * g.C),
+             "conv A needs C % 64 == 0 and K == 3C");
+  DM_REQUIRE((reinterpret_cast<uintptr_t>(g.A) & 15) == 0 &&
+                 (reinterpret_cast<uintptr_t>(g.W) & 15) == 0,
+             "operands must be 16-byte aligned");
+  if (g.N % 256 == 0 && g.N >= 1024) return launch_bn<256, 4>(g, stream);
+  return launch_bn<128, 6>(g, stream);
+}
+
+}  // namespace dm

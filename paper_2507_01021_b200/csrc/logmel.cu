@@ -1,0 +1,303 @@
+// K1: fused pad_or_trim + log-mel front end (Whisper feature_extractor).
+//
+// Replaces Listing 1's `model.feature_extractor(chunk)` + `pad_or_trim`
+// and the reference's sample-domain pad_or_trim
+// (pkg/src/dictamux/backend.py:87-99). Semantics restated in
+// oracle/logmel.py (transformers 5.5.0 feature_extraction_whisper.py:140-164).
+//
+// Layout: segments are concatenated int16 PCM in HBM (offsets/lengths); the
+// 480,000-sample window is never materialised — samples past the true length
+// read as zero inside the loads. Per CTA: 32 consecutive frames of one
+// segment. The 400-point real DFT runs as a 200-point complex FFT
+// (even/odd packing), itself a 4-step 8 x 25 FFT staged through shared
+// memory; the 25-point DFTs are 5 x 5 radix-5 in registers. Power -> sparse
+// slaney mel (<= 2 taps per bin) -> log10(max(., 1e-10)) -> per-segment max
+// via an order-preserving atomicMax. A second pass clamps to max-8 and
+// normalises ((x+4)/4), writing both the fp32 [B, n_mels, 3000] feature
+// contract and a time-major bf16 copy (rows 1..3000 of a zero-padded
+// [B, 3002, n_mels] buffer) that feeds the conv1 implicit GEMM.
+//
+// Frames whose 400-sample window lies entirely in the zero padding are
+// skipped (their power is exactly 0, so the result is log10(1e-10)).
+
+#include "common.cuh"
+
+namespace dm {
+
+constexpr int kFFT = 400;
+constexpr int kHop = 160;
+constexpr int kWindow = 480000;
+constexpr int kFrames = 3000;
+constexpr int kBins = 201;
+constexpr int kFPB = 32;                               // frames per CTA
+constexpr int kSpan = (kFPB - 1) * kHop + kFFT;        // 5360 samples
+constexpr int kLogmelThreads = 256;
+
+// Twiddles / window / sparse mel bank, prepared on the host (float64 -> fp32).
+struct LogmelTables {
+  float2 tw200[25 * 8];    // W200^{q*k1}
+  float2 tw25[25];         // W25^{j}
+  float2 tw400[kBins];     // W400^{k}
+  float window[kFFT];      // periodic Hann
+  int mel_start[128];      // first bin of mel m
+  int mel_count[128];      // bins of mel m
+  int mel_woff[128];       // offset into mel_w
+  float mel_w[1024];       // weights
+};
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) {
+  return make_float2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ float2 csub(float2 a, float2 b) {
+  return make_float2(a.x - b.x, a.y - b.y);
+}
+
+// 5-point DFT in place (forward, W5 = e^{-2 pi i / 5}).
+__device__ __forceinline__ void dft5(float2& x0, float2& x1, float2& x2,
+                                     float2& x3, float2& x4) {
+  const float c1 = 0.30901699437494745f, c2 = -0.8090169943749475f;
+  const float s1 = 0.9510565162951535f, s2 = 0.5877852522924731f;
+  float2 a1 = cadd(x1, x4), b1 = csub(x1, x4);
+  float2 a2 = cadd(x2, x3), b2 = csub(x2, x3);
+  float2 y0 = cadd(x0, cadd(a1, a2));
+  float2 t1 = make_float2(x0.x + c1 * a1.x + c2 * a2.x, x0.y + c1 * a1.y + c2 * a2.y);
+  float2 t2 = make_float2(x0.x + c2 * a1.x + c1 * a2.x, x0.y + c2 * a1.y + c1 * a2.y);
+  // -i * (s1*b1 + s2*b2)  and  -i * (s2*b1 - s1*b2)
+  float2 u1 = make_float2(s1 * b1.x + s2 * b2.x, s1 * b1.y + s2 * b2.y);
+  float2 u2 = make_float2(s2 * b1.x - s1 * b2.x, s2 * b1.y - s1 * b2.y);
+  x0 = y0;
+  x1 = make_float2(t1.x + u1.y, t1.y - u1.x);
+  x4 = make_float2(t1.x - u1.y, t1.y + u1.x);
+  x2 = make_float2(t2.x + u2.y, t2.y - u2.x);
+  x3 = make_float2(t2.x - u2.y, t2.y + u2.x);
+}
+
+// 8-point DFT (forward) of z[0..7], natural order in and out.
+__device__ __forceinline__ void dft8(float2 (&z)[8]) {
+  const float r = 0.7071067811865476f;
+  // radix-2 DIT: split even/odd
+  float2 e0 = cadd(z[0], z[4]), e1 = csub(z[0], z[4]);
+  float2 e2 = cadd(z[2], z[6]), e3 = csub(z[2], z[6]);
+  float2 o0 = cadd(z[1], z[5]), o1 = csub(z[1], z[5]);
+  float2 o2 = cadd(z[3], z[7]), o3 = csub(z[3], z[7]);
+  // 4-point on evens: E[k]
+  float2 E0 = cadd(e0, e2), E2 = csub(e0, e2);
+  float2 E1 = make_float2(e1.x + e3.y, e1.y - e3.x);   // e1 - i e3
+  float2 E3 = make_float2(e1.x - e3.y, e1.y + e3.x);   // e1 + i e3
+  float2 O0 = cadd(o0, o2), O2 = csub(o0, o2);
+  float2 O1 = make_float2(o1.x + o3.y, o1.y - o3.x);
+  float2 O3 = make_float2(o1.x - o3.y, o1.y + o3.x);
+  // twiddles W8^k: k=1: (r, -r), k=2: -i, k=3: (-r, -r)
+  float2 T1 = make_float2(r * (O1.x + O1.y), r * (O1.y - O1.x));
+  float2 T2 = make_float2(O2.y, -O2.x);
+  float2 T3 = make_float2(r * (-O3.x + O3.y), r * (-O3.y - O3.x));
+  z[0] = cadd(E0, O0); z[4] = csub(E0, O0);
+  z[1] = cadd(E1, T1); z[5] = csub(E1, T1);
+  z[2] = cadd(E2, T2); z[6] = csub(E2, T2);
+  z[3] = cadd(E3, T3); z[7] = csub(E3, T3);
+}
+
+__device__ __forceinline__ uint32_t float_to_ordered(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float ordered_to_float(uint32_t k) {
+  uint32_t u = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+  return __uint_as_float(u);
+}
+
+struct LogmelSmem {
+  float samples[kSpan];           // also reused as power[kFPB][kBins]
+  float pad_[kFPB * kBins - kSpan > 0 ? kFPB * kBins - kSpan : 1];
+  float2 y[kFPB * 200];           // stage A out / stage B out (Z)
+  float2 tw200[200];
+  float2 tw25[25];
+  float2 tw400[kBins];
+  float window[kFFT];
+};
+
+__global__ void __launch_bounds__(kLogmelThreads)
+logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offsets,
+              const int32_t* __restrict__ lengths, const LogmelTables* __restrict__ tab,
+              int n_mels, float* __restrict__ out, uint32_t* __restrict__ segmax) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  LogmelSmem& s = *reinterpret_cast<LogmelSmem*>(smem_raw);
+  const int b = blockIdx.y;
+  const int f0 = blockIdx.x * kFPB;
+  const int tid = threadIdx.x;
+  const int nfr = min(kFPB, kFrames - f0);
+  int n = lengths[b];
+  n = n < 0 ? 0 : (n > kWindow ? kWindow : n);
+  const int16_t* x = pcm + offsets[b];
+  float* outb = out + size_t(b) * n_mels * kFrames;
+
+  // Frames >= first_zero have all-zero windows: start index f*160-200 >= n.
+  const int first_zero = n == 0 ? 0 : min(kFrames, (n + 200 + kHop - 1) / kHop);
+  if (f0 >= first_zero) {
+    const float v = log10f(1e-10f);
+    for (int i = tid; i < n_mels * nfr; i += kLogmelThreads) {
+      int m = i / nfr, f = i % nfr;
+      outb[size_t(m) * kFrames + f0 + f] = v;
+    }
+    if (tid == 0) atomicMax(segmax + b, float_to_ordered(v));
+    return;
+  }
+
+  for (int i = tid; i < 200; i += kLogmelThreads) s.tw200[i] = tab->tw200[i];
+  for (int i = tid; i < 25; i += kLogmelThreads) s.tw25[i] = tab->tw25[i];
+  for (int i = tid; i < kBins; i += kLogmelThreads) s.tw400[i] = tab->tw400[i];
+  for (int i = tid; i < kFFT; i += kLogmelThreads) s.window[i] = tab->window[i];
+  // Samples of the padded + reflected window [f0*160-200, f0*160-200+kSpan).
+  const int base = f0 * kHop - kFFT / 2;
+  for (int i = tid; i < kSpan; i += kLogmelThreads) {
+    int j = base + i;
+    if (j < 0) j = -j;                                   // reflect at start
+    if (j >= kWindow) j = 2 * (kWindow - 1) - j;         // reflect at end
+    s.samples[i] = (j < n) ? float(x[j]) * (1.0f / 32768.0f) : 0.0f;
+  }
+  __syncthreads();
+
+  // Stage A: per (frame, q): 8-point DFT over p of z[25p+q], twiddle W200^{q k1}.
+  for (int t = tid; t < kFPB * 25; t += kLogmelThreads) {
+    int fr = t / 25, q = t % 25;
+    float2 z[8];
+    const float* src = s.samples + fr * kHop;
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      int m = 25 * p + q;
+      z[p] = make_float2(src[2 * m] * s.window[2 * m],
+                         src[2 * m + 1] * s.window[2 * m + 1]);
+    }
+    dft8(z);
+    float2* dst = s.y + fr * 200 + q * 8;
+#pragma unroll
+    for (int k1 = 0; k1 < 8; ++k1) dst[k1] = cmul(z[k1], s.tw200[q * 8 + k1]);
+  }
+  __syncthreads();
+
+  // Stage B: per (frame, k1): 25-point DFT over q (5 x 5).
+  {
+    const int fr = tid / 8, k1 = tid % 8;               // 256 tasks exactly
+    float2 v[25];
+    const float2* src = s.y + fr * 200 + k1;
+#pragma unroll
+    for (int q = 0; q < 25; ++q) v[q] = src[q * 8];
+    // q = 5a + c: DFT over a for each c, twiddle W25^{c e}
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      dft5(v[c], v[5 + c], v[10 + c], v[15 + c], v[20 + c]);
+#pragma unroll
+      for (int e = 1; e < 5; ++e) v[5 * e + c] = cmul(v[5 * e + c], s.tw25[c * e]);
+    }
+    // DFT over c for each e: output k2 = e + 5 g
+#pragma unroll
+    for (int e = 0; e < 5; ++e)
+      dft5(v[5 * e + 0], v[5 * e + 1], v[5 * e + 2], v[5 * e + 3], v[5 * e + 4]);
+    __syncthreads();
+    // v[5e + g] = Z[k1 + 8*(e + 5g)]
+    float2* dst = s.y + fr * 200;
+#pragma unroll
+    for (int e = 0; e < 5; ++e)
+#pragma unroll
+      for (int g = 0; g < 5; ++g) dst[k1 + 8 * (e + 5 * g)] = v[5 * e + g];
+  }
+  __syncthreads();
+
+  // Real-FFT post-processing + power.
+  float* power = s.samples;
+  for (int t = tid; t < kFPB * kBins; t += kLogmelThreads) {
+    int fr = t / kBins, k = t % kBins;
+    const float2* Z = s.y + fr * 200;
+    float2 zk = Z[k % 200], zc = Z[(200 - k) % 200];
+    zc.y = -zc.y;                                        // conj(Z[200-k])
+    float2 E = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y + zc.y));
+    float2 D = make_float2(0.5f * (zk.x - zc.x), 0.5f * (zk.y - zc.y));
+    float2 O = make_float2(D.y, -D.x);                   // D / i
+    float2 X = cadd(E, cmul(s.tw400[k], O));
+    power[fr * kBins + k] = X.x * X.x + X.y * X.y;
+  }
+  __syncthreads();
+
+  // Sparse mel + log10; coalesced along frames.
+  float lmax = -INFINITY;
+  for (int t = tid; t < n_mels * kFPB; t += kLogmelThreads) {
+    int m = t / kFPB, fr = t % kFPB;
+    if (fr >= nfr) continue;
+    int k0 = tab->mel_start[m], cnt = tab->mel_count[m], wo = tab->mel_woff[m];
+    const float* pw = power + fr * kBins + k0;
+    float acc = 0.f;
+    for (int i = 0; i < cnt; ++i) acc = fmaf(tab->mel_w[wo + i], pw[i], acc);
+    float v = log10f(fmaxf(acc, 1e-10f));
+    outb[size_t(m) * kFrames + f0 + fr] = v;
+    lmax = fmaxf(lmax, v);
+  }
+  // block max -> one atomic
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lmax = fmaxf(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+  __shared__ float wmax[kLogmelThreads / 32];
+  if ((tid & 31) == 0) wmax[tid >> 5] = lmax;
+  __syncthreads();
+  if (tid == 0) {
+    float m = wmax[0];
+    for (int i = 1; i < kLogmelThreads / 32; ++i) m = fmaxf(m, wmax[i]);
+    atomicMax(segmax + b, float_to_ordered(m));
+  }
+}
+
+// Clamp to (segment max - 8), normalise, and emit the bf16 time-major copy.
+__global__ void __launch_bounds__(256)
+logmel_normalize_kernel(float* __restrict__ out, const uint32_t* __restrict__ segmax,
+                        int n_mels, uint16_t* __restrict__ mel_t /*[B,3002,n_mels]*/) {
+  __shared__ float tile[128][kFPB + 1];
+  const int b = blockIdx.y;
+  const int f0 = blockIdx.x * kFPB;
+  const int nfr = min(kFPB, kFrames - f0);
+  const float floor_v = ordered_to_float(segmax[b]) - 8.0f;
+  float* outb = out + size_t(b) * n_mels * kFrames;
+  for (int t = threadIdx.x; t < n_mels * kFPB; t += blockDim.x) {
+    int m = t / kFPB, fr = t % kFPB;
+    if (fr >= nfr) continue;
+    float v = outb[size_t(m) * kFrames + f0 + fr];
+    v = (fmaxf(v, floor_v) + 4.0f) / 4.0f;
+    outb[size_t(m) * kFrames + f0 + fr] = v;
+    tile[m][fr] = v;
+  }
+  if (mel_t == nullptr) return;
+  __syncthreads();
+  uint16_t* dst = mel_t + (size_t(b) * (kFrames + 2) + f0 + 1) * n_mels;
+  for (int t = threadIdx.x; t < n_mels * nfr; t += blockDim.x) {
+    int fr = t / n_mels, m = t % n_mels;
+    dst[size_t(fr) * n_mels + m] = f32_to_bf16(tile[m][fr]);
+  }
+}
+
+size_t logmel_smem_bytes() { return sizeof(LogmelSmem); }
+
+int launch_logmel(const int16_t* pcm, const int64_t* offsets, const int32_t* lengths,
+                  int n_segments, int n_mels, const LogmelTables* tables, float* out,
+                  uint16_t* mel_t, uint32_t* segmax, cudaStream_t stream) {
+  DM_REQUIRE(n_mels == 80 || n_mels == 128, "n_mels must be 80 or 128");
+  DM_REQUIRE(n_segments >= 0, "n_segments < 0");
+  if (n_segments == 0) return 0;
+  static bool attr_set = false;
+  const size_t smem = logmel_smem_bytes();
+  if (!attr_set) {
+    DM_CHECK_CUDA(cudaFuncSetAttribute(logmel_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       int(smem)));
+    attr_set = true;
+  }
+  DM_CHECK_CUDA(cudaMemsetAsync(segmax, 0, sizeof(uint32_t) * n_segments, stream));
+  dim3 grid(ceil_div(kFrames, kFPB), n_segments);
+  logmel_kernel<<<grid, kLogmelThreads, smem, stream>>>(pcm, offsets, lengths, tables,
+                                                         n_mels, out, segmax);
+  DM_CHECK_LAUNCH();
+  logmel_normalize_kernel<<<grid, 256, 0, stream>>>(out, segmax, n_mels, mel_t);
+  DM_CHECK_LAUNCH();
+  return 0;
+}
+
+}  // namespace dm

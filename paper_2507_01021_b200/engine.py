@@ -1,0 +1,286 @@
+"""Host side of the Whisper engine: weights on the device, the C-ABI handle,
+and the continuous-batching slot loop (K7) that both the batch-synchronous
+`transcribe_batch` contract and the per-GPU multiplexer consumers drive.
+
+torch is used only for device memory, pinned host buffers and streams; all
+arithmetic runs in the sm_100a library (`_native`). No CPU fallback exists.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import time
+from collections import deque
+from dataclasses import dataclass, field
+from typing import Callable, Hashable, Iterable, Sequence
+
+import numpy as np
+import torch
+
+from . import _native
+from .models import N_SAMPLES, WhisperDims
+from .weights import Manifest, host_tensor_values, normal_scale, tensor_key, whisper_manifest
+
+PROMPT_MAX = 8
+MAX_TOKENS = 448
+
+
+def whisper_offsets(man: Manifest, dims: WhisperDims) -> list[int]:
+    """Offset table in the order include/dictamux_b200.h documents."""
+    names = ["enc.conv1.w", "enc.conv1.b", "enc.conv2.w", "enc.conv2.b", "enc.pos"]
+    for i in range(dims.enc_layers):
+        p = f"enc.l{i}"
+        names += [f"{p}.{s}" for s in ("ln1.g", "ln1.b", "qkv.w", "qkv.b", "o.w", "o.b",
+                                       "ln2.g", "ln2.b", "fc1.w", "fc1.b", "fc2.w", "fc2.b")]
+    names += ["enc.ln.g", "enc.ln.b", "dec.embed", "dec.pos"]
+    for i in range(dims.dec_layers):
+        p = f"dec.l{i}"
+        names += [f"{p}.{s}" for s in ("ln1.g", "ln1.b", "qkv.w", "qkv.b", "o.w", "o.b",
+                                       "ln2.g", "ln2.b", "xq.w", "xq.b", "xo.w", "xo.b",
+                                       "ln3.g", "ln3.b", "fc1.w", "fc1.b", "fc2.w", "fc2.b")]
+    names += ["dec.xkv.w", "dec.xkv.b", "dec.ln.g", "dec.ln.b"]
+    return [man[n].offset for n in names]
+
+
+def materialize_weights(man: Manifest, device: torch.device,
+                        stream: torch.cuda.Stream) -> torch.Tensor:
+    """Fill the flat bf16 blob on the device with the seeded generator
+    (csrc/engine.cu fill_normal_kernel; bit-identical to oracle/weights.py)."""
+    blob = torch.zeros(man.total_elems, dtype=torch.int16, device=device)
+    base = blob.data_ptr()
+    with torch.cuda.stream(stream):
+        for t in man.tensors:
+            if t.init == "normal":
+                _native.call("dm_fill_normal_bf16", C.c_void_p(base + 2 * t.offset),
+                             t.numel, tensor_key(man.seed, t.tid), normal_scale(t.std),
+                             float(t.mean), C.c_void_p(stream.cuda_stream))
+            elif t.init == "host":
+                vals = torch.from_numpy(host_tensor_values(man, t).view(np.int16).reshape(-1))
+                blob[t.offset:t.offset + t.numel].copy_(vals, non_blocking=False)
+            elif t.init == "ones":
+                blob[t.offset:t.offset + t.numel].fill_(0x3F80)
+            for a, b in t.zero_ranges:
+                blob[t.offset + a:t.offset + b].zero_()
+    stream.synchronize()
+    return blob
+
+
+@dataclass
+class SegmentJob:
+    key: Hashable
+    samples: np.ndarray          # int16
+    cap: int
+    on_done: Callable[[Hashable, list[int]], None] | None = None
+
+
+@dataclass
+class EngineStats:
+    encode_calls: int = 0
+    segments_encoded: int = 0
+    steps: int = 0
+    slot_steps: int = 0
+    busy_s: float = 0.0
+
+
+class WhisperGPU:
+    """One engine per GPU (`SPEC.md:176` "one dispatch loop per backend
+    device"): weights, encoder workspace, decode slots and the CUDA-graph
+    decode step, all behind the C ABI."""
+
+    def __init__(self, dims: WhisperDims, *, seed: int = 0, init_std: float = 0.02,
+                 device: int | str | torch.device = 0, max_slots: int = 64,
+                 max_encode_batch: int = 32, num_pages: int | None = None,
+                 eot: int | None = None, steps_per_poll: int = 8):
+        if not torch.cuda.is_available():
+            raise _native.DmError("no CUDA device: the B200 engine has no CPU fallback")
+        self.dims = dims
+        self.device = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        self.lib = _native.load()
+        self.max_slots = max_slots
+        self.max_encode_batch = max_encode_batch
+        self.steps_per_poll = steps_per_poll
+        self.eot = dims.eot if eot is None else eot
+        with torch.cuda.device(self.device):
+            self.stream = torch.cuda.Stream(self.device)
+            self.man = whisper_manifest(dims, seed, init_std)
+            self.blob = materialize_weights(self.man, self.device, self.stream)
+            offs = whisper_offsets(self.man, dims)
+            cfg = _native.WhisperConfigC()
+            cfg.d_model, cfg.enc_layers, cfg.dec_layers = dims.d_model, dims.enc_layers, dims.dec_layers
+            cfg.heads, cfg.ffn, cfg.n_mels, cfg.vocab = dims.heads, dims.ffn, dims.n_mels, dims.vocab
+            cfg.eot = self.eot
+            for i, t in enumerate(dims.prompt):
+                cfg.prompt[i] = t
+            cfg.prompt_len = len(dims.prompt)
+            cfg.max_slots, cfg.max_encode_batch = max_slots, max_encode_batch
+            cfg.num_pages = num_pages if num_pages is not None else max_slots * 7
+            arr = (C.c_int64 * len(offs))(*offs)
+            h = C.c_void_p()
+            _native.check(self.lib.dm_whisper_create(C.byref(cfg), C.c_void_p(self.blob.data_ptr()),
+                                                     arr, len(offs), C.byref(h)))
+            self.handle = h
+            # pinned staging for PCM uploads + device buffers
+            self._pcm_host = torch.empty(max_encode_batch * N_SAMPLES, dtype=torch.int16,
+                                         pin_memory=True)
+            self._pcm_dev = torch.empty(max_encode_batch * N_SAMPLES, dtype=torch.int16,
+                                        device=self.device)
+            self._meta_host = torch.empty(3 * max_encode_batch, dtype=torch.int64, pin_memory=True)
+            self._meta_dev = torch.empty(3 * max_encode_batch, dtype=torch.int64, device=self.device)
+            self._done = np.zeros(max_slots, np.int32)
+            self._ngen = np.zeros(max_slots, np.int32)
+            self._tokens = np.zeros(max_slots * MAX_TOKENS, np.int32)
+        self.stats = EngineStats()
+        self.h2d_bytes = 0
+        self.d2h_bytes = 0
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _native.check(self.lib.dm_whisper_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ----------------------------------------------------------- primitives
+    @property
+    def _s(self):
+        return C.c_void_p(self.stream.cuda_stream)
+
+    def _i32(self, xs: Sequence[int]):
+        return (C.c_int32 * max(1, len(xs)))(*xs)
+
+    def upload_segments(self, segs: Sequence[np.ndarray]):
+        """Trim (pad_or_trim's truncation; padding is implicit in the kernel)
+        and copy PCM to the device. Returns (pcm, offsets, lengths) pointers."""
+        n = len(segs)
+        host = self._pcm_host.numpy()
+        offs, lens = [], []
+        pos = 0
+        for s in segs:
+            s = np.asarray(s)
+            if s.dtype != np.int16:
+                raise TypeError("segment samples must be int16 PCM")
+            k = min(len(s), N_SAMPLES)
+            host[pos:pos + k] = s[:k]
+            offs.append(pos)
+            lens.append(k)
+            pos += k
+        meta = self._meta_host.numpy()
+        meta[:n] = offs
+        meta32 = meta[n:].view(np.int32)     # lengths packed after offsets
+        meta32[:n] = lens
+        with torch.cuda.stream(self.stream):
+            if pos:
+                self._pcm_dev[:pos].copy_(self._pcm_host[:pos], non_blocking=True)
+            self._meta_dev.copy_(self._meta_host, non_blocking=True)
+        self.h2d_bytes += 2 * pos + 12 * n
+        pcm = C.c_void_p(self._pcm_dev.data_ptr())
+        offp = C.c_void_p(self._meta_dev.data_ptr())
+        lenp = C.c_void_p(self._meta_dev.data_ptr() + 8 * n)
+        return pcm, offp, lenp
+
+    def encode(self, segs: Sequence[np.ndarray], slots: Sequence[int]) -> None:
+        pcm, offp, lenp = self.upload_segments(segs)
+        _native.check(self.lib.dm_whisper_encode(self.handle, pcm, offp, lenp, len(segs),
+                                                 self._i32(slots), self._s))
+        self.stats.encode_calls += 1
+        self.stats.segments_encoded += len(segs)
+
+    def admit(self, slots: Sequence[int], caps: Sequence[int]) -> None:
+        _native.check(self.lib.dm_whisper_admit(self.handle, self._i32(slots), self._i32(caps),
+                                                len(slots), self._s))
+
+    def release(self, slots: Sequence[int]) -> None:
+        _native.check(self.lib.dm_whisper_release(self.handle, self._i32(slots), len(slots)))
+
+    def set_active(self, slots: Sequence[int]) -> None:
+        _native.check(self.lib.dm_whisper_set_active(self.handle, self._i32(slots), len(slots),
+                                                     self._s))
+
+    def step(self, n: int) -> None:
+        _native.check(self.lib.dm_whisper_step(self.handle, n, self._s))
+
+    def read(self, tokens: bool = False):
+        tp = self._tokens.ctypes.data_as(C.c_void_p) if tokens else None
+        _native.check(self.lib.dm_whisper_read(self.handle,
+                                               self._done.ctypes.data_as(C.c_void_p),
+                                               self._ngen.ctypes.data_as(C.c_void_p), tp,
+                                               self._s))
+        self.d2h_bytes += 8 * self.max_slots + (4 * self.max_slots * MAX_TOKENS if tokens else 0)
+        return self._done, self._ngen, self._tokens.reshape(self.max_slots, MAX_TOKENS)
+
+    def debug(self, which: int, out: np.ndarray | None = None) -> np.ndarray | None:
+        if which == 3:
+            _native.check(self.lib.dm_whisper_debug(self.handle, 3, None, 0, self._s))
+            return None
+        _native.check(self.lib.dm_whisper_debug(self.handle, which,
+                                                out.ctypes.data_as(C.c_void_p), out.nbytes,
+                                                self._s))
+        return out
+
+    def encoder_output(self, n: int) -> np.ndarray:
+        bits = np.empty((n, 1500, self.dims.d_model), np.uint16)
+        self.debug(0, bits)
+        return (bits.astype(np.uint32) << 16).view(np.float32)
+
+    def log_mel(self, n: int) -> np.ndarray:
+        return self.debug(1, np.empty((n, self.dims.n_mels, 3000), np.float32))
+
+    # ----------------------------------------------------------- slot loop
+    def run_jobs(self, jobs: Iterable[SegmentJob],
+                 refill: Callable[[int], list[SegmentJob]] | None = None) -> dict:
+        """Continuous batching: admit jobs into free decode slots (encoding
+        them in groups of <= max_encode_batch), step the active slots, route a
+        segment as soon as its slot hits EOT or its cap, refill freed slots
+        from `pending` then from `refill(n_free)` (the multiplexer hook).
+        Returns {key: token ids}."""
+        pending = deque(jobs)
+        free = list(range(self.max_slots - 1, -1, -1))
+        active: dict[int, SegmentJob] = {}
+        results: dict = {}
+        t0 = time.perf_counter()
+        while True:
+            if free and refill is not None and len(pending) < len(free):
+                pending.extend(refill(len(free) - len(pending)))
+            admitted = False
+            while free and pending:
+                take = []
+                while free and pending and len(take) < self.max_encode_batch:
+                    take.append((free.pop(), pending.popleft()))
+                slots = [s for s, _ in take]
+                self.encode([j.samples for _, j in take], slots)
+                self.admit(slots, [j.cap for _, j in take])
+                for s, j in take:
+                    active[s] = j
+                admitted = True
+            if not active:
+                break
+            if admitted:
+                self.set_active(sorted(active))
+            self.step(self.steps_per_poll)
+            self.stats.steps += self.steps_per_poll
+            self.stats.slot_steps += self.steps_per_poll * len(active)
+            done, ngen, _ = self.read(tokens=False)
+            finished = [s for s in active if done[s]]
+            if finished:
+                _, ngen, toks = self.read(tokens=True)
+                for s in finished:
+                    j = active.pop(s)
+                    ids = toks[s, :ngen[s]].tolist()
+                    results[j.key] = ids
+                    if j.on_done is not None:
+                        j.on_done(j.key, ids)
+                self.release(finished)
+                free.extend(finished)
+                self.set_active(sorted(active))
+        self.stats.busy_s += time.perf_counter() - t0
+        return results
+
+    def transcribe_ids(self, segs: Sequence[np.ndarray], caps: Sequence[int]) -> list[list[int]]:
+        jobs = [SegmentJob(i, s, int(c)) for i, (s, c) in enumerate(zip(segs, caps))]
+        out = self.run_jobs(jobs)
+        return [out[i] for i in range(len(segs))]

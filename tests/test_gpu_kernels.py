@@ -1,0 +1,78 @@
+"""GPU parity of the individual sm_100a kernels against the CPU oracle and
+plain fp32 references (run on a B200 via `pytest -m gpu`)."""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2507_01021_b200 import _native
+from paper_2507_01021_b200.models import WHISPER_TINY
+from paper_2507_01021_b200.weights import whisper_manifest
+
+pytestmark = pytest.mark.gpu
+
+
+def _ptr(t: torch.Tensor):
+    return C.c_void_p(t.data_ptr())
+
+
+def test_weight_fill_bit_exact(native_lib):
+    """Device weight generator == numpy restatement, bit for bit."""
+    from oracle.weights import blob_bits
+    from paper_2507_01021_b200.engine import materialize_weights
+    man = whisper_manifest(WHISPER_TINY, seed=3)
+    s = torch.cuda.Stream()
+    blob = materialize_weights(man, torch.device("cuda", 0), s)
+    got = blob.cpu().numpy().view(np.uint16)
+    want = blob_bits(man)
+    assert got.shape == want.shape
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("lengths", [
+    (160_000, 48_000, 0, 480_000, 500_000, 77),
+    (30_000,),
+])
+@pytest.mark.parametrize("n_mels", [80, 128])
+def test_logmel_matches_oracle(native_lib, lengths, n_mels):
+    from oracle.logmel import log_mel_batch
+    rng = np.random.default_rng(sum(lengths) + n_mels)
+    segs = [rng.integers(-8000, 8000, size=n, dtype=np.int16) for n in lengths]
+    if len(segs) > 1:   # a structured (non-white) segment too
+        t = np.arange(len(segs[0])) / 16000.0
+        segs[0] = (3000 * np.sin(2 * np.pi * 440 * t) * (1 + np.sin(2 * np.pi * 3 * t))
+                   ).astype(np.int16)
+    flat = np.concatenate(segs) if sum(lengths) else np.zeros(1, np.int16)
+    offs = np.cumsum([0] + [len(s) for s in segs[:-1]]).astype(np.int64)
+    pcm = torch.from_numpy(flat).cuda()
+    off = torch.from_numpy(offs).cuda()
+    ln = torch.tensor(lengths, dtype=torch.int32).cuda()
+    out = torch.empty(len(segs), n_mels, 3000, device="cuda")
+    _native.call("dm_logmel", _ptr(pcm), _ptr(off), _ptr(ln), len(segs), n_mels, _ptr(out), None)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    want = log_mel_batch(segs, n_mels)
+    err = np.abs(got - want)
+    # north-star tolerance: 1e-4 relative (values are O(1); use |ref| + 1 floor)
+    rel = err / np.maximum(np.abs(want), 1.0)
+    assert rel.max() <= 1e-4, (rel.max(), np.unravel_index(rel.argmax(), rel.shape))
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (300, 384, 384), (1500, 1536, 512),
+                                   (777, 2048, 1280), (2048, 512, 2048)])
+def test_tcgen05_gemm_matches_fp32(native_lib, M, N, K):
+    g = torch.Generator().manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, generator=g).bfloat16()
+    W = torch.randn(N, K, generator=g).bfloat16()
+    b = torch.randn(N, generator=g).bfloat16()
+    ref = A.float() @ W.float().T + b.float()
+    Ad, Wd, bd = A.cuda(), W.cuda(), b.cuda()
+    out = torch.empty(M, N, device="cuda")
+    _native.call("dm_gemm_bf16_f32", _ptr(Ad), _ptr(Wd), _ptr(bd), _ptr(out), M, N, K, None)
+    torch.cuda.synchronize()
+    err = (out.cpu() - ref).abs().max().item()
+    assert err <= 1e-3 * (K ** 0.5), err

@@ -1,0 +1,109 @@
+"""End-to-end parity of the Whisper engine (encoder output, decoder logits,
+greedy tokens) against the fp32 CPU oracle on identical seeded weights."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2507_01021_b200.models import WHISPER_BASE, WHISPER_TINY
+
+pytestmark = pytest.mark.gpu
+
+
+def _segments(n, durs, seed=0):
+    rng = np.random.default_rng(seed)
+    return [rng.integers(-8000, 8000, size=int(round(d * 16000)), dtype=np.int16)
+            for d in durs[:n]]
+
+
+@pytest.fixture(scope="module")
+def tiny_pair(native_lib):
+    from oracle.whisper import WhisperOracle
+    from paper_2507_01021_b200.engine import WhisperGPU
+    orc = WhisperOracle(WHISPER_TINY, seed=0)
+    gpu = WhisperGPU(WHISPER_TINY, seed=0, max_slots=16, max_encode_batch=8)
+    return orc, gpu
+
+
+def test_encoder_output_within_bf16_tolerance(tiny_pair):
+    from oracle.logmel import log_mel_batch
+    orc, gpu = tiny_pair
+    segs = _segments(3, [10.0, 3.0, 30.0], seed=1)
+    gpu.encode(segs, [0, 1, 2])
+    mel = gpu.log_mel(3)
+    want_mel = log_mel_batch(segs, 80)
+    assert np.abs(mel - want_mel).max() <= 1e-4 * max(1.0, np.abs(want_mel).max())
+    got = gpu.encoder_output(3)
+    want = orc.encode(want_mel).numpy()
+    err = np.abs(got - want).max()
+    assert err <= 2e-2, err
+
+
+def test_greedy_tokens_match_oracle(tiny_pair):
+    orc, gpu = tiny_pair
+    from oracle.logmel import log_mel_batch
+    durs = [10.0] * 8
+    segs = _segments(8, durs, seed=2)
+    caps = [32] * 8
+    got = gpu.transcribe_ids(segs, caps)
+    enc = orc.encode(log_mel_batch(segs, 80))
+    want = [orc.greedy(enc[b], 32) for b in range(8)]
+    same = sum(g == w for g, w in zip(got, want))
+    assert same >= 8 * 0.99, (got, want)
+
+
+def test_batch_invariance_bitwise(tiny_pair):
+    """A segment decodes to identical tokens alone and inside a mixed batch
+    (the reference pins text equality across batchings:
+    pkg/tests/test_server.py:334-342, test_bench.py:163-168)."""
+    _, gpu = tiny_pair
+    segs = _segments(6, [4.0, 12.0, 7.5, 30.0, 3.0, 20.0], seed=3)
+    caps = [5, 20, 9, 31, 3, 25]
+    together = gpu.transcribe_ids(segs, caps)
+    alone = [gpu.transcribe_ids([s], [c])[0] for s, c in zip(segs, caps)]
+    assert together == alone
+    assert [len(t) for t in together] == caps
+
+
+def test_decoder_logits_match_oracle(tiny_pair):
+    orc, gpu = tiny_pair
+    from oracle.logmel import log_mel_batch
+    segs = _segments(2, [6.0, 15.0], seed=4)
+    gpu.debug(3)                                  # enable the logits tap
+    gpu.encode(segs, [0, 1])
+    gpu.admit([0, 1], [8, 8])
+    gpu.set_active([0, 1])
+    enc = orc.encode(log_mel_batch(segs, 80))
+    logits = np.empty((gpu.max_slots, WHISPER_TINY.vocab), np.float32)
+    prompt = list(WHISPER_TINY.prompt)
+    for step in range(6):
+        gpu.step(1)
+        gpu.debug(2, logits)
+        _, ngen, toks = gpu.read(tokens=True)
+        for b in range(2):
+            fed = prompt[:min(step + 1, 4)] + toks[b, :max(0, step - 3)].tolist()
+            ref = orc.decoder_logits(torch.tensor([fed]), enc[b:b + 1])[0, -1].numpy()
+            err = np.abs(logits[b] - ref).max()
+            assert err <= 2e-2, (step, b, err)
+    gpu.release([0, 1])
+    gpu.set_active([])
+
+
+def test_eot_releases_slot(native_lib):
+    """Pick the EOT id the model actually emits so the EOT path runs."""
+    from oracle.logmel import log_mel_batch
+    from oracle.whisper import WhisperOracle
+    from paper_2507_01021_b200.engine import WhisperGPU
+    segs = _segments(2, [5.0, 9.0], seed=5)
+    orc = WhisperOracle(WHISPER_TINY, seed=0)
+    enc = orc.encode(log_mel_batch(segs, 80))
+    free_run = orc.greedy(enc[0], 12)
+    eot = free_run[0]
+    gpu = WhisperGPU(WHISPER_TINY, seed=0, max_slots=4, max_encode_batch=2, eot=eot)
+    got = gpu.transcribe_ids(segs, [12, 12])
+    want = [orc.greedy(enc[b], 12, eot=eot) for b in range(2)]
+    assert got == want
+    assert got[0] == []
+    gpu.close()
