@@ -113,7 +113,10 @@ DM_API int dm_whisper_read(void* handle, int32_t* done, int32_t* n_gen, int32_t*
  *  which = 0: encoder output of the last encode, [n, 1500, d] bf16 bits
  *  which = 1: log-mel of the last encode, [n, n_mels, 3000] fp32
  *  which = 2: logits of the last step, [max_slots, vocab] fp32 (enable first)
- *  which = 3: enable the logits tap (bytes ignored) */
+ *  which = 3: enable the logits tap (bytes ignored)
+ *  which = 4: run only the first `bytes` encoder layers in later encodes
+ *  which = 5: fp32 residual stream before the final LN, [n, 1500, d]
+ *  which = 6: attention output of the last encoder layer run, [n, 1500, d] bf16 */
 DM_API int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void* stream);
 
 #ifdef __cplusplus

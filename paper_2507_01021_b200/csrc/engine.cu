@@ -169,6 +169,7 @@ struct WhisperEngine {
   int32_t* slot_dev = nullptr;   // [E]
   int32_t* slot_host = nullptr;  // pinned [E]
   int last_n = 0;
+  int enc_stop = 1 << 30;        // debug: run only the first enc_stop layers
   // decode
   DecodeState st{};
   int32_t* prompt_dev = nullptr;
@@ -338,7 +339,7 @@ static int encoder_forward(WhisperEngine* e, const int16_t* pcm, const int64_t* 
     g.W = Wt; g.N = N;
     return g;
   };
-  for (int l = 0; l < e->L; ++l) {
+  for (int l = 0; l < e->L && l < e->enc_stop; ++l) {
     const int b0 = e->enc_layer_base(l);
     if (int rc = launch_layernorm_bf16(e->resid, e->W(b0 + 0), e->W(b0 + 1), e->lnb, M, d, s))
       return rc;
@@ -667,6 +668,9 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
       }
       return 0;
     }
+    case 4: e->enc_stop = int(bytes); return 0;
+    case 5: src = e->resid; avail = size_t(e->last_n) * 1500 * e->d * 4; break;
+    case 6: src = e->attn_out; avail = size_t(e->last_n) * 1500 * e->d * 2; break;
     default: DM_REQUIRE(false, "unknown debug tap");
   }
   DM_REQUIRE(bytes <= avail, "debug copy larger than the tapped buffer");
