@@ -250,7 +250,7 @@ logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offse
 // Clamp to (segment max - 8), normalise, and emit the bf16 time-major copy.
 __global__ void __launch_bounds__(256)
 logmel_normalize_kernel(float* __restrict__ out, const uint32_t* __restrict__ segmax,
-                        int n_mels, uint16_t* __restrict__ mel_t /*[B,3002,n_mels]*/) {
+                        int n_mels, uint16_t* __restrict__ mel_t /*[B,3002,ldt]*/, int ldt) {
   __shared__ float tile[128][kFPB + 1];
   const int b = blockIdx.y;
   const int f0 = blockIdx.x * kFPB;
@@ -267,10 +267,10 @@ logmel_normalize_kernel(float* __restrict__ out, const uint32_t* __restrict__ se
   }
   if (mel_t == nullptr) return;
   __syncthreads();
-  uint16_t* dst = mel_t + (size_t(b) * (kFrames + 2) + f0 + 1) * n_mels;
+  uint16_t* dst = mel_t + (size_t(b) * (kFrames + 2) + f0 + 1) * ldt;
   for (int t = threadIdx.x; t < n_mels * nfr; t += blockDim.x) {
     int fr = t / n_mels, m = t % n_mels;
-    dst[size_t(fr) * n_mels + m] = f32_to_bf16(tile[m][fr]);
+    dst[size_t(fr) * ldt + m] = f32_to_bf16(tile[m][fr]);
   }
 }
 
@@ -295,7 +295,9 @@ int launch_logmel(const int16_t* pcm, const int64_t* offsets, const int32_t* len
   logmel_kernel<<<grid, kLogmelThreads, smem, stream>>>(pcm, offsets, lengths, tables,
                                                          n_mels, out, segmax);
   DM_CHECK_LAUNCH();
-  logmel_normalize_kernel<<<grid, 256, 0, stream>>>(out, segmax, n_mels, mel_t);
+  // time-major copy rows are padded to 64 (n_mels <= 64) or 128 channels
+  const int ldt = n_mels <= 64 ? 64 : 128;
+  logmel_normalize_kernel<<<grid, 256, 0, stream>>>(out, segmax, n_mels, mel_t, ldt);
   DM_CHECK_LAUNCH();
   return 0;
 }
