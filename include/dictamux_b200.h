@@ -119,6 +119,14 @@ DM_API int dm_whisper_read(void* handle, int32_t* done, int32_t* n_gen, int32_t*
  *  which = 6: attention output of the last encoder layer run, [n, 1500, d] bf16 */
 DM_API int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void* stream);
 
+/* Telemetry: out[0..3] = kernels launched, decode steps, encode calls, segments. */
+DM_API int dm_whisper_stats(void* handle, int64_t* out, int n);
+/* Time one decode kernel over the current active slots with CUDA events on
+ * `stream` (idempotent kernels only): which = 0 cross-attention(layer),
+ * 1 self-attention(layer), 2 LM head. avg_ms = mean over iters launches. */
+DM_API int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float* avg_ms,
+                                  void* stream);
+
 #ifdef __cplusplus
 }
 #endif

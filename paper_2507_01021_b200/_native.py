@@ -18,7 +18,7 @@ EXPORTS = (
     "dm_gemm_bf16_f32", "dm_whisper_create", "dm_whisper_destroy",
     "dm_whisper_encode", "dm_whisper_admit", "dm_whisper_release",
     "dm_whisper_set_active", "dm_whisper_step", "dm_whisper_read",
-    "dm_whisper_debug",
+    "dm_whisper_debug", "dm_whisper_stats", "dm_whisper_time_kernel",
 )
 
 
@@ -72,6 +72,8 @@ def load(build_if_missing: bool = False):
             "dm_whisper_step": [P, C.c_int, P],
             "dm_whisper_read": [P, P, P, P, P],
             "dm_whisper_debug": [P, C.c_int, P, C.c_size_t, P],
+            "dm_whisper_stats": [P, P, C.c_int],
+            "dm_whisper_time_kernel": [P, C.c_int, C.c_int, C.c_int, P, P],
         }
         for name, args in sig.items():
             fn = getattr(lib, name)

@@ -185,6 +185,10 @@ struct WhisperEngine {
   cudaGraphExec_t step_exec = nullptr;
   cudaGraph_t step_graph = nullptr;
   int gemv_counter_base = 0, xattn_counter_base = 0;
+  // telemetry: kernels launched (graph nodes counted per replay)
+  long long launches = 0, steps = 0, encodes = 0, segments = 0;
+  int step_kernels() const { return 1 + 11 * Ld + 3; }
+  int encode_kernels() const { return 2 + 2 + 7 * L + 1 + 1; }
 
   int alloc(void** p, size_t bytes, bool zero = true) {
     DM_CHECK_CUDA(cudaMalloc(p, bytes));
@@ -530,6 +534,9 @@ int dm_whisper_encode(void* handle, const int16_t* pcm, const int64_t* offsets,
   DM_CHECK_CUDA(cudaMemcpyAsync(e->slot_dev, e->slot_host, sizeof(int32_t) * n,
                                 cudaMemcpyHostToDevice, s));
   e->last_n = n;
+  e->encodes += 1;
+  e->segments += n;
+  e->launches += e->encode_kernels();
   return encoder_forward(e, pcm, offsets, lengths, n, s);
 }
 
@@ -587,6 +594,7 @@ int dm_whisper_admit(void* handle, const int32_t* slot_ids, const int32_t* caps,
   std::memcpy(args, e->staging, sizeof(int32_t) * 2 * n);
   admit_kernel<<<ceil_div(n, 64), 64, 0, s>>>(e->st, args, n);
   DM_CHECK_LAUNCH();
+  e->launches += 1;
   DM_CHECK_CUDA(cudaStreamSynchronize(s));   // host table / staging consumed
   return 0;
 }
@@ -631,6 +639,46 @@ int dm_whisper_step(void* handle, int n_steps, void* stream) {
     if (int rc = build_step_graph(e)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(e->step_exec, s));
+  e->steps += n_steps;
+  e->launches += (long long)n_steps * e->step_kernels();
+  return 0;
+}
+
+int dm_whisper_stats(void* handle, int64_t* out, int n) {
+  auto* e = static_cast<WhisperEngine*>(handle);
+  DM_REQUIRE(e != nullptr && out != nullptr && n >= 4, "need 4 outputs");
+  out[0] = e->launches; out[1] = e->steps; out[2] = e->encodes; out[3] = e->segments;
+  return 0;
+}
+
+int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float* avg_ms,
+                           void* stream) {
+  auto* e = static_cast<WhisperEngine*>(handle);
+  DM_REQUIRE(e != nullptr && avg_ms != nullptr && iters >= 1, "bad arguments");
+  DM_REQUIRE(layer >= 0 && layer < e->Ld, "layer out of range");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaEvent_t a, b;
+  DM_CHECK_CUDA(cudaEventCreate(&a));
+  DM_CHECK_CUDA(cudaEventCreate(&b));
+  DM_CHECK_CUDA(cudaEventRecord(a, s));
+  for (int i = 0; i < iters; ++i) {
+    int rc = 0;
+    switch (which) {
+      case 0: rc = launch_cross_attn(e->st, layer, e->xattn_counter_base, s); break;
+      case 1: rc = launch_self_attn(e->st, layer, s); break;
+      case 2: rc = launch_lm_head(e->st, e->W(e->after_enc() + 2), s); break;
+      default: DM_REQUIRE(false, "unknown kernel id");
+    }
+    if (rc) return rc;
+  }
+  DM_CHECK_CUDA(cudaEventRecord(b, s));
+  DM_CHECK_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  DM_CHECK_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *avg_ms = ms / iters;
+  e->launches += iters;
   return 0;
 }
 

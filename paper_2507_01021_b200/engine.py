@@ -66,6 +66,14 @@ def materialize_weights(man: Manifest, device: torch.device,
     return blob
 
 
+@dataclass(frozen=True)
+class ResidentPCM:
+    """A segment whose int16 PCM already sits in the engine's resident device
+    buffer (set_resident) at [offset, offset + length)."""
+    offset: int
+    length: int
+
+
 @dataclass
 class SegmentJob:
     key: Hashable
@@ -131,6 +139,8 @@ class WhisperGPU:
             self._ngen = np.zeros(max_slots, np.int32)
             self._tokens = np.zeros(max_slots * MAX_TOKENS, np.int32)
         self.stats = EngineStats()
+        self._held: set[int] = set()       # slots holding self-KV pages
+        self._resident: torch.Tensor | None = None
         self.h2d_bytes = 0
         self.d2h_bytes = 0
 
@@ -153,10 +163,23 @@ class WhisperGPU:
     def _i32(self, xs: Sequence[int]):
         return (C.c_int32 * max(1, len(xs)))(*xs)
 
+    def set_resident(self, pcm_dev: torch.Tensor | None) -> None:
+        """Register a device int16 buffer that ResidentPCM jobs index into."""
+        self._resident = pcm_dev
+
     def upload_segments(self, segs: Sequence[np.ndarray]):
         """Trim (pad_or_trim's truncation; padding is implicit in the kernel)
         and copy PCM to the device. Returns (pcm, offsets, lengths) pointers."""
         n = len(segs)
+        if n and all(isinstance(s, ResidentPCM) for s in segs):
+            meta = self._meta_host.numpy()
+            meta[:n] = [s.offset for s in segs]
+            meta[n:].view(np.int32)[:n] = [min(s.length, N_SAMPLES) for s in segs]
+            with torch.cuda.stream(self.stream):
+                self._meta_dev.copy_(self._meta_host, non_blocking=True)
+            self.stream.synchronize()
+            return (C.c_void_p(self._resident.data_ptr()), C.c_void_p(self._meta_dev.data_ptr()),
+                    C.c_void_p(self._meta_dev.data_ptr() + 8 * n))
         host = self._pcm_host.numpy()
         offs, lens = [], []
         pos = 0
@@ -193,9 +216,18 @@ class WhisperGPU:
     def admit(self, slots: Sequence[int], caps: Sequence[int]) -> None:
         _native.check(self.lib.dm_whisper_admit(self.handle, self._i32(slots), self._i32(caps),
                                                 len(slots), self._s))
+        self._held.update(slots)
 
     def release(self, slots: Sequence[int]) -> None:
         _native.check(self.lib.dm_whisper_release(self.handle, self._i32(slots), len(slots)))
+        self._held.difference_update(slots)
+
+    def reset(self) -> None:
+        """Drop every slot (after a failed run): free pages, empty active set."""
+        self.stream.synchronize()
+        if self._held:
+            self.release(sorted(self._held))
+        self.set_active([])
 
     def set_active(self, slots: Sequence[int]) -> None:
         _native.check(self.lib.dm_whisper_set_active(self.handle, self._i32(slots), len(slots),
@@ -221,6 +253,18 @@ class WhisperGPU:
                                                 out.ctypes.data_as(C.c_void_p), out.nbytes,
                                                 self._s))
         return out
+
+    def counters(self) -> dict:
+        out = np.zeros(4, np.int64)
+        _native.check(self.lib.dm_whisper_stats(self.handle, out.ctypes.data_as(C.c_void_p), 4))
+        return dict(launches=int(out[0]), steps=int(out[1]), encodes=int(out[2]),
+                    segments=int(out[3]))
+
+    def time_kernel(self, which: int, layer: int = 0, iters: int = 20) -> float:
+        ms = C.c_float()
+        _native.check(self.lib.dm_whisper_time_kernel(self.handle, which, layer, iters,
+                                                      C.byref(ms), self._s))
+        return ms.value
 
     def encoder_output(self, n: int) -> np.ndarray:
         bits = np.empty((n, 1500, self.dims.d_model), np.uint16)
