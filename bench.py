@@ -248,6 +248,12 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
         barrier(world)
         return start.elapsed_time(end), out
 
+    if args.profile:
+        # single timed-path step, nothing else (for ncu launch lists)
+        eng.run_jobs(res_jobs())
+        torch.cuda.synchronize(dev)
+        print(json.dumps({"profile_step_done": True, **eng.counters()}), flush=True)
+        return
     for _ in range(args.warmup):
         timed(lambda: eng.run_jobs(res_jobs()))
     c0 = eng.counters()
@@ -357,6 +363,8 @@ def main():
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--ref-segments-per-step", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true",
+                    help="run exactly one resident-input step and exit (ncu)")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if world > 1:
