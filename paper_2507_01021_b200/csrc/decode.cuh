@@ -1,12 +1,20 @@
 // K6: batched greedy decode step kernels (Listing 1 `model.model.generate`,
 // PAPER.md:57-59) over continuous-batching slots.
+//
+// Activations live in "row space": row i < n_active is the i-th active slot
+// (slot = active[i]); persistent per-segment state (self-KV pages, cross-KV,
+// position, cap, tokens) is slot-indexed. Activations that feed a projection
+// are stored as a bf16 hi/lo pair (x = hi + lo exactly to ~2^-17 relative) so
+// the projections run on tcgen05 with fp32 accumulation while keeping fp32
+// activation precision (SURVEY.md §7 "Design rule").
 #pragma once
 
 #include "common.cuh"
 
 namespace dm {
 
-// Shared per-engine decode state (device pointers).
+constexpr int kRows = 64;          // max active slots = MMA N
+
 struct DecodeState {
   int max_slots, d, heads, layers, ffn, vocab;
   int page_tokens;       // self-KV tokens per page (64)
@@ -15,7 +23,7 @@ struct DecodeState {
   int prompt_len;
   const int32_t* prompt;       // [prompt_len]
   // slot bookkeeping
-  const int32_t* active;       // [max_slots] slot ids, first *n_active valid
+  const int32_t* active;       // [kRows] slot of row i
   const int32_t* n_active;     // device scalar
   int32_t* pos;                // [S] position of the token being fed
   int32_t* cur_tok;            // [S]
@@ -26,51 +34,58 @@ struct DecodeState {
   const int32_t* page_table;   // [S, pages_per_slot]
   uint16_t* kv_pool;           // [pages][L][2][H][page_tokens][64] bf16
   const uint16_t* xkv;         // [L][S][2][H][1500][64] bf16
-  // activations (fp32)
-  float* x;                    // [S, d] residual stream
-  float* xn;                   // [S, d] LN output
-  float* q;                    // [S, d]
-  float* attn;                 // [S, d]
-  float* h1;                   // [S, ffn]
-  // split-K / split-KV scratch
-  float* part;                 // scratch partials
+  // row-space activations
+  float* x;                    // [kRows, d] residual stream (fp32)
+  uint16_t *xh, *xl;           // [kRows, d]   LN output, bf16 hi/lo
+  float* q;                    // [kRows, d]   attention query (pre-scaled)
+  uint16_t *ah, *al;           // [kRows, d]   attention output hi/lo
+  uint16_t *hh, *hl;           // [kRows, ffn] fc1 output hi/lo
+  // scratch
+  float* part;                 // split-K / split-KV partials
   int32_t* counters;           // zero-initialised tile counters
-  float* amax_val;             // [tiles, S]
-  int32_t* amax_idx;           // [tiles, S]
-  float* logits_dbg;           // optional [S, vocab]
+  float* amax_val;             // [vocab tiles, kRows]
+  int32_t* amax_idx;           // [vocab tiles, kRows]
+  float* logits_dbg;           // optional [kRows, vocab]
   int xsplits;                 // cross-attention key splits
 };
 
-enum GemvEpi : int {
-  GV_STORE = 0,     // y[slot, n] = acc + b
-  GV_GELU = 1,      // y = gelu(acc + b)
-  GV_RESID = 2,     // x[slot, n] += acc + b
-  GV_SCALE = 3,     // y = (acc + b) * scale
-  GV_QKV = 4,       // q (scaled) / append k, v to the slot's self-KV page
+enum TcGemvEpi : int {
+  TV_STORE = 0,     // y[r, n] = (acc + b) * scale                 (fp32)
+  TV_GELU_HILO = 1, // yh/yl[r, n] = split(gelu(acc + b))         (bf16 pair)
+  TV_RESID = 2,     // x[r, n] += acc + b
+  TV_QKV = 3,       // q (scaled) / append k, v to the row's self-KV page
+  TV_ARGMAX = 4,    // per-row (max, lowest index) over this 128-row vocab tile
 };
 
-struct GemvArgs {
-  const float* X;          // [S, K] fp32 (slot-indexed)
-  const uint16_t* W;       // [N, K] bf16
+struct TcGemvArgs {
   const uint16_t* bias;    // [N] nullable
-  float* Y;                // [S, N] or residual
   int N, K;
   int epi;
   float scale;
-  int layer;               // GV_QKV: layer index
-  int splits;              // K splits (fixed per shape; never depends on R)
-  int counter_base;        // offset into DecodeState::counters
+  int layer;               // TV_QKV
+  int splits;              // K splits (fixed per shape; never depends on rows)
+  int counter_base;
+  float* y;                // TV_STORE / TV_RESID target [kRows, N]
+  uint16_t *yh, *yl;       // TV_GELU_HILO targets
 };
 
-int launch_gemv(const DecodeState& st, const GemvArgs& a, cudaStream_t stream);
-int gemv_splits(int N, int K);
+// Pre-encoded TMA maps of one projection: weights [N, K] and the hi/lo input.
+struct TcGemvMaps {
+  CUtensorMap w, xh, xl;
+};
+
+int make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                 uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+int tc_gemv_splits(int N, int K);
+size_t tc_gemv_part_floats(int N, int K);
+int launch_tc_gemv(const DecodeState& st, const TcGemvMaps& maps, const TcGemvArgs& a,
+                   cudaStream_t stream);
 int launch_decode_ln(const DecodeState& st, const float* x, const uint16_t* g,
-                     const uint16_t* b, float* y, cudaStream_t stream);
+                     const uint16_t* b, cudaStream_t stream);
 int launch_embed(const DecodeState& st, const uint16_t* embed, const uint16_t* pos_emb,
                  cudaStream_t stream);
 int launch_self_attn(const DecodeState& st, int layer, cudaStream_t stream);
 int launch_cross_attn(const DecodeState& st, int layer, int counter_base, cudaStream_t stream);
-int launch_lm_head(const DecodeState& st, const uint16_t* embed, cudaStream_t stream);
 int launch_finalize(const DecodeState& st, cudaStream_t stream);
 
 }  // namespace dm

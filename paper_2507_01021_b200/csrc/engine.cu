@@ -185,6 +185,7 @@ struct WhisperEngine {
   cudaGraphExec_t step_exec = nullptr;
   cudaGraph_t step_graph = nullptr;
   int gemv_counter_base = 0, xattn_counter_base = 0;
+  std::vector<TcGemvMaps> maps;   // [Ld * 6 + 1]: per layer qkv,o,xq,xo,fc1,fc2; LM head
   // telemetry: kernels launched (graph nodes counted per replay)
   long long launches = 0, steps = 0, encodes = 0, segments = 0;
   int step_kernels() const { return 1 + 11 * Ld + 3; }
@@ -286,26 +287,47 @@ static int engine_init(WhisperEngine* e) {
   uint16_t* xkv = nullptr;
   if (e->alloc_t(&xkv, size_t(e->Ld) * S * 2 * e->H * 1500 * 64)) return 2;
   st.xkv = xkv;
-  if (e->alloc_t(&st.x, size_t(S) * d)) return 2;
-  if (e->alloc_t(&st.xn, size_t(S) * d)) return 2;
-  if (e->alloc_t(&st.q, size_t(S) * d)) return 2;
-  if (e->alloc_t(&st.attn, size_t(S) * d)) return 2;
-  if (e->alloc_t(&st.h1, size_t(S) * e->F)) return 2;
+  if (e->alloc_t(&st.x, size_t(kRows) * d)) return 2;
+  if (e->alloc_t(&st.xh, size_t(kRows) * d)) return 2;
+  if (e->alloc_t(&st.xl, size_t(kRows) * d)) return 2;
+  if (e->alloc_t(&st.q, size_t(kRows) * d)) return 2;
+  if (e->alloc_t(&st.ah, size_t(kRows) * d)) return 2;
+  if (e->alloc_t(&st.al, size_t(kRows) * d)) return 2;
+  if (e->alloc_t(&st.hh, size_t(kRows) * e->F)) return 2;
+  if (e->alloc_t(&st.hl, size_t(kRows) * e->F)) return 2;
   // cross-attention key splits: enough CTAs to cover the chip at full batch
   st.xsplits = 1;
   while (S * e->H * st.xsplits < 2 * kNumSMs && st.xsplits < 8) st.xsplits *= 2;
-  // split-K partial scratch: max over GEMV shapes and cross-attn partials
-  size_t part = 0;
-  const int shapes[5][2] = {{3 * d, d}, {d, d}, {e->F, d}, {d, e->F}, {d, d}};
-  for (auto& sh : shapes) part = std::max(part, size_t(gemv_splits(sh[0], sh[1])) * 64 * sh[0]);
-  part = std::max(part, size_t(S) * e->H * st.xsplits * 66);
+  // split-K partial scratch: max over projection shapes and cross-attn partials
+  size_t part = size_t(kRows) * e->H * st.xsplits * 66;
+  const int shapes[4][2] = {{3 * d, d}, {d, d}, {e->F, d}, {d, e->F}};
+  for (auto& sh : shapes) part = std::max(part, tc_gemv_part_floats(sh[0], sh[1]));
   if (e->alloc_t(&st.part, part)) return 2;
   e->gemv_counter_base = 0;
   e->xattn_counter_base = 4096;
-  if (e->alloc_t(&st.counters, 4096 + size_t(S) * e->H)) return 2;
-  const int tiles = ceil_div(c.vocab, 64);
-  if (e->alloc_t(&st.amax_val, size_t(tiles) * S)) return 2;
-  if (e->alloc_t(&st.amax_idx, size_t(tiles) * S)) return 2;
+  if (e->alloc_t(&st.counters, 4096 + size_t(kRows) * e->H)) return 2;
+  const int tiles = ceil_div(c.vocab, 128);
+  if (e->alloc_t(&st.amax_val, size_t(tiles) * kRows)) return 2;
+  if (e->alloc_t(&st.amax_idx, size_t(tiles) * kRows)) return 2;
+  // TMA maps of every decoder projection (weights [N, K] + hi/lo inputs)
+  auto mk = [&](TcGemvMaps& m, int wi, int N, int K, const uint16_t* xh, const uint16_t* xl) {
+    if (make_tmap_2d(&m.w, e->W(wi), K, N, uint64_t(K) * 2, 64, 128)) return 2;
+    if (make_tmap_2d(&m.xh, xh, K, kRows, uint64_t(K) * 2, 64, kRows)) return 2;
+    if (make_tmap_2d(&m.xl, xl, K, kRows, uint64_t(K) * 2, 64, kRows)) return 2;
+    return 0;
+  };
+  e->maps.resize(size_t(e->Ld) * 6 + 1);
+  for (int l = 0; l < e->Ld; ++l) {
+    const int b0 = e->dec_layer_base(l);
+    TcGemvMaps* m = &e->maps[size_t(l) * 6];
+    if (mk(m[0], b0 + 2, 3 * d, d, st.xh, st.xl)) return 2;        // qkv
+    if (mk(m[1], b0 + 4, d, d, st.ah, st.al)) return 2;            // o
+    if (mk(m[2], b0 + 8, d, d, st.xh, st.xl)) return 2;            // xq
+    if (mk(m[3], b0 + 10, d, d, st.ah, st.al)) return 2;           // xo
+    if (mk(m[4], b0 + 14, e->F, d, st.xh, st.xl)) return 2;        // fc1
+    if (mk(m[5], b0 + 16, d, e->F, st.hh, st.hl)) return 2;        // fc2
+  }
+  if (mk(e->maps.back(), e->after_enc() + 2, c.vocab, d, st.xh, st.xl)) return 2;   // LM head
   st.logits_dbg = nullptr;
   DM_CHECK_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
   DM_CHECK_CUDA(cudaDeviceSynchronize());
@@ -399,28 +421,35 @@ static int record_step(WhisperEngine* e, cudaStream_t s) {
   if (int rc = launch_embed(st, embed, pos_emb, s)) return rc;
   for (int l = 0; l < e->Ld; ++l) {
     const int b0 = e->dec_layer_base(l);
-    auto gv = [&](const float* X, int wi, float* Y, int N, int K, int epi, float scale) {
-      GemvArgs g;
-      g.X = X; g.W = e->W(wi); g.bias = e->W(wi + 1); g.Y = Y; g.N = N; g.K = K; g.epi = epi;
-      g.scale = scale; g.layer = l; g.splits = gemv_splits(N, K);
-      g.counter_base = e->gemv_counter_base;
-      return launch_gemv(st, g, s);
+    const TcGemvMaps* m = &e->maps[size_t(l) * 6];
+    auto gv = [&](const TcGemvMaps& mp, int wi, int N, int K, int epi, float scale, float* y,
+                  uint16_t* yh, uint16_t* yl) {
+      TcGemvArgs g{};
+      g.bias = e->W(wi + 1); g.N = N; g.K = K; g.epi = epi; g.scale = scale; g.layer = l;
+      g.splits = tc_gemv_splits(N, K); g.counter_base = e->gemv_counter_base;
+      g.y = y; g.yh = yh; g.yl = yl;
+      return launch_tc_gemv(st, mp, g, s);
     };
-    if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 0), e->W(b0 + 1), st.xn, s)) return rc;
-    if (int rc = gv(st.xn, b0 + 2, nullptr, 3 * d, d, GV_QKV, 0.125f)) return rc;
+    if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 0), e->W(b0 + 1), s)) return rc;
+    if (int rc = gv(m[0], b0 + 2, 3 * d, d, TV_QKV, 0.125f, nullptr, nullptr, nullptr)) return rc;
     if (int rc = launch_self_attn(st, l, s)) return rc;
-    if (int rc = gv(st.attn, b0 + 4, st.x, d, d, GV_RESID, 1.f)) return rc;
-    if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 6), e->W(b0 + 7), st.xn, s)) return rc;
-    if (int rc = gv(st.xn, b0 + 8, st.q, d, d, GV_SCALE, 0.125f)) return rc;
+    if (int rc = gv(m[1], b0 + 4, d, d, TV_RESID, 1.f, st.x, nullptr, nullptr)) return rc;
+    if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 6), e->W(b0 + 7), s)) return rc;
+    if (int rc = gv(m[2], b0 + 8, d, d, TV_STORE, 0.125f, st.q, nullptr, nullptr)) return rc;
     if (int rc = launch_cross_attn(st, l, e->xattn_counter_base, s)) return rc;
-    if (int rc = gv(st.attn, b0 + 10, st.x, d, d, GV_RESID, 1.f)) return rc;
-    if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 12), e->W(b0 + 13), st.xn, s)) return rc;
-    if (int rc = gv(st.xn, b0 + 14, st.h1, e->F, d, GV_GELU, 1.f)) return rc;
-    if (int rc = gv(st.h1, b0 + 16, st.x, d, e->F, GV_RESID, 1.f)) return rc;
+    if (int rc = gv(m[3], b0 + 10, d, d, TV_RESID, 1.f, st.x, nullptr, nullptr)) return rc;
+    if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 12), e->W(b0 + 13), s)) return rc;
+    if (int rc = gv(m[4], b0 + 14, e->F, d, TV_GELU_HILO, 1.f, nullptr, st.hh, st.hl)) return rc;
+    if (int rc = gv(m[5], b0 + 16, d, e->F, TV_RESID, 1.f, st.x, nullptr, nullptr)) return rc;
   }
   const int x = e->after_dec();
-  if (int rc = launch_decode_ln(st, st.x, e->W(x + 2), e->W(x + 3), st.xn, s)) return rc;
-  if (int rc = launch_lm_head(st, embed, s)) return rc;
+  if (int rc = launch_decode_ln(st, st.x, e->W(x + 2), e->W(x + 3), s)) return rc;
+  {
+    TcGemvArgs g{};
+    g.bias = nullptr; g.N = e->cfg.vocab; g.K = d; g.epi = TV_ARGMAX; g.scale = 1.f;
+    g.splits = 1; g.counter_base = e->gemv_counter_base;
+    if (int rc = launch_tc_gemv(st, e->maps.back(), g, s)) return rc;
+  }
   if (int rc = launch_finalize(st, s)) return rc;
   return 0;
 }
@@ -666,7 +695,12 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
     switch (which) {
       case 0: rc = launch_cross_attn(e->st, layer, e->xattn_counter_base, s); break;
       case 1: rc = launch_self_attn(e->st, layer, s); break;
-      case 2: rc = launch_lm_head(e->st, e->W(e->after_enc() + 2), s); break;
+      case 2: {
+        TcGemvArgs g{};
+        g.N = e->cfg.vocab; g.K = e->d; g.epi = TV_ARGMAX; g.scale = 1.f; g.splits = 1;
+        rc = launch_tc_gemv(e->st, e->maps.back(), g, s);
+        break;
+      }
       default: DM_REQUIRE(false, "unknown kernel id");
     }
     if (rc) return rc;
@@ -707,11 +741,11 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
     case 1: src = e->mel; avail = size_t(e->last_n) * e->nm * 3000 * 4; break;
     case 2:
       DM_REQUIRE(e->st.logits_dbg != nullptr, "logits tap not enabled");
-      src = e->st.logits_dbg; avail = size_t(e->cfg.max_slots) * e->cfg.vocab * 4;
+      src = e->st.logits_dbg; avail = size_t(kRows) * e->cfg.vocab * 4;
       break;
     case 3: {
       if (!e->st.logits_dbg) {
-        if (e->alloc_t(&e->st.logits_dbg, size_t(e->cfg.max_slots) * e->cfg.vocab)) return 2;
+        if (e->alloc_t(&e->st.logits_dbg, size_t(kRows) * e->cfg.vocab)) return 2;
         if (int rc = build_step_graph(e)) return rc;   // re-capture with the tap
       }
       return 0;

@@ -375,6 +375,15 @@ static int launch_bn(const GemmArgs& g, cudaStream_t stream) {
   return 0;
 }
 
+int make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
+                 uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+  DM_REQUIRE(tma_available(), "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t str[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  return make_map(m, ptr, 2, dims, str, box);
+}
+
 int make_attn_maps(const uint16_t* q, const uint16_t* k, const uint16_t* vt, int bh, int t_pad,
                    CUtensorMap* mq, CUtensorMap* mk, CUtensorMap* mv) {
   DM_REQUIRE(tma_available(), "cuTensorMapEncodeTiled entry point unavailable");
