@@ -15,7 +15,7 @@ namespace dm {
 
 // ============================================================ tcgen05 GEMV
 constexpr int kTvThreads = 192;     // w0 TMA, w1 MMA, w2..5 epilogue
-constexpr int kTvStages = 4;
+constexpr int kTvStages = 3;
 constexpr int kTvWBytes = 128 * 64 * 2;   // W tile: 128 rows x 64 k
 constexpr int kTvXBytes = kRows * 64 * 2; // X tile: 64 rows x 64 k (hi or lo)
 constexpr int kTvStageBytes = kTvWBytes + 2 * kTvXBytes;
@@ -26,7 +26,7 @@ __device__ __forceinline__ void split_hilo(float v, uint16_t& hi, uint16_t& lo) 
   lo = f32_to_bf16(v - bf16_to_f32(hi));
 }
 
-__global__ void __launch_bounds__(kTvThreads, 1)
+__global__ void __launch_bounds__(kTvThreads, 2)
 tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap txh,
                const __grid_constant__ CUtensorMap txl, const DecodeState st,
                const TcGemvArgs a) {
@@ -159,11 +159,31 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             }
           break;
         case TV_RESID:
-          if (nvalid)
+          if (nvalid) {
+            float* __restrict__ y = a.y + n;
+            float old[kRows];
 #pragma unroll
-            for (int r = 0; r < kRows; ++r) a.y[size_t(r) * a.N + n] += v[r] + b;
+            for (int r = 0; r < kRows; ++r) old[r] = y[size_t(r) * a.N];
+#pragma unroll
+            for (int r = 0; r < kRows; ++r) y[size_t(r) * a.N] = old[r] + (v[r] + b);
+          }
           break;
         case TV_QKV: {
+          // per-row self-KV write base for this layer, computed once per CTA
+          long long* kvbase = reinterpret_cast<long long*>(red_v);
+          if (threadIdx.x >= 64 && threadIdx.x < 64 + kRows) {
+            const int r = threadIdx.x - 64;
+            long long off = -1;
+            if (r < R) {
+              const int slot = st.active[r];
+              const int p = st.pos[slot];
+              const int page = st.page_table[slot * st.pages_per_slot + p / st.page_tokens];
+              off = ((long long)(page * st.layers + a.layer) * 2 * st.heads * st.page_tokens +
+                     (p % st.page_tokens)) * 64;
+            }
+            kvbase[r] = off;
+          }
+          named_bar_sync(1, 128);
           if (!nvalid) break;
           const int d = st.d;
           if (n < d) {
@@ -173,49 +193,44 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             const int kv = n < 2 * d ? 0 : 1;
             const int c = n - (kv + 1) * d;
             const int h = c / 64, j = c % 64;
+            const long long col = (long long)(kv * st.heads + h) * st.page_tokens * 64 + j;
+            uint16_t* __restrict__ pool = st.kv_pool;
 #pragma unroll
             for (int r = 0; r < kRows; ++r) {
-              if (r >= R) break;
-              const int slot = st.active[r];
-              const int p = st.pos[slot];
-              const int page = st.page_table[slot * st.pages_per_slot + p / st.page_tokens];
-              const size_t idx = ((((size_t(page) * st.layers + a.layer) * 2 + kv) * st.heads + h) *
-                                      st.page_tokens + (p % st.page_tokens)) * 64 + j;
-              st.kv_pool[idx] = f32_to_bf16(v[r] + b);
+              const long long base = kvbase[r];
+              if (base >= 0) pool[base + col] = f32_to_bf16(v[r] + b);
             }
           }
           break;
         }
         case TV_ARGMAX: {
-          // per row: max over this tile's 128 vocabulary ids, ties -> lowest id
+          // per row: max over this tile's 128 vocabulary ids, ties -> lowest id.
+          // Transpose through smem (the operand ring is idle once MMAs are done).
+          float* tr = reinterpret_cast<float*>(smem);          // [kRows][129]
 #pragma unroll
           for (int r = 0; r < kRows; ++r) {
-            float best = nvalid ? v[r] : -INFINITY;
-            int bidx = nvalid ? n : 0x7FFFFFFF;
-            if (st.logits_dbg && nvalid && r < R) st.logits_dbg[size_t(r) * st.vocab + n] = v[r];
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-              const float ob = __shfl_xor_sync(0xffffffffu, best, off);
-              const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
-              if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
-            }
-            if (lane == 0) {
-              red_v[quad * kRows + r] = best;
-              red_i[quad * kRows + r] = bidx;
-            }
+            const float val = nvalid ? v[r] : -INFINITY;
+            tr[r * 129 + f] = val;
+            if (st.logits_dbg && nvalid && r < R) st.logits_dbg[size_t(r) * st.vocab + n] = val;
           }
           named_bar_sync(1, 128);
-          if (threadIdx.x >= 64 && threadIdx.x < 64 + kRows) {
-            const int r = threadIdx.x - 64;
-            float best = red_v[r];
-            int bidx = red_i[r];
-            for (int qd = 1; qd < 4; ++qd) {
-              const float ob = red_v[qd * kRows + r];
-              const int oi = red_i[qd * kRows + r];
-              if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+          {
+            const int t = threadIdx.x - 64;              // 0..127: row t/2, half t%2
+            const int r = t >> 1, half = t & 1;
+            float best = -INFINITY;
+            int bidx = 0x7FFFFFFF;
+            const float* row = tr + r * 129 + half * 64;
+            for (int i = 0; i < 64; ++i) {
+              const float x = row[i];
+              if (x > best) { best = x; bidx = tile * 128 + half * 64 + i; }
             }
-            st.amax_val[size_t(tile) * kRows + r] = best;
-            st.amax_idx[size_t(tile) * kRows + r] = bidx;
+            const float ob = __shfl_xor_sync(0xffffffffu, best, 1);
+            const int oi = __shfl_xor_sync(0xffffffffu, bidx, 1);
+            if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+            if (half == 0) {
+              st.amax_val[size_t(tile) * kRows + r] = best;
+              st.amax_idx[size_t(tile) * kRows + r] = bidx;
+            }
           }
           break;
         }
@@ -351,38 +366,6 @@ int launch_embed(const DecodeState& st, const uint16_t* embed, const uint16_t* p
 // Lane-per-key online softmax: every lane owns whole keys (64-dim dot product
 // and V accumulation in registers, no per-key shuffles); lanes, warps and
 // key splits are merged at the end in a fixed order.
-__device__ __forceinline__ float dot_bf16_row(const uint16_t* __restrict__ krow,
-                                              const float (&q)[64]) {
-  const uint4* k4 = reinterpret_cast<const uint4*>(krow);
-  float acc = 0.f;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    uint4 w = __ldg(k4 + c);
-    uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      acc = fmaf(q[8 * c + 2 * u], __uint_as_float(ws[u] << 16), acc);
-      acc = fmaf(q[8 * c + 2 * u + 1], __uint_as_float(ws[u] & 0xFFFF0000u), acc);
-    }
-  }
-  return acc;
-}
-
-__device__ __forceinline__ void axpy_bf16_row(const uint16_t* __restrict__ vrow, float p,
-                                              float (&o)[64]) {
-  const uint4* v4 = reinterpret_cast<const uint4*>(vrow);
-#pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    uint4 w = __ldg(v4 + c);
-    uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      o[8 * c + 2 * u] = fmaf(p, __uint_as_float(ws[u] << 16), o[8 * c + 2 * u]);
-      o[8 * c + 2 * u + 1] = fmaf(p, __uint_as_float(ws[u] & 0xFFFF0000u), o[8 * c + 2 * u + 1]);
-    }
-  }
-}
-
 constexpr float kLog2e = 1.4426950408889634f;
 
 // Merge (m, l, o[64]) across the 32 lanes of a warp, fixed butterfly order.
@@ -403,31 +386,16 @@ __device__ __forceinline__ void warp_merge(float& m, float& l, float (&o)[64]) {
   m = mw;
 }
 
-template <class KRowFn, class VRowFn>
-__device__ __forceinline__ void attend_keys(const float (&q)[64], int k0, int k1, int stride,
-                                            int first, KRowFn krow, VRowFn vrow, float& m,
-                                            float& l, float (&o)[64]) {
-  m = -INFINITY;
-  l = 0.f;
-#pragma unroll
-  for (int i = 0; i < 64; ++i) o[i] = 0.f;
-  for (int t = k0 + first; t < k1; t += stride) {
-    const float s = dot_bf16_row(krow(t), q);
-    const float mn = fmaxf(m, s);
-    const float corr = exp2f((m - mn) * kLog2e);
-    const float p = exp2f((s - mn) * kLog2e);
-    l = l * corr + p;
-#pragma unroll
-    for (int i = 0; i < 64; ++i) o[i] *= corr;
-    axpy_bf16_row(vrow(t), p, o);
-    m = mn;
-  }
-}
+constexpr int kDaWarps = 4;                    // compute warps (lane = key)
+constexpr int kDaThreads = (kDaWarps + 1) * 32; // + 1 TMA producer warp
+constexpr int kDaKeys = 128;                    // keys per stage (2 boxes of 64)
+constexpr int kDaStages = 2;
+constexpr int kDaBox = 64 * 128;                // 64 keys x 128 B
+constexpr int kDaStageBytes = 4 * kDaBox;       // K0 K1 V0 V1
+constexpr int kDaSmem = kDaStages * kDaStageBytes + 1024 + 2048;
 
-constexpr int kAttnWarps = 4;
-
-// Cross-warp merge through smem. Warp 0 lanes then hold dims (2 lane, 2 lane+1)
-// of the merged (m, l, o); returns them via out refs.
+// Cross-warp merge of (m, l, o[64]) through smem; afterwards every lane of
+// the calling warps holds dims (2 lane, 2 lane + 1) of the merged state.
 __device__ void block_merge(float m, float l, const float (&o)[64], float* smem_o,
                             float* smem_ml, float& mm, float& ll, float& o0, float& o1) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -437,11 +405,11 @@ __device__ void block_merge(float m, float l, const float (&o)[64], float* smem_
 #pragma unroll
     for (int i = 0; i < 64; ++i) smem_o[warp * 64 + i] = o[i];
   }
-  __syncthreads();
+  named_bar_sync(1, kDaWarps * 32);
   mm = -INFINITY;
-  for (int w = 0; w < kAttnWarps; ++w) mm = fmaxf(mm, smem_ml[2 * w]);
+  for (int w = 0; w < kDaWarps; ++w) mm = fmaxf(mm, smem_ml[2 * w]);
   ll = 0.f; o0 = 0.f; o1 = 0.f;
-  for (int w = 0; w < kAttnWarps; ++w) {
+  for (int w = 0; w < kDaWarps; ++w) {
     const float mw = smem_ml[2 * w];
     const float f = (mw == -INFINITY) ? 0.f : exp2f((mw - mm) * kLog2e);
     ll += smem_ml[2 * w + 1] * f;
@@ -460,79 +428,154 @@ __device__ __forceinline__ void store_hilo2(const DecodeState& st, int r, int h,
   *reinterpret_cast<uint32_t*>(st.al + idx) = uint32_t(l0) | (uint32_t(l1) << 16);
 }
 
-__global__ void __launch_bounds__(kAttnWarps * 32)
-self_attn_kernel(const DecodeState st, int layer) {
-  __shared__ float s_o[kAttnWarps * 64];
-  __shared__ float s_ml[2 * kAttnWarps];
-  const int r = blockIdx.x, h = blockIdx.y;
-  if (r >= *st.n_active) return;
-  const int slot = st.active[r];
-  const int nk = st.pos[slot] + 1;                 // keys 0..pos (incl. current)
-  float q[64];
-  const float* qp = st.q + size_t(r) * st.d + h * 64;
-#pragma unroll
-  for (int c = 0; c < 64; ++c) q[c] = qp[c];
-  const int* pt = st.page_table + slot * st.pages_per_slot;
-  const size_t kv_stride = size_t(st.heads) * st.page_tokens * 64;   // k -> v
-  auto krow = [&](int t) {
-    const int page = pt[t / st.page_tokens];
-    return st.kv_pool + ((((size_t(page) * st.layers + layer) * 2 + 0) * st.heads + h) *
-                             st.page_tokens + t % st.page_tokens) * 64;
-  };
-  auto vrow = [&](int t) { return krow(t) + kv_stride; };
-  float m, l, o[64];
-  attend_keys(q, 0, nk, kAttnWarps * 32, threadIdx.x, krow, vrow, m, l, o);
-  warp_merge(m, l, o);
-  float mm, ll, o0, o1;
-  block_merge(m, l, o, s_o, s_ml, mm, ll, o0, o1);
-  if (threadIdx.x < 32) store_hilo2(st, r, h, threadIdx.x, o0 / ll, o1 / ll);
-}
+// Decode attention for one (row, head[, key split]). K/V tiles stream through
+// a 2-stage smem ring by TMA (128B-swizzled, so a lane reading its own key row
+// chunk-by-chunk is bank-conflict free while q stays in registers); every
+// compute lane owns whole keys. kCross: keys = the slot's 1500 cross-KV rows
+// (split over blockIdx.z); else: keys 0..pos of the paged self-KV cache.
+template <bool kCross>
+__global__ void __launch_bounds__(kDaThreads)
+dec_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, int layer,
+                int counter_base) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kDaStages * kDaStageBytes);
+  uint64_t* empty = full + kDaStages;
+  float* s_ml = reinterpret_cast<float*>(empty + kDaStages);     // [2 * warps]
+  float* s_o = s_ml + 2 * kDaWarps;                                // [warps * 64]
+  int* is_last = reinterpret_cast<int*>(s_o + kDaWarps * 64);
 
-__global__ void __launch_bounds__(kAttnWarps * 32)
-cross_attn_kernel(const DecodeState st, int layer, int counter_base) {
-  __shared__ float s_o[kAttnWarps * 64];
-  __shared__ float s_ml[2 * kAttnWarps];
-  __shared__ int is_last;
   const int r = blockIdx.x, h = blockIdx.y, sp = blockIdx.z;
   if (r >= *st.n_active) return;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int slot = st.active[r];
-  const int xs = st.xsplits;
-  const int per = ceil_div(1500, xs);
-  const int k0 = sp * per, k1 = min(1500, k0 + per);
-  float q[64];
-  const float* qp = st.q + size_t(r) * st.d + h * 64;
+  int k0, k1;
+  if (kCross) {
+    const int per = ceil_div(ceil_div(1500, st.xsplits), kDaKeys) * kDaKeys;
+    k0 = sp * per;
+    k1 = min(1500, k0 + per);
+  } else {
+    k0 = 0;
+    k1 = st.pos[slot] + 1;
+  }
+  const int nchunks = k1 > k0 ? ceil_div(k1 - k0, kDaKeys) : 0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kDaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kDaWarps);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  if (warp == kDaWarps) {
+    // ---------------- TMA producer
+    if (elect_one()) {
+      tma_prefetch_desc(&tm);
+      const int* pt = st.page_table + slot * st.pages_per_slot;
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c % kDaStages;
+        mbar_wait(&empty[s], ((c / kDaStages) & 1) ^ 1);
+        uint8_t* base = smem + s * kDaStageBytes;
+        mbar_arrive_expect_tx(&full[s], kDaStageBytes);
 #pragma unroll
-  for (int c = 0; c < 64; ++c) q[c] = qp[c];
-  const uint16_t* kbase =
-      st.xkv + (((size_t(layer) * st.max_slots + slot) * 2 + 0) * st.heads + h) * 1500 * 64;
-  const size_t vofs = size_t(st.heads) * 1500 * 64;
-  auto krow = [&](int t) { return kbase + size_t(t) * 64; };
-  auto vrow = [&](int t) { return kbase + vofs + size_t(t) * 64; };
-  float m, l, o[64];
-  attend_keys(q, k0, k1, kAttnWarps * 32, threadIdx.x, krow, vrow, m, l, o);
+        for (int half = 0; half < 2; ++half) {
+          const int t = k0 + c * kDaKeys + half * 64;
+          int row_k, row_v;
+          if (kCross) {
+            row_k = (((layer * st.max_slots + slot) * 2 + 0) * st.heads + h) * 1500 + t;
+            row_v = row_k + st.heads * 1500;
+          } else {
+            const int page = pt[min(t / st.page_tokens, st.pages_per_slot - 1)];
+            row_k = (((page * st.layers + layer) * 2 + 0) * st.heads + h) * st.page_tokens;
+            row_v = row_k + st.heads * st.page_tokens;
+          }
+          tma_load_2d(base + half * kDaBox, &tm, &full[s], 0, row_k);
+          tma_load_2d(base + (2 + half) * kDaBox, &tm, &full[s], 0, row_v);
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- compute warps: lane owns key (chunk base + 32 warp + lane)
+  float q[64];
+  {
+    const float4* qp = reinterpret_cast<const float4*>(st.q + size_t(r) * st.d + h * 64);
+#pragma unroll
+    for (int c = 0; c < 16; ++c) {
+      const float4 v = qp[c];
+      q[4 * c] = v.x; q[4 * c + 1] = v.y; q[4 * c + 2] = v.z; q[4 * c + 3] = v.w;
+    }
+  }
+  float m = -INFINITY, l = 0.f, o[64];
+#pragma unroll
+  for (int i = 0; i < 64; ++i) o[i] = 0.f;
+  const int half = warp >> 1;
+  const int rr = (warp & 1) * 32 + lane;              // row within the 64-key box
+  const int sw = rr & 7;                              // 128B swizzle phase
+  for (int c = 0; c < nchunks; ++c) {
+    const int s = c % kDaStages;
+    mbar_wait(&full[s], (c / kDaStages) & 1);
+    const int t = k0 + c * kDaKeys + warp * 32 + lane;
+    if (t < k1) {
+      const uint8_t* krow = smem + s * kDaStageBytes + half * kDaBox + rr * 128;
+      const uint8_t* vrow = krow + 2 * kDaBox;
+      float sc = 0.f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint4 w = *reinterpret_cast<const uint4*>(krow + ((j ^ sw) << 4));
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          sc = fmaf(q[8 * j + 2 * u], __uint_as_float(ws[u] << 16), sc);
+          sc = fmaf(q[8 * j + 2 * u + 1], __uint_as_float(ws[u] & 0xFFFF0000u), sc);
+        }
+      }
+      const float mn = fmaxf(m, sc);
+      const float corr = exp2f((m - mn) * kLog2e);
+      const float p = exp2f((sc - mn) * kLog2e);
+      l = l * corr + p;
+      m = mn;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint4 w = *reinterpret_cast<const uint4*>(vrow + ((j ^ sw) << 4));
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          o[8 * j + 2 * u] = fmaf(o[8 * j + 2 * u], corr, p * __uint_as_float(ws[u] << 16));
+          o[8 * j + 2 * u + 1] =
+              fmaf(o[8 * j + 2 * u + 1], corr, p * __uint_as_float(ws[u] & 0xFFFF0000u));
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
   warp_merge(m, l, o);
   float mm, ll, o0, o1;
   block_merge(m, l, o, s_o, s_ml, mm, ll, o0, o1);
-  if (xs == 1) {
-    if (threadIdx.x < 32) store_hilo2(st, r, h, threadIdx.x, o0 / ll, o1 / ll);
+  if (!kCross || st.xsplits == 1) {
+    if (warp == 0) store_hilo2(st, r, h, lane, o0 / ll, o1 / ll);
     return;
   }
-  // partial -> scratch [row][h][split][66]
-  const int lane = threadIdx.x;
+  // split partial -> scratch [row][h][split][66]; last split CTA merges in order
+  const int xs = st.xsplits;
   float* part = st.part + ((size_t(r) * st.heads + h) * xs + sp) * 66;
-  if (lane < 32) {
+  if (warp == 0) {
     part[2 + 2 * lane] = o0;
     part[3 + 2 * lane] = o1;
     if (lane == 0) { part[0] = mm; part[1] = ll; }
+    __threadfence();
   }
-  __threadfence();
-  __syncthreads();
+  named_bar_sync(1, kDaWarps * 32);
   if (threadIdx.x == 0) {
     const int prev = atomicAdd(&st.counters[counter_base + r * st.heads + h], 1);
-    is_last = prev == xs - 1;
+    *is_last = prev == xs - 1;
   }
-  __syncthreads();
-  if (!is_last || threadIdx.x >= 32) return;
+  named_bar_sync(1, kDaWarps * 32);
+  if (!*is_last || warp != 0) return;
   __threadfence();
   const float* pb = st.part + (size_t(r) * st.heads + h) * xs * 66;
   float gm = -INFINITY;
@@ -549,16 +592,30 @@ cross_attn_kernel(const DecodeState st, int layer, int counter_base) {
   if (lane == 0) st.counters[counter_base + r * st.heads + h] = 0;
 }
 
-int launch_self_attn(const DecodeState& st, int layer, cudaStream_t stream) {
-  dim3 grid(kRows, st.heads);
-  self_attn_kernel<<<grid, kAttnWarps * 32, 0, stream>>>(st, layer);
+int launch_self_attn(const DecodeState& st, const CUtensorMap& kv_map, int layer,
+                     cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    DM_CHECK_CUDA(cudaFuncSetAttribute(dec_attn_kernel<false>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kDaSmem));
+    attr = true;
+  }
+  dim3 grid(kRows, st.heads, 1);
+  dec_attn_kernel<false><<<grid, kDaThreads, kDaSmem, stream>>>(kv_map, st, layer, 0);
   DM_CHECK_LAUNCH();
   return 0;
 }
 
-int launch_cross_attn(const DecodeState& st, int layer, int counter_base, cudaStream_t stream) {
+int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
+                      int counter_base, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    DM_CHECK_CUDA(cudaFuncSetAttribute(dec_attn_kernel<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kDaSmem));
+    attr = true;
+  }
   dim3 grid(kRows, st.heads, st.xsplits);
-  cross_attn_kernel<<<grid, kAttnWarps * 32, 0, stream>>>(st, layer, counter_base);
+  dec_attn_kernel<true><<<grid, kDaThreads, kDaSmem, stream>>>(xkv_map, st, layer, counter_base);
   DM_CHECK_LAUNCH();
   return 0;
 }

@@ -84,8 +84,10 @@ int launch_decode_ln(const DecodeState& st, const float* x, const uint16_t* g,
                      const uint16_t* b, cudaStream_t stream);
 int launch_embed(const DecodeState& st, const uint16_t* embed, const uint16_t* pos_emb,
                  cudaStream_t stream);
-int launch_self_attn(const DecodeState& st, int layer, cudaStream_t stream);
-int launch_cross_attn(const DecodeState& st, int layer, int counter_base, cudaStream_t stream);
+int launch_self_attn(const DecodeState& st, const CUtensorMap& kv_map, int layer,
+                     cudaStream_t stream);
+int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
+                      int counter_base, cudaStream_t stream);
 int launch_finalize(const DecodeState& st, cudaStream_t stream);
 
 }  // namespace dm

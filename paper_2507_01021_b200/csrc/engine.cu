@@ -186,6 +186,7 @@ struct WhisperEngine {
   cudaGraph_t step_graph = nullptr;
   int gemv_counter_base = 0, xattn_counter_base = 0;
   std::vector<TcGemvMaps> maps;   // [Ld * 6 + 1]: per layer qkv,o,xq,xo,fc1,fc2; LM head
+  CUtensorMap kv_map, xkv_map;    // self-KV pool / cross-KV cache as [rows, 64] bf16
   // telemetry: kernels launched (graph nodes counted per replay)
   long long launches = 0, steps = 0, encodes = 0, segments = 0;
   int step_kernels() const { return 1 + 11 * Ld + 3; }
@@ -297,7 +298,7 @@ static int engine_init(WhisperEngine* e) {
   if (e->alloc_t(&st.hl, size_t(kRows) * e->F)) return 2;
   // cross-attention key splits: enough CTAs to cover the chip at full batch
   st.xsplits = 1;
-  while (S * e->H * st.xsplits < 2 * kNumSMs && st.xsplits < 8) st.xsplits *= 2;
+  while (S * e->H * st.xsplits < 4 * kNumSMs && st.xsplits < 8) st.xsplits *= 2;
   // split-K partial scratch: max over projection shapes and cross-attn partials
   size_t part = size_t(kRows) * e->H * st.xsplits * 66;
   const int shapes[4][2] = {{3 * d, d}, {d, d}, {e->F, d}, {d, e->F}};
@@ -328,6 +329,11 @@ static int engine_init(WhisperEngine* e) {
     if (mk(m[5], b0 + 16, d, e->F, st.hh, st.hl)) return 2;        // fc2
   }
   if (mk(e->maps.back(), e->after_enc() + 2, c.vocab, d, st.xh, st.xl)) return 2;   // LM head
+  if (make_tmap_2d(&e->kv_map, st.kv_pool, 64, uint64_t(c.num_pages) * e->Ld * 2 * e->H * 64, 128,
+                   64, 64))
+    return 2;
+  if (make_tmap_2d(&e->xkv_map, st.xkv, 64, uint64_t(e->Ld) * S * 2 * e->H * 1500, 128, 64, 64))
+    return 2;
   st.logits_dbg = nullptr;
   DM_CHECK_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
   DM_CHECK_CUDA(cudaDeviceSynchronize());
@@ -432,11 +438,11 @@ static int record_step(WhisperEngine* e, cudaStream_t s) {
     };
     if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 0), e->W(b0 + 1), s)) return rc;
     if (int rc = gv(m[0], b0 + 2, 3 * d, d, TV_QKV, 0.125f, nullptr, nullptr, nullptr)) return rc;
-    if (int rc = launch_self_attn(st, l, s)) return rc;
+    if (int rc = launch_self_attn(st, e->kv_map, l, s)) return rc;
     if (int rc = gv(m[1], b0 + 4, d, d, TV_RESID, 1.f, st.x, nullptr, nullptr)) return rc;
     if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 6), e->W(b0 + 7), s)) return rc;
     if (int rc = gv(m[2], b0 + 8, d, d, TV_STORE, 0.125f, st.q, nullptr, nullptr)) return rc;
-    if (int rc = launch_cross_attn(st, l, e->xattn_counter_base, s)) return rc;
+    if (int rc = launch_cross_attn(st, e->xkv_map, l, e->xattn_counter_base, s)) return rc;
     if (int rc = gv(m[3], b0 + 10, d, d, TV_RESID, 1.f, st.x, nullptr, nullptr)) return rc;
     if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 12), e->W(b0 + 13), s)) return rc;
     if (int rc = gv(m[4], b0 + 14, e->F, d, TV_GELU_HILO, 1.f, nullptr, st.hh, st.hl)) return rc;
@@ -693,8 +699,8 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
   for (int i = 0; i < iters; ++i) {
     int rc = 0;
     switch (which) {
-      case 0: rc = launch_cross_attn(e->st, layer, e->xattn_counter_base, s); break;
-      case 1: rc = launch_self_attn(e->st, layer, s); break;
+      case 0: rc = launch_cross_attn(e->st, e->xkv_map, layer, e->xattn_counter_base, s); break;
+      case 1: rc = launch_self_attn(e->st, e->kv_map, layer, s); break;
       case 2: {
         TcGemvArgs g{};
         g.N = e->cfg.vocab; g.K = e->d; g.epi = TV_ARGMAX; g.scale = 1.f; g.splits = 1;
