@@ -26,6 +26,78 @@ __device__ __forceinline__ void split_hilo(float v, uint16_t& hi, uint16_t& lo) 
   lo = f32_to_bf16(v - bf16_to_f32(hi));
 }
 
+// Epilogue on 32 rows [r0, r0+32) of one feature column n (values v[0..32)).
+template <int EPI>
+__device__ __forceinline__ void tv_epilogue32(const DecodeState& st, const TcGemvArgs& a, int n,
+                                              bool nvalid, float b, int r0, const float (&v)[32],
+                                              const long long* kvbase, float* tr, int f) {
+  switch (EPI) {
+    case TV_STORE:
+      if (nvalid) {
+        float* __restrict__ y = a.y + n;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) y[size_t(r0 + i) * a.N] = (v[i] + b) * a.scale;
+      }
+      break;
+    case TV_GELU_HILO:
+      if (nvalid) {
+        uint16_t* __restrict__ yh = a.yh + n;
+        uint16_t* __restrict__ yl = a.yl + n;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          uint16_t hi, lo;
+          split_hilo(gelu_erf(v[i] + b), hi, lo);
+          yh[size_t(r0 + i) * a.N] = hi;
+          yl[size_t(r0 + i) * a.N] = lo;
+        }
+      }
+      break;
+    case TV_RESID:
+      if (nvalid) {
+        float* __restrict__ y = a.y + n;
+        float old[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) old[i] = y[size_t(r0 + i) * a.N];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) y[size_t(r0 + i) * a.N] = old[i] + (v[i] + b);
+      }
+      break;
+    case TV_QKV: {
+      if (!nvalid) break;
+      const int d = st.d;
+      if (n < d) {
+        float* __restrict__ q = st.q + n;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) q[size_t(r0 + i) * d] = (v[i] + b) * a.scale;
+      } else {
+        const int kv = n < 2 * d ? 0 : 1;
+        const int c = n - (kv + 1) * d;
+        const int h = c / 64, j = c % 64;
+        const long long col = (long long)(kv * st.heads + h) * st.page_tokens * 64 + j;
+        uint16_t* __restrict__ pool = st.kv_pool;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const long long base = kvbase[r0 + i];
+          if (base >= 0) pool[base + col] = f32_to_bf16(v[i] + b);
+        }
+      }
+      break;
+    }
+    case TV_ARGMAX: {
+      const int R = *st.n_active;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float val = nvalid ? v[i] : -INFINITY;
+        tr[(r0 + i) * 129 + f] = val;
+        if (st.logits_dbg && nvalid && r0 + i < R)
+          st.logits_dbg[size_t(r0 + i) * st.vocab + n] = val;
+      }
+      break;
+    }
+  }
+}
+
+template <int EPI, bool SPLIT>
 __global__ void __launch_bounds__(kTvThreads, 2)
 tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap txh,
                const __grid_constant__ CUtensorMap txl, const DecodeState st,
@@ -38,8 +110,7 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   uint64_t* mma_done = empty + kTvStages;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + 1);
   int* is_last = reinterpret_cast<int*>(tmem_slot + 1);
-  float* red_v = reinterpret_cast<float*>(smem + kTvStages * kTvStageBytes + 128);   // [4][64]
-  int* red_i = reinterpret_cast<int*>(red_v + 4 * kRows);                            // [4][64]
+  long long* kvbase = reinterpret_cast<long long*>(smem + kTvStages * kTvStageBytes + 128);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int tile = blockIdx.x, split = blockIdx.y;
@@ -101,142 +172,92 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     const int quad = warp & 3;
     const int f = quad * 32 + lane;                // feature within the tile
     const int n = tile * 128 + f;
-    const int R = min(*st.n_active, kRows);
+    const bool nvalid = n < a.N;
+    const float b = (nvalid && a.bias) ? bf16_to_f32(a.bias[n]) : 0.f;
+    const int et = threadIdx.x - 64;               // 0..127 among epilogue threads
+    if (EPI == TV_QKV && et < kRows) {
+      // per-row self-KV write base for this layer
+      const int r = et;
+      long long off = -1;
+      if (r < *st.n_active) {
+        const int slot = st.active[r];
+        const int p = st.pos[slot];
+        const int page = st.page_table[slot * st.pages_per_slot + p / st.page_tokens];
+        off = ((long long)(page * st.layers + a.layer) * 2 * st.heads * st.page_tokens +
+               (p % st.page_tokens)) * 64;
+      }
+      kvbase[r] = off;
+    }
     mbar_wait(mma_done, 0);
     tc_fence_after();
-    float v[kRows];
-    {
-      uint32_t r[32];
-      tmem_ld32(tmem + (uint32_t(quad * 32) << 16), r);
-      tmem_wait_ld();
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-      tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + 32, r);
-      tmem_wait_ld();
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[32 + i] = __uint_as_float(r[i]);
-    }
-    if (a.splits > 1) {
+    float* tr = reinterpret_cast<float*>(smem);    // ARGMAX transpose [kRows][129]
+    if (SPLIT) {
       float* part = st.part;
       const size_t base = (size_t(split) * tiles + tile) * kRows * 128;
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        uint32_t rr[32];
+        tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + c * 32, rr);
+        tmem_wait_ld();
 #pragma unroll
-      for (int r = 0; r < kRows; ++r) part[base + size_t(r) * 128 + f] = v[r];
+        for (int i = 0; i < 32; ++i) part[base + size_t(c * 32 + i) * 128 + f] = __uint_as_float(rr[i]);
+      }
       __threadfence();
       named_bar_sync(1, 128);
-      if (threadIdx.x == 64) {
+      if (et == 0) {
         const int prev = atomicAdd(&st.counters[a.counter_base + tile], 1);
         *is_last = (prev == a.splits - 1);
       }
       named_bar_sync(1, 128);
-      if (!*is_last) goto done;
-      __threadfence();
+      if (*is_last) {
+        __threadfence();
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          float v[32];
 #pragma unroll
-      for (int r = 0; r < kRows; ++r) {
-        float acc = 0.f;
-        for (int s = 0; s < a.splits; ++s)
-          acc += __ldcg(&part[(size_t(s) * tiles + tile) * kRows * 128 + size_t(r) * 128 + f]);
-        v[r] = acc;
-      }
-      if (threadIdx.x == 64) st.counters[a.counter_base + tile] = 0;
-    }
-    {
-      const bool nvalid = n < a.N;
-      const float b = (nvalid && a.bias) ? bf16_to_f32(a.bias[n]) : 0.f;
-      switch (a.epi) {
-        case TV_STORE:
-          if (nvalid)
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+#pragma unroll 1
+          for (int s = 0; s < a.splits; ++s) {
+            const float* ps = part + (size_t(s) * tiles + tile) * kRows * 128 + size_t(c * 32) * 128 + f;
 #pragma unroll
-            for (int r = 0; r < kRows; ++r) a.y[size_t(r) * a.N + n] = (v[r] + b) * a.scale;
-          break;
-        case TV_GELU_HILO:
-          if (nvalid)
-#pragma unroll
-            for (int r = 0; r < kRows; ++r) {
-              uint16_t hi, lo;
-              split_hilo(gelu_erf(v[r] + b), hi, lo);
-              a.yh[size_t(r) * a.N + n] = hi;
-              a.yl[size_t(r) * a.N + n] = lo;
-            }
-          break;
-        case TV_RESID:
-          if (nvalid) {
-            float* __restrict__ y = a.y + n;
-            float old[kRows];
-#pragma unroll
-            for (int r = 0; r < kRows; ++r) old[r] = y[size_t(r) * a.N];
-#pragma unroll
-            for (int r = 0; r < kRows; ++r) y[size_t(r) * a.N] = old[r] + (v[r] + b);
+            for (int i = 0; i < 32; ++i) v[i] += __ldcg(ps + size_t(i) * 128);
           }
-          break;
-        case TV_QKV: {
-          // per-row self-KV write base for this layer, computed once per CTA
-          long long* kvbase = reinterpret_cast<long long*>(red_v);
-          if (threadIdx.x >= 64 && threadIdx.x < 64 + kRows) {
-            const int r = threadIdx.x - 64;
-            long long off = -1;
-            if (r < R) {
-              const int slot = st.active[r];
-              const int p = st.pos[slot];
-              const int page = st.page_table[slot * st.pages_per_slot + p / st.page_tokens];
-              off = ((long long)(page * st.layers + a.layer) * 2 * st.heads * st.page_tokens +
-                     (p % st.page_tokens)) * 64;
-            }
-            kvbase[r] = off;
-          }
-          named_bar_sync(1, 128);
-          if (!nvalid) break;
-          const int d = st.d;
-          if (n < d) {
-#pragma unroll
-            for (int r = 0; r < kRows; ++r) st.q[size_t(r) * d + n] = (v[r] + b) * a.scale;
-          } else {
-            const int kv = n < 2 * d ? 0 : 1;
-            const int c = n - (kv + 1) * d;
-            const int h = c / 64, j = c % 64;
-            const long long col = (long long)(kv * st.heads + h) * st.page_tokens * 64 + j;
-            uint16_t* __restrict__ pool = st.kv_pool;
-#pragma unroll
-            for (int r = 0; r < kRows; ++r) {
-              const long long base = kvbase[r];
-              if (base >= 0) pool[base + col] = f32_to_bf16(v[r] + b);
-            }
-          }
-          break;
+          tv_epilogue32<EPI>(st, a, n, nvalid, b, c * 32, v, kvbase, tr, f);
         }
-        case TV_ARGMAX: {
-          // per row: max over this tile's 128 vocabulary ids, ties -> lowest id.
-          // Transpose through smem (the operand ring is idle once MMAs are done).
-          float* tr = reinterpret_cast<float*>(smem);          // [kRows][129]
+        if (et == 0) st.counters[a.counter_base + tile] = 0;
+      }
+    } else {
+      if (EPI == TV_QKV) named_bar_sync(1, 128);    // kvbase ready
+#pragma unroll 1
+      for (int c = 0; c < 2; ++c) {
+        uint32_t rr[32];
+        tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + c * 32, rr);
+        tmem_wait_ld();
+        float v[32];
 #pragma unroll
-          for (int r = 0; r < kRows; ++r) {
-            const float val = nvalid ? v[r] : -INFINITY;
-            tr[r * 129 + f] = val;
-            if (st.logits_dbg && nvalid && r < R) st.logits_dbg[size_t(r) * st.vocab + n] = val;
-          }
-          named_bar_sync(1, 128);
-          {
-            const int t = threadIdx.x - 64;              // 0..127: row t/2, half t%2
-            const int r = t >> 1, half = t & 1;
-            float best = -INFINITY;
-            int bidx = 0x7FFFFFFF;
-            const float* row = tr + r * 129 + half * 64;
-            for (int i = 0; i < 64; ++i) {
-              const float x = row[i];
-              if (x > best) { best = x; bidx = tile * 128 + half * 64 + i; }
-            }
-            const float ob = __shfl_xor_sync(0xffffffffu, best, 1);
-            const int oi = __shfl_xor_sync(0xffffffffu, bidx, 1);
-            if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
-            if (half == 0) {
-              st.amax_val[size_t(tile) * kRows + r] = best;
-              st.amax_idx[size_t(tile) * kRows + r] = bidx;
-            }
-          }
-          break;
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]);
+        tv_epilogue32<EPI>(st, a, n, nvalid, b, c * 32, v, kvbase, tr, f);
+      }
+      if (EPI == TV_ARGMAX) {
+        // per row: max over this tile's 128 vocabulary ids, ties -> lowest id
+        named_bar_sync(1, 128);
+        const int r = et >> 1, half = et & 1;
+        float best = -INFINITY;
+        int bidx = 0x7FFFFFFF;
+        const float* row = tr + r * 129 + half * 64;
+        for (int i = 0; i < 64; ++i) {
+          const float x = row[i];
+          if (x > best) { best = x; bidx = tile * 128 + half * 64 + i; }
+        }
+        const float ob = __shfl_xor_sync(0xffffffffu, best, 1);
+        const int oi = __shfl_xor_sync(0xffffffffu, bidx, 1);
+        if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+        if (half == 0) {
+          st.amax_val[size_t(tile) * kRows + r] = best;
+          st.amax_idx[size_t(tile) * kRows + r] = bidx;
         }
       }
     }
-  done:;
   }
   tc_fence_before();
   __syncthreads();
@@ -261,20 +282,40 @@ size_t tc_gemv_part_floats(int N, int K) {
   return s > 1 ? size_t(s) * ceil_div(N, 128) * kRows * 128 : 0;
 }
 
+template <int EPI, bool SPLIT>
+static int launch_tv(const DecodeState& st, const TcGemvMaps& maps, const TcGemvArgs& a,
+                     cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    DM_CHECK_CUDA(cudaFuncSetAttribute(tc_gemv_kernel<EPI, SPLIT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kTvSmem));
+    attr = true;
+  }
+  dim3 grid(ceil_div(a.N, 128), a.splits);
+  tc_gemv_kernel<EPI, SPLIT><<<grid, kTvThreads, kTvSmem, stream>>>(maps.w, maps.xh, maps.xl, st, a);
+  DM_CHECK_LAUNCH();
+  return 0;
+}
+
 int launch_tc_gemv(const DecodeState& st, const TcGemvMaps& maps, const TcGemvArgs& a,
                    cudaStream_t stream) {
   DM_REQUIRE(a.K % 64 == 0, "K must be a multiple of 64");
   DM_REQUIRE((a.K / 64) % a.splits == 0, "splits must divide K/64");
-  static bool attr = false;
-  if (!attr) {
-    DM_CHECK_CUDA(cudaFuncSetAttribute(tc_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       kTvSmem));
-    attr = true;
+  const bool sp = a.splits > 1;
+  switch (a.epi) {
+    case TV_STORE: return sp ? launch_tv<TV_STORE, true>(st, maps, a, stream)
+                             : launch_tv<TV_STORE, false>(st, maps, a, stream);
+    case TV_GELU_HILO: return sp ? launch_tv<TV_GELU_HILO, true>(st, maps, a, stream)
+                                 : launch_tv<TV_GELU_HILO, false>(st, maps, a, stream);
+    case TV_RESID: return sp ? launch_tv<TV_RESID, true>(st, maps, a, stream)
+                             : launch_tv<TV_RESID, false>(st, maps, a, stream);
+    case TV_QKV: return sp ? launch_tv<TV_QKV, true>(st, maps, a, stream)
+                           : launch_tv<TV_QKV, false>(st, maps, a, stream);
+    case TV_ARGMAX:
+      DM_REQUIRE(!sp, "argmax epilogue runs without split-K");
+      return launch_tv<TV_ARGMAX, false>(st, maps, a, stream);
+    default: DM_REQUIRE(false, "unknown epilogue");
   }
-  dim3 grid(ceil_div(a.N, 128), a.splits);
-  tc_gemv_kernel<<<grid, kTvThreads, kTvSmem, stream>>>(maps.w, maps.xh, maps.xl, st, a);
-  DM_CHECK_LAUNCH();
-  return 0;
 }
 
 // ============================================================ LayerNorm
