@@ -508,7 +508,9 @@ int dm_fill_normal_bf16(uint16_t* dst, uint64_t numel, uint64_t key, float scale
 int dm_logmel(const int16_t* pcm, const int64_t* offsets, const int32_t* lengths, int n,
               int n_mels, float* out, void* stream) {
   DM_REQUIRE(n >= 0, "n < 0");
+  DM_REQUIRE(n_mels == 80 || n_mels == 128, "n_mels must be 80 or 128");
   if (n == 0) return 0;
+  DM_REQUIRE(pcm && offsets && lengths && out, "null pointer");
   const LogmelTables* tab = nullptr;
   if (int rc = get_logmel_tables(n_mels, &tab)) return rc;
   uint32_t* segmax = nullptr;

@@ -160,13 +160,13 @@ class DispatchLoop(threading.Thread):
         super().__init__(name="dispatch-loop", daemon=True)
         self.queue, self.policy, self.backend = queue, policy, backend
         self.result_router, self.poll_interval_ms, self.clock = result_router, poll_interval_ms, clock
-        self._stop = threading.Event()
+        self._stop_requested = threading.Event()
         self.batches_dispatched = 0
 
     def run(self) -> None:
-        while not self._stop.is_set() and not self.queue.closed:
+        while not self._stop_requested.is_set() and not self.queue.closed:
             self.queue.wait_for_work(self.poll_interval_ms / 1000.0)
-            if self._stop.is_set() or self.queue.closed:
+            if self._stop_requested.is_set() or self.queue.closed:
                 break
             batch = self.queue.try_form_batch(self.policy, self.clock())
             if batch is not None:
@@ -191,7 +191,7 @@ class DispatchLoop(threading.Thread):
 
     def shutdown(self, timeout: float = 30.0) -> None:
         self.queue.close()
-        self._stop.set()
+        self._stop_requested.set()
         self.join(timeout=timeout)
 
 
@@ -209,7 +209,7 @@ class GpuConsumer(threading.Thread):
         self.result_router, self.cap_fn = result_router, cap_fn
         self.silence_is_empty = silence_is_empty
         self.poll_interval_ms, self.clock = poll_interval_ms, clock
-        self._stop = threading.Event()
+        self._stop_requested = threading.Event()
         self._inflight: dict[str, tuple[QueueEntry, float, float]] = {}
         self.segments_done = 0
         self.audio_s_done = 0.0
@@ -266,9 +266,9 @@ class GpuConsumer(threading.Thread):
             self.engine.reset()
 
     def run(self) -> None:
-        while not self._stop.is_set() and not self.queue.closed:
+        while not self._stop_requested.is_set() and not self.queue.closed:
             self.queue.wait_for_work(self.poll_interval_ms / 1000.0)
-            if self._stop.is_set() or self.queue.closed:
+            if self._stop_requested.is_set() or self.queue.closed:
                 break
             jobs = self._jobs_for(self.queue.try_form_batch(self.policy, self.clock()))
             if jobs:
@@ -283,7 +283,7 @@ class GpuConsumer(threading.Thread):
 
     def shutdown(self, timeout: float = 60.0) -> None:
         self.queue.close()
-        self._stop.set()
+        self._stop_requested.set()
         self.join(timeout=timeout)
 
 
@@ -304,6 +304,6 @@ class Multiplexer:
     def shutdown(self, timeout: float = 120.0) -> None:
         self.queue.close()
         for c in self.consumers:
-            c._stop.set()
+            c._stop_requested.set()
         for c in self.consumers:
             c.join(timeout=timeout)
