@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 namespace dm {
 
@@ -112,6 +113,33 @@ __device__ __forceinline__ bool elect_one() {
       : "=r"(pred)
       : "r"(0xffffffffu));
   return pred != 0;
+}
+
+// ------------------------------------------------------------ PDL
+// Programmatic dependent launch: kernels of the decode-step graph are launched
+// with programmaticStreamSerialization, so a kernel's CTAs may start while its
+// predecessor drains. pdl_wait() blocks the calling thread until the
+// predecessor grid completed and its writes are visible; pdl_trigger() lets
+// the successor grid launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ------------------------------------------------------------ TMA

@@ -137,13 +137,24 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
 
   if (warp == 0) {
     if (elect_one()) {
+      // weights do not depend on the predecessor: start their stream first
+      const int pre = kb_per < kTvStages ? kb_per : kTvStages;
+      for (int i = 0; i < pre; ++i) {
+        uint8_t* base = smem + i * kTvStageBytes;
+        mbar_arrive_expect_tx(&full[i], kTvStageBytes);
+        tma_load_2d(base, &tw, &full[i], (kb0 + i) * 64, tile * 128);
+      }
+      pdl_wait();
+      pdl_trigger();
       for (int i = 0; i < kb_per; ++i) {
         const int s = i % kTvStages;
-        mbar_wait(&empty[s], ((i / kTvStages) & 1) ^ 1);
         uint8_t* base = smem + s * kTvStageBytes;
-        mbar_arrive_expect_tx(&full[s], kTvStageBytes);
         const int kc = (kb0 + i) * 64;
-        tma_load_2d(base, &tw, &full[s], kc, tile * 128);
+        if (i >= pre) {
+          mbar_wait(&empty[s], ((i / kTvStages) & 1) ^ 1);
+          mbar_arrive_expect_tx(&full[s], kTvStageBytes);
+          tma_load_2d(base, &tw, &full[s], kc, tile * 128);
+        }
         tma_load_2d(base + kTvWBytes, &txh, &full[s], kc, 0);
         tma_load_2d(base + kTvWBytes + kTvXBytes, &txl, &full[s], kc, 0);
       }
@@ -175,6 +186,7 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     const bool nvalid = n < a.N;
     const float b = (nvalid && a.bias) ? bf16_to_f32(a.bias[n]) : 0.f;
     const int et = threadIdx.x - 64;               // 0..127 among epilogue threads
+    pdl_wait();
     if (EPI == TV_QKV && et < kRows) {
       // per-row self-KV write base for this layer
       const int r = et;
@@ -292,8 +304,8 @@ static int launch_tv(const DecodeState& st, const TcGemvMaps& maps, const TcGemv
     attr = true;
   }
   dim3 grid(ceil_div(a.N, 128), a.splits);
-  tc_gemv_kernel<EPI, SPLIT><<<grid, kTvThreads, kTvSmem, stream>>>(maps.w, maps.xh, maps.xl, st, a);
-  DM_CHECK_LAUNCH();
+  DM_CHECK_CUDA(launch_pdl(tc_gemv_kernel<EPI, SPLIT>, grid, dim3(kTvThreads), kTvSmem, stream,
+                           maps.w, maps.xh, maps.xl, st, a));
   return 0;
 }
 
@@ -325,6 +337,8 @@ __global__ void __launch_bounds__(256)
 decode_ln_kernel(const DecodeState st, const float* __restrict__ x, const uint16_t* g,
                  const uint16_t* b) {
   const int r = blockIdx.x * 8 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  pdl_wait();
+  pdl_trigger();
   if (r >= *st.n_active) return;
   const int d = st.d, n4 = d / 4;
   const float4* xr = reinterpret_cast<const float4*>(x + size_t(r) * d);
@@ -374,7 +388,8 @@ int launch_decode_ln(const DecodeState& st, const float* x, const uint16_t* g,
                      const uint16_t* b, cudaStream_t stream) {
   dim3 grid(kRows / 8);
   switch (st.d / 128) {
-#define DM_DLN(n) case n: decode_ln_kernel<n><<<grid, 256, 0, stream>>>(st, x, g, b); break;
+#define DM_DLN(n) \
+  case n: DM_CHECK_CUDA(launch_pdl(decode_ln_kernel<n>, grid, dim3(256), 0, stream, st, x, g, b)); break;
     DM_DLN(1) DM_DLN(2) DM_DLN(3) DM_DLN(4) DM_DLN(5) DM_DLN(6) DM_DLN(7) DM_DLN(8)
     DM_DLN(9) DM_DLN(10)
 #undef DM_DLN
@@ -388,6 +403,8 @@ int launch_decode_ln(const DecodeState& st, const float* x, const uint16_t* g,
 __global__ void embed_kernel(const DecodeState st, const uint16_t* __restrict__ embed,
                              const uint16_t* __restrict__ pos_emb) {
   const int r = blockIdx.x;
+  pdl_wait();
+  pdl_trigger();
   if (r >= *st.n_active) return;
   const int slot = st.active[r];
   const int tok = st.cur_tok[slot], p = st.pos[slot];
@@ -398,8 +415,7 @@ __global__ void embed_kernel(const DecodeState st, const uint16_t* __restrict__ 
 
 int launch_embed(const DecodeState& st, const uint16_t* embed, const uint16_t* pos_emb,
                  cudaStream_t stream) {
-  embed_kernel<<<kRows, 128, 0, stream>>>(st, embed, pos_emb);
-  DM_CHECK_LAUNCH();
+  DM_CHECK_CUDA(launch_pdl(embed_kernel, dim3(kRows), dim3(128), 0, stream, st, embed, pos_emb));
   return 0;
 }
 
@@ -488,9 +504,11 @@ dec_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, in
   int* is_last = reinterpret_cast<int*>(s_o + kDaWarps * 64);
 
   const int r = blockIdx.x, h = blockIdx.y, sp = blockIdx.z;
+  // n_active / active[] are host-set before the step graph: safe before pdl_wait
   if (r >= *st.n_active) return;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int slot = st.active[r];
+  if (!kCross) pdl_wait();                 // pos / self-KV come from predecessors
   int k0, k1;
   if (kCross) {
     const int per = ceil_div(ceil_div(1500, st.xsplits), kDaKeys) * kDaKeys;
@@ -541,6 +559,8 @@ dec_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, in
   }
 
   // ---------------- compute warps: lane owns key (chunk base + 32 warp + lane)
+  if (kCross) pdl_wait();                  // q comes from the predecessor
+  pdl_trigger();
   float q[64];
   {
     const float4* qp = reinterpret_cast<const float4*>(st.q + size_t(r) * st.d + h * 64);
@@ -642,8 +662,8 @@ int launch_self_attn(const DecodeState& st, const CUtensorMap& kv_map, int layer
     attr = true;
   }
   dim3 grid(kRows, st.heads, 1);
-  dec_attn_kernel<false><<<grid, kDaThreads, kDaSmem, stream>>>(kv_map, st, layer, 0);
-  DM_CHECK_LAUNCH();
+  DM_CHECK_CUDA(launch_pdl(dec_attn_kernel<false>, grid, dim3(kDaThreads), kDaSmem, stream, kv_map,
+                           st, layer, 0));
   return 0;
 }
 
@@ -656,8 +676,8 @@ int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int lay
     attr = true;
   }
   dim3 grid(kRows, st.heads, st.xsplits);
-  dec_attn_kernel<true><<<grid, kDaThreads, kDaSmem, stream>>>(xkv_map, st, layer, counter_base);
-  DM_CHECK_LAUNCH();
+  DM_CHECK_CUDA(launch_pdl(dec_attn_kernel<true>, grid, dim3(kDaThreads), kDaSmem, stream, xkv_map,
+                           st, layer, counter_base));
   return 0;
 }
 
@@ -666,6 +686,8 @@ int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int lay
 // id), then the greedy state machine (prompt forcing, EOT, per-slot cap).
 __global__ void finalize_kernel(const DecodeState st) {
   const int r = blockIdx.x * 4 + threadIdx.x / 32, lane = threadIdx.x % 32;
+  pdl_wait();
+  pdl_trigger();
   if (r >= *st.n_active) return;
   const int slot = st.active[r];
   const int tiles = ceil_div(st.vocab, 128);
@@ -699,8 +721,7 @@ __global__ void finalize_kernel(const DecodeState st) {
 }
 
 int launch_finalize(const DecodeState& st, cudaStream_t stream) {
-  finalize_kernel<<<kRows / 4, 128, 0, stream>>>(st);
-  DM_CHECK_LAUNCH();
+  DM_CHECK_CUDA(launch_pdl(finalize_kernel, dim3(kRows / 4), dim3(128), 0, stream, st));
   return 0;
 }
 
