@@ -1,0 +1,37 @@
+"""whisper-large-v3 (cfg3/cfg4 model: d1280, 32+32 layers, 128 mels, V51866)
+on the B200 engine vs the CPU oracle on one segment (parity subset)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from paper_2507_01021_b200.models import WHISPER_LARGE_V3
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def test_large_v3_parity(native_lib):
+    import torch
+    from oracle.logmel import log_mel_batch
+    from oracle.whisper import WhisperOracle
+    from paper_2507_01021_b200.engine import WhisperGPU
+    rng = np.random.default_rng(33)
+    segs = [rng.integers(-8000, 8000, size=n, dtype=np.int16) for n in (160_000, 64_000)]
+    gpu = WhisperGPU(WHISPER_LARGE_V3, seed=0, max_slots=4, max_encode_batch=2)
+    got = gpu.transcribe_ids(segs, [8, 8])
+    gpu.encode(segs, [0, 1])
+    mel = gpu.log_mel(2)
+    enc_gpu = gpu.encoder_output(2)
+    gpu.close()
+    del gpu
+    torch.cuda.empty_cache()
+    want_mel = log_mel_batch(segs, 128)
+    assert np.abs(mel - want_mel).max() <= 1e-4 * max(1.0, float(np.abs(want_mel).max()))
+    torch.set_num_threads(max(1, torch.get_num_threads()))
+    orc = WhisperOracle(WHISPER_LARGE_V3, seed=0)
+    enc = orc.encode(want_mel)
+    err = float(np.abs(enc_gpu - enc.numpy()).max())
+    assert err <= 2e-2, err
+    want = [orc.greedy(enc[b], 8) for b in range(2)]
+    assert got == want
