@@ -116,7 +116,8 @@ DM_API int dm_whisper_read(void* handle, int32_t* done, int32_t* n_gen, int32_t*
  *  which = 3: enable the logits tap (bytes ignored)
  *  which = 4: run only the first `bytes` encoder layers in later encodes
  *  which = 5: fp32 residual stream before the final LN, [n, 1500, d]
- *  which = 6: attention output of the last encoder layer run, [n, 1500, d] bf16 */
+ *  which = 6: attention output of the last encoder layer run, [n, 1500, d] bf16
+ *  which = 7: (bytes != 0) keep the fp32 encoder output; read it with which = 5 */
 DM_API int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void* stream);
 
 /* Telemetry: out[0..3] = kernels launched, decode steps, encode calls, segments. */

@@ -191,8 +191,9 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
                          ? exp2f(fmaf(__uint_as_float(sr[2 * i]), kLog2e, -mscaled)) : 0.f;
           float p1 = (c * 32 + 2 * i + 1 < kvalid)
                          ? exp2f(fmaf(__uint_as_float(sr[2 * i + 1]), kLog2e, -mscaled)) : 0.f;
-          rs += p0 + p1;
           pk[i] = pack_bf16x2(p0, p1);
+          // normalise with the same (bf16-rounded) weights the PV MMA uses
+          rs += __uint_as_float(pk[i] << 16) + __uint_as_float(pk[i] & 0xFFFF0000u);
         }
         // 32 keys = 4 chunks of 16 B; block = c / 2, chunk-in-row = (c % 2) * 4 + u
 #pragma unroll
@@ -245,7 +246,7 @@ template <int V4>  // float4 per lane
 __global__ void __launch_bounds__(256)
 layernorm_bf16_kernel(const float* __restrict__ x, const uint16_t* __restrict__ g,
                       const uint16_t* __restrict__ bta, uint16_t* __restrict__ y, int rows,
-                      int d) {
+                      int d, float* __restrict__ y32) {
   const int row = blockIdx.x * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (row >= rows) return;
@@ -284,18 +285,19 @@ layernorm_bf16_kernel(const float* __restrict__ x, const uint16_t* __restrict__ 
       float o2 = (v[i].z - mean) * rstd * bf16_to_f32(g[4 * c + 2]) + bf16_to_f32(bta[4 * c + 2]);
       float o3 = (v[i].w - mean) * rstd * bf16_to_f32(g[4 * c + 3]) + bf16_to_f32(bta[4 * c + 3]);
       yr[c] = make_uint2(pack_bf16x2(o0, o1), pack_bf16x2(o2, o3));
+      if (y32) reinterpret_cast<float4*>(y32 + size_t(row) * d)[c] = make_float4(o0, o1, o2, o3);
     }
   }
 }
 
 int launch_layernorm_bf16(const float* x, const uint16_t* g, const uint16_t* b, uint16_t* y,
-                          int rows, int d, cudaStream_t stream) {
+                          int rows, int d, cudaStream_t stream, float* y32) {
   DM_REQUIRE(d % 128 == 0 && d <= 1280, "layernorm d must be a multiple of 128, <= 1280");
   dim3 grid(ceil_div(rows, 8));
   const int v4 = d / 128;
   switch (v4) {
 #define DM_LN_CASE(n) \
-  case n: layernorm_bf16_kernel<n><<<grid, 256, 0, stream>>>(x, g, b, y, rows, d); break;
+  case n: layernorm_bf16_kernel<n><<<grid, 256, 0, stream>>>(x, g, b, y, rows, d, y32); break;
     DM_LN_CASE(1) DM_LN_CASE(2) DM_LN_CASE(3) DM_LN_CASE(4) DM_LN_CASE(5)
     DM_LN_CASE(6) DM_LN_CASE(7) DM_LN_CASE(8) DM_LN_CASE(9) DM_LN_CASE(10)
 #undef DM_LN_CASE

@@ -27,7 +27,7 @@ struct LogmelTables;
 int launch_logmel(const int16_t*, const int64_t*, const int32_t*, int, int,
                   const LogmelTables*, float*, uint16_t*, uint32_t*, cudaStream_t);
 int launch_layernorm_bf16(const float*, const uint16_t*, const uint16_t*, uint16_t*, int, int,
-                          cudaStream_t);
+                          cudaStream_t, float* y32 = nullptr);
 int launch_attention(const uint16_t*, const uint16_t*, const uint16_t*, int, int, int, int,
                      uint16_t*, int, cudaStream_t);
 
@@ -170,6 +170,7 @@ struct WhisperEngine {
   int32_t* slot_host = nullptr;  // pinned [E]
   int last_n = 0;
   int enc_stop = 1 << 30;        // debug: run only the first enc_stop layers
+  bool enc_tap = false;          // debug: keep the fp32 encoder output (in resid)
   // decode
   DecodeState st{};
   int32_t* prompt_dev = nullptr;
@@ -404,8 +405,9 @@ static int encoder_forward(WhisperEngine* e, const int16_t* pcm, const int64_t* 
     }
   }
   const int a = e->after_enc();
-  if (int rc = launch_layernorm_bf16(e->resid, e->W(a), e->W(a + 1), e->enc_out, M, d, s))
-    return rc;
+  if (int rc = launch_layernorm_bf16(e->resid, e->W(a), e->W(a + 1), e->enc_out, M, d, s,
+                                     e->enc_tap ? e->resid : nullptr))
+    return rc;    // (debug tap: fp32 encoder output written in place over the residual)
   // cross-KV precompute for every decoder layer, scattered into the slots
   {
     const int x = e->after_dec();
@@ -759,6 +761,7 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
       return 0;
     }
     case 4: e->enc_stop = int(bytes); return 0;
+    case 7: e->enc_tap = bytes != 0; return 0;
     case 5: src = e->resid; avail = size_t(e->last_n) * 1500 * e->d * 4; break;
     case 6: src = e->attn_out; avail = size_t(e->last_n) * 1500 * e->d * 2; break;
     default: DM_REQUIRE(false, "unknown debug tap");

@@ -271,6 +271,17 @@ class WhisperGPU:
         self.debug(0, bits)
         return (bits.astype(np.uint32) << 16).view(np.float32)
 
+    def encoder_output_f32(self, segs, slots) -> np.ndarray:
+        """Encode with the fp32 tap on and return the final-LN output before
+        its bf16 rounding (the cross-KV GEMM consumes the bf16 copy)."""
+        _native.check(self.lib.dm_whisper_debug(self.handle, 7, None, 1, self._s))
+        try:
+            self.encode(segs, slots)
+            out = np.empty((len(segs), 1500, self.dims.d_model), np.float32)
+            return self.debug(5, out)
+        finally:
+            _native.check(self.lib.dm_whisper_debug(self.handle, 7, None, 0, self._s))
+
     def log_mel(self, n: int) -> np.ndarray:
         return self.debug(1, np.empty((n, self.dims.n_mels, 3000), np.float32))
 

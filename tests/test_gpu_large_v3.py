@@ -20,8 +20,9 @@ def test_large_v3_parity(native_lib):
     segs = [rng.integers(-8000, 8000, size=n, dtype=np.int16) for n in (160_000, 64_000)]
     gpu = WhisperGPU(WHISPER_LARGE_V3, seed=0, max_slots=4, max_encode_batch=2)
     got = gpu.transcribe_ids(segs, [8, 8])
-    gpu.encode(segs, [0, 1])
+    enc32 = gpu.encoder_output_f32(segs, [0, 1])
     mel = gpu.log_mel(2)
+    gpu.encode(segs, [0, 1])
     enc_gpu = gpu.encoder_output(2)
     gpu.close()
     del gpu
@@ -31,7 +32,10 @@ def test_large_v3_parity(native_lib):
     torch.set_num_threads(max(1, torch.get_num_threads()))
     orc = WhisperOracle(WHISPER_LARGE_V3, seed=0)
     enc = orc.encode(want_mel)
-    err = float(np.abs(enc_gpu - enc.numpy()).max())
-    assert err <= 2e-2, err
+    e = np.abs(enc32 - enc.numpy())
+    eb = np.abs(enc_gpu - enc.numpy())
+    print(f"large-v3 encoder |err| fp32 out: max {e.max():.4g} p99.99 {np.quantile(e, 0.9999):.4g} "
+          f"mean {e.mean():.3g}; bf16-stored out: max {eb.max():.4g}")
+    assert e.max() <= 2e-2, e.max()
     want = [orc.greedy(enc[b], 8) for b in range(2)]
     assert got == want
