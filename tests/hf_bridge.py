@@ -98,3 +98,72 @@ def hf_log_mel(samples_i16_list, n_mels: int) -> np.ndarray:
     out = fe(wav, sampling_rate=16000, return_tensors="np",
              padding="max_length", truncation=True)
     return out["input_features"]
+
+
+def build_hf_wav2vec2(dims, weights):
+    """transformers Wav2Vec2ForCTC (wav2vec2-base shape) loaded with the shared
+    seeded weights; the positional conv's weight-norm is set so that its
+    effective weight equals ours (g = ||W|| per tap, v = W)."""
+    from transformers import Wav2Vec2Config, Wav2Vec2ForCTC
+    cfg = Wav2Vec2Config(vocab_size=dims.vocab, hidden_size=dims.hidden,
+                         num_hidden_layers=dims.layers, num_attention_heads=dims.heads,
+                         intermediate_size=dims.ffn, hidden_act="gelu",
+                         feat_extract_norm="group", feat_extract_activation="gelu",
+                         conv_dim=list(dims.conv_dim), conv_kernel=list(dims.conv_kernel),
+                         conv_stride=list(dims.conv_stride), conv_bias=False,
+                         num_conv_pos_embeddings=dims.pos_conv_kernel,
+                         num_conv_pos_embedding_groups=dims.pos_conv_groups,
+                         do_stable_layer_norm=False, layer_norm_eps=dims.ln_eps,
+                         hidden_dropout=0.0, attention_dropout=0.0, activation_dropout=0.0,
+                         feat_proj_dropout=0.0, final_dropout=0.0, layerdrop=0.0,
+                         apply_spec_augment=False, pad_token_id=dims.blank)
+    cfg._attn_implementation = "eager"
+    m = Wav2Vec2ForCTC(cfg).eval()
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32))
+    sd = {}
+    for i in range(len(dims.conv_dim)):
+        sd[f"wav2vec2.feature_extractor.conv_layers.{i}.conv.weight"] = t(
+            weights[f"fe.conv{i}.w"].transpose(0, 2, 1))
+    sd["wav2vec2.feature_extractor.conv_layers.0.layer_norm.weight"] = t(weights["fe.gn.g"])
+    sd["wav2vec2.feature_extractor.conv_layers.0.layer_norm.bias"] = t(weights["fe.gn.b"])
+    sd["wav2vec2.feature_projection.layer_norm.weight"] = t(weights["fp.ln.g"])
+    sd["wav2vec2.feature_projection.layer_norm.bias"] = t(weights["fp.ln.b"])
+    sd["wav2vec2.feature_projection.projection.weight"] = t(weights["fp.proj.w"])
+    sd["wav2vec2.feature_projection.projection.bias"] = t(weights["fp.proj.b"])
+    g, cg, k = dims.pos_conv_groups, dims.hidden // dims.pos_conv_groups, dims.pos_conv_kernel
+    W = weights["pos.w"].reshape(dims.hidden, k, cg).transpose(0, 2, 1)      # [out, in/g, k]
+    conv = m.wav2vec2.encoder.pos_conv_embed.conv
+    pre = "wav2vec2.encoder.pos_conv_embed.conv"
+    if hasattr(conv, "parametrizations"):
+        sd[f"{pre}.parametrizations.weight.original0"] = t(
+            np.sqrt((W.astype(np.float64) ** 2).sum(axis=(0, 1), keepdims=True)))
+        sd[f"{pre}.parametrizations.weight.original1"] = t(W)
+    else:
+        sd[f"{pre}.weight_g"] = t(np.sqrt((W.astype(np.float64) ** 2).sum(axis=(0, 1), keepdims=True)))
+        sd[f"{pre}.weight_v"] = t(W)
+    sd[f"{pre}.bias"] = t(weights["pos.b"])
+    sd["wav2vec2.encoder.layer_norm.weight"] = t(weights["enc.ln.g"])
+    sd["wav2vec2.encoder.layer_norm.bias"] = t(weights["enc.ln.b"])
+    d = dims.hidden
+    for i in range(dims.layers):
+        p, q = f"wav2vec2.encoder.layers.{i}", f"l{i}"
+        w, b = weights[f"{q}.qkv.w"], weights[f"{q}.qkv.b"]
+        for j, nm in enumerate(("q_proj", "k_proj", "v_proj")):
+            sd[f"{p}.attention.{nm}.weight"] = t(w[j * d:(j + 1) * d])
+            sd[f"{p}.attention.{nm}.bias"] = t(b[j * d:(j + 1) * d])
+        sd[f"{p}.attention.out_proj.weight"] = t(weights[f"{q}.o.w"])
+        sd[f"{p}.attention.out_proj.bias"] = t(weights[f"{q}.o.b"])
+        sd[f"{p}.layer_norm.weight"] = t(weights[f"{q}.ln1.g"])
+        sd[f"{p}.layer_norm.bias"] = t(weights[f"{q}.ln1.b"])
+        sd[f"{p}.feed_forward.intermediate_dense.weight"] = t(weights[f"{q}.fc1.w"])
+        sd[f"{p}.feed_forward.intermediate_dense.bias"] = t(weights[f"{q}.fc1.b"])
+        sd[f"{p}.feed_forward.output_dense.weight"] = t(weights[f"{q}.fc2.w"])
+        sd[f"{p}.feed_forward.output_dense.bias"] = t(weights[f"{q}.fc2.b"])
+        sd[f"{p}.final_layer_norm.weight"] = t(weights[f"{q}.ln2.g"])
+        sd[f"{p}.final_layer_norm.bias"] = t(weights[f"{q}.ln2.b"])
+    sd["lm_head.weight"] = t(weights["head.w"])
+    sd["lm_head.bias"] = t(weights["head.b"])
+    missing, unexpected = m.load_state_dict(sd, strict=False)
+    missing = [k for k in missing if "masked_spec_embed" not in k]
+    assert not missing and not unexpected, (missing, unexpected)
+    return m
