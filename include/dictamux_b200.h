@@ -120,6 +120,31 @@ DM_API int dm_whisper_read(void* handle, int32_t* done, int32_t* n_gen, int32_t*
  *  which = 7: (bytes != 0) keep the fp32 encoder output; read it with which = 5 */
 DM_API int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void* stream);
 
+/* ------------------------------------------------------------ CTC engine (cfg5)
+ * wav2vec2-base-shaped encoder-only CTC ("CTC models"; the
+ * reference's segment-independence contract SPEC.md:13,103,515).
+ * Weight offsets, in order: fe.conv0..6.w, fe.gn.g, fe.gn.b, fp.ln.g, fp.ln.b,
+ * fp.proj.w, fp.proj.b, pos.w, pos.b, enc.ln.g, enc.ln.b, per layer
+ * (qkv.w qkv.b o.w o.b ln1.g ln1.b fc1.w fc1.b fc2.w fc2.b ln2.g ln2.b), head.w, head.b. */
+typedef struct dm_ctc_config {
+  int hidden, layers, heads, ffn, vocab;
+  int max_batch;          /* segments per dm_ctc_transcribe call */
+  int max_samples;        /* longest segment (16 kHz samples) */
+} dm_ctc_config;
+
+DM_API int dm_ctc_create(const dm_ctc_config* cfg, const uint16_t* weights, const int64_t* offsets,
+                         int n_offsets, void** handle);
+DM_API int dm_ctc_destroy(void* handle);
+/* Greedy CTC for n segments: pcm on the device, offsets/lengths on the HOST
+ * (frame bookkeeping is host-side). Results stay on the device until read. */
+DM_API int dm_ctc_transcribe(void* handle, const int16_t* pcm, const int64_t* offsets,
+                             const int32_t* lengths, int n, void* stream);
+/* tokens: [n, rows_per_segment] collapsed ids (first counts[i] valid per row). */
+DM_API int dm_ctc_read(void* handle, int32_t* tokens, int32_t* counts, int32_t* rows_per_segment,
+                       void* stream);
+/* which = 0: per-frame argmax ids [n * rows] int32; 1: final hidden [n * rows, 768] fp32 */
+DM_API int dm_ctc_debug(void* handle, int which, void* host_dst, size_t bytes, void* stream);
+
 /* Telemetry: out[0..3] = kernels launched, decode steps, encode calls, segments. */
 DM_API int dm_whisper_stats(void* handle, int64_t* out, int n);
 /* Time one decode kernel over the current active slots with CUDA events on

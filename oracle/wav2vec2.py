@@ -87,6 +87,11 @@ class Wav2Vec2Oracle:
 
     @torch.no_grad()
     def logits(self, samples_i16: np.ndarray) -> torch.Tensor:
+        return self._lin(self.hidden(samples_i16), "head")
+
+    @torch.no_grad()
+    def hidden(self, samples_i16: np.ndarray) -> torch.Tensor:
+        """Final encoder hidden states [T', 768] (input to the CTC head)."""
         d = self.dims
         h = self.features(samples_i16)                                   # [T', 768]
         g, cg = d.pos_conv_groups, d.hidden // d.pos_conv_groups
@@ -105,7 +110,7 @@ class Wav2Vec2Oracle:
             a = a.transpose(0, 1).reshape(T, d.hidden)
             x = self._ln(x + self._lin(a, f"{p}.o"), f"{p}.ln1")
             x = self._ln(x + self._lin(F.gelu(self._lin(x, f"{p}.fc1")), f"{p}.fc2"), f"{p}.ln2")
-        return self._lin(x, "head")
+        return x
 
     def transcribe_ids(self, samples_i16: np.ndarray) -> list[int]:
         if frames_for(len(samples_i16), self.dims) == 0:

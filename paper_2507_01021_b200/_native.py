@@ -19,6 +19,7 @@ EXPORTS = (
     "dm_whisper_encode", "dm_whisper_admit", "dm_whisper_release",
     "dm_whisper_set_active", "dm_whisper_step", "dm_whisper_read",
     "dm_whisper_debug", "dm_whisper_stats", "dm_whisper_time_kernel",
+    "dm_ctc_create", "dm_ctc_destroy", "dm_ctc_transcribe", "dm_ctc_read", "dm_ctc_debug",
 )
 
 
@@ -33,6 +34,11 @@ class WhisperConfigC(C.Structure):
                 ("prompt", C.c_int * 8), ("prompt_len", C.c_int),
                 ("max_slots", C.c_int), ("max_encode_batch", C.c_int),
                 ("num_pages", C.c_int)]
+
+
+class CtcConfigC(C.Structure):
+    _fields_ = [("hidden", C.c_int), ("layers", C.c_int), ("heads", C.c_int), ("ffn", C.c_int),
+                ("vocab", C.c_int), ("max_batch", C.c_int), ("max_samples", C.c_int)]
 
 
 _lib = None
@@ -74,6 +80,11 @@ def load(build_if_missing: bool = False):
             "dm_whisper_debug": [P, C.c_int, P, C.c_size_t, P],
             "dm_whisper_stats": [P, P, C.c_int],
             "dm_whisper_time_kernel": [P, C.c_int, C.c_int, C.c_int, P, P],
+            "dm_ctc_create": [C.POINTER(CtcConfigC), P, P, C.c_int, C.POINTER(C.c_void_p)],
+            "dm_ctc_destroy": [P],
+            "dm_ctc_transcribe": [P, P, P, P, C.c_int, P],
+            "dm_ctc_read": [P, P, P, P, P],
+            "dm_ctc_debug": [P, C.c_int, P, C.c_size_t, P],
         }
         for name, args in sig.items():
             fn = getattr(lib, name)

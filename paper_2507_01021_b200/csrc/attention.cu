@@ -35,8 +35,9 @@ struct AttnSmemLayout {
 __global__ void __launch_bounds__(kAttnThreads, 1)
 attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
-                    const __grid_constant__ CUtensorMap tm_vt, int T, int t_pad,
-                    int heads, uint16_t* __restrict__ out, int ldo) {
+                    const __grid_constant__ CUtensorMap tm_vt, int T_rows, int t_pad,
+                    int heads, uint16_t* __restrict__ out, int ldo,
+                    const int32_t* __restrict__ seg_len) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
@@ -53,6 +54,9 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int qt = blockIdx.x, bh = blockIdx.y;
+  // per-segment valid length (variable-length CTC batches); whisper: all 1500
+  const int T = seg_len ? seg_len[bh / heads] : T_rows;
+  if (qt * 128 >= T) return;
   const int nb = ceil_div(T, 128);
 
   if (warp == 0 && lane == 0) {
@@ -222,7 +226,7 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
     if (t < T) {
       const float inv = 1.0f / l_run;
       const int b = bh / heads, h = bh % heads;
-      uint4* dst = reinterpret_cast<uint4*>(out + (size_t(b) * T + t) * ldo + h * 64);
+      uint4* dst = reinterpret_cast<uint4*>(out + (size_t(b) * T_rows + t) * ldo + h * 64);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         dst[i] = make_uint4(pack_bf16x2(o[8 * i] * inv, o[8 * i + 1] * inv),
@@ -312,7 +316,8 @@ int make_attn_maps(const uint16_t* q, const uint16_t* k, const uint16_t* vt, int
                    CUtensorMap* mq, CUtensorMap* mk, CUtensorMap* mv);
 
 int launch_attention(const uint16_t* q, const uint16_t* k, const uint16_t* vt, int n_seg,
-                     int heads, int T, int t_pad, uint16_t* out, int ldo, cudaStream_t stream) {
+                     int heads, int T, int t_pad, uint16_t* out, int ldo, cudaStream_t stream,
+                     const int32_t* seg_len) {
   DM_REQUIRE(t_pad % 128 == 0 && t_pad >= T, "t_pad must be a multiple of 128 >= T");
   CUtensorMap mq, mk, mv;
   if (make_attn_maps(q, k, vt, n_seg * heads, t_pad, &mq, &mk, &mv)) return 2;
@@ -325,7 +330,7 @@ int launch_attention(const uint16_t* q, const uint16_t* k, const uint16_t* vt, i
   }
   dim3 grid(ceil_div(T, 128), n_seg * heads);
   attn_tcgen05_kernel<<<grid, kAttnThreads, AttnSmemLayout::total, stream>>>(
-      mq, mk, mv, T, t_pad, heads, out, ldo);
+      mq, mk, mv, T, t_pad, heads, out, ldo, seg_len);
   DM_CHECK_LAUNCH();
   return 0;
 }

@@ -29,7 +29,7 @@ int launch_logmel(const int16_t*, const int64_t*, const int32_t*, int, int,
 int launch_layernorm_bf16(const float*, const uint16_t*, const uint16_t*, uint16_t*, int, int,
                           cudaStream_t, float* y32 = nullptr);
 int launch_attention(const uint16_t*, const uint16_t*, const uint16_t*, int, int, int, int,
-                     uint16_t*, int, cudaStream_t);
+                     uint16_t*, int, cudaStream_t, const int32_t* seg_len = nullptr);
 
 // ------------------------------------------------------------ log-mel tables
 struct LogmelTablesHost {

@@ -42,7 +42,7 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, const GemmArgs
   float v[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-  if (e.bias != nullptr) {
+  if (e.bias != nullptr) {     // (EPI_W2V_POS carries its bias in e.pos, indexed by channel)
     const uint4* bp = reinterpret_cast<const uint4*>(e.bias + n0);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -59,6 +59,7 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, const GemmArgs
   const int N = g.N;
   switch (e.mode) {
     case EPI_GELU_BF16:
+    case EPI_GELU_F32:
     case EPI_CONV1:
     case EPI_CONV2_POS:
 #pragma unroll
@@ -103,6 +104,7 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, const GemmArgs
       break;
     }
     case EPI_RESID_F32:
+    case EPI_GELU_F32:
     case EPI_STORE_F32: {
       float4* dst = reinterpret_cast<float4*>(static_cast<float*>(e.out) +
                                               (size_t(b) * g.T + t) * e.ldo + n0);
@@ -121,7 +123,7 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, const GemmArgs
       // global row -> (segment, position)
       const int d = N / 3;
       const int row = b * g.T + t;
-      const int seg = row / 1500, pos = row % 1500;
+      const int seg = row / e.seg_rows, pos = row % e.seg_rows;
       const int region = n0 / d, h = (n0 % d) / 64, j0 = n0 % 64;
       const size_t head = size_t(seg) * e.heads + h;
       if (region < 2) {
@@ -144,7 +146,7 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, const GemmArgs
     case EPI_XKV: {
       const int d = N / (2 * e.layers);
       const int row = b * g.T + t;
-      const int seg = row / 1500, pos = row % 1500;
+      const int seg = row / e.seg_rows, pos = row % e.seg_rows;
       const int slot = e.slot_ids[seg];
       const int l = n0 / (2 * d), kv = (n0 / d) % 2, h = (n0 % d) / 64, j0 = n0 % 64;
       size_t idx = ((((size_t(l) * e.n_slots + slot) * 2 + kv) * e.heads + h) * 1500 + pos) * 64 + j0;
@@ -155,6 +157,51 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, const GemmArgs
                             pack_bf16x2(v[8 * i + 2], v[8 * i + 3]),
                             pack_bf16x2(v[8 * i + 4], v[8 * i + 5]),
                             pack_bf16x2(v[8 * i + 6], v[8 * i + 7]));
+      break;
+    }
+    case EPI_W2V_PROJ: {
+      const int row = b * g.T + t;
+      const int seg = row / e.seg_rows, pos = row % e.seg_rows;
+      const bool valid = pos < e.seg_len[seg];
+      float4* dst = reinterpret_cast<float4*>(static_cast<float*>(e.out) + size_t(row) * e.ldo + n0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        dst[i] = valid ? make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3])
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      // grouped bf16 copy: channel ch -> group ch / cpg, slot ch % cpg (64-wide groups)
+      uint16_t* gp = e.grp + (size_t(seg) * (e.seg_rows + 2 * e.grp_pad) + e.grp_pad + pos) *
+                                 (size_t(N) / e.grp_cpg * 64);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int ch = n0 + i;
+        gp[(ch / e.grp_cpg) * 64 + ch % e.grp_cpg] = valid ? f32_to_bf16(v[i]) : uint16_t(0);
+      }
+      break;
+    }
+    case EPI_W2V_POS: {
+      // n0 covers 32 of a 64-wide group tile; slots >= cpg are padding
+      const int grp_i = n0 / 64, j0 = n0 % 64;
+      if (j0 >= e.grp_cpg) break;
+      const int row = b * g.T + t;
+      float* x = static_cast<float*>(e.out) + size_t(row) * e.ldo;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int j = j0 + i;
+        if (j < e.grp_cpg) {
+          const int ch = grp_i * e.grp_cpg + j;
+          x[ch] += gelu_erf(v[i] + bf16_to_f32(e.pos[ch]));
+        }
+      }
+      break;
+    }
+    case EPI_CTC_ARGMAX: {
+      if (n0 != 0) break;
+      float best = v[0];
+      int bi = 0;
+#pragma unroll
+      for (int i = 1; i < 32; ++i)
+        if (i < N && v[i] > best) { best = v[i]; bi = i; }
+      static_cast<int32_t*>(e.out)[size_t(b) * g.T + t] = bi;
       break;
     }
     default:
@@ -224,7 +271,8 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
           if (g.a_mode == A_FLAT) {
             tma_load_3d(sa, &tmap_a, &full[stage], kb * kBK, mt * kBM, b);
           } else {
-            const int tap = kb / geo.cpb, c0 = (kb % geo.cpb) * kBK;
+            const int tap = kb / geo.cpb;
+            const int c0 = (kb % geo.cpb) * kBK + (g.grouped ? nt * kBK : 0);
             if (g.a_mode == A_CONV_S1)
               tma_load_3d(sa, &tmap_a, &full[stage], c0, mt * kBM + tap, b);
             else
@@ -339,14 +387,15 @@ static int launch_bn(const GemmArgs& g, cudaStream_t stream) {
     cuuint32_t box[3] = {kBK, kBM, 1};
     if (make_map(&ma, g.A, 3, dims, str, box)) return 2;
   } else if (g.a_mode == A_CONV_S1) {
-    cuuint64_t dims[3] = {cuuint64_t(g.C), cuuint64_t(g.T + 2), cuuint64_t(g.Bt)};
-    cuuint64_t str[2] = {cuuint64_t(g.C) * 2, cuuint64_t(g.C) * 2 * (g.T + 2)};
+    const int rows = g.a_rows ? g.a_rows : g.T + 2;
+    cuuint64_t dims[3] = {cuuint64_t(g.C), cuuint64_t(rows), cuuint64_t(g.Bt)};
+    cuuint64_t str[2] = {cuuint64_t(g.C) * 2, cuuint64_t(g.C) * 2 * rows};
     cuuint32_t box[3] = {kBK, kBM, 1};
     if (make_map(&ma, g.A, 3, dims, str, box)) return 2;
   } else {
-    cuuint64_t dims[4] = {cuuint64_t(g.C), 2, cuuint64_t(g.T + 1), cuuint64_t(g.Bt)};
-    cuuint64_t str[3] = {cuuint64_t(g.C) * 2, cuuint64_t(g.C) * 4,
-                         cuuint64_t(g.C) * 2 * (2 * g.T + 2)};
+    const int rows = g.a_rows ? g.a_rows : 2 * g.T + 2;     // must be even
+    cuuint64_t dims[4] = {cuuint64_t(g.C), 2, cuuint64_t(rows / 2), cuuint64_t(g.Bt)};
+    cuuint64_t str[3] = {cuuint64_t(g.C) * 2, cuuint64_t(g.C) * 4, cuuint64_t(g.C) * 2 * rows};
     cuuint32_t box[4] = {kBK, 1, kBM, 1};
     if (make_map(&ma, g.A, 4, dims, str, box)) return 2;
   }
@@ -361,7 +410,7 @@ static int launch_bn(const GemmArgs& g, cudaStream_t stream) {
   geo.NT = ceil_div(g.N, BN);
   geo.tiles = g.Bt * geo.MT * geo.NT;
   geo.KB = ceil_div(g.K, kBK);
-  geo.cpb = g.C > 0 ? g.C / kBK : 1;
+  geo.cpb = g.grouped ? 1 : (g.C > 0 ? g.C / kBK : 1);
   const int smem = GemmSmem<BN, STAGES>::kBytes;
   static bool attr = false;
   if (!attr) {
@@ -408,11 +457,15 @@ int launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   DM_REQUIRE(g.K > 0 && g.N > 0 && g.T > 0 && g.Bt > 0, "empty GEMM");
   DM_REQUIRE(g.N % 32 == 0, "N must be a multiple of 32");
   DM_REQUIRE(g.K % 8 == 0, "K must be a multiple of 8 (16-byte rows)");
-  DM_REQUIRE(g.a_mode == A_FLAT || (g.C % kBK == 0 && g.K == 3 * g.C),
-             "conv A needs C % 64 == 0 and K == 3C");
+  DM_REQUIRE(g.a_mode == A_FLAT || (g.C % kBK == 0 && (g.grouped || g.K % g.C == 0)),
+             "conv A needs C % 64 == 0 and K == taps * C");
+  DM_REQUIRE(!g.grouped || (g.a_mode == A_CONV_S1 && g.K % kBK == 0),
+             "grouped conv: stride-1 conv mode, K = taps * 64");
+  DM_REQUIRE(g.a_mode != A_CONV_S2 || g.a_rows % 2 == 0, "stride-2 conv input rows must be even");
   DM_REQUIRE((reinterpret_cast<uintptr_t>(g.A) & 15) == 0 &&
                  (reinterpret_cast<uintptr_t>(g.W) & 15) == 0,
              "operands must be 16-byte aligned");
+  if (g.grouped) return launch_bn<64, 8>(g, stream);
   if (g.N % 256 == 0 && g.N >= 1024) return launch_bn<256, 4>(g, stream);
   return launch_bn<128, 6>(g, stream);
 }
