@@ -149,7 +149,9 @@ DM_API int dm_ctc_debug(void* handle, int which, void* host_dst, size_t bytes, v
 DM_API int dm_whisper_stats(void* handle, int64_t* out, int n);
 /* Time one decode kernel over the current active slots with CUDA events on
  * `stream` (idempotent kernels only): which = 0 cross-attention(layer),
- * 1 self-attention(layer), 2 LM head. avg_ms = mean over iters launches. */
+ * 1 self-attention(layer), 2 LM head, 3 decoder LN, 4 cross-q projection,
+ * 5 fc2 projection (split-K), 6 empty PDL kernel (launch floor).
+ * avg_ms = mean over iters back-to-back launches. */
 DM_API int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float* avg_ms,
                                   void* stream);
 

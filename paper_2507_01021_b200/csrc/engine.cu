@@ -420,6 +420,15 @@ static int encoder_forward(WhisperEngine* e, const int16_t* pcm, const int64_t* 
   return 0;
 }
 
+__global__ void pdl_floor_kernel() {
+  pdl_wait();
+  pdl_trigger();
+}
+static int launch_pdl_floor(cudaStream_t s) {
+  DM_CHECK_CUDA(launch_pdl(pdl_floor_kernel, dim3(1), dim3(32), 0, s));
+  return 0;
+}
+
 static int record_step(WhisperEngine* e, cudaStream_t s) {
   DecodeState& st = e->st;
   const int d = e->d;
@@ -696,33 +705,68 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
   DM_REQUIRE(e != nullptr && avg_ms != nullptr && iters >= 1, "bad arguments");
   DM_REQUIRE(layer >= 0 && layer < e->Ld, "layer out of range");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // capture `iters` back-to-back launches in a graph so the timing sees the
+  // GPU-side launch/complete latency, not host submission
+  auto launch_one = [&](cudaStream_t cs) -> int {
+    switch (which) {
+      case 0: return launch_cross_attn(e->st, e->xkv_map, layer, e->xattn_counter_base, cs);
+      case 1: return launch_self_attn(e->st, e->kv_map, layer, cs);
+      case 2: {
+        TcGemvArgs g{};
+        g.N = e->cfg.vocab; g.K = e->d; g.epi = TV_ARGMAX; g.scale = 1.f; g.splits = 1;
+        return launch_tc_gemv(e->st, e->maps.back(), g, cs);
+      }
+      case 3: {
+        const int b0 = e->dec_layer_base(layer);
+        return launch_decode_ln(e->st, e->st.x, e->W(b0 + 6), e->W(b0 + 7), cs);
+      }
+      case 4: {
+        const int b0 = e->dec_layer_base(layer);
+        TcGemvArgs g{};
+        g.bias = e->W(b0 + 9); g.N = e->d; g.K = e->d; g.epi = TV_STORE; g.scale = 0.125f;
+        g.layer = layer; g.splits = tc_gemv_splits(e->d, e->d); g.y = e->st.q;
+        return launch_tc_gemv(e->st, e->maps[size_t(layer) * 6 + 2], g, cs);
+      }
+      case 5: {
+        const int b0 = e->dec_layer_base(layer);
+        TcGemvArgs g{};
+        g.bias = e->W(b0 + 17); g.N = e->d; g.K = e->F; g.epi = TV_RESID; g.scale = 1.f;
+        g.layer = layer; g.splits = tc_gemv_splits(e->d, e->F); g.y = e->st.x;
+        g.counter_base = e->gemv_counter_base;
+        return launch_tc_gemv(e->st, e->maps[size_t(layer) * 6 + 5], g, cs);
+      }
+      case 6: return launch_pdl_floor(cs);
+      default: set_error("unknown kernel id"); return 1;
+    }
+  };
+  DM_CHECK_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+  int rc = 0;
+  for (int i = 0; i < iters && rc == 0; ++i) rc = launch_one(e->cap_stream);
+  cudaGraph_t g = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &g);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  DM_CHECK_CUDA(ce);
+  cudaGraphExec_t ge = nullptr;
+  DM_CHECK_CUDA(cudaGraphInstantiate(&ge, g, 0));
+  DM_CHECK_CUDA(cudaGraphLaunch(ge, s));           // warm-up
   cudaEvent_t a, b;
   DM_CHECK_CUDA(cudaEventCreate(&a));
   DM_CHECK_CUDA(cudaEventCreate(&b));
   DM_CHECK_CUDA(cudaEventRecord(a, s));
-  for (int i = 0; i < iters; ++i) {
-    int rc = 0;
-    switch (which) {
-      case 0: rc = launch_cross_attn(e->st, e->xkv_map, layer, e->xattn_counter_base, s); break;
-      case 1: rc = launch_self_attn(e->st, e->kv_map, layer, s); break;
-      case 2: {
-        TcGemvArgs g{};
-        g.N = e->cfg.vocab; g.K = e->d; g.epi = TV_ARGMAX; g.scale = 1.f; g.splits = 1;
-        rc = launch_tc_gemv(e->st, e->maps.back(), g, s);
-        break;
-      }
-      default: DM_REQUIRE(false, "unknown kernel id");
-    }
-    if (rc) return rc;
-  }
+  DM_CHECK_CUDA(cudaGraphLaunch(ge, s));
   DM_CHECK_CUDA(cudaEventRecord(b, s));
   DM_CHECK_CUDA(cudaEventSynchronize(b));
   float ms = 0.f;
   DM_CHECK_CUDA(cudaEventElapsedTime(&ms, a, b));
   cudaEventDestroy(a);
   cudaEventDestroy(b);
+  cudaGraphExecDestroy(ge);
+  cudaGraphDestroy(g);
   *avg_ms = ms / iters;
-  e->launches += iters;
+  e->launches += 2LL * iters;
   return 0;
 }
 

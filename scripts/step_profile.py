@@ -43,6 +43,9 @@ for n in (64, 48, 32, 16, 8, 1):
     xkv = n * dims.dec_layers * 2 * 1500 * dims.d_model * 2
     res[n] = {"step_ms": round(ms, 4), "xkv_GBps": round(xkv / ms / 1e6, 1)}
 out["decode_step"] = res
-out["xattn_ms_layer0_full"] = eng.time_kernel(0, 0, 20)
-out["lmhead_ms"] = eng.time_kernel(2, 0, 20)
+names = {0: "cross_attn", 1: "self_attn", 2: "lm_head", 3: "decode_ln", 4: "gemv_xq",
+         5: "gemv_fc2_splitk", 6: "empty_pdl_floor"}
+for n in (64, 1):
+    eng.set_active(slots[:n])
+    out[f"kernel_us_rows{n}"] = {names[w]: round(1000 * eng.time_kernel(w, 0, 50), 2) for w in names}
 print(json.dumps(out, indent=1))
