@@ -342,7 +342,8 @@ def measure_roofline(eng, dims, args) -> dict:
     ms = statistics.mean(eng.time_kernel(0, layer=l, iters=20) for l in range(dims.dec_layers))
     eng.release(slots)
     eng.set_active([])
-    bytes_per_launch = S * 2 * 1500 * dims.d_model * 2
+    rows = sum(1 for s in slots if s % eng.decode_groups == 0)     # decode group 0's rows
+    bytes_per_launch = rows * 2 * 1500 * dims.d_model * 2
     achieved = bytes_per_launch / (ms / 1000.0) / 1e9
     return {"kernel": "cross_attn_kernel (decode K6)", "bound": "hbm", "achieved": achieved,
             "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,

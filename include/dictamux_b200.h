@@ -76,6 +76,8 @@ typedef struct dm_whisper_config {
   int max_slots;          /* concurrent decode slots (<= 64) */
   int max_encode_batch;   /* segments per dm_whisper_encode call */
   int num_pages;          /* self-KV pages of 64 tokens in the pool */
+  int decode_groups;      /* independent decode groups (slot s -> group s % G), each with its
+                             own step graph and stream; <= 0 means 1 */
 } dm_whisper_config;
 
 /* Weight offsets (elements into the bf16 blob), in this order:
@@ -112,7 +114,7 @@ DM_API int dm_whisper_read(void* handle, int32_t* done, int32_t* n_gen, int32_t*
 /* Debug/parity taps (synchronous copies to host):
  *  which = 0: encoder output of the last encode, [n, 1500, d] bf16 bits
  *  which = 1: log-mel of the last encode, [n, n_mels, 3000] fp32
- *  which = 2: logits of the last step, [max_slots, vocab] fp32 (enable first)
+ *  which = 2: logits of the last step, [64 rows of decode group 0, vocab] fp32 (enable first)
  *  which = 3: enable the logits tap (bytes ignored)
  *  which = 4: run only the first `bytes` encoder layers in later encodes
  *  which = 5: fp32 residual stream before the final LN, [n, 1500, d]

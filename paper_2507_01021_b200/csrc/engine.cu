@@ -187,6 +187,21 @@ struct WhisperEngine {
   cudaGraph_t step_graph = nullptr;
   int gemv_counter_base = 0, xattn_counter_base = 0;
   std::vector<TcGemvMaps> maps;   // [Ld * 6 + 1]: per layer qkv,o,xq,xo,fc1,fc2; LM head
+  // Independent decode groups (slot s belongs to group s % G): each has its own
+  // row-space activations, active list, scratch, step graph and stream, so the
+  // groups' latency-bound kernel chains overlap on the GPU.
+  struct Group {
+    DecodeState st{};
+    std::vector<TcGemvMaps> maps;
+    int32_t* active_dev = nullptr;
+    int32_t* n_active_dev = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+  };
+  std::vector<Group> groups;
+  cudaEvent_t step_start = nullptr;
   CUtensorMap kv_map, xkv_map;    // self-KV pool / cross-KV cache as [rows, 64] bf16
   // telemetry: kernels launched (graph nodes counted per replay)
   long long launches = 0, steps = 0, encodes = 0, segments = 0;
@@ -205,8 +220,14 @@ struct WhisperEngine {
   }
 
   ~WhisperEngine() {
-    if (step_exec) cudaGraphExecDestroy(step_exec);
-    if (step_graph) cudaGraphDestroy(step_graph);
+    for (auto& g : groups) {
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+      if (g.graph) cudaGraphDestroy(g.graph);
+      if (g.stream) cudaStreamDestroy(g.stream);
+      if (g.done) cudaEventDestroy(g.done);
+    }
+    if (step_start) cudaEventDestroy(step_start);
+
     if (cap_stream) cudaStreamDestroy(cap_stream);
     for (void* p : allocs) cudaFree(p);
     if (slot_host) cudaFreeHost(slot_host);
@@ -256,7 +277,7 @@ static int engine_init(WhisperEngine* e) {
   if (e->alloc_t(&e->enc_out, rows * d, false)) return 2;
   if (e->alloc_t(&e->slot_dev, E)) return 2;
   DM_CHECK_CUDA(cudaMallocHost(&e->slot_host, sizeof(int32_t) * E));
-  DM_CHECK_CUDA(cudaMallocHost(&e->staging, sizeof(int32_t) * (4 * 64 * 8 + 4096)));
+  DM_CHECK_CUDA(cudaMallocHost(&e->staging, sizeof(int32_t) * (64 * 65 + 4096 + 256)));
 
   // decode state
   DecodeState& st = e->st;
@@ -289,53 +310,73 @@ static int engine_init(WhisperEngine* e) {
   uint16_t* xkv = nullptr;
   if (e->alloc_t(&xkv, size_t(e->Ld) * S * 2 * e->H * 1500 * 64)) return 2;
   st.xkv = xkv;
-  if (e->alloc_t(&st.x, size_t(kRows) * d)) return 2;
-  if (e->alloc_t(&st.xh, size_t(kRows) * d)) return 2;
-  if (e->alloc_t(&st.xl, size_t(kRows) * d)) return 2;
-  if (e->alloc_t(&st.q, size_t(kRows) * d)) return 2;
-  if (e->alloc_t(&st.ah, size_t(kRows) * d)) return 2;
-  if (e->alloc_t(&st.al, size_t(kRows) * d)) return 2;
-  if (e->alloc_t(&st.hh, size_t(kRows) * e->F)) return 2;
-  if (e->alloc_t(&st.hl, size_t(kRows) * e->F)) return 2;
-  // cross-attention key splits: enough CTAs to cover the chip at full batch
-  st.xsplits = 1;
-  while (S * e->H * st.xsplits < 4 * kNumSMs && st.xsplits < 8) st.xsplits *= 2;
-  // split-K partial scratch: max over projection shapes and cross-attn partials
-  size_t part = size_t(kRows) * e->H * st.xsplits * 66;
-  const int shapes[4][2] = {{3 * d, d}, {d, d}, {e->F, d}, {d, e->F}};
-  for (auto& sh : shapes) part = std::max(part, tc_gemv_part_floats(sh[0], sh[1]));
-  if (e->alloc_t(&st.part, part)) return 2;
+  const int G = std::max(1, std::min(c.decode_groups > 0 ? c.decode_groups : 1, S));
+  const int Sg = ceil_div(S, G);
+  e->groups.resize(G);
+  const int tiles = ceil_div(c.vocab, 128);
+  for (int gi = 0; gi < G; ++gi) {
+    WhisperEngine::Group& gr = e->groups[gi];
+    DecodeState& gs = gr.st;
+    gs = st;                                   // shared slot-indexed state
+    if (e->alloc_t(&gr.active_dev, kRows)) return 2;
+    if (e->alloc_t(&gr.n_active_dev, 1)) return 2;
+    gs.active = gr.active_dev; gs.n_active = gr.n_active_dev;
+    if (e->alloc_t(&gs.x, size_t(kRows) * d)) return 2;
+    if (e->alloc_t(&gs.xh, size_t(kRows) * d)) return 2;
+    if (e->alloc_t(&gs.xl, size_t(kRows) * d)) return 2;
+    if (e->alloc_t(&gs.q, size_t(kRows) * d)) return 2;
+    if (e->alloc_t(&gs.ah, size_t(kRows) * d)) return 2;
+    if (e->alloc_t(&gs.al, size_t(kRows) * d)) return 2;
+    if (e->alloc_t(&gs.hh, size_t(kRows) * e->F)) return 2;
+    if (e->alloc_t(&gs.hl, size_t(kRows) * e->F)) return 2;
+    // cross-attention key splits: enough CTAs to cover the chip at full group batch
+    gs.xsplits = 1;
+    while (Sg * e->H * gs.xsplits < 4 * kNumSMs && gs.xsplits < 8) gs.xsplits *= 2;
+    size_t part = size_t(kRows) * e->H * gs.xsplits * 66;
+    const int shapes[4][2] = {{3 * d, d}, {d, d}, {e->F, d}, {d, e->F}};
+    for (auto& sh : shapes) part = std::max(part, tc_gemv_part_floats(sh[0], sh[1]));
+    if (e->alloc_t(&gs.part, part)) return 2;
+    if (e->alloc_t(&gs.counters, 4096 + size_t(kRows) * e->H)) return 2;
+    if (e->alloc_t(&gs.amax_val, size_t(tiles) * kRows)) return 2;
+    if (e->alloc_t(&gs.amax_idx, size_t(tiles) * kRows)) return 2;
+    gs.logits_dbg = nullptr;
+    // TMA maps of every decoder projection (weights [N, K] + this group's hi/lo inputs)
+    auto mk = [&](TcGemvMaps& m, int wi, int N, int K, const uint16_t* xh, const uint16_t* xl) {
+      if (make_tmap_2d(&m.w, e->W(wi), K, N, uint64_t(K) * 2, 64, 128)) return 2;
+      if (make_tmap_2d(&m.xh, xh, K, kRows, uint64_t(K) * 2, 64, kRows)) return 2;
+      if (make_tmap_2d(&m.xl, xl, K, kRows, uint64_t(K) * 2, 64, kRows)) return 2;
+      return 0;
+    };
+    gr.maps.resize(size_t(e->Ld) * 6 + 1);
+    for (int l = 0; l < e->Ld; ++l) {
+      const int b0 = e->dec_layer_base(l);
+      TcGemvMaps* m = &gr.maps[size_t(l) * 6];
+      if (mk(m[0], b0 + 2, 3 * d, d, gs.xh, gs.xl)) return 2;        // qkv
+      if (mk(m[1], b0 + 4, d, d, gs.ah, gs.al)) return 2;            // o
+      if (mk(m[2], b0 + 8, d, d, gs.xh, gs.xl)) return 2;            // xq
+      if (mk(m[3], b0 + 10, d, d, gs.ah, gs.al)) return 2;           // xo
+      if (mk(m[4], b0 + 14, e->F, d, gs.xh, gs.xl)) return 2;        // fc1
+      if (mk(m[5], b0 + 16, d, e->F, gs.hh, gs.hl)) return 2;        // fc2
+    }
+    if (mk(gr.maps.back(), e->after_enc() + 2, c.vocab, d, gs.xh, gs.xl)) return 2;  // LM head
+    DM_CHECK_CUDA(cudaStreamCreateWithFlags(&gr.stream, cudaStreamNonBlocking));
+    DM_CHECK_CUDA(cudaEventCreateWithFlags(&gr.done, cudaEventDisableTiming));
+  }
+  DM_CHECK_CUDA(cudaEventCreateWithFlags(&e->step_start, cudaEventDisableTiming));
   e->gemv_counter_base = 0;
   e->xattn_counter_base = 4096;
-  if (e->alloc_t(&st.counters, 4096 + size_t(kRows) * e->H)) return 2;
-  const int tiles = ceil_div(c.vocab, 128);
-  if (e->alloc_t(&st.amax_val, size_t(tiles) * kRows)) return 2;
-  if (e->alloc_t(&st.amax_idx, size_t(tiles) * kRows)) return 2;
-  // TMA maps of every decoder projection (weights [N, K] + hi/lo inputs)
-  auto mk = [&](TcGemvMaps& m, int wi, int N, int K, const uint16_t* xh, const uint16_t* xl) {
-    if (make_tmap_2d(&m.w, e->W(wi), K, N, uint64_t(K) * 2, 64, 128)) return 2;
-    if (make_tmap_2d(&m.xh, xh, K, kRows, uint64_t(K) * 2, 64, kRows)) return 2;
-    if (make_tmap_2d(&m.xl, xl, K, kRows, uint64_t(K) * 2, 64, kRows)) return 2;
-    return 0;
-  };
-  e->maps.resize(size_t(e->Ld) * 6 + 1);
-  for (int l = 0; l < e->Ld; ++l) {
-    const int b0 = e->dec_layer_base(l);
-    TcGemvMaps* m = &e->maps[size_t(l) * 6];
-    if (mk(m[0], b0 + 2, 3 * d, d, st.xh, st.xl)) return 2;        // qkv
-    if (mk(m[1], b0 + 4, d, d, st.ah, st.al)) return 2;            // o
-    if (mk(m[2], b0 + 8, d, d, st.xh, st.xl)) return 2;            // xq
-    if (mk(m[3], b0 + 10, d, d, st.ah, st.al)) return 2;           // xo
-    if (mk(m[4], b0 + 14, e->F, d, st.xh, st.xl)) return 2;        // fc1
-    if (mk(m[5], b0 + 16, d, e->F, st.hh, st.hl)) return 2;        // fc2
+  {
+    // group 0 doubles as the engine's default state (debug / timing probes)
+    DecodeState shared = st;
+    st = e->groups[0].st;
+    e->maps = e->groups[0].maps;
+    (void)shared;
   }
-  if (mk(e->maps.back(), e->after_enc() + 2, c.vocab, d, st.xh, st.xl)) return 2;   // LM head
   if (make_tmap_2d(&e->kv_map, st.kv_pool, 64, uint64_t(c.num_pages) * e->Ld * 2 * e->H * 64, 128,
                    64, 64))
     return 2;
   if (make_tmap_2d(&e->xkv_map, st.xkv, 64, uint64_t(e->Ld) * S * 2 * e->H * 1500, 128, 64, 64))
     return 2;
-  st.logits_dbg = nullptr;
   DM_CHECK_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
   DM_CHECK_CUDA(cudaDeviceSynchronize());
   return 0;
@@ -429,8 +470,8 @@ static int launch_pdl_floor(cudaStream_t s) {
   return 0;
 }
 
-static int record_step(WhisperEngine* e, cudaStream_t s) {
-  DecodeState& st = e->st;
+static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t s) {
+  DecodeState& st = grp.st;
   const int d = e->d;
   const int a = e->after_enc();
   const uint16_t* embed = e->W(a + 2);
@@ -438,7 +479,7 @@ static int record_step(WhisperEngine* e, cudaStream_t s) {
   if (int rc = launch_embed(st, embed, pos_emb, s)) return rc;
   for (int l = 0; l < e->Ld; ++l) {
     const int b0 = e->dec_layer_base(l);
-    const TcGemvMaps* m = &e->maps[size_t(l) * 6];
+    const TcGemvMaps* m = &grp.maps[size_t(l) * 6];
     auto gv = [&](const TcGemvMaps& mp, int wi, int N, int K, int epi, float scale, float* y,
                   uint16_t* yh, uint16_t* yl) {
       TcGemvArgs g{};
@@ -465,32 +506,35 @@ static int record_step(WhisperEngine* e, cudaStream_t s) {
     TcGemvArgs g{};
     g.bias = nullptr; g.N = e->cfg.vocab; g.K = d; g.epi = TV_ARGMAX; g.scale = 1.f;
     g.splits = 1; g.counter_base = e->gemv_counter_base;
-    if (int rc = launch_tc_gemv(st, e->maps.back(), g, s)) return rc;
+    if (int rc = launch_tc_gemv(st, grp.maps.back(), g, s)) return rc;
   }
   if (int rc = launch_finalize(st, s)) return rc;
   return 0;
 }
 
 static int build_step_graph(WhisperEngine* e) {
-  if (e->step_exec) {
-    cudaGraphExecDestroy(e->step_exec);
-    e->step_exec = nullptr;
+  for (auto& grp : e->groups) {
+    if (grp.exec) {
+      cudaGraphExecDestroy(grp.exec);
+      grp.exec = nullptr;
+    }
+    if (grp.graph) {
+      cudaGraphDestroy(grp.graph);
+      grp.graph = nullptr;
+    }
+    DM_CHECK_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = record_step(e, grp, e->cap_stream);
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    DM_CHECK_CUDA(ce);
+    grp.graph = g;
+    DM_CHECK_CUDA(cudaGraphInstantiate(&grp.exec, g, 0));
   }
-  if (e->step_graph) {
-    cudaGraphDestroy(e->step_graph);
-    e->step_graph = nullptr;
-  }
-  DM_CHECK_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
-  int rc = record_step(e, e->cap_stream);
-  cudaGraph_t g = nullptr;
-  cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &g);
-  if (rc) {
-    if (g) cudaGraphDestroy(g);
-    return rc;
-  }
-  DM_CHECK_CUDA(ce);
-  e->step_graph = g;
-  DM_CHECK_CUDA(cudaGraphInstantiate(&e->step_exec, g, 0));
+  e->step_exec = e->groups[0].exec;     // marks "built"
   return 0;
 }
 
@@ -666,16 +710,24 @@ int dm_whisper_set_active(void* handle, const int32_t* slot_ids, int n, void* st
   DM_REQUIRE(n >= 0 && n <= e->cfg.max_slots, "bad n");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   DM_CHECK_CUDA(cudaStreamSynchronize(s));
-  e->staging[0] = n;
+  const int G = int(e->groups.size());
+  // staging layout per group: [count, slots...] at stride kRows + 1
+  for (int g = 0; g < G; ++g) e->staging[g * (kRows + 1)] = 0;
   for (int i = 0; i < n; ++i) {
     DM_REQUIRE(slot_ids[i] >= 0 && slot_ids[i] < e->cfg.max_slots, "slot id out of range");
-    e->staging[1 + i] = slot_ids[i];
+    const int g = slot_ids[i] % G;
+    int32_t* row = e->staging + g * (kRows + 1);
+    DM_REQUIRE(row[0] < kRows, "too many active slots in one decode group");
+    row[1 + row[0]++] = slot_ids[i];
   }
-  DM_CHECK_CUDA(cudaMemcpyAsync(e->n_active_dev, e->staging, sizeof(int32_t),
-                                cudaMemcpyHostToDevice, s));
-  if (n)
-    DM_CHECK_CUDA(cudaMemcpyAsync(e->active_dev, e->staging + 1, sizeof(int32_t) * n,
+  for (int g = 0; g < G; ++g) {
+    int32_t* row = e->staging + g * (kRows + 1);
+    DM_CHECK_CUDA(cudaMemcpyAsync(e->groups[g].n_active_dev, row, sizeof(int32_t),
                                   cudaMemcpyHostToDevice, s));
+    if (row[0])
+      DM_CHECK_CUDA(cudaMemcpyAsync(e->groups[g].active_dev, row + 1, sizeof(int32_t) * row[0],
+                                    cudaMemcpyHostToDevice, s));
+  }
   DM_CHECK_CUDA(cudaStreamSynchronize(s));
   return 0;
 }
@@ -686,7 +738,17 @@ int dm_whisper_step(void* handle, int n_steps, void* stream) {
   if (!e->step_exec)
     if (int rc = build_step_graph(e)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(e->step_exec, s));
+  if (e->groups.size() == 1) {
+    for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(e->groups[0].exec, s));
+  } else {
+    DM_CHECK_CUDA(cudaEventRecord(e->step_start, s));
+    for (auto& grp : e->groups) {
+      DM_CHECK_CUDA(cudaStreamWaitEvent(grp.stream, e->step_start, 0));
+      for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(grp.exec, grp.stream));
+      DM_CHECK_CUDA(cudaEventRecord(grp.done, grp.stream));
+    }
+    for (auto& grp : e->groups) DM_CHECK_CUDA(cudaStreamWaitEvent(s, grp.done, 0));
+  }
   e->steps += n_steps;
   e->launches += (long long)n_steps * e->step_kernels();
   return 0;
@@ -800,7 +862,8 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
     case 3: {
       if (!e->st.logits_dbg) {
         if (e->alloc_t(&e->st.logits_dbg, size_t(kRows) * e->cfg.vocab)) return 2;
-        if (int rc = build_step_graph(e)) return rc;   // re-capture with the tap
+        e->groups[0].st.logits_dbg = e->st.logits_dbg;    // tap: decode group 0 rows
+        if (int rc = build_step_graph(e)) return rc;      // re-capture with the tap
       }
       return 0;
     }

@@ -99,7 +99,8 @@ class WhisperGPU:
     def __init__(self, dims: WhisperDims, *, seed: int = 0, init_std: float = 0.02,
                  device: int | str | torch.device = 0, max_slots: int = 64,
                  max_encode_batch: int = 32, num_pages: int | None = None,
-                 eot: int | None = None, steps_per_poll: int = 8):
+                 eot: int | None = None, steps_per_poll: int = 8,
+                 decode_groups: int | None = None):
         if not torch.cuda.is_available():
             raise _native.DmError("no CUDA device: the B200 engine has no CPU fallback")
         self.dims = dims
@@ -123,6 +124,10 @@ class WhisperGPU:
             cfg.prompt_len = len(dims.prompt)
             cfg.max_slots, cfg.max_encode_batch = max_slots, max_encode_batch
             cfg.num_pages = num_pages if num_pages is not None else max_slots * 7
+            if decode_groups is None:
+                decode_groups = 2 if max_slots >= 16 else 1
+            cfg.decode_groups = decode_groups
+            self.decode_groups = decode_groups
             arr = (C.c_int64 * len(offs))(*offs)
             h = C.c_void_p()
             _native.check(self.lib.dm_whisper_create(C.byref(cfg), C.c_void_p(self.blob.data_ptr()),

@@ -71,10 +71,11 @@ def test_decoder_logits_match_oracle(tiny_pair):
     orc, gpu = tiny_pair
     from oracle.logmel import log_mel_batch
     segs = _segments(2, [6.0, 15.0], seed=4)
-    gpu.debug(3)                                  # enable the logits tap
-    gpu.encode(segs, [0, 1])
-    gpu.admit([0, 1], [8, 8])
-    gpu.set_active([0, 1])
+    gpu.debug(3)                                  # enable the logits tap (decode group 0)
+    slots = [0, gpu.decode_groups]                # two slots of decode group 0 -> rows 0, 1
+    gpu.encode(segs, slots)
+    gpu.admit(slots, [8, 8])
+    gpu.set_active(slots)
     enc = orc.encode(log_mel_batch(segs, 80))
     logits = np.empty((gpu.max_slots, WHISPER_TINY.vocab), np.float32)
     prompt = list(WHISPER_TINY.prompt)
@@ -87,7 +88,7 @@ def test_decoder_logits_match_oracle(tiny_pair):
             ref = orc.decoder_logits(torch.tensor([fed]), enc[b:b + 1])[0, -1].numpy()
             err = np.abs(logits[b] - ref).max()
             assert err <= 2e-2, (step, b, err)
-    gpu.release([0, 1])
+    gpu.release(slots)
     gpu.set_active([])
 
 
