@@ -125,7 +125,7 @@ class WhisperGPU:
             cfg.max_slots, cfg.max_encode_batch = max_slots, max_encode_batch
             cfg.num_pages = num_pages if num_pages is not None else max_slots * 7
             if decode_groups is None:
-                decode_groups = 2 if max_slots >= 16 else 1
+                decode_groups = 1
             cfg.decode_groups = decode_groups
             self.decode_groups = decode_groups
             arr = (C.c_int64 * len(offs))(*offs)

@@ -23,7 +23,7 @@ def tiny_pair(native_lib):
     from oracle.whisper import WhisperOracle
     from paper_2507_01021_b200.engine import WhisperGPU
     orc = WhisperOracle(WHISPER_TINY, seed=0)
-    gpu = WhisperGPU(WHISPER_TINY, seed=0, max_slots=16, max_encode_batch=8)
+    gpu = WhisperGPU(WHISPER_TINY, seed=0, max_slots=16, max_encode_batch=8, decode_groups=2)
     return orc, gpu
 
 
@@ -84,7 +84,7 @@ def test_decoder_logits_match_oracle(tiny_pair):
         gpu.debug(2, logits)
         _, ngen, toks = gpu.read(tokens=True)
         for b in range(2):
-            fed = prompt[:min(step + 1, 4)] + toks[b, :max(0, step - 3)].tolist()
+            fed = prompt[:min(step + 1, 4)] + toks[slots[b], :max(0, step - 3)].tolist()
             ref = orc.decoder_logits(torch.tensor([fed]), enc[b:b + 1])[0, -1].numpy()
             err = np.abs(logits[b] - ref).max()
             assert err <= 2e-2, (step, b, err)
