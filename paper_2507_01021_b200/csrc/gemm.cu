@@ -18,7 +18,8 @@ namespace dm {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kGemmThreads = 192;   // w0 TMA, w1 MMA + TMEM alloc, w2..5 epilogue
+constexpr int kGemmThreads = 320;   // w0 TMA, w1 MMA + TMEM alloc, w2..9 epilogue
+constexpr int kEpiWarps = 8;        // two warpgroups, each drains half of the tile's columns
 
 __device__ __forceinline__ void tma_load_4d(void* smem_dst, const CUtensorMap* m,
                                             uint64_t* bar, int c0, int c1, int c2,
@@ -244,7 +245,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tmem_full[s], 1);
-      mbar_init(&tmem_empty[s], 4);      // one arrive per epilogue warp
+      mbar_init(&tmem_empty[s], kEpiWarps);   // one arrive per epilogue warp
     }
     fence_barrier_init();
   }
@@ -314,8 +315,10 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
       }
     }
   } else {
-    // ---------------- epilogue warps (2..5): TMEM lane quadrant = warp % 4
+    // ---------------- epilogue warps (2..9): TMEM lane quadrant = warp % 4,
+    // column half = (warp - 2) / 4
     const int quad = warp & 3;
+    const int chalf = (warp - 2) >> 2;
     int it = 0;
     for (int tile = blockIdx.x; tile < geo.tiles; tile += gridDim.x, ++it) {
       const int nt = tile % geo.NT;
@@ -328,7 +331,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
       const int t = mt * kBM + quad * 32 + lane;
       const int row_valid = t < g.T;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = chalf * (BN / 2); c < (chalf + 1) * (BN / 2); c += 32) {
         const int n0 = nt * BN + c;
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(quad * 32) << 16) + as * BN + c, r);
