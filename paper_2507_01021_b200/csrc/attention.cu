@@ -1,9 +1,10 @@
 // K4: encoder self-attention (non-causal, 1500 x 1500 x 64 per head) on
-// tcgen05. One CTA per (128-query tile, segment*head). Warp roles:
-//   w0: TMA producer (Q once, then K / V^T tiles through a 2-stage ring)
-//   w1: MMA issuer (S_j = Q K_j^T into a double-buffered TMEM tile,
-//       PV_j = P_j V_j into a double-buffered 64-column TMEM tile)
-//   w2..5: softmax, one query row per thread (TMEM lane = row): row max /
+// tcgen05. One CTA per (two 128-query tiles, segment*head). Warp roles:
+//   w0: TMA producer (both Q tiles once, then K / V^T tiles through a 2-stage ring)
+//   w1: MMA issuer (S_t = Q_t K_j^T into TMEM, PV_t = P_t V_j into TMEM,
+//       alternating between the two query tiles t)
+//   w2..9: softmax, two warpgroups (one per query tile), one query row per
+//       thread (TMEM lane = row): row max (3-input FMNMX) /
 //       exp2 / row sum entirely in registers (no shuffles), P_j written as
 //       bf16 straight into the 128B-swizzled K-major smem layout the next MMA
 //       reads, PV_j folded into a register accumulator with the online-softmax
@@ -16,7 +17,7 @@
 
 namespace dm {
 
-constexpr int kAttnThreads = 192;
+constexpr int kAttnThreads = 320;    // w0 TMA, w1 MMA, w2..5 softmax tile A, w6..9 tile B
 constexpr int kAttnKS = 2;           // K/V ring depth
 constexpr int kQBytes = 128 * 128;   // 128 rows x 64 bf16
 constexpr int kKBytes = 128 * 128;
@@ -24,14 +25,29 @@ constexpr int kVBytes = 2 * 64 * 128;  // two 64-key boxes of [64 dims x 64 keys
 constexpr int kPBytes = 2 * 128 * 128; // two 64-key column blocks of [128 rows x 64 keys]
 
 struct AttnSmemLayout {
-  static constexpr int q = 0;
-  static constexpr int k = q + kQBytes;
+  static constexpr int q = 0;                          // [2 tiles]
+  static constexpr int k = q + 2 * kQBytes;
   static constexpr int v = k + kAttnKS * kKBytes;
-  static constexpr int p = v + kAttnKS * kVBytes;
+  static constexpr int p = v + kAttnKS * kVBytes;      // [2 tiles]
   static constexpr int bars = p + 2 * kPBytes;
   static constexpr int total = bars + 256 + 1024;
 };
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float ex2(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// One CTA per (pair of 128-query tiles, segment*head). The two tiles share
+// every K/V tile; each has its own S (128 TMEM cols), O (64 cols) and P (smem)
+// and its own softmax warpgroup, so the tensor core works on one tile while
+// the other tile's softmax runs.
 __global__ void __launch_bounds__(kAttnThreads, 1)
 attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
@@ -45,18 +61,18 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;            // [KS]
   uint64_t* kv_empty = kv_full + kAttnKS;  // [KS]
-  uint64_t* s_full = kv_empty + kAttnKS;   // [2]
-  uint64_t* s_empty = s_full + 2;          // [2]
-  uint64_t* p_full = s_empty + 2;          // [2]
-  uint64_t* o_full = p_full + 2;           // [2]
-  uint64_t* o_empty = o_full + 2;          // [2]
+  uint64_t* s_full = kv_empty + kAttnKS;   // [2 tiles]
+  uint64_t* s_empty = s_full + 2;          // [2 tiles]
+  uint64_t* p_full = s_empty + 2;          // [2 tiles]
+  uint64_t* o_full = p_full + 2;           // [2 tiles]
+  uint64_t* o_empty = o_full + 2;          // [2 tiles]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int qt = blockIdx.x, bh = blockIdx.y;
+  const int qp = blockIdx.x, bh = blockIdx.y;
   // per-segment valid length (variable-length CTC batches); whisper: all 1500
   const int T = seg_len ? seg_len[bh / heads] : T_rows;
-  if (qt * 128 >= T) return;
+  if (qp * 256 >= T) return;
   const int nb = ceil_div(T, 128);
 
   if (warp == 0 && lane == 0) {
@@ -79,11 +95,13 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // TMEM columns: S tile t at 128 t, O tile t at 256 + 64 t
 
   if (warp == 0) {
     if (elect_one()) {
-      mbar_arrive_expect_tx(q_full, kQBytes);
-      tma_load_2d(smem + AttnSmemLayout::q, &tm_q, q_full, 0, bh * t_pad + qt * 128);
+      mbar_arrive_expect_tx(q_full, 2 * kQBytes);
+      tma_load_2d(smem + AttnSmemLayout::q, &tm_q, q_full, 0, bh * t_pad + qp * 256);
+      tma_load_2d(smem + AttnSmemLayout::q + kQBytes, &tm_q, q_full, 0, bh * t_pad + qp * 256 + 128);
       for (int j = 0; j < nb; ++j) {
         const int st = j % kAttnKS;
         mbar_wait(&kv_empty[st], ((j / kAttnKS) & 1) ^ 1);
@@ -98,62 +116,66 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
   } else if (warp == 1) {
     constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128);
     constexpr uint32_t idesc_o = umma_idesc_bf16(128, 64);
-    const uint32_t sq = smem_u32(smem + AttnSmemLayout::q);
     mbar_wait(q_full, 0);
-    auto issue_pv = [&](int j) {
-      const int pb = j & 1, st = j % kAttnKS;
-      mbar_wait(&p_full[pb], (j >> 1) & 1);
-      mbar_wait(&o_empty[pb], ((j >> 1) & 1) ^ 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sp = smem_u32(smem + AttnSmemLayout::p + pb * kPBytes);
-        const uint32_t sv = smem_u32(smem + AttnSmemLayout::v + st * kVBytes);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t a = sp + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-          const uint32_t bb = sv + (kk >> 2) * (64 * 128) + (kk & 3) * 32;
-          umma_bf16_ss(tmem + 256 + pb * 64, umma_desc_sw128(a), umma_desc_sw128(bb), idesc_o,
-                       kk != 0);
-        }
-        umma_commit(&o_full[pb]);
-        umma_commit(&kv_empty[st]);
-      }
-      __syncwarp();
-    };
     for (int j = 0; j < nb; ++j) {
-      const int st = j % kAttnKS, sb = j & 1;
+      const int st = j % kAttnKS;
+      const uint32_t ph = j & 1;
       mbar_wait(&kv_full[st], (j / kAttnKS) & 1);
-      mbar_wait(&s_empty[sb], ((j >> 1) & 1) ^ 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sk = smem_u32(smem + AttnSmemLayout::k + st * kKBytes);
+      const uint32_t sk = smem_u32(smem + AttnSmemLayout::k + st * kKBytes);
+      const uint32_t sv = smem_u32(smem + AttnSmemLayout::v + st * kVBytes);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_bf16_ss(tmem + sb * 128, umma_desc_sw128(sq + kk * 32),
-                       umma_desc_sw128(sk + kk * 32), idesc_s, kk != 0);
-        umma_commit(&s_full[sb]);
+      for (int t = 0; t < 2; ++t) {          // S_t = Q_t K_j^T
+        mbar_wait(&s_empty[t], ph ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sq = smem_u32(smem + AttnSmemLayout::q + t * kQBytes);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_bf16_ss(tmem + t * 128, umma_desc_sw128(sq + kk * 32),
+                         umma_desc_sw128(sk + kk * 32), idesc_s, kk != 0);
+          umma_commit(&s_full[t]);
+        }
+        __syncwarp();
       }
-      __syncwarp();
-      if (j >= 1) issue_pv(j - 1);
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {          // PV_t = P_t V_j
+        mbar_wait(&p_full[t], ph);
+        mbar_wait(&o_empty[t], ph ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sp = smem_u32(smem + AttnSmemLayout::p + t * kPBytes);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t a = sp + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+            const uint32_t bb = sv + (kk >> 2) * (64 * 128) + (kk & 3) * 32;
+            umma_bf16_ss(tmem + 256 + t * 64, umma_desc_sw128(a), umma_desc_sw128(bb), idesc_o,
+                         kk != 0);
+          }
+          umma_commit(&o_full[t]);
+          if (t == 1) umma_commit(&kv_empty[st]);
+        }
+        __syncwarp();
+      }
     }
-    issue_pv(nb - 1);
   } else {
+    const int t = (warp - 2) >> 2;                        // query tile of this warpgroup
     const int quad = warp & 3;
     const int r = quad * 32 + lane;                       // query row in tile
     const uint32_t lane_off = uint32_t(quad * 32) << 16;
+    const uint32_t s_col = t * 128, o_col = 256 + t * 64;
     constexpr float kLog2e = 1.4426950408889634f;
     float m_run = -INFINITY, l_run = 0.f, alpha_prev = 0.f;
     float o[64];
 #pragma unroll
     for (int i = 0; i < 64; ++i) o[i] = 0.f;
+    uint8_t* prow = smem + AttnSmemLayout::p + t * kPBytes + r * 128;
     auto fold_pv = [&](int j) {
-      const int ob = j & 1;
-      mbar_wait(&o_full[ob], (j >> 1) & 1);
+      mbar_wait(&o_full[t], j & 1);
       tc_fence_after();
       uint32_t pv[32];
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        tmem_ld32(tmem + lane_off + 256 + ob * 64 + c * 32, pv);
+        tmem_ld32(tmem + lane_off + o_col + c * 32, pv);
         tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 32; ++i)
@@ -161,43 +183,63 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[ob]);
+      if (lane == 0) mbar_arrive(&o_empty[t]);
     };
     for (int j = 0; j < nb; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&s_full[sb], (j >> 1) & 1);
+      mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
-      const int kvalid = T - j * 128;                    // keys valid in this block
-      // pass 1: row max
-      float mx = m_run;
+      const int kvalid = T - j * 128;                     // < 128 only on the tail block
       uint32_t sr[32];
+      // pass 1: row max (3-input max)
+      float mx = m_run;
+      if (kvalid >= 128) {
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        tmem_ld32(tmem + lane_off + sb * 128 + c * 32, sr);
-        tmem_wait_ld();
+        for (int c = 0; c < 4; ++c) {
+          tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
+          tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c * 32 + i < kvalid) mx = fmaxf(mx, __uint_as_float(sr[i]));
+          for (int i = 0; i < 32; i += 2)
+            mx = fmax3(mx, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i < kvalid) mx = fmaxf(mx, __uint_as_float(sr[i]));
+        }
       }
-      const float alpha = exp2f((m_run - mx) * kLog2e);
+      const float alpha = ex2((m_run - mx) * kLog2e);
       const float mscaled = mx * kLog2e;
-      // pass 2: p = exp(s - m), row sum, bf16 P into swizzled smem
+      // the previous PV must have consumed P before it is overwritten
+      if (j >= 1) fold_pv(j - 1);
+      // pass 2: p = exp2(s log2e - m log2e), row sum, bf16 P into swizzled smem
       float rs = 0.f;
-      uint8_t* prow = smem + AttnSmemLayout::p + sb * kPBytes + r * 128;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
-        tmem_ld32(tmem + lane_off + sb * 128 + c * 32, sr);
+        tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
         tmem_wait_ld();
         uint32_t pk[16];
+        if (kvalid >= 128) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          float p0 = (c * 32 + 2 * i < kvalid)
-                         ? exp2f(fmaf(__uint_as_float(sr[2 * i]), kLog2e, -mscaled)) : 0.f;
-          float p1 = (c * 32 + 2 * i + 1 < kvalid)
-                         ? exp2f(fmaf(__uint_as_float(sr[2 * i + 1]), kLog2e, -mscaled)) : 0.f;
-          pk[i] = pack_bf16x2(p0, p1);
-          // normalise with the same (bf16-rounded) weights the PV MMA uses
-          rs += __uint_as_float(pk[i] << 16) + __uint_as_float(pk[i] & 0xFFFF0000u);
+          for (int i = 0; i < 16; ++i) {
+            const float p0 = ex2(fmaf(__uint_as_float(sr[2 * i]), kLog2e, -mscaled));
+            const float p1 = ex2(fmaf(__uint_as_float(sr[2 * i + 1]), kLog2e, -mscaled));
+            rs += p0 + p1;
+            pk[i] = pack_bf16x2(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float p0 = (c * 32 + 2 * i < kvalid)
+                                 ? ex2(fmaf(__uint_as_float(sr[2 * i]), kLog2e, -mscaled)) : 0.f;
+            const float p1 = (c * 32 + 2 * i + 1 < kvalid)
+                                 ? ex2(fmaf(__uint_as_float(sr[2 * i + 1]), kLog2e, -mscaled)) : 0.f;
+            rs += p0 + p1;
+            pk[i] = pack_bf16x2(p0, p1);
+          }
         }
         // 32 keys = 4 chunks of 16 B; block = c / 2, chunk-in-row = (c % 2) * 4 + u
 #pragma unroll
@@ -212,21 +254,20 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&s_empty[sb]);
-        mbar_arrive(&p_full[sb]);
+        mbar_arrive(&s_empty[t]);
+        mbar_arrive(&p_full[t]);
       }
       l_run = l_run * alpha + rs;
       m_run = mx;
-      if (j >= 1) fold_pv(j - 1);
       alpha_prev = alpha;
     }
     fold_pv(nb - 1);
     // normalise and store this query row
-    const int t = qt * 128 + r;
-    if (t < T) {
+    const int tq = qp * 256 + t * 128 + r;
+    if (tq < T) {
       const float inv = 1.0f / l_run;
       const int b = bh / heads, h = bh % heads;
-      uint4* dst = reinterpret_cast<uint4*>(out + (size_t(b) * T_rows + t) * ldo + h * 64);
+      uint4* dst = reinterpret_cast<uint4*>(out + (size_t(b) * T_rows + tq) * ldo + h * 64);
 #pragma unroll
       for (int i = 0; i < 8; ++i)
         dst[i] = make_uint4(pack_bf16x2(o[8 * i] * inv, o[8 * i + 1] * inv),
@@ -328,7 +369,7 @@ int launch_attention(const uint16_t* q, const uint16_t* k, const uint16_t* vt, i
                                        AttnSmemLayout::total));
     attr = true;
   }
-  dim3 grid(ceil_div(T, 128), n_seg * heads);
+  dim3 grid(ceil_div(T, 256), n_seg * heads);
   attn_tcgen05_kernel<<<grid, kAttnThreads, AttnSmemLayout::total, stream>>>(
       mq, mk, mv, T, t_pad, heads, out, ldo, seg_len);
   DM_CHECK_LAUNCH();
