@@ -78,6 +78,9 @@ typedef struct dm_whisper_config {
   int num_pages;          /* self-KV pages of 64 tokens in the pool */
   int decode_groups;      /* independent decode groups (slot s -> group s % G), each with its
                              own step graph and stream; <= 0 means 1 */
+  int persistent_decode;  /* 1: whole decode steps run in one persistent cooperative kernel
+                             (one CTA per SM, grid barriers between phases); 0: CUDA graph of
+                             per-phase kernels with programmatic dependent launch */
 } dm_whisper_config;
 
 /* Weight offsets (elements into the bf16 blob), in this order:

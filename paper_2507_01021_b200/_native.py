@@ -33,7 +33,8 @@ class WhisperConfigC(C.Structure):
                 ("n_mels", C.c_int), ("vocab", C.c_int), ("eot", C.c_int),
                 ("prompt", C.c_int * 8), ("prompt_len", C.c_int),
                 ("max_slots", C.c_int), ("max_encode_batch", C.c_int),
-                ("num_pages", C.c_int), ("decode_groups", C.c_int)]
+                ("num_pages", C.c_int), ("decode_groups", C.c_int),
+                ("persistent_decode", C.c_int)]
 
 
 class CtcConfigC(C.Structure):

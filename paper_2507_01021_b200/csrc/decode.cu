@@ -11,6 +11,8 @@
 
 #include "decode.cuh"
 
+#include <vector>
+
 namespace dm {
 
 // ============================================================ tcgen05 GEMV
@@ -446,7 +448,7 @@ __device__ __forceinline__ void warp_merge(float& m, float& l, float (&o)[64]) {
 constexpr int kDaWarps = 4;                    // compute warps (lane = key)
 constexpr int kDaThreads = (kDaWarps + 1) * 32; // + 1 TMA producer warp
 constexpr int kDaKeys = 128;                    // keys per stage (2 boxes of 64)
-constexpr int kDaStages = 2;
+constexpr int kDaStages = 3;
 constexpr int kDaBox = 64 * 128;                // 64 keys x 128 B
 constexpr int kDaStageBytes = 4 * kDaBox;       // K0 K1 V0 V1
 constexpr int kDaSmem = kDaStages * kDaStageBytes + 1024 + 2048;
@@ -722,6 +724,637 @@ __global__ void finalize_kernel(const DecodeState st) {
 
 int launch_finalize(const DecodeState& st, cudaStream_t stream) {
   DM_CHECK_CUDA(launch_pdl(finalize_kernel, dim3(kRows / 4), dim3(128), 0, stream, st));
+  return 0;
+}
+
+
+
+// ============================================================ persistent decode
+// One cooperative CTA per SM runs whole greedy decode steps: every phase of
+// the step (embed, per layer LN / QKV / self-attn / O / LN / cross-q /
+// cross-attn / cross-o / LN / fc1 / fc2, final LN, LM head, finalize) is a
+// list of work items spread over the CTAs, separated by grid barriers. This
+// removes the ~70 dependent kernel launches (and their TMEM allocation,
+// barrier setup and tail) per step; the TMA ring, the two TMEM accumulators
+// and all mbarriers persist across phases and steps. Per-item arithmetic is
+// identical to the standalone kernels above (same fixed reduction orders).
+constexpr int kMkThreads = 256;          // w0 TMA, w1 MMA, w4..7 epilogue / attention roles
+constexpr int kMkStages = 3;
+constexpr int kMkStage = 32768;          // GEMV: W 16K + Xh 8K + Xl 8K; attention: K0 K1 V0 V1
+constexpr int kMkTr = kRows * 129 * 4;   // argmax transpose
+constexpr int kMkSmem = kMkStages * kMkStage + kMkTr + 4096 + 1024;
+
+struct MkLayerW {
+  const uint16_t *ln1g, *ln1b, *qkvb, *ob, *ln2g, *ln2b, *xqb, *xob, *ln3g, *ln3b, *fc1b, *fc2b;
+};
+
+struct MkParams {
+  DecodeState st;
+  const TcGemvMaps* maps;          // device [Ld * 6 + 1]
+  const CUtensorMap* attn_maps;    // device [2]: self-KV pool, cross-KV cache
+  const MkLayerW* lw;              // device [Ld]
+  const uint16_t *lnfg, *lnfb, *embed, *pos_emb;
+  unsigned* gbar;                  // grid barrier counter, zero at launch
+  int n_steps;
+  int sp_qkv, sp_dd, sp_fc1, sp_fc2;
+};
+
+struct MkBars {
+  uint64_t full[kMkStages], empty[kMkStages];
+  uint64_t tm_full[2], tm_empty[2];
+  uint64_t afull[kMkStages], aempty[kMkStages];
+  uint32_t tmem;
+  int flag;
+};
+
+struct MkRing {
+  int p = 0, m = 0, mn = 0, en = 0, ap = 0, ac = 0;
+};
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+__device__ __forceinline__ void mk_grid_sync(unsigned* bar, unsigned& target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    target += gridDim.x;
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    long long spins = 0;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (++spins > (1ll << 30)) asm volatile("trap;");
+    } while (v < target);
+    __threadfence();                      // also invalidates this SM's L1
+  }
+  __syncthreads();
+}
+
+// LN of row r: fp32 x -> bf16 hi/lo (runtime d <= 1280)
+__device__ __forceinline__ void mk_ln_row(const DecodeState& st, int r, const uint16_t* g,
+                                          const uint16_t* b) {
+  const int lane = threadIdx.x % 32, d = st.d, n4 = d / 4;
+  const float4* xr = reinterpret_cast<const float4*>(st.x + size_t(r) * d);
+  float4 v[10];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    const int c = lane + 32 * k;
+    v[k] = c < n4 ? __ldcg(xr + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / d;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    const int c = lane + 32 * k;
+    if (c < n4) {
+      const float a0 = v[k].x - mean, a1 = v[k].y - mean, a2 = v[k].z - mean, a3 = v[k].w - mean;
+      q += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = rsqrtf(q / d + 1e-5f);
+  uint2* yh = reinterpret_cast<uint2*>(st.xh + size_t(r) * d);
+  uint2* yl = reinterpret_cast<uint2*>(st.xl + size_t(r) * d);
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    const int c = lane + 32 * k;
+    if (c < n4) {
+      const float o[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+      uint16_t hi[4], lo[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float val = (o[u] - mean) * rstd * bf16_to_f32(g[4 * c + u]) + bf16_to_f32(b[4 * c + u]);
+        split_hilo(val, hi[u], lo[u]);
+      }
+      yh[c] = make_uint2(uint32_t(hi[0]) | (uint32_t(hi[1]) << 16), uint32_t(hi[2]) | (uint32_t(hi[3]) << 16));
+      yl[c] = make_uint2(uint32_t(lo[0]) | (uint32_t(lo[1]) << 16), uint32_t(lo[2]) | (uint32_t(lo[3]) << 16));
+    }
+  }
+}
+
+__device__ __noinline__ void mk_ln_phase(const DecodeState& st, int R, const uint16_t* g,
+                                            const uint16_t* b) {
+  const int gw = blockIdx.x * (kMkThreads / 32) + threadIdx.x / 32;
+  for (int r = gw; r < R; r += gridDim.x * (kMkThreads / 32)) mk_ln_row(st, r, g, b);
+}
+
+__device__ __forceinline__ void mk_embed_phase(const MkParams& P, int R) {
+  const DecodeState& st = P.st;
+  const int gw = blockIdx.x * (kMkThreads / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int r = gw; r < R; r += gridDim.x * (kMkThreads / 32)) {
+    const int slot = st.active[r];
+    const int tok = __ldcg(st.cur_tok + slot), p = __ldcg(st.pos + slot);
+    for (int c = lane; c < st.d; c += 32)
+      st.x[size_t(r) * st.d + c] =
+          bf16_to_f32(P.embed[size_t(tok) * st.d + c]) + bf16_to_f32(P.pos_emb[size_t(p) * st.d + c]);
+  }
+}
+
+__device__ __forceinline__ void mk_finalize_phase(const DecodeState& st, int R) {
+  const int gw = blockIdx.x * (kMkThreads / 32) + threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tiles = ceil_div(st.vocab, 128);
+  for (int r = gw; r < R; r += gridDim.x * (kMkThreads / 32)) {
+    const int slot = st.active[r];
+    float best = -INFINITY;
+    int bidx = 0x7FFFFFFF;
+    for (int t = lane; t < tiles; t += 32) {
+      const float v = __ldcg(st.amax_val + size_t(t) * kRows + r);
+      const int id = __ldcg(st.amax_idx + size_t(t) * kRows + r);
+      if (v > best || (v == best && id < bidx)) { best = v; bidx = id; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const float ob = __shfl_xor_sync(0xffffffffu, best, off);
+      const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+      if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+    }
+    if (lane != 0 || __ldcg(st.done + slot)) continue;
+    const int p = __ldcg(st.pos + slot);
+    if (p + 1 < st.prompt_len) {
+      st.cur_tok[slot] = st.prompt[p + 1];
+      st.pos[slot] = p + 1;
+      continue;
+    }
+    if (bidx == st.eot) { st.done[slot] = 1; continue; }
+    const int g = __ldcg(st.n_gen + slot);
+    st.out_tokens[slot * 448 + g] = bidx;
+    st.n_gen[slot] = g + 1;
+    if (g + 1 >= __ldcg(st.cap + slot)) { st.done[slot] = 1; continue; }
+    st.cur_tok[slot] = bidx;
+    st.pos[slot] = p + 1;
+  }
+}
+
+template <int EPI, bool SPLIT>
+__device__ __noinline__ void mk_gemv(const DecodeState& st, const TcGemvMaps* maps, const TcGemvArgs& a,
+                        uint8_t* smem, MkBars& B, MkRing& rg, float* tr, long long* kvbase, int R) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tiles = ceil_div(a.N, 128), items = tiles * a.splits;
+  const int kb_per = (a.K / 64) / a.splits;
+  if (warp == 0) {
+    if (lane == 0) {
+      fence_proxy_async_global();          // activations written by generic stores
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int tile = item % tiles, split = item / tiles;
+        for (int i = 0; i < kb_per; ++i, ++rg.p) {
+          const int s = rg.p % kMkStages;
+          mbar_wait(&B.empty[s], ((rg.p / kMkStages) & 1) ^ 1);
+          uint8_t* base = smem + s * kMkStage;
+          mbar_arrive_expect_tx(&B.full[s], kMkStage);
+          const int kc = (split * kb_per + i) * 64;
+          tma_load_2d(base, &maps->w, &B.full[s], kc, tile * 128);
+          tma_load_2d(base + kTvWBytes, &maps->xh, &B.full[s], kc, 0);
+          tma_load_2d(base + kTvWBytes + kTvXBytes, &maps->xl, &B.full[s], kc, 0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = umma_idesc_bf16(128, kRows);
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++rg.mn) {
+      const int buf = rg.mn & 1;
+      mbar_wait(&B.tm_empty[buf], ((rg.mn >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = B.tmem + buf * 64;
+      for (int i = 0; i < kb_per; ++i, ++rg.m) {
+        const int s = rg.m % kMkStages;
+        mbar_wait(&B.full[s], (rg.m / kMkStages) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sw = smem_u32(smem + s * kMkStage);
+          const uint32_t sh = sw + kTvWBytes, sl = sh + kTvXBytes;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            umma_bf16_ss(d_tmem, umma_desc_sw128(sw + k * 32), umma_desc_sw128(sh + k * 32), idesc,
+                         (i | k) != 0);
+            umma_bf16_ss(d_tmem, umma_desc_sw128(sw + k * 32), umma_desc_sw128(sl + k * 32), idesc, 1);
+          }
+          umma_commit(&B.empty[s]);
+          if (i == kb_per - 1) umma_commit(&B.tm_full[buf]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    const int quad = warp & 3;
+    const int f = quad * 32 + lane;
+    const int et = threadIdx.x - 128;                  // 0..127
+    if (EPI == TV_QKV) {
+      if (et < kRows) {
+        long long off = -1;
+        if (et < R) {
+          const int slot = st.active[et];
+          const int p = __ldcg(st.pos + slot);
+          const int page = st.page_table[slot * st.pages_per_slot + p / st.page_tokens];
+          off = ((long long)(page * st.layers + a.layer) * 2 * st.heads * st.page_tokens +
+                 (p % st.page_tokens)) * 64;
+        }
+        kvbase[et] = off;
+      }
+      named_bar_sync(1, 128);
+    }
+    for (int item = blockIdx.x; item < items; item += gridDim.x, ++rg.en) {
+      const int tile = item % tiles, split = item / tiles;
+      const int n = tile * 128 + f;
+      const bool nvalid = n < a.N;
+      const float b = (nvalid && a.bias) ? bf16_to_f32(a.bias[n]) : 0.f;
+      const int buf = rg.en & 1;
+      mbar_wait(&B.tm_full[buf], (rg.en >> 1) & 1);
+      tc_fence_after();
+      float v0[32], v1[32];
+      {
+        uint32_t rr[32];
+        tmem_ld32(B.tmem + (uint32_t(quad * 32) << 16) + buf * 64, rr);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v0[i] = __uint_as_float(rr[i]);
+        tmem_ld32(B.tmem + (uint32_t(quad * 32) << 16) + buf * 64 + 32, rr);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v1[i] = __uint_as_float(rr[i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&B.tm_empty[buf]);
+      if (SPLIT) {
+        float* part = st.part;
+        const size_t base = (size_t(split) * tiles + tile) * kRows * 128;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          part[base + size_t(i) * 128 + f] = v0[i];
+          part[base + size_t(32 + i) * 128 + f] = v1[i];
+        }
+        __threadfence();
+        named_bar_sync(1, 128);
+        if (et == 0) {
+          const int prev = atomicAdd(&st.counters[a.counter_base + tile], 1);
+          B.flag = (prev == a.splits - 1);
+        }
+        named_bar_sync(1, 128);
+        const int last = B.flag;
+        named_bar_sync(1, 128);                      // flag consumed before the next item
+        if (!last) continue;
+        __threadfence();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) { v0[i] = 0.f; v1[i] = 0.f; }
+        for (int s = 0; s < a.splits; ++s) {
+          const float* ps = part + (size_t(s) * tiles + tile) * kRows * 128 + f;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            v0[i] += __ldcg(ps + size_t(i) * 128);
+            v1[i] += __ldcg(ps + size_t(32 + i) * 128);
+          }
+        }
+        if (et == 0) st.counters[a.counter_base + tile] = 0;
+      }
+      tv_epilogue32<EPI>(st, a, n, nvalid, b, 0, v0, kvbase, tr, f);
+      tv_epilogue32<EPI>(st, a, n, nvalid, b, 32, v1, kvbase, tr, f);
+      if (EPI == TV_ARGMAX) {
+        named_bar_sync(1, 128);
+        const int r = et >> 1, half = et & 1;
+        float best = -INFINITY;
+        int bidx = 0x7FFFFFFF;
+        const float* row = tr + r * 129 + half * 64;
+        for (int i = 0; i < 64; ++i) {
+          const float x = row[i];
+          if (x > best) { best = x; bidx = tile * 128 + half * 64 + i; }
+        }
+        const float ob = __shfl_xor_sync(0xffffffffu, best, 1);
+        const int oi = __shfl_xor_sync(0xffffffffu, bidx, 1);
+        if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+        if (half == 0) {
+          st.amax_val[size_t(tile) * kRows + r] = best;
+          st.amax_idx[size_t(tile) * kRows + r] = bidx;
+        }
+        named_bar_sync(1, 128);                      // tr reused by the next item
+      }
+    }
+  }
+}
+
+template <bool kCross>
+__device__ __noinline__ void mk_attn(const DecodeState& st, const CUtensorMap* tm, int layer, uint8_t* smem,
+                        MkBars& B, MkRing& rg, float* s_o, float* s_ml, int counter_base, int R) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int xs = kCross ? st.xsplits : 1;
+  const int items = R * st.heads * xs;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int r = item / (st.heads * xs), h = (item / xs) % st.heads, sp = item % xs;
+    const int slot = st.active[r];
+    int k0, k1;
+    if (kCross) {
+      const int per = ceil_div(ceil_div(1500, xs), kDaKeys) * kDaKeys;
+      k0 = sp * per;
+      k1 = min(1500, k0 + per);
+    } else {
+      k0 = 0;
+      k1 = __ldcg(st.pos + slot) + 1;
+    }
+    const int nchunks = k1 > k0 ? ceil_div(k1 - k0, kDaKeys) : 0;
+    if (warp == kDaWarps) {
+      if (lane == 0) {
+        fence_proxy_async_global();
+        const int* pt = st.page_table + slot * st.pages_per_slot;
+        for (int c = 0; c < nchunks; ++c, ++rg.ap) {
+          const int s = rg.ap % kMkStages;
+          mbar_wait(&B.aempty[s], ((rg.ap / kMkStages) & 1) ^ 1);
+          uint8_t* base = smem + s * kMkStage;
+          mbar_arrive_expect_tx(&B.afull[s], kDaStageBytes);
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            const int t = k0 + c * kDaKeys + half * 64;
+            int row_k, row_v;
+            if (kCross) {
+              row_k = (((layer * st.max_slots + slot) * 2 + 0) * st.heads + h) * 1500 + t;
+              row_v = row_k + st.heads * 1500;
+            } else {
+              const int page = pt[min(t / st.page_tokens, st.pages_per_slot - 1)];
+              row_k = (((page * st.layers + layer) * 2 + 0) * st.heads + h) * st.page_tokens;
+              row_v = row_k + st.heads * st.page_tokens;
+            }
+            tma_load_2d(base + half * kDaBox, tm, &B.afull[s], 0, row_k);
+            tma_load_2d(base + (2 + half) * kDaBox, tm, &B.afull[s], 0, row_v);
+          }
+        }
+      }
+      continue;
+    }
+    if (warp > kDaWarps) continue;
+    float q[64];
+    {
+      const float4* qp = reinterpret_cast<const float4*>(st.q + size_t(r) * st.d + h * 64);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        const float4 v = __ldcg(qp + c);
+        q[4 * c] = v.x; q[4 * c + 1] = v.y; q[4 * c + 2] = v.z; q[4 * c + 3] = v.w;
+      }
+    }
+    float m = -INFINITY, l = 0.f, o[64];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) o[i] = 0.f;
+    const int half = warp >> 1;
+    const int rr = (warp & 1) * 32 + lane;
+    const int sw = rr & 7;
+    for (int c = 0; c < nchunks; ++c, ++rg.ac) {
+      const int s = rg.ac % kMkStages;
+      mbar_wait(&B.afull[s], (rg.ac / kMkStages) & 1);
+      const int t = k0 + c * kDaKeys + warp * 32 + lane;
+      if (t < k1) {
+        const uint8_t* krow = smem + s * kMkStage + half * kDaBox + rr * 128;
+        const uint8_t* vrow = krow + 2 * kDaBox;
+        float sc = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 w = *reinterpret_cast<const uint4*>(krow + ((j ^ sw) << 4));
+          const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            sc = fmaf(q[8 * j + 2 * u], __uint_as_float(ws[u] << 16), sc);
+            sc = fmaf(q[8 * j + 2 * u + 1], __uint_as_float(ws[u] & 0xFFFF0000u), sc);
+          }
+        }
+        const float mn = fmaxf(m, sc);
+        const float corr = exp2f((m - mn) * kLog2e);
+        const float p = exp2f((sc - mn) * kLog2e);
+        l = l * corr + p;
+        m = mn;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 w = *reinterpret_cast<const uint4*>(vrow + ((j ^ sw) << 4));
+          const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            o[8 * j + 2 * u] = fmaf(o[8 * j + 2 * u], corr, p * __uint_as_float(ws[u] << 16));
+            o[8 * j + 2 * u + 1] =
+                fmaf(o[8 * j + 2 * u + 1], corr, p * __uint_as_float(ws[u] & 0xFFFF0000u));
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&B.aempty[s]);
+    }
+    warp_merge(m, l, o);
+    float mm, ll, o0, o1;
+    block_merge(m, l, o, s_o, s_ml, mm, ll, o0, o1);
+    if (!kCross || xs == 1) {
+      if (warp == 0) store_hilo2(st, r, h, lane, o0 / ll, o1 / ll);
+    } else {
+      float* part = st.part + ((size_t(r) * st.heads + h) * xs + sp) * 66;
+      if (warp == 0) {
+        part[2 + 2 * lane] = o0;
+        part[3 + 2 * lane] = o1;
+        if (lane == 0) { part[0] = mm; part[1] = ll; }
+        __threadfence();
+      }
+      named_bar_sync(1, kDaWarps * 32);
+      if (threadIdx.x == 0) {
+        const int prev = atomicAdd(&st.counters[counter_base + r * st.heads + h], 1);
+        B.flag = prev == xs - 1;
+      }
+      named_bar_sync(1, kDaWarps * 32);
+      if (B.flag && warp == 0) {
+        __threadfence();
+        const float* pb = st.part + (size_t(r) * st.heads + h) * xs * 66;
+        float gm = -INFINITY;
+        for (int s = 0; s < xs; ++s) gm = fmaxf(gm, __ldcg(pb + s * 66));
+        float gl = 0.f, g0 = 0.f, g1 = 0.f;
+        for (int s = 0; s < xs; ++s) {
+          const float ms = __ldcg(pb + s * 66);
+          const float fct = (ms == -INFINITY) ? 0.f : exp2f((ms - gm) * kLog2e);
+          gl += __ldcg(pb + s * 66 + 1) * fct;
+          g0 += __ldcg(pb + s * 66 + 2 + 2 * lane) * fct;
+          g1 += __ldcg(pb + s * 66 + 3 + 2 * lane) * fct;
+        }
+        store_hilo2(st, r, h, lane, g0 / gl, g1 / gl);
+        if (lane == 0) st.counters[counter_base + r * st.heads + h] = 0;
+      }
+    }
+    named_bar_sync(1, kDaWarps * 32);                // s_o / s_ml / flag reused next item
+  }
+}
+
+__global__ void __launch_bounds__(kMkThreads, 1) decode_mega_kernel(const MkParams P) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+  float* tr = reinterpret_cast<float*>(smem + kMkStages * kMkStage);
+  uint8_t* misc = smem + kMkStages * kMkStage + kMkTr;
+  MkBars& B = *reinterpret_cast<MkBars*>(misc);
+  long long* kvbase = reinterpret_cast<long long*>(misc + 512);
+  float* s_o = reinterpret_cast<float*>(misc + 1024);          // [4 * 64]
+  float* s_ml = s_o + 4 * 64;                                   // [8]
+  const DecodeState& st = P.st;
+  const int warp = threadIdx.x / 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMkStages; ++s) {
+      mbar_init(&B.full[s], 1);
+      mbar_init(&B.empty[s], 1);
+      mbar_init(&B.afull[s], 1);
+      mbar_init(&B.aempty[s], kDaWarps);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&B.tm_full[s], 1);
+      mbar_init(&B.tm_empty[s], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(&B.tmem, 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  MkRing rg;
+  unsigned target = 0;
+  const int R = min(*st.n_active, kRows);
+  const int d = st.d, F = st.ffn;
+  for (int step = 0; step < P.n_steps; ++step) {
+    mk_embed_phase(P, R);
+    mk_grid_sync(P.gbar, target);
+    for (int l = 0; l < st.layers; ++l) {
+      const MkLayerW& w = P.lw[l];
+      const TcGemvMaps* m = P.maps + size_t(l) * 6;
+      TcGemvArgs a{};
+      a.layer = l;
+      a.counter_base = 0;
+      mk_ln_phase(st, R, w.ln1g, w.ln1b);
+      mk_grid_sync(P.gbar, target);
+      a.bias = w.qkvb; a.N = 3 * d; a.K = d; a.scale = 0.125f; a.splits = P.sp_qkv;
+      if (a.splits > 1) mk_gemv<TV_QKV, true>(st, m + 0, a, smem, B, rg, tr, kvbase, R);
+      else mk_gemv<TV_QKV, false>(st, m + 0, a, smem, B, rg, tr, kvbase, R);
+      mk_grid_sync(P.gbar, target);
+      mk_attn<false>(st, &P.attn_maps[0], l, smem, B, rg, s_o, s_ml, 4096, R);
+      mk_grid_sync(P.gbar, target);
+      a.bias = w.ob; a.N = d; a.K = d; a.scale = 1.f; a.splits = P.sp_dd; a.y = st.x;
+      if (a.splits > 1) mk_gemv<TV_RESID, true>(st, m + 1, a, smem, B, rg, tr, kvbase, R);
+      else mk_gemv<TV_RESID, false>(st, m + 1, a, smem, B, rg, tr, kvbase, R);
+      mk_grid_sync(P.gbar, target);
+      mk_ln_phase(st, R, w.ln2g, w.ln2b);
+      mk_grid_sync(P.gbar, target);
+      a.bias = w.xqb; a.scale = 0.125f; a.y = st.q;
+      if (a.splits > 1) mk_gemv<TV_STORE, true>(st, m + 2, a, smem, B, rg, tr, kvbase, R);
+      else mk_gemv<TV_STORE, false>(st, m + 2, a, smem, B, rg, tr, kvbase, R);
+      mk_grid_sync(P.gbar, target);
+      mk_attn<true>(st, &P.attn_maps[1], l, smem, B, rg, s_o, s_ml, 4096, R);
+      mk_grid_sync(P.gbar, target);
+      a.bias = w.xob; a.scale = 1.f; a.y = st.x;
+      if (a.splits > 1) mk_gemv<TV_RESID, true>(st, m + 3, a, smem, B, rg, tr, kvbase, R);
+      else mk_gemv<TV_RESID, false>(st, m + 3, a, smem, B, rg, tr, kvbase, R);
+      mk_grid_sync(P.gbar, target);
+      mk_ln_phase(st, R, w.ln3g, w.ln3b);
+      mk_grid_sync(P.gbar, target);
+      a.bias = w.fc1b; a.N = F; a.K = d; a.splits = P.sp_fc1; a.yh = st.hh; a.yl = st.hl;
+      if (a.splits > 1) mk_gemv<TV_GELU_HILO, true>(st, m + 4, a, smem, B, rg, tr, kvbase, R);
+      else mk_gemv<TV_GELU_HILO, false>(st, m + 4, a, smem, B, rg, tr, kvbase, R);
+      mk_grid_sync(P.gbar, target);
+      a.bias = w.fc2b; a.N = d; a.K = F; a.splits = P.sp_fc2; a.y = st.x;
+      if (a.splits > 1) mk_gemv<TV_RESID, true>(st, m + 5, a, smem, B, rg, tr, kvbase, R);
+      else mk_gemv<TV_RESID, false>(st, m + 5, a, smem, B, rg, tr, kvbase, R);
+      mk_grid_sync(P.gbar, target);
+    }
+    mk_ln_phase(st, R, P.lnfg, P.lnfb);
+    mk_grid_sync(P.gbar, target);
+    {
+      TcGemvArgs a{};
+      a.N = st.vocab; a.K = d; a.scale = 1.f; a.splits = 1;
+      mk_gemv<TV_ARGMAX, false>(st, P.maps + size_t(st.layers) * 6, a, smem, B, rg, tr, kvbase, R);
+    }
+    mk_grid_sync(P.gbar, target);
+    mk_finalize_phase(st, R);
+    mk_grid_sync(P.gbar, target);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(B.tmem, 128);
+  }
+}
+
+int launch_decode_mega(const MkParams& P, cudaStream_t stream);
+
+// Host-side builder: device copies of the per-layer pointers and tensor maps.
+struct MkHost {
+  MkLayerW* lw = nullptr;
+  TcGemvMaps* maps = nullptr;
+  CUtensorMap* attn_maps = nullptr;
+  unsigned* gbar = nullptr;
+};
+
+int mk_setup(const DecodeState& st, const std::vector<TcGemvMaps>& maps, const CUtensorMap& kv_map,
+             const CUtensorMap& xkv_map, const std::vector<const uint16_t*>& layer_ptrs,
+             void** handle) {
+  auto* h = new MkHost();
+  const int L = st.layers;
+  std::vector<MkLayerW> lw(L);
+  for (int l = 0; l < L; ++l) {
+    const uint16_t* const* p = &layer_ptrs[size_t(l) * 12];
+    lw[l] = MkLayerW{p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7], p[8], p[9], p[10], p[11]};
+  }
+  DM_CHECK_CUDA(cudaMalloc(&h->lw, sizeof(MkLayerW) * L));
+  DM_CHECK_CUDA(cudaMemcpy(h->lw, lw.data(), sizeof(MkLayerW) * L, cudaMemcpyHostToDevice));
+  DM_CHECK_CUDA(cudaMalloc(&h->maps, sizeof(TcGemvMaps) * maps.size()));
+  DM_CHECK_CUDA(cudaMemcpy(h->maps, maps.data(), sizeof(TcGemvMaps) * maps.size(),
+                           cudaMemcpyHostToDevice));
+  CUtensorMap am[2] = {kv_map, xkv_map};
+  DM_CHECK_CUDA(cudaMalloc(&h->attn_maps, sizeof(am)));
+  DM_CHECK_CUDA(cudaMemcpy(h->attn_maps, am, sizeof(am), cudaMemcpyHostToDevice));
+  DM_CHECK_CUDA(cudaMalloc(&h->gbar, 256));
+  *handle = h;
+  return 0;
+}
+
+void mk_free(void* handle) {
+  auto* h = static_cast<MkHost*>(handle);
+  if (!h) return;
+  cudaFree(h->lw);
+  cudaFree(h->maps);
+  cudaFree(h->attn_maps);
+  cudaFree(h->gbar);
+  delete h;
+}
+
+int mk_launch(void* handle, const DecodeState& st, const uint16_t* lnfg, const uint16_t* lnfb,
+              const uint16_t* embed, const uint16_t* pos_emb, int n_steps, cudaStream_t stream) {
+  auto* h = static_cast<MkHost*>(handle);
+  MkParams P{};
+  P.st = st;
+  P.maps = h->maps;
+  P.attn_maps = h->attn_maps;
+  P.lw = h->lw;
+  P.lnfg = lnfg; P.lnfb = lnfb; P.embed = embed; P.pos_emb = pos_emb;
+  P.gbar = h->gbar;
+  P.n_steps = n_steps;
+  P.sp_qkv = tc_gemv_splits(3 * st.d, st.d);
+  P.sp_dd = tc_gemv_splits(st.d, st.d);
+  P.sp_fc1 = tc_gemv_splits(st.ffn, st.d);
+  P.sp_fc2 = tc_gemv_splits(st.d, st.ffn);
+  return launch_decode_mega(P, stream);
+}
+
+int launch_decode_mega(const MkParams& P, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    DM_CHECK_CUDA(cudaFuncSetAttribute(decode_mega_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kMkSmem));
+    attr = true;
+  }
+  DM_CHECK_CUDA(cudaMemsetAsync(P.gbar, 0, sizeof(unsigned), stream));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(kNumSMs);
+  cfg.blockDim = dim3(kMkThreads);
+  cfg.dynamicSmemBytes = kMkSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeCooperative;
+  attrs[0].val.cooperative = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  DM_CHECK_CUDA(cudaLaunchKernelEx(&cfg, decode_mega_kernel, P));
   return 0;
 }
 

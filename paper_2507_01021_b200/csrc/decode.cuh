@@ -11,6 +11,8 @@
 
 #include "common.cuh"
 
+#include <vector>
+
 namespace dm {
 
 constexpr int kRows = 64;          // max active slots = MMA N
@@ -89,5 +91,15 @@ int launch_self_attn(const DecodeState& st, const CUtensorMap& kv_map, int layer
 int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
                       int counter_base, cudaStream_t stream);
 int launch_finalize(const DecodeState& st, cudaStream_t stream);
+
+// Persistent decode (one cooperative CTA per SM runs n_steps whole steps).
+// layer_ptrs: per layer 12 pointers (ln1 g/b, qkv b, o b, ln2 g/b, xq b, xo b,
+// ln3 g/b, fc1 b, fc2 b).
+int mk_setup(const DecodeState& st, const std::vector<TcGemvMaps>& maps, const CUtensorMap& kv_map,
+             const CUtensorMap& xkv_map, const std::vector<const uint16_t*>& layer_ptrs,
+             void** handle);
+void mk_free(void* handle);
+int mk_launch(void* handle, const DecodeState& st, const uint16_t* lnfg, const uint16_t* lnfb,
+              const uint16_t* embed, const uint16_t* pos_emb, int n_steps, cudaStream_t stream);
 
 }  // namespace dm

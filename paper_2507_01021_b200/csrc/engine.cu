@@ -202,6 +202,7 @@ struct WhisperEngine {
   };
   std::vector<Group> groups;
   cudaEvent_t step_start = nullptr;
+  void* mega = nullptr;            // persistent decode state (cfg.persistent_decode)
   CUtensorMap kv_map, xkv_map;    // self-KV pool / cross-KV cache as [rows, 64] bf16
   // telemetry: kernels launched (graph nodes counted per replay)
   long long launches = 0, steps = 0, encodes = 0, segments = 0;
@@ -220,6 +221,7 @@ struct WhisperEngine {
   }
 
   ~WhisperEngine() {
+    if (mega) mk_free(mega);
     for (auto& g : groups) {
       if (g.exec) cudaGraphExecDestroy(g.exec);
       if (g.graph) cudaGraphDestroy(g.graph);
@@ -378,6 +380,16 @@ static int engine_init(WhisperEngine* e) {
   if (make_tmap_2d(&e->xkv_map, st.xkv, 64, uint64_t(e->Ld) * S * 2 * e->H * 1500, 128, 64, 64))
     return 2;
   DM_CHECK_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
+  if (c.persistent_decode) {
+    DM_REQUIRE(G == 1, "persistent decode runs one decode group");
+    std::vector<const uint16_t*> lp;
+    for (int l = 0; l < e->Ld; ++l) {
+      const int b0 = e->dec_layer_base(l);
+      const int idx[12] = {0, 1, 3, 5, 6, 7, 9, 11, 12, 13, 15, 17};
+      for (int j : idx) lp.push_back(e->W(b0 + j));
+    }
+    if (int rc = mk_setup(st, e->maps, e->kv_map, e->xkv_map, lp, &e->mega)) return rc;
+  }
   DM_CHECK_CUDA(cudaDeviceSynchronize());
   return 0;
 }
@@ -735,9 +747,18 @@ int dm_whisper_set_active(void* handle, const int32_t* slot_ids, int n, void* st
 int dm_whisper_step(void* handle, int n_steps, void* stream) {
   auto* e = static_cast<WhisperEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
-  if (!e->step_exec)
+  if (!e->mega && !e->step_exec)
     if (int rc = build_step_graph(e)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (e->mega) {
+    const int x = e->after_dec(), a = e->after_enc();
+    if (int rc = mk_launch(e->mega, e->st, e->W(x + 2), e->W(x + 3), e->W(a + 2), e->W(a + 3),
+                           n_steps, s))
+      return rc;
+    e->steps += n_steps;
+    e->launches += n_steps > 0 ? 2 : 0;
+    return 0;
+  }
   if (e->groups.size() == 1) {
     for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(e->groups[0].exec, s));
   } else {

@@ -10,9 +10,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--model", default="whisper-base")
 ap.add_argument("--slots", type=int, default=64)
 ap.add_argument("--encode-batch", type=int, default=32)
+ap.add_argument("--persistent", action="store_true")
 args = ap.parse_args()
 dims = get_model(args.model)
-eng = WhisperGPU(dims, max_slots=args.slots, max_encode_batch=args.encode_batch)
+eng = WhisperGPU(dims, max_slots=args.slots, max_encode_batch=args.encode_batch,
+                 persistent_decode=args.persistent)
 rng = np.random.default_rng(0)
 segs = [rng.integers(-8000, 8000, size=480000, dtype=np.int16) for _ in range(args.encode_batch)]
 ev = lambda: torch.cuda.Event(enable_timing=True)

@@ -108,3 +108,27 @@ def test_eot_releases_slot(native_lib):
     assert got == want
     assert got[0] == []
     gpu.close()
+
+
+@pytest.fixture(scope="module")
+def tiny_persistent(native_lib):
+    from paper_2507_01021_b200.engine import WhisperGPU
+    return WhisperGPU(WHISPER_TINY, seed=0, max_slots=16, max_encode_batch=8,
+                      persistent_decode=True)
+
+
+def test_persistent_decode_matches_graph_and_oracle(tiny_pair, tiny_persistent):
+    """The persistent decode kernel (whole steps in one cooperative launch)
+    yields exactly the graph path's tokens, which equal the oracle's."""
+    orc, gpu = tiny_pair
+    from oracle.logmel import log_mel_batch
+    segs = _segments(6, [4.0, 12.0, 7.5, 30.0, 3.0, 20.0], seed=7)
+    caps = [5, 20, 9, 31, 3, 25]
+    got_p = tiny_persistent.transcribe_ids(segs, caps)
+    got_g = gpu.transcribe_ids(segs, caps)
+    assert got_p == got_g
+    enc = orc.encode(log_mel_batch(segs, 80))
+    want = [orc.greedy(enc[b], c) for b, c in enumerate(caps)]
+    assert got_p == want
+    alone = [tiny_persistent.transcribe_ids([s], [c])[0] for s, c in zip(segs, caps)]
+    assert alone == got_p
