@@ -755,6 +755,7 @@ struct MkParams {
   const MkLayerW* lw;              // device [Ld]
   const uint16_t *lnfg, *lnfb, *embed, *pos_emb;
   unsigned* gbar;                  // grid barrier counter, zero at launch
+  unsigned long long* timing;      // optional: globaltimer at each barrier (block 0)
   int n_steps;
   int sp_qkv, sp_dd, sp_fc1, sp_fc2;
 };
@@ -775,7 +776,8 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-__device__ __forceinline__ void mk_grid_sync(unsigned* bar, unsigned& target) {
+__device__ __forceinline__ void mk_grid_sync(unsigned* bar, unsigned& target,
+                                             unsigned long long* timing = nullptr) {
   __syncthreads();
   if (threadIdx.x == 0) {
     target += gridDim.x;
@@ -788,6 +790,11 @@ __device__ __forceinline__ void mk_grid_sync(unsigned* bar, unsigned& target) {
       if (++spins > (1ll << 30)) asm volatile("trap;");
     } while (v < target);
     __threadfence();                      // also invalidates this SM's L1
+    if (timing && blockIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      timing[target / gridDim.x - 1] = t;
+    }
   }
   __syncthreads();
 }
@@ -1214,7 +1221,7 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mega_kernel(const MkPara
   const int d = st.d, F = st.ffn;
   for (int step = 0; step < P.n_steps; ++step) {
     mk_embed_phase(P, R);
-    mk_grid_sync(P.gbar, target);
+    mk_grid_sync(P.gbar, target, P.timing);
     for (int l = 0; l < st.layers; ++l) {
       const MkLayerW& w = P.lw[l];
       const TcGemvMaps* m = P.maps + size_t(l) * 6;
@@ -1222,50 +1229,50 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mega_kernel(const MkPara
       a.layer = l;
       a.counter_base = 0;
       mk_ln_phase(st, R, w.ln1g, w.ln1b);
-      mk_grid_sync(P.gbar, target);
+      mk_grid_sync(P.gbar, target, P.timing);
       a.bias = w.qkvb; a.N = 3 * d; a.K = d; a.scale = 0.125f; a.splits = P.sp_qkv;
       if (a.splits > 1) mk_gemv<TV_QKV, true>(st, m + 0, a, smem, B, rg, tr, kvbase, R);
       else mk_gemv<TV_QKV, false>(st, m + 0, a, smem, B, rg, tr, kvbase, R);
-      mk_grid_sync(P.gbar, target);
+      mk_grid_sync(P.gbar, target, P.timing);
       mk_attn<false>(st, &P.attn_maps[0], l, smem, B, rg, s_o, s_ml, 4096, R);
-      mk_grid_sync(P.gbar, target);
+      mk_grid_sync(P.gbar, target, P.timing);
       a.bias = w.ob; a.N = d; a.K = d; a.scale = 1.f; a.splits = P.sp_dd; a.y = st.x;
       if (a.splits > 1) mk_gemv<TV_RESID, true>(st, m + 1, a, smem, B, rg, tr, kvbase, R);
       else mk_gemv<TV_RESID, false>(st, m + 1, a, smem, B, rg, tr, kvbase, R);
-      mk_grid_sync(P.gbar, target);
+      mk_grid_sync(P.gbar, target, P.timing);
       mk_ln_phase(st, R, w.ln2g, w.ln2b);
-      mk_grid_sync(P.gbar, target);
+      mk_grid_sync(P.gbar, target, P.timing);
       a.bias = w.xqb; a.scale = 0.125f; a.y = st.q;
       if (a.splits > 1) mk_gemv<TV_STORE, true>(st, m + 2, a, smem, B, rg, tr, kvbase, R);
       else mk_gemv<TV_STORE, false>(st, m + 2, a, smem, B, rg, tr, kvbase, R);
-      mk_grid_sync(P.gbar, target);
+      mk_grid_sync(P.gbar, target, P.timing);
       mk_attn<true>(st, &P.attn_maps[1], l, smem, B, rg, s_o, s_ml, 4096, R);
-      mk_grid_sync(P.gbar, target);
+      mk_grid_sync(P.gbar, target, P.timing);
       a.bias = w.xob; a.scale = 1.f; a.y = st.x;
       if (a.splits > 1) mk_gemv<TV_RESID, true>(st, m + 3, a, smem, B, rg, tr, kvbase, R);
       else mk_gemv<TV_RESID, false>(st, m + 3, a, smem, B, rg, tr, kvbase, R);
-      mk_grid_sync(P.gbar, target);
+      mk_grid_sync(P.gbar, target, P.timing);
       mk_ln_phase(st, R, w.ln3g, w.ln3b);
-      mk_grid_sync(P.gbar, target);
+      mk_grid_sync(P.gbar, target, P.timing);
       a.bias = w.fc1b; a.N = F; a.K = d; a.splits = P.sp_fc1; a.yh = st.hh; a.yl = st.hl;
       if (a.splits > 1) mk_gemv<TV_GELU_HILO, true>(st, m + 4, a, smem, B, rg, tr, kvbase, R);
       else mk_gemv<TV_GELU_HILO, false>(st, m + 4, a, smem, B, rg, tr, kvbase, R);
-      mk_grid_sync(P.gbar, target);
+      mk_grid_sync(P.gbar, target, P.timing);
       a.bias = w.fc2b; a.N = d; a.K = F; a.splits = P.sp_fc2; a.y = st.x;
       if (a.splits > 1) mk_gemv<TV_RESID, true>(st, m + 5, a, smem, B, rg, tr, kvbase, R);
       else mk_gemv<TV_RESID, false>(st, m + 5, a, smem, B, rg, tr, kvbase, R);
-      mk_grid_sync(P.gbar, target);
+      mk_grid_sync(P.gbar, target, P.timing);
     }
     mk_ln_phase(st, R, P.lnfg, P.lnfb);
-    mk_grid_sync(P.gbar, target);
+    mk_grid_sync(P.gbar, target, P.timing);
     {
       TcGemvArgs a{};
       a.N = st.vocab; a.K = d; a.scale = 1.f; a.splits = 1;
       mk_gemv<TV_ARGMAX, false>(st, P.maps + size_t(st.layers) * 6, a, smem, B, rg, tr, kvbase, R);
     }
-    mk_grid_sync(P.gbar, target);
+    mk_grid_sync(P.gbar, target, P.timing);
     mk_finalize_phase(st, R);
-    mk_grid_sync(P.gbar, target);
+    mk_grid_sync(P.gbar, target, P.timing);
   }
   tc_fence_before();
   __syncthreads();
@@ -1319,7 +1326,8 @@ void mk_free(void* handle) {
 }
 
 int mk_launch(void* handle, const DecodeState& st, const uint16_t* lnfg, const uint16_t* lnfb,
-              const uint16_t* embed, const uint16_t* pos_emb, int n_steps, cudaStream_t stream) {
+              const uint16_t* embed, const uint16_t* pos_emb, int n_steps, cudaStream_t stream,
+              unsigned long long* timing) {
   auto* h = static_cast<MkHost*>(handle);
   MkParams P{};
   P.st = st;
@@ -1328,6 +1336,7 @@ int mk_launch(void* handle, const DecodeState& st, const uint16_t* lnfg, const u
   P.lw = h->lw;
   P.lnfg = lnfg; P.lnfb = lnfb; P.embed = embed; P.pos_emb = pos_emb;
   P.gbar = h->gbar;
+  P.timing = timing;
   P.n_steps = n_steps;
   P.sp_qkv = tc_gemv_splits(3 * st.d, st.d);
   P.sp_dd = tc_gemv_splits(st.d, st.d);

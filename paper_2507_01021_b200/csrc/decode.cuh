@@ -100,6 +100,7 @@ int mk_setup(const DecodeState& st, const std::vector<TcGemvMaps>& maps, const C
              void** handle);
 void mk_free(void* handle);
 int mk_launch(void* handle, const DecodeState& st, const uint16_t* lnfg, const uint16_t* lnfb,
-              const uint16_t* embed, const uint16_t* pos_emb, int n_steps, cudaStream_t stream);
+              const uint16_t* embed, const uint16_t* pos_emb, int n_steps, cudaStream_t stream,
+              unsigned long long* timing = nullptr);
 
 }  // namespace dm

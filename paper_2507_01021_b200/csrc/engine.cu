@@ -203,6 +203,7 @@ struct WhisperEngine {
   std::vector<Group> groups;
   cudaEvent_t step_start = nullptr;
   void* mega = nullptr;            // persistent decode state (cfg.persistent_decode)
+  unsigned long long* mk_timing = nullptr;   // debug: per-barrier globaltimer stamps
   CUtensorMap kv_map, xkv_map;    // self-KV pool / cross-KV cache as [rows, 64] bf16
   // telemetry: kernels launched (graph nodes counted per replay)
   long long launches = 0, steps = 0, encodes = 0, segments = 0;
@@ -753,7 +754,7 @@ int dm_whisper_step(void* handle, int n_steps, void* stream) {
   if (e->mega) {
     const int x = e->after_dec(), a = e->after_enc();
     if (int rc = mk_launch(e->mega, e->st, e->W(x + 2), e->W(x + 3), e->W(a + 2), e->W(a + 3),
-                           n_steps, s))
+                           n_steps, s, e->mk_timing))
       return rc;
     e->steps += n_steps;
     e->launches += n_steps > 0 ? 2 : 0;
@@ -890,6 +891,13 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
     }
     case 4: e->enc_stop = int(bytes); return 0;
     case 7: e->enc_tap = bytes != 0; return 0;
+    case 8:
+      if (!e->mk_timing && e->alloc_t(&e->mk_timing, 1 << 16)) return 2;
+      return 0;
+    case 9:
+      DM_REQUIRE(e->mk_timing != nullptr, "timing tap not enabled");
+      src = e->mk_timing; avail = size_t(8) << 16;
+      break;
     case 5: src = e->resid; avail = size_t(e->last_n) * 1500 * e->d * 4; break;
     case 6: src = e->attn_out; avail = size_t(e->last_n) * 1500 * e->d * 2; break;
     default: DM_REQUIRE(false, "unknown debug tap");
