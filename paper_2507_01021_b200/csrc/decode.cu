@@ -59,7 +59,7 @@ __device__ __forceinline__ void tv_epilogue32(const DecodeState& st, const TcGem
         float* __restrict__ y = a.y + n;
         float old[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) old[i] = y[size_t(r0 + i) * a.N];
+        for (int i = 0; i < 32; ++i) old[i] = __ldcg(y + size_t(r0 + i) * a.N);
 #pragma unroll
         for (int i = 0; i < 32; ++i) y[size_t(r0 + i) * a.N] = old[i] + (v[i] + b);
       }
@@ -778,18 +778,20 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 
 __device__ __forceinline__ void mk_grid_sync(unsigned* bar, unsigned& target,
                                              unsigned long long* timing = nullptr) {
+  // bar.sync orders the CTA's phase writes before thread 0's release-add
+  // (cumulative at gpu scope); thread 0's acquire-load + bar.sync orders every
+  // thread's next-phase reads after all CTAs' writes. Cross-CTA data is read
+  // with ld.global.cg or TMA (L2), never through a possibly stale L1 line.
   __syncthreads();
   if (threadIdx.x == 0) {
     target += gridDim.x;
-    __threadfence();
-    atomicAdd(bar, 1u);
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
     unsigned v;
     long long spins = 0;
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
       if (++spins > (1ll << 30)) asm volatile("trap;");
     } while (v < target);
-    __threadfence();                      // also invalidates this SM's L1
     if (timing && blockIdx.x == 0) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -253,8 +253,8 @@ class WhisperGPU:
         return self._done, self._ngen, self._tokens.reshape(self.max_slots, MAX_TOKENS)
 
     def debug(self, which: int, out: np.ndarray | None = None) -> np.ndarray | None:
-        if which == 3:
-            _native.check(self.lib.dm_whisper_debug(self.handle, 3, None, 0, self._s))
+        if which in (3, 8):
+            _native.check(self.lib.dm_whisper_debug(self.handle, which, None, 0, self._s))
             return None
         _native.check(self.lib.dm_whisper_debug(self.handle, which,
                                                 out.ctypes.data_as(C.c_void_p), out.nbytes,

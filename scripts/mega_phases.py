@@ -26,7 +26,7 @@ names = ["embed"] + [f"L{l}.{p}" for l in range(L) for p in ("ln1", "qkv", "self
 d = np.diff(ts[:2 * per_step].astype(np.int64)) / 1000.0
 step2 = d[per_step - 1: 2 * per_step - 1]
 agg = {}
-for n, v in zip(names[1:] + names[:1], step2):
+for n, v in zip(names, step2):
     k = n.split(".")[-1]
     agg[k] = agg.get(k, 0) + v
 print(json.dumps({"rows": rows, "step_us": float(step2.sum()), "by_phase_us": {k: round(v, 1) for k, v in agg.items()}}, indent=1))
