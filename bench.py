@@ -345,8 +345,16 @@ def measure_roofline(eng, dims, args) -> dict:
     rows = sum(1 for s in slots if s % eng.decode_groups == 0)     # decode group 0's rows
     bytes_per_launch = rows * 2 * 1500 * dims.d_model * 2
     achieved = bytes_per_launch / (ms / 1000.0) / 1e9
-    return {"kernel": "cross_attn_kernel (decode K6)", "bound": "hbm", "achieved": achieved,
-            "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+    traffic = None
+    tf = ROOT / "profiles" / "r01_xattn_traffic.json"
+    if tf.exists():     # dram read+write of one ncu --set full capture (64 rows), scaled to rows
+        t = _j.loads(tf.read_text())
+        traffic = (t["dram_bytes_read"] + t["dram_bytes_write"]) * rows / t["rows"]
+    return {"kernel": "dec_attn_kernel<cross> (decode K6)", "bound": "hbm", "achieved": achieved,
+            "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/r01_xattn_traffic.json)",
+            "timing": "CUDA events on the engine stream around a graph of 20 back-to-back launches "
+                      "per decoder layer at a full 64-row batch, after the timed region",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback",
             "bytes_per_launch": bytes_per_launch, "avg_launch_ms": ms,
             "per_unit": "2*1500*d*2 B per active slot per layer"}
