@@ -99,39 +99,61 @@ __device__ __forceinline__ void tv_epilogue32(const DecodeState& st, const TcGem
   }
 }
 
+// Persistent-over-N GEMV: CTA (c, split) owns N tiles c, c + gridDim.x, ...
+// for one K split. Its activation operand (all k-blocks of the split, hi and
+// lo, <= 128 KB) is loaded once; weight tiles stream through a 3-stage TMA
+// ring (the first stages are issued before griddepcontrol.wait: weights never
+// depend on the predecessor); accumulators alternate between two 64-column
+// TMEM buffers so the epilogue of tile i overlaps the MMAs of tile i + 1.
+constexpr int kTvWStages = 3;
+constexpr int kTvMaxKb = 8;
+__host__ __device__ constexpr int tv_smem_bytes(int kb, bool argmax) {
+  return kb * 2 * kTvXBytes + kTvWStages * kTvWBytes + (argmax ? kRows * 129 * 4 : 0) + 1024 + 1024;
+}
+
 template <int EPI, bool SPLIT>
-__global__ void __launch_bounds__(kTvThreads, 2)
+__global__ void __launch_bounds__(kTvThreads, 1)
 tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap txh,
                const __grid_constant__ CUtensorMap txl, const DecodeState st,
                const TcGemvArgs a) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTvStages * kTvStageBytes);
-  uint64_t* empty = full + kTvStages;
-  uint64_t* mma_done = empty + kTvStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mma_done + 1);
+  const int kb_per = (a.K / 64) / a.splits;
+  uint8_t* xs = smem;                                        // [kb][hi 8K | lo 8K]
+  uint8_t* ws = smem + kb_per * 2 * kTvXBytes;               // [stage] 16K
+  float* tr = reinterpret_cast<float*>(ws + kTvWStages * kTvWBytes);   // ARGMAX only
+  uint8_t* misc = reinterpret_cast<uint8_t*>(tr) + (EPI == TV_ARGMAX ? kRows * 129 * 4 : 0);
+  uint64_t* wfull = reinterpret_cast<uint64_t*>(misc);
+  uint64_t* wempty = wfull + kTvWStages;
+  uint64_t* xfull = wempty + kTvWStages;
+  uint64_t* tm_full = xfull + 1;                             // [2]
+  uint64_t* tm_empty = tm_full + 2;                          // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 2);
   int* is_last = reinterpret_cast<int*>(tmem_slot + 1);
-  long long* kvbase = reinterpret_cast<long long*>(smem + kTvStages * kTvStageBytes + 128);
+  long long* kvbase = reinterpret_cast<long long*>(misc + 256);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int tile = blockIdx.x, split = blockIdx.y;
-  const int tiles = gridDim.x;
-  const int kb_per = (a.K / 64) / a.splits;
+  const int split = blockIdx.y;
+  const int tiles = ceil_div(a.N, 128);
   const int kb0 = split * kb_per;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tw);
     tma_prefetch_desc(&txh);
     tma_prefetch_desc(&txl);
-    for (int s = 0; s < kTvStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < kTvWStages; ++s) {
+      mbar_init(&wfull[s], 1);
+      mbar_init(&wempty[s], 1);
     }
-    mbar_init(mma_done, 1);
+    mbar_init(xfull, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tm_full[s], 1);
+      mbar_init(&tm_empty[s], 4);
+    }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 64);
+  if (warp == 1) tmem_alloc(tmem_slot, 128);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -139,119 +161,132 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
 
   if (warp == 0) {
     if (elect_one()) {
-      // weights do not depend on the predecessor: start their stream first
-      const int pre = kb_per < kTvStages ? kb_per : kTvStages;
-      for (int i = 0; i < pre; ++i) {
-        uint8_t* base = smem + i * kTvStageBytes;
-        mbar_arrive_expect_tx(&full[i], kTvStageBytes);
-        tma_load_2d(base, &tw, &full[i], (kb0 + i) * 64, tile * 128);
-      }
+      // weight stream: independent of the predecessor kernel
+      int wi = 0;
+      auto issue_w = [&](int tile, int i) {
+        const int s = wi % kTvWStages;
+        mbar_wait(&wempty[s], ((wi / kTvWStages) & 1) ^ 1);
+        mbar_arrive_expect_tx(&wfull[s], kTvWBytes);
+        tma_load_2d(ws + s * kTvWBytes, &tw, &wfull[s], (kb0 + i) * 64, tile * 128);
+        ++wi;
+      };
+      const int total = ((tiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1) * kb_per;
+      const int pre = total < kTvWStages ? total : kTvWStages;
+      for (int q = 0; q < pre; ++q)
+        issue_w(blockIdx.x + (q / kb_per) * gridDim.x, q % kb_per);
       pdl_wait();
       pdl_trigger();
+      mbar_arrive_expect_tx(xfull, kb_per * 2 * kTvXBytes);
       for (int i = 0; i < kb_per; ++i) {
-        const int s = i % kTvStages;
-        uint8_t* base = smem + s * kTvStageBytes;
-        const int kc = (kb0 + i) * 64;
-        if (i >= pre) {
-          mbar_wait(&empty[s], ((i / kTvStages) & 1) ^ 1);
-          mbar_arrive_expect_tx(&full[s], kTvStageBytes);
-          tma_load_2d(base, &tw, &full[s], kc, tile * 128);
-        }
-        tma_load_2d(base + kTvWBytes, &txh, &full[s], kc, 0);
-        tma_load_2d(base + kTvWBytes + kTvXBytes, &txl, &full[s], kc, 0);
+        tma_load_2d(xs + i * 2 * kTvXBytes, &txh, xfull, (kb0 + i) * 64, 0);
+        tma_load_2d(xs + i * 2 * kTvXBytes + kTvXBytes, &txl, xfull, (kb0 + i) * 64, 0);
       }
+      for (int q = pre; q < total; ++q) issue_w(blockIdx.x + (q / kb_per) * gridDim.x, q % kb_per);
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = umma_idesc_bf16(128, kRows);
-    for (int i = 0; i < kb_per; ++i) {
-      const int s = i % kTvStages;
-      mbar_wait(&full[s], (i / kTvStages) & 1);
+    mbar_wait(xfull, 0);
+    int wi = 0, it = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+      const int buf = it & 1;
+      mbar_wait(&tm_empty[buf], ((it >> 1) & 1) ^ 1);
       tc_fence_after();
-      if (elect_one()) {
-        const uint32_t sw = smem_u32(smem + s * kTvStageBytes);
-        const uint32_t sh = sw + kTvWBytes, sl = sh + kTvXBytes;
+      for (int i = 0; i < kb_per; ++i, ++wi) {
+        const int s = wi % kTvWStages;
+        mbar_wait(&wfull[s], (wi / kTvWStages) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t sw = smem_u32(ws + s * kTvWBytes);
+          const uint32_t sh = smem_u32(xs + i * 2 * kTvXBytes), sl = sh + kTvXBytes;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          umma_bf16_ss(tmem, umma_desc_sw128(sw + k * 32), umma_desc_sw128(sh + k * 32), idesc,
-                       (i | k) != 0);
-          umma_bf16_ss(tmem, umma_desc_sw128(sw + k * 32), umma_desc_sw128(sl + k * 32), idesc, 1);
+          for (int k = 0; k < 4; ++k) {
+            umma_bf16_ss(tmem + buf * 64, umma_desc_sw128(sw + k * 32),
+                         umma_desc_sw128(sh + k * 32), idesc, (i | k) != 0);
+            umma_bf16_ss(tmem + buf * 64, umma_desc_sw128(sw + k * 32),
+                         umma_desc_sw128(sl + k * 32), idesc, 1);
+          }
+          umma_commit(&wempty[s]);
+          if (i == kb_per - 1) umma_commit(&tm_full[buf]);
         }
-        umma_commit(&empty[s]);
-        if (i == kb_per - 1) umma_commit(mma_done);
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else {
     const int quad = warp & 3;
     const int f = quad * 32 + lane;                // feature within the tile
-    const int n = tile * 128 + f;
-    const bool nvalid = n < a.N;
-    const float b = (nvalid && a.bias) ? bf16_to_f32(a.bias[n]) : 0.f;
     const int et = threadIdx.x - 64;               // 0..127 among epilogue threads
     pdl_wait();
-    if (EPI == TV_QKV && et < kRows) {
-      // per-row self-KV write base for this layer
-      const int r = et;
-      long long off = -1;
-      if (r < *st.n_active) {
-        const int slot = st.active[r];
-        const int p = st.pos[slot];
-        const int page = st.page_table[slot * st.pages_per_slot + p / st.page_tokens];
-        off = ((long long)(page * st.layers + a.layer) * 2 * st.heads * st.page_tokens +
-               (p % st.page_tokens)) * 64;
+    const int R = min(*st.n_active, kRows);
+    if (EPI == TV_QKV) {
+      if (et < kRows) {
+        long long off = -1;
+        if (et < R) {
+          const int slot = st.active[et];
+          const int p = st.pos[slot];
+          const int page = st.page_table[slot * st.pages_per_slot + p / st.page_tokens];
+          off = ((long long)(page * st.layers + a.layer) * 2 * st.heads * st.page_tokens +
+                 (p % st.page_tokens)) * 64;
+        }
+        kvbase[et] = off;
       }
-      kvbase[r] = off;
+      named_bar_sync(1, 128);
     }
-    mbar_wait(mma_done, 0);
-    tc_fence_after();
-    float* tr = reinterpret_cast<float*>(smem);    // ARGMAX transpose [kRows][129]
-    if (SPLIT) {
-      float* part = st.part;
-      const size_t base = (size_t(split) * tiles + tile) * kRows * 128;
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
+    int it = 0;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+      const int n = tile * 128 + f;
+      const bool nvalid = n < a.N;
+      const float b = (nvalid && a.bias) ? bf16_to_f32(a.bias[n]) : 0.f;
+      const int buf = it & 1;
+      mbar_wait(&tm_full[buf], (it >> 1) & 1);
+      tc_fence_after();
+      float v0[32], v1[32];
+      {
         uint32_t rr[32];
-        tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + c * 32, rr);
+        tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + buf * 64, rr);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) part[base + size_t(c * 32 + i) * 128 + f] = __uint_as_float(rr[i]);
+        for (int i = 0; i < 32; ++i) v0[i] = __uint_as_float(rr[i]);
+        tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + buf * 64 + 32, rr);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v1[i] = __uint_as_float(rr[i]);
       }
-      __threadfence();
-      named_bar_sync(1, 128);
-      if (et == 0) {
-        const int prev = atomicAdd(&st.counters[a.counter_base + tile], 1);
-        *is_last = (prev == a.splits - 1);
-      }
-      named_bar_sync(1, 128);
-      if (*is_last) {
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tm_empty[buf]);
+      if (SPLIT) {
+        float* part = st.part;
+        const size_t base = (size_t(split) * tiles + tile) * kRows * 128;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          part[base + size_t(i) * 128 + f] = v0[i];
+          part[base + size_t(32 + i) * 128 + f] = v1[i];
+        }
         __threadfence();
-#pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          float v[32];
+        named_bar_sync(1, 128);
+        if (et == 0) {
+          const int prev = atomicAdd(&st.counters[a.counter_base + tile], 1);
+          *is_last = (prev == a.splits - 1);
+        }
+        named_bar_sync(1, 128);
+        const int last = *is_last;
+        named_bar_sync(1, 128);
+        if (!last) continue;
+        __threadfence();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 0.f;
-#pragma unroll 1
-          for (int s = 0; s < a.splits; ++s) {
-            const float* ps = part + (size_t(s) * tiles + tile) * kRows * 128 + size_t(c * 32) * 128 + f;
+        for (int i = 0; i < 32; ++i) { v0[i] = 0.f; v1[i] = 0.f; }
+        for (int s = 0; s < a.splits; ++s) {
+          const float* ps = part + (size_t(s) * tiles + tile) * kRows * 128 + f;
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] += __ldcg(ps + size_t(i) * 128);
+          for (int i = 0; i < 32; ++i) {
+            v0[i] += __ldcg(ps + size_t(i) * 128);
+            v1[i] += __ldcg(ps + size_t(32 + i) * 128);
           }
-          tv_epilogue32<EPI>(st, a, n, nvalid, b, c * 32, v, kvbase, tr, f);
         }
         if (et == 0) st.counters[a.counter_base + tile] = 0;
       }
-    } else {
-      if (EPI == TV_QKV) named_bar_sync(1, 128);    // kvbase ready
-#pragma unroll 1
-      for (int c = 0; c < 2; ++c) {
-        uint32_t rr[32];
-        tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + c * 32, rr);
-        tmem_wait_ld();
-        float v[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(rr[i]);
-        tv_epilogue32<EPI>(st, a, n, nvalid, b, c * 32, v, kvbase, tr, f);
-      }
+      tv_epilogue32<EPI>(st, a, n, nvalid, b, 0, v0, kvbase, tr, f);
+      tv_epilogue32<EPI>(st, a, n, nvalid, b, 32, v1, kvbase, tr, f);
       if (EPI == TV_ARGMAX) {
         // per row: max over this tile's 128 vocabulary ids, ties -> lowest id
         named_bar_sync(1, 128);
@@ -270,6 +305,7 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           st.amax_val[size_t(tile) * kRows + r] = best;
           st.amax_idx[size_t(tile) * kRows + r] = bidx;
         }
+        named_bar_sync(1, 128);                    // tr reused by the next tile
       }
     }
   }
@@ -277,7 +313,7 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 64);
+    tmem_dealloc(tmem, 128);
   }
 }
 
@@ -299,15 +335,21 @@ size_t tc_gemv_part_floats(int N, int K) {
 template <int EPI, bool SPLIT>
 static int launch_tv(const DecodeState& st, const TcGemvMaps& maps, const TcGemvArgs& a,
                      cudaStream_t stream) {
+  const int kb_per = (a.K / 64) / a.splits;
+  DM_REQUIRE(kb_per <= kTvMaxKb, "decode GEMV: at most 8 k-blocks per split");
+  const int smem = tv_smem_bytes(kTvMaxKb, EPI == TV_ARGMAX);
   static bool attr = false;
   if (!attr) {
     DM_CHECK_CUDA(cudaFuncSetAttribute(tc_gemv_kernel<EPI, SPLIT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kTvSmem));
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
-  dim3 grid(ceil_div(a.N, 128), a.splits);
-  DM_CHECK_CUDA(launch_pdl(tc_gemv_kernel<EPI, SPLIT>, grid, dim3(kTvThreads), kTvSmem, stream,
-                           maps.w, maps.xh, maps.xl, st, a));
+  const int tiles = ceil_div(a.N, 128);
+  const int per_split = std::max(1, std::min(tiles, kNumSMs / a.splits));
+  dim3 grid(per_split, a.splits);
+  DM_CHECK_CUDA(launch_pdl(tc_gemv_kernel<EPI, SPLIT>, grid, dim3(kTvThreads),
+                           size_t(tv_smem_bytes(kb_per, EPI == TV_ARGMAX)), stream, maps.w,
+                           maps.xh, maps.xl, st, a));
   return 0;
 }
 
