@@ -32,13 +32,16 @@ __device__ __forceinline__ void split_hilo(float v, uint16_t& hi, uint16_t& lo) 
 template <int EPI>
 __device__ __forceinline__ void tv_epilogue32(const DecodeState& st, const TcGemvArgs& a, int n,
                                               bool nvalid, float b, int r0, const float (&v)[32],
-                                              const long long* kvbase, float* tr, int f) {
+                                              const long long* kvbase, float* tr, int f,
+                                              int R = kRows) {
+  if (EPI != TV_ARGMAX && r0 >= R) return;        // inactive rows: nothing to write
   switch (EPI) {
     case TV_STORE:
       if (nvalid) {
         float* __restrict__ y = a.y + n;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) y[size_t(r0 + i) * a.N] = (v[i] + b) * a.scale;
+        for (int i = 0; i < 32; ++i)
+          if (r0 + i < R) y[size_t(r0 + i) * a.N] = (v[i] + b) * a.scale;
       }
       break;
     case TV_GELU_HILO:
@@ -47,6 +50,7 @@ __device__ __forceinline__ void tv_epilogue32(const DecodeState& st, const TcGem
         uint16_t* __restrict__ yl = a.yl + n;
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
+          if (r0 + i >= R) continue;
           uint16_t hi, lo;
           split_hilo(gelu_erf(v[i] + b), hi, lo);
           yh[size_t(r0 + i) * a.N] = hi;
@@ -59,9 +63,10 @@ __device__ __forceinline__ void tv_epilogue32(const DecodeState& st, const TcGem
         float* __restrict__ y = a.y + n;
         float old[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) old[i] = __ldcg(y + size_t(r0 + i) * a.N);
+        for (int i = 0; i < 32; ++i) old[i] = r0 + i < R ? __ldcg(y + size_t(r0 + i) * a.N) : 0.f;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) y[size_t(r0 + i) * a.N] = old[i] + (v[i] + b);
+        for (int i = 0; i < 32; ++i)
+          if (r0 + i < R) y[size_t(r0 + i) * a.N] = old[i] + (v[i] + b);
       }
       break;
     case TV_QKV: {
@@ -70,7 +75,8 @@ __device__ __forceinline__ void tv_epilogue32(const DecodeState& st, const TcGem
       if (n < d) {
         float* __restrict__ q = st.q + n;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) q[size_t(r0 + i) * d] = (v[i] + b) * a.scale;
+        for (int i = 0; i < 32; ++i)
+          if (r0 + i < R) q[size_t(r0 + i) * d] = (v[i] + b) * a.scale;
       } else {
         const int kv = n < 2 * d ? 0 : 1;
         const int c = n - (kv + 1) * d;
@@ -109,6 +115,7 @@ constexpr int kTvWStages = 3;
 constexpr int kTvMaxKb = 8;
 __host__ __device__ constexpr int tv_smem_bytes(int kb, bool argmax) {
   return kb * 2 * kTvXBytes + kTvWStages * kTvWBytes + (argmax ? kRows * 129 * 4 : 0) + 1024 + 1024;
+  // (misc: barriers + flags at +0, kvbase[64] at +256)
 }
 
 template <int EPI, bool SPLIT>
@@ -129,9 +136,11 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   uint64_t* xfull = wempty + kTvWStages;
   uint64_t* tm_full = xfull + 1;                             // [2]
   uint64_t* tm_empty = tm_full + 2;                          // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 2);
+  uint64_t* xready = tm_empty + 2;                           // fused-LN operand written
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xready + 1);
   int* is_last = reinterpret_cast<int*>(tmem_slot + 1);
   long long* kvbase = reinterpret_cast<long long*>(misc + 256);
+  const bool fused_ln = a.ln_g != nullptr;
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int split = blockIdx.y;
@@ -147,6 +156,7 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       mbar_init(&wempty[s], 1);
     }
     mbar_init(xfull, 1);
+    mbar_init(xready, 4);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tm_full[s], 1);
       mbar_init(&tm_empty[s], 4);
@@ -176,16 +186,18 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         issue_w(blockIdx.x + (q / kb_per) * gridDim.x, q % kb_per);
       pdl_wait();
       pdl_trigger();
-      mbar_arrive_expect_tx(xfull, kb_per * 2 * kTvXBytes);
-      for (int i = 0; i < kb_per; ++i) {
-        tma_load_2d(xs + i * 2 * kTvXBytes, &txh, xfull, (kb0 + i) * 64, 0);
-        tma_load_2d(xs + i * 2 * kTvXBytes + kTvXBytes, &txl, xfull, (kb0 + i) * 64, 0);
+      if (!fused_ln) {
+        mbar_arrive_expect_tx(xfull, kb_per * 2 * kTvXBytes);
+        for (int i = 0; i < kb_per; ++i) {
+          tma_load_2d(xs + i * 2 * kTvXBytes, &txh, xfull, (kb0 + i) * 64, 0);
+          tma_load_2d(xs + i * 2 * kTvXBytes + kTvXBytes, &txl, xfull, (kb0 + i) * 64, 0);
+        }
       }
       for (int q = pre; q < total; ++q) issue_w(blockIdx.x + (q / kb_per) * gridDim.x, q % kb_per);
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = umma_idesc_bf16(128, kRows);
-    mbar_wait(xfull, 0);
+    mbar_wait(fused_ln ? xready : xfull, 0);
     int wi = 0, it = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
       const int buf = it & 1;
@@ -217,6 +229,74 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     const int et = threadIdx.x - 64;               // 0..127 among epilogue threads
     pdl_wait();
     const int R = min(*st.n_active, kRows);
+    if (fused_ln) {
+      // LayerNorm of the 64 rows (warp per row), written as bf16 hi/lo straight
+      // into the 128B-swizzled K-major operand tiles of this CTA's K range.
+      const int K = a.K, nchunk = K / 8;          // 16-byte chunks of 8 bf16 per row
+      const int c_lo = kb0 * 8, c_hi = (kb0 + kb_per) * 8;
+      for (int r = quad; r < kRows; r += 4) {
+        float4 v[2 * 5];                           // up to 1280 / 256 = 5 chunks per lane
+        const float4* xr = reinterpret_cast<const float4*>(a.ln_x + size_t(r) * K);
+        float s = 0.f;
+#pragma unroll
+        for (int m = 0; m < 5; ++m) {
+          const int ci = lane + 32 * m;
+          if (ci < nchunk && r < R) {
+            v[2 * m] = __ldcg(xr + 2 * ci);
+            v[2 * m + 1] = __ldcg(xr + 2 * ci + 1);
+          } else {
+            v[2 * m] = v[2 * m + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          s += (v[2 * m].x + v[2 * m].y) + (v[2 * m].z + v[2 * m].w) +
+               (v[2 * m + 1].x + v[2 * m + 1].y) + (v[2 * m + 1].z + v[2 * m + 1].w);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const float mean = s / K;
+        float q = 0.f;
+#pragma unroll
+        for (int m = 0; m < 5; ++m) {
+          const int ci = lane + 32 * m;
+          if (ci < nchunk) {
+            const float e[8] = {v[2 * m].x, v[2 * m].y, v[2 * m].z, v[2 * m].w,
+                                v[2 * m + 1].x, v[2 * m + 1].y, v[2 * m + 1].z, v[2 * m + 1].w};
+#pragma unroll
+            for (int u = 0; u < 8; ++u) q += (e[u] - mean) * (e[u] - mean);
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+        const float rstd = rsqrtf(q / K + 1e-5f);
+#pragma unroll
+        for (int m = 0; m < 5; ++m) {
+          const int ci = lane + 32 * m;
+          if (ci < c_lo || ci >= c_hi || ci >= nchunk) continue;
+          const float e[8] = {v[2 * m].x, v[2 * m].y, v[2 * m].z, v[2 * m].w,
+                              v[2 * m + 1].x, v[2 * m + 1].y, v[2 * m + 1].z, v[2 * m + 1].w};
+          const uint4 gw = __ldg(reinterpret_cast<const uint4*>(a.ln_g) + ci);
+          const uint4 bw = __ldg(reinterpret_cast<const uint4*>(a.ln_b) + ci);
+          const uint32_t gs[4] = {gw.x, gw.y, gw.z, gw.w}, bs[4] = {bw.x, bw.y, bw.z, bw.w};
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint16_t h0, l0, h1, l1;
+            split_hilo((e[2 * u] - mean) * rstd * __uint_as_float(gs[u] << 16) +
+                           __uint_as_float(bs[u] << 16), h0, l0);
+            split_hilo((e[2 * u + 1] - mean) * rstd * __uint_as_float(gs[u] & 0xFFFF0000u) +
+                           __uint_as_float(bs[u] & 0xFFFF0000u), h1, l1);
+            hi[u] = uint32_t(h0) | (uint32_t(h1) << 16);
+            lo[u] = uint32_t(l0) | (uint32_t(l1) << 16);
+          }
+          const int kb = ci / 8 - kb0, j = ci % 8;
+          uint8_t* tile = xs + kb * 2 * kTvXBytes + r * 128 + ((j ^ (r & 7)) << 4);
+          *reinterpret_cast<uint4*>(tile) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+          *reinterpret_cast<uint4*>(tile + kTvXBytes) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(xready);
+    }
     if (EPI == TV_QKV) {
       if (et < kRows) {
         long long off = -1;
@@ -285,8 +365,8 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         }
         if (et == 0) st.counters[a.counter_base + tile] = 0;
       }
-      tv_epilogue32<EPI>(st, a, n, nvalid, b, 0, v0, kvbase, tr, f);
-      tv_epilogue32<EPI>(st, a, n, nvalid, b, 32, v1, kvbase, tr, f);
+      tv_epilogue32<EPI>(st, a, n, nvalid, b, 0, v0, kvbase, tr, f, R);
+      tv_epilogue32<EPI>(st, a, n, nvalid, b, 32, v1, kvbase, tr, f, R);
       if (EPI == TV_ARGMAX) {
         // per row: max over this tile's 128 vocabulary ids, ties -> lowest id
         named_bar_sync(1, 128);

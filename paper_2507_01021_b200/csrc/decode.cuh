@@ -69,6 +69,10 @@ struct TcGemvArgs {
   int counter_base;
   float* y;                // TV_STORE / TV_RESID target [kRows, N]
   uint16_t *yh, *yl;       // TV_GELU_HILO targets
+  // fused LayerNorm prologue: if ln_g != nullptr the activation operand is
+  // LN(ln_x) (fp32 [kRows, K]) built in shared memory instead of TMA-loaded
+  const float* ln_x;
+  const uint16_t *ln_g, *ln_b;
 };
 
 // Pre-encoded TMA maps of one projection: weights [N, K] and the hi/lo input.

@@ -207,7 +207,7 @@ struct WhisperEngine {
   CUtensorMap kv_map, xkv_map;    // self-KV pool / cross-KV cache as [rows, 64] bf16
   // telemetry: kernels launched (graph nodes counted per replay)
   long long launches = 0, steps = 0, encodes = 0, segments = 0;
-  int step_kernels() const { return 1 + 11 * Ld + 3; }
+  int step_kernels() const { return 1 + 8 * Ld + 2; }
   int encode_kernels() const { return 2 + 2 + 7 * L + 1 + 1; }
 
   int alloc(void** p, size_t bytes, bool zero = true) {
@@ -494,31 +494,34 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
     const int b0 = e->dec_layer_base(l);
     const TcGemvMaps* m = &grp.maps[size_t(l) * 6];
     auto gv = [&](const TcGemvMaps& mp, int wi, int N, int K, int epi, float scale, float* y,
-                  uint16_t* yh, uint16_t* yl) {
+                  uint16_t* yh, uint16_t* yl, int ln_wi) {
       TcGemvArgs g{};
       g.bias = e->W(wi + 1); g.N = N; g.K = K; g.epi = epi; g.scale = scale; g.layer = l;
       g.splits = tc_gemv_splits(N, K); g.counter_base = e->gemv_counter_base;
       g.y = y; g.yh = yh; g.yl = yl;
+      if (ln_wi >= 0) {               // LayerNorm fused into the projection's operand
+        g.ln_x = st.x; g.ln_g = e->W(ln_wi); g.ln_b = e->W(ln_wi + 1);
+      }
       return launch_tc_gemv(st, mp, g, s);
     };
-    if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 0), e->W(b0 + 1), s)) return rc;
-    if (int rc = gv(m[0], b0 + 2, 3 * d, d, TV_QKV, 0.125f, nullptr, nullptr, nullptr)) return rc;
+    if (int rc = gv(m[0], b0 + 2, 3 * d, d, TV_QKV, 0.125f, nullptr, nullptr, nullptr, b0 + 0))
+      return rc;
     if (int rc = launch_self_attn(st, e->kv_map, l, s)) return rc;
-    if (int rc = gv(m[1], b0 + 4, d, d, TV_RESID, 1.f, st.x, nullptr, nullptr)) return rc;
-    if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 6), e->W(b0 + 7), s)) return rc;
-    if (int rc = gv(m[2], b0 + 8, d, d, TV_STORE, 0.125f, st.q, nullptr, nullptr)) return rc;
+    if (int rc = gv(m[1], b0 + 4, d, d, TV_RESID, 1.f, st.x, nullptr, nullptr, -1)) return rc;
+    if (int rc = gv(m[2], b0 + 8, d, d, TV_STORE, 0.125f, st.q, nullptr, nullptr, b0 + 6))
+      return rc;
     if (int rc = launch_cross_attn(st, e->xkv_map, l, e->xattn_counter_base, s)) return rc;
-    if (int rc = gv(m[3], b0 + 10, d, d, TV_RESID, 1.f, st.x, nullptr, nullptr)) return rc;
-    if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 12), e->W(b0 + 13), s)) return rc;
-    if (int rc = gv(m[4], b0 + 14, e->F, d, TV_GELU_HILO, 1.f, nullptr, st.hh, st.hl)) return rc;
-    if (int rc = gv(m[5], b0 + 16, d, e->F, TV_RESID, 1.f, st.x, nullptr, nullptr)) return rc;
+    if (int rc = gv(m[3], b0 + 10, d, d, TV_RESID, 1.f, st.x, nullptr, nullptr, -1)) return rc;
+    if (int rc = gv(m[4], b0 + 14, e->F, d, TV_GELU_HILO, 1.f, nullptr, st.hh, st.hl, b0 + 12))
+      return rc;
+    if (int rc = gv(m[5], b0 + 16, d, e->F, TV_RESID, 1.f, st.x, nullptr, nullptr, -1)) return rc;
   }
   const int x = e->after_dec();
-  if (int rc = launch_decode_ln(st, st.x, e->W(x + 2), e->W(x + 3), s)) return rc;
   {
     TcGemvArgs g{};
     g.bias = nullptr; g.N = e->cfg.vocab; g.K = d; g.epi = TV_ARGMAX; g.scale = 1.f;
     g.splits = 1; g.counter_base = e->gemv_counter_base;
+    g.ln_x = st.x; g.ln_g = e->W(x + 2); g.ln_b = e->W(x + 3);     // final LN fused
     if (int rc = launch_tc_gemv(st, grp.maps.back(), g, s)) return rc;
   }
   if (int rc = launch_finalize(st, s)) return rc;
