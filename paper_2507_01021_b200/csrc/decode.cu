@@ -65,8 +65,14 @@ __device__ __forceinline__ void tv_epilogue32(const DecodeState& st, const TcGem
 #pragma unroll
         for (int i = 0; i < 32; ++i) old[i] = r0 + i < R ? __ldcg(y + size_t(r0 + i) * a.N) : 0.f;
 #pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (r0 + i < R) y[size_t(r0 + i) * a.N] = old[i] + (v[i] + b);
+        for (int i = 0; i < 32; ++i) {
+          const float nv = old[i] + (v[i] + b);
+          if (r0 + i < R) y[size_t(r0 + i) * a.N] = nv;
+          if (tr) tr[(r0 + i) * 129 + f] = nv;     // row statistics for the next LayerNorm
+        }
+      } else if (tr) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) tr[(r0 + i) * 129 + f] = 0.f;
       }
       break;
     case TV_QKV: {
@@ -114,8 +120,10 @@ __device__ __forceinline__ void tv_epilogue32(const DecodeState& st, const TcGem
 constexpr int kTvWStages = 3;
 constexpr int kTvMaxKb = 8;
 __host__ __device__ constexpr int tv_smem_bytes(int kb, bool argmax) {
-  return kb * 2 * kTvXBytes + kTvWStages * kTvWBytes + (argmax ? kRows * 129 * 4 : 0) + 1024 + 1024;
-  // (misc: barriers + flags at +0, kvbase[64] at +256)
+  return kb * 2 * kTvXBytes + kTvWStages * kTvWBytes + (argmax ? kRows * 129 * 4 : 0) + 1024 + 2048;
+}
+__host__ __device__ constexpr bool tv_uses_tr(int epi) { return epi == TV_ARGMAX || epi == TV_RESID;
+  // (misc: barriers + flags at +0, kvbase[64] at +256, LN stats[64][2] at +768)
 }
 
 template <int EPI, bool SPLIT>
@@ -129,8 +137,9 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   const int kb_per = (a.K / 64) / a.splits;
   uint8_t* xs = smem;                                        // [kb][hi 8K | lo 8K]
   uint8_t* ws = smem + kb_per * 2 * kTvXBytes;               // [stage] 16K
-  float* tr = reinterpret_cast<float*>(ws + kTvWStages * kTvWBytes);   // ARGMAX only
-  uint8_t* misc = reinterpret_cast<uint8_t*>(tr) + (EPI == TV_ARGMAX ? kRows * 129 * 4 : 0);
+  constexpr bool kTr = EPI == TV_ARGMAX || EPI == TV_RESID;
+  float* tr = reinterpret_cast<float*>(ws + kTvWStages * kTvWBytes);   // ARGMAX / RESID stats
+  uint8_t* misc = reinterpret_cast<uint8_t*>(tr) + (kTr ? kRows * 129 * 4 : 0);
   uint64_t* wfull = reinterpret_cast<uint64_t*>(misc);
   uint64_t* wempty = wfull + kTvWStages;
   uint64_t* xfull = wempty + kTvWStages;
@@ -230,68 +239,54 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     pdl_wait();
     const int R = min(*st.n_active, kRows);
     if (fused_ln) {
-      // LayerNorm of the 64 rows (warp per row), written as bf16 hi/lo straight
-      // into the 128B-swizzled K-major operand tiles of this CTA's K range.
-      const int K = a.K, nchunk = K / 8;          // 16-byte chunks of 8 bf16 per row
-      const int c_lo = kb0 * 8, c_hi = (kb0 + kb_per) * 8;
-      for (int r = quad; r < kRows; r += 4) {
-        float4 v[2 * 5];                           // up to 1280 / 256 = 5 chunks per lane
-        const float4* xr = reinterpret_cast<const float4*>(a.ln_x + size_t(r) * K);
-        float s = 0.f;
-#pragma unroll
-        for (int m = 0; m < 5; ++m) {
-          const int ci = lane + 32 * m;
-          if (ci < nchunk && r < R) {
-            v[2 * m] = __ldcg(xr + 2 * ci);
-            v[2 * m + 1] = __ldcg(xr + 2 * ci + 1);
-          } else {
-            v[2 * m] = v[2 * m + 1] = make_float4(0.f, 0.f, 0.f, 0.f);
+      // LayerNorm of the active rows into the 128B-swizzled K-major operand
+      // tiles of this CTA's K range. (a) statistics: two threads per row, many
+      // independent L2 loads per thread; (b) normalise + split hi/lo + store,
+      // one 16-byte chunk per thread per step, coalesced along the row.
+      float* stats = reinterpret_cast<float*>(kvbase + kRows);   // [kRows][2]
+      const int K = a.K;
+      if (et < kRows) {
+        // statistics from the producer's per-tile partials (fixed tile order)
+        const int r = et, nt = K / 128;
+        float s1 = 0.f, s2 = 0.f;
+        if (r < R)
+          for (int t = 0; t < nt; ++t) {
+            s1 += __ldcg(st.ln_part + (size_t(t) * kRows + r) * 2);
+            s2 += __ldcg(st.ln_part + (size_t(t) * kRows + r) * 2 + 1);
           }
-          s += (v[2 * m].x + v[2 * m].y) + (v[2 * m].z + v[2 * m].w) +
-               (v[2 * m + 1].x + v[2 * m + 1].y) + (v[2 * m + 1].z + v[2 * m + 1].w);
+        const float mean = s1 / K;
+        const float var = fmaxf(s2 / K - mean * mean, 0.f);
+        stats[2 * r] = mean;
+        stats[2 * r + 1] = rsqrtf(var + 1e-5f);
+      }
+      named_bar_sync(1, 128);
+      const int nck = kb_per * 8;                 // 16-byte chunks per row in this K range
+#pragma unroll 4
+      for (int idx = et; idx < R * nck; idx += 128) {
+        const int r = idx / nck, cl = idx % nck;
+        const int ci = kb0 * 8 + cl;              // chunk index within the row
+        const float4* xr = reinterpret_cast<const float4*>(a.ln_x + size_t(r) * K + ci * 8);
+        const float4 x0 = __ldcg(xr), x1 = __ldcg(xr + 1);
+        const float e[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+        const float mean = stats[2 * r], rstd = stats[2 * r + 1];
+        const uint4 gw = __ldg(reinterpret_cast<const uint4*>(a.ln_g) + ci);
+        const uint4 bw = __ldg(reinterpret_cast<const uint4*>(a.ln_b) + ci);
+        const uint32_t gs[4] = {gw.x, gw.y, gw.z, gw.w}, bs[4] = {bw.x, bw.y, bw.z, bw.w};
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint16_t h0, l0, h1, l1;
+          split_hilo((e[2 * u] - mean) * rstd * __uint_as_float(gs[u] << 16) +
+                         __uint_as_float(bs[u] << 16), h0, l0);
+          split_hilo((e[2 * u + 1] - mean) * rstd * __uint_as_float(gs[u] & 0xFFFF0000u) +
+                         __uint_as_float(bs[u] & 0xFFFF0000u), h1, l1);
+          hi[u] = uint32_t(h0) | (uint32_t(h1) << 16);
+          lo[u] = uint32_t(l0) | (uint32_t(l1) << 16);
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        const float mean = s / K;
-        float q = 0.f;
-#pragma unroll
-        for (int m = 0; m < 5; ++m) {
-          const int ci = lane + 32 * m;
-          if (ci < nchunk) {
-            const float e[8] = {v[2 * m].x, v[2 * m].y, v[2 * m].z, v[2 * m].w,
-                                v[2 * m + 1].x, v[2 * m + 1].y, v[2 * m + 1].z, v[2 * m + 1].w};
-#pragma unroll
-            for (int u = 0; u < 8; ++u) q += (e[u] - mean) * (e[u] - mean);
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-        const float rstd = rsqrtf(q / K + 1e-5f);
-#pragma unroll
-        for (int m = 0; m < 5; ++m) {
-          const int ci = lane + 32 * m;
-          if (ci < c_lo || ci >= c_hi || ci >= nchunk) continue;
-          const float e[8] = {v[2 * m].x, v[2 * m].y, v[2 * m].z, v[2 * m].w,
-                              v[2 * m + 1].x, v[2 * m + 1].y, v[2 * m + 1].z, v[2 * m + 1].w};
-          const uint4 gw = __ldg(reinterpret_cast<const uint4*>(a.ln_g) + ci);
-          const uint4 bw = __ldg(reinterpret_cast<const uint4*>(a.ln_b) + ci);
-          const uint32_t gs[4] = {gw.x, gw.y, gw.z, gw.w}, bs[4] = {bw.x, bw.y, bw.z, bw.w};
-          uint32_t hi[4], lo[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            uint16_t h0, l0, h1, l1;
-            split_hilo((e[2 * u] - mean) * rstd * __uint_as_float(gs[u] << 16) +
-                           __uint_as_float(bs[u] << 16), h0, l0);
-            split_hilo((e[2 * u + 1] - mean) * rstd * __uint_as_float(gs[u] & 0xFFFF0000u) +
-                           __uint_as_float(bs[u] & 0xFFFF0000u), h1, l1);
-            hi[u] = uint32_t(h0) | (uint32_t(h1) << 16);
-            lo[u] = uint32_t(l0) | (uint32_t(l1) << 16);
-          }
-          const int kb = ci / 8 - kb0, j = ci % 8;
-          uint8_t* tile = xs + kb * 2 * kTvXBytes + r * 128 + ((j ^ (r & 7)) << 4);
-          *reinterpret_cast<uint4*>(tile) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-          *reinterpret_cast<uint4*>(tile + kTvXBytes) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-        }
+        const int kb = cl / 8, j = cl % 8;
+        uint8_t* tile = xs + kb * 2 * kTvXBytes + r * 128 + ((j ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(tile) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(tile + kTvXBytes) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -365,8 +360,24 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         }
         if (et == 0) st.counters[a.counter_base + tile] = 0;
       }
-      tv_epilogue32<EPI>(st, a, n, nvalid, b, 0, v0, kvbase, tr, f, R);
-      tv_epilogue32<EPI>(st, a, n, nvalid, b, 32, v1, kvbase, tr, f, R);
+      tv_epilogue32<EPI>(st, a, n, nvalid, b, 0, v0, kvbase, kTr ? tr : nullptr, f, R);
+      tv_epilogue32<EPI>(st, a, n, nvalid, b, 32, v1, kvbase, kTr ? tr : nullptr, f, R);
+      if (EPI == TV_RESID && st.ln_part) {
+        // per-row (sum, sum sq) of the updated residual over this 128-feature tile
+        named_bar_sync(1, 128);
+        const int r = et >> 1, half = et & 1;
+        const float* row = tr + r * 129 + half * 64;
+        float s1 = 0.f, s2 = 0.f;
+#pragma unroll 8
+        for (int i = 0; i < 64; ++i) { s1 += row[i]; s2 += row[i] * row[i]; }
+        s1 += __shfl_xor_sync(0xffffffffu, s1, 1);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, 1);
+        if (half == 0) {
+          st.ln_part[(size_t(tile) * kRows + r) * 2] = s1;
+          st.ln_part[(size_t(tile) * kRows + r) * 2 + 1] = s2;
+        }
+        named_bar_sync(1, 128);                    // tr reused by the next tile
+      }
       if (EPI == TV_ARGMAX) {
         // per row: max over this tile's 128 vocabulary ids, ties -> lowest id
         named_bar_sync(1, 128);
@@ -417,7 +428,7 @@ static int launch_tv(const DecodeState& st, const TcGemvMaps& maps, const TcGemv
                      cudaStream_t stream) {
   const int kb_per = (a.K / 64) / a.splits;
   DM_REQUIRE(kb_per <= kTvMaxKb, "decode GEMV: at most 8 k-blocks per split");
-  const int smem = tv_smem_bytes(kTvMaxKb, EPI == TV_ARGMAX);
+  const int smem = tv_smem_bytes(kTvMaxKb, tv_uses_tr(EPI));
   static bool attr = false;
   if (!attr) {
     DM_CHECK_CUDA(cudaFuncSetAttribute(tc_gemv_kernel<EPI, SPLIT>,
@@ -428,7 +439,7 @@ static int launch_tv(const DecodeState& st, const TcGemvMaps& maps, const TcGemv
   const int per_split = std::max(1, std::min(tiles, kNumSMs / a.splits));
   dim3 grid(per_split, a.splits);
   DM_CHECK_CUDA(launch_pdl(tc_gemv_kernel<EPI, SPLIT>, grid, dim3(kTvThreads),
-                           size_t(tv_smem_bytes(kb_per, EPI == TV_ARGMAX)), stream, maps.w,
+                           size_t(tv_smem_bytes(kb_per, tv_uses_tr(EPI))), stream, maps.w,
                            maps.xh, maps.xl, st, a));
   return 0;
 }
@@ -532,9 +543,40 @@ __global__ void embed_kernel(const DecodeState st, const uint16_t* __restrict__ 
   if (r >= *st.n_active) return;
   const int slot = st.active[r];
   const int tok = st.cur_tok[slot], p = st.pos[slot];
-  for (int c = threadIdx.x; c < st.d; c += blockDim.x)
-    st.x[size_t(r) * st.d + c] =
+  float s1 = 0.f, s2 = 0.f;
+  for (int c = threadIdx.x; c < st.d; c += blockDim.x) {
+    const float v =
         bf16_to_f32(embed[size_t(tok) * st.d + c]) + bf16_to_f32(pos_emb[size_t(p) * st.d + c]);
+    st.x[size_t(r) * st.d + c] = v;
+    s1 += v;
+    s2 += v * v;
+  }
+  if (st.ln_part) {
+    // (sum, sum sq) of the row for the fused LayerNorm: per 128-feature tile t,
+    // threads t*128 .. own features c = t*128 + threadIdx.x (blockDim == 128)
+    __shared__ float red[2][4];
+    const int d = st.d, nt = d / 128;
+    for (int t = 0; t < nt; ++t) {
+      const int c = t * 128 + threadIdx.x;
+      float v = 0.f;
+      if (c < d)
+        v = bf16_to_f32(embed[size_t(tok) * d + c]) + bf16_to_f32(pos_emb[size_t(p) * d + c]);
+      float a1 = v, a2 = v * v;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+      }
+      if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = a1; red[1][threadIdx.x >> 5] = a2; }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        st.ln_part[(size_t(t) * kRows + r) * 2] = (red[0][0] + red[0][1]) + (red[0][2] + red[0][3]);
+        st.ln_part[(size_t(t) * kRows + r) * 2 + 1] = (red[1][0] + red[1][1]) + (red[1][2] + red[1][3]);
+      }
+      __syncthreads();
+    }
+  }
+  (void)s1; (void)s2;
 }
 
 int launch_embed(const DecodeState& st, const uint16_t* embed, const uint16_t* pos_emb,

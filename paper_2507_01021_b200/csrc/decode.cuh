@@ -48,6 +48,9 @@ struct DecodeState {
   float* amax_val;             // [vocab tiles, kRows]
   int32_t* amax_idx;           // [vocab tiles, kRows]
   float* logits_dbg;           // optional [kRows, vocab]
+  float* ln_part;              // [d / 128][kRows][2]: per 128-feature tile, per row, (sum, sum sq)
+                               // of the residual stream, written by its producer (embed or a
+                               // residual-add projection) for the next fused LayerNorm
   int xsplits;                 // cross-attention key splits
 };
 

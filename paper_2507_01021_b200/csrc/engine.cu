@@ -342,6 +342,7 @@ static int engine_init(WhisperEngine* e) {
     if (e->alloc_t(&gs.counters, 4096 + size_t(kRows) * e->H)) return 2;
     if (e->alloc_t(&gs.amax_val, size_t(tiles) * kRows)) return 2;
     if (e->alloc_t(&gs.amax_idx, size_t(tiles) * kRows)) return 2;
+    if (e->alloc_t(&gs.ln_part, size_t(d / 128) * kRows * 2)) return 2;
     gs.logits_dbg = nullptr;
     // TMA maps of every decoder projection (weights [N, K] + this group's hi/lo inputs)
     auto mk = [&](TcGemvMaps& m, int wi, int N, int K, const uint16_t* xh, const uint16_t* xl) {
