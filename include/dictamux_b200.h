@@ -81,6 +81,8 @@ typedef struct dm_whisper_config {
   int persistent_decode;  /* 1: whole decode steps run in one persistent cooperative kernel
                              (one CTA per SM, grid barriers between phases); 0: CUDA graph of
                              per-phase kernels with programmatic dependent launch */
+  int fuse_ln;            /* 1: decoder LayerNorms fused into the following projections (fewer
+                             kernels; wins at low active-slot counts); 0: separate LN kernels */
 } dm_whisper_config;
 
 /* Weight offsets (elements into the bf16 blob), in this order:

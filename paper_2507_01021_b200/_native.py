@@ -34,7 +34,7 @@ class WhisperConfigC(C.Structure):
                 ("prompt", C.c_int * 8), ("prompt_len", C.c_int),
                 ("max_slots", C.c_int), ("max_encode_batch", C.c_int),
                 ("num_pages", C.c_int), ("decode_groups", C.c_int),
-                ("persistent_decode", C.c_int)]
+                ("persistent_decode", C.c_int), ("fuse_ln", C.c_int)]
 
 
 class CtcConfigC(C.Structure):

@@ -360,8 +360,9 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         }
         if (et == 0) st.counters[a.counter_base + tile] = 0;
       }
-      tv_epilogue32<EPI>(st, a, n, nvalid, b, 0, v0, kvbase, kTr ? tr : nullptr, f, R);
-      tv_epilogue32<EPI>(st, a, n, nvalid, b, 32, v1, kvbase, kTr ? tr : nullptr, f, R);
+      float* trp = (EPI == TV_ARGMAX || (EPI == TV_RESID && st.ln_part)) ? tr : nullptr;
+      tv_epilogue32<EPI>(st, a, n, nvalid, b, 0, v0, kvbase, trp, f, R);
+      tv_epilogue32<EPI>(st, a, n, nvalid, b, 32, v1, kvbase, trp, f, R);
       if (EPI == TV_RESID && st.ln_part) {
         // per-row (sum, sum sq) of the updated residual over this 128-feature tile
         named_bar_sync(1, 128);
@@ -408,13 +409,13 @@ tc_gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   }
 }
 
+// Smallest K split (a divisor of K/64) that leaves <= 8 k-blocks per CTA, so
+// the CTA's activation operand fits in shared memory. Depends only on K.
 int tc_gemv_splits(int N, int K) {
-  const int tiles = ceil_div(N, 128);
+  (void)N;
   const int kb = K / 64;
-  for (int s = 1; s <= kb; ++s) {
-    if (kb % s) continue;
-    if (kb / s <= 8 || tiles * s * 2 > 2 * kNumSMs) return s;
-  }
+  for (int s = 1; s <= kb; ++s)
+    if (kb % s == 0 && kb / s <= kTvMaxKb) return s;
   return kb;
 }
 
@@ -458,9 +459,8 @@ int launch_tc_gemv(const DecodeState& st, const TcGemvMaps& maps, const TcGemvAr
                              : launch_tv<TV_RESID, false>(st, maps, a, stream);
     case TV_QKV: return sp ? launch_tv<TV_QKV, true>(st, maps, a, stream)
                            : launch_tv<TV_QKV, false>(st, maps, a, stream);
-    case TV_ARGMAX:
-      DM_REQUIRE(!sp, "argmax epilogue runs without split-K");
-      return launch_tv<TV_ARGMAX, false>(st, maps, a, stream);
+    case TV_ARGMAX: return sp ? launch_tv<TV_ARGMAX, true>(st, maps, a, stream)
+                              : launch_tv<TV_ARGMAX, false>(st, maps, a, stream);
     default: DM_REQUIRE(false, "unknown epilogue");
   }
 }

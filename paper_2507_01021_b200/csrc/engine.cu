@@ -207,7 +207,7 @@ struct WhisperEngine {
   CUtensorMap kv_map, xkv_map;    // self-KV pool / cross-KV cache as [rows, 64] bf16
   // telemetry: kernels launched (graph nodes counted per replay)
   long long launches = 0, steps = 0, encodes = 0, segments = 0;
-  int step_kernels() const { return 1 + 8 * Ld + 2; }
+  int step_kernels() const { return cfg.fuse_ln ? 1 + 8 * Ld + 2 : 1 + 11 * Ld + 3; }
   int encode_kernels() const { return 2 + 2 + 7 * L + 1 + 1; }
 
   int alloc(void** p, size_t bytes, bool zero = true) {
@@ -336,13 +336,13 @@ static int engine_init(WhisperEngine* e) {
     gs.xsplits = 1;
     while (Sg * e->H * gs.xsplits < 4 * kNumSMs && gs.xsplits < 8) gs.xsplits *= 2;
     size_t part = size_t(kRows) * e->H * gs.xsplits * 66;
-    const int shapes[4][2] = {{3 * d, d}, {d, d}, {e->F, d}, {d, e->F}};
+    const int shapes[5][2] = {{3 * d, d}, {d, d}, {e->F, d}, {d, e->F}, {c.vocab, d}};
     for (auto& sh : shapes) part = std::max(part, tc_gemv_part_floats(sh[0], sh[1]));
     if (e->alloc_t(&gs.part, part)) return 2;
     if (e->alloc_t(&gs.counters, 4096 + size_t(kRows) * e->H)) return 2;
     if (e->alloc_t(&gs.amax_val, size_t(tiles) * kRows)) return 2;
     if (e->alloc_t(&gs.amax_idx, size_t(tiles) * kRows)) return 2;
-    if (e->alloc_t(&gs.ln_part, size_t(d / 128) * kRows * 2)) return 2;
+    if (c.fuse_ln && e->alloc_t(&gs.ln_part, size_t(d / 128) * kRows * 2)) return 2;
     gs.logits_dbg = nullptr;
     // TMA maps of every decoder projection (weights [N, K] + this group's hi/lo inputs)
     auto mk = [&](TcGemvMaps& m, int wi, int N, int K, const uint16_t* xh, const uint16_t* xl) {
@@ -505,24 +505,38 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
       }
       return launch_tc_gemv(st, mp, g, s);
     };
-    if (int rc = gv(m[0], b0 + 2, 3 * d, d, TV_QKV, 0.125f, nullptr, nullptr, nullptr, b0 + 0))
+    const bool fl = e->cfg.fuse_ln != 0;
+    if (!fl)
+      if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 0), e->W(b0 + 1), s)) return rc;
+    if (int rc = gv(m[0], b0 + 2, 3 * d, d, TV_QKV, 0.125f, nullptr, nullptr, nullptr,
+                    fl ? b0 + 0 : -1))
       return rc;
     if (int rc = launch_self_attn(st, e->kv_map, l, s)) return rc;
     if (int rc = gv(m[1], b0 + 4, d, d, TV_RESID, 1.f, st.x, nullptr, nullptr, -1)) return rc;
-    if (int rc = gv(m[2], b0 + 8, d, d, TV_STORE, 0.125f, st.q, nullptr, nullptr, b0 + 6))
+    if (!fl)
+      if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 6), e->W(b0 + 7), s)) return rc;
+    if (int rc = gv(m[2], b0 + 8, d, d, TV_STORE, 0.125f, st.q, nullptr, nullptr,
+                    fl ? b0 + 6 : -1))
       return rc;
     if (int rc = launch_cross_attn(st, e->xkv_map, l, e->xattn_counter_base, s)) return rc;
     if (int rc = gv(m[3], b0 + 10, d, d, TV_RESID, 1.f, st.x, nullptr, nullptr, -1)) return rc;
-    if (int rc = gv(m[4], b0 + 14, e->F, d, TV_GELU_HILO, 1.f, nullptr, st.hh, st.hl, b0 + 12))
+    if (!fl)
+      if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 12), e->W(b0 + 13), s)) return rc;
+    if (int rc = gv(m[4], b0 + 14, e->F, d, TV_GELU_HILO, 1.f, nullptr, st.hh, st.hl,
+                    fl ? b0 + 12 : -1))
       return rc;
     if (int rc = gv(m[5], b0 + 16, d, e->F, TV_RESID, 1.f, st.x, nullptr, nullptr, -1)) return rc;
   }
   const int x = e->after_dec();
+  if (!e->cfg.fuse_ln)
+    if (int rc = launch_decode_ln(st, st.x, e->W(x + 2), e->W(x + 3), s)) return rc;
   {
     TcGemvArgs g{};
     g.bias = nullptr; g.N = e->cfg.vocab; g.K = d; g.epi = TV_ARGMAX; g.scale = 1.f;
-    g.splits = 1; g.counter_base = e->gemv_counter_base;
-    g.ln_x = st.x; g.ln_g = e->W(x + 2); g.ln_b = e->W(x + 3);     // final LN fused
+    g.splits = tc_gemv_splits(e->cfg.vocab, d); g.counter_base = e->gemv_counter_base;
+    if (e->cfg.fuse_ln) {                  // final LN fused
+      g.ln_x = st.x; g.ln_g = e->W(x + 2); g.ln_b = e->W(x + 3);
+    }
     if (int rc = launch_tc_gemv(st, grp.maps.back(), g, s)) return rc;
   }
   if (int rc = launch_finalize(st, s)) return rc;
@@ -801,7 +815,12 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
       case 1: return launch_self_attn(e->st, e->kv_map, layer, cs);
       case 2: {
         TcGemvArgs g{};
-        g.N = e->cfg.vocab; g.K = e->d; g.epi = TV_ARGMAX; g.scale = 1.f; g.splits = 1;
+        g.N = e->cfg.vocab; g.K = e->d; g.epi = TV_ARGMAX; g.scale = 1.f;
+        g.splits = tc_gemv_splits(e->cfg.vocab, e->d);
+        const int xx = e->after_dec();
+        if (e->cfg.fuse_ln) {
+          g.ln_x = e->st.x; g.ln_g = e->W(xx + 2); g.ln_b = e->W(xx + 3);
+        }
         return launch_tc_gemv(e->st, e->maps.back(), g, cs);
       }
       case 3: {

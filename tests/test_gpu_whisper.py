@@ -132,3 +132,17 @@ def test_persistent_decode_matches_graph_and_oracle(tiny_pair, tiny_persistent):
     assert got_p == want
     alone = [tiny_persistent.transcribe_ids([s], [c])[0] for s, c in zip(segs, caps)]
     assert alone == got_p
+
+
+def test_fused_layernorm_decode_matches(tiny_pair, native_lib):
+    """fuse_ln=1 (LayerNorm built inside the projections from producer-side
+    row statistics) gives the oracle's tokens too."""
+    from oracle.logmel import log_mel_batch
+    from paper_2507_01021_b200.engine import WhisperGPU
+    orc, _ = tiny_pair
+    eng = WhisperGPU(WHISPER_TINY, seed=0, max_slots=8, max_encode_batch=4, fuse_ln=True)
+    segs = _segments(4, [5.0, 11.0, 3.0, 25.0], seed=9)
+    got = eng.transcribe_ids(segs, [6, 10, 4, 12])
+    enc = orc.encode(log_mel_batch(segs, 80))
+    assert got == [orc.greedy(enc[b], c) for b, c in enumerate([6, 10, 4, 12])]
+    eng.close()
