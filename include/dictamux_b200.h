@@ -152,6 +152,10 @@ DM_API int dm_ctc_read(void* handle, int32_t* tokens, int32_t* counts, int32_t* 
 /* which = 0: per-frame argmax ids [n * rows] int32; 1: final hidden [n * rows, 768] fp32 */
 DM_API int dm_ctc_debug(void* handle, int which, void* host_dst, size_t bytes, void* stream);
 
+/* Microbenchmark: cost of one grid-wide barrier of the persistent decode kernel
+ * (148 cooperative CTAs x 256 threads, release/acquire counter), microseconds. */
+DM_API int dm_bench_grid_barrier(int iters, float* us_per_barrier);
+
 /* Telemetry: out[0..3] = kernels launched, decode steps, encode calls, segments. */
 DM_API int dm_whisper_stats(void* handle, int64_t* out, int n);
 /* Time one decode kernel over the current active slots with CUDA events on

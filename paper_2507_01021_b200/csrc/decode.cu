@@ -1450,6 +1450,43 @@ __global__ void __launch_bounds__(kMkThreads, 1) decode_mega_kernel(const MkPara
 
 int launch_decode_mega(const MkParams& P, cudaStream_t stream);
 
+__global__ void __launch_bounds__(kMkThreads, 1) grid_barrier_bench_kernel(unsigned* bar, int iters) {
+  unsigned target = 0;
+  for (int i = 0; i < iters; ++i) mk_grid_sync(bar, target);
+}
+
+int bench_grid_barrier(int iters, float* us_per_barrier) {
+  unsigned* bar = nullptr;
+  DM_CHECK_CUDA(cudaMalloc(&bar, 256));
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    DM_CHECK_CUDA(cudaMemset(bar, 0, 256));
+    cudaEvent_t a, b;
+    DM_CHECK_CUDA(cudaEventCreate(&a));
+    DM_CHECK_CUDA(cudaEventCreate(&b));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kNumSMs);
+    cfg.blockDim = dim3(kMkThreads);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    DM_CHECK_CUDA(cudaEventRecord(a));
+    DM_CHECK_CUDA(cudaLaunchKernelEx(&cfg, grid_barrier_bench_kernel, bar, iters));
+    DM_CHECK_CUDA(cudaEventRecord(b));
+    DM_CHECK_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    DM_CHECK_CUDA(cudaEventElapsedTime(&ms, a, b));
+    best = fminf(best, ms);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  cudaFree(bar);
+  *us_per_barrier = best * 1000.f / iters;
+  return 0;
+}
+
 // Host-side builder: device copies of the per-layer pointers and tensor maps.
 struct MkHost {
   MkLayerW* lw = nullptr;

@@ -30,6 +30,7 @@ int launch_layernorm_bf16(const float*, const uint16_t*, const uint16_t*, uint16
                           cudaStream_t, float* y32 = nullptr);
 int launch_attention(const uint16_t*, const uint16_t*, const uint16_t*, int, int, int, int,
                      uint16_t*, int, cudaStream_t, const int32_t* seg_len = nullptr);
+int bench_grid_barrier(int iters, float* us_per_barrier);
 
 // ------------------------------------------------------------ log-mel tables
 struct LogmelTablesHost {
@@ -792,6 +793,11 @@ int dm_whisper_step(void* handle, int n_steps, void* stream) {
   e->steps += n_steps;
   e->launches += (long long)n_steps * e->step_kernels();
   return 0;
+}
+
+int dm_bench_grid_barrier(int iters, float* us_per_barrier) {
+  DM_REQUIRE(iters >= 1 && us_per_barrier != nullptr, "bad arguments");
+  return bench_grid_barrier(iters, us_per_barrier);
 }
 
 int dm_whisper_stats(void* handle, int64_t* out, int n) {
