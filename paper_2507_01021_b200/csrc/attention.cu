@@ -190,17 +190,26 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
       tc_fence_after();
       const int kvalid = T - j * 128;                     // < 128 only on the tail block
       uint32_t sr[32];
-      // pass 1: row max (3-input max)
+      // pass 1: row max (3-input max, independent accumulators, two TMEM
+      // loads in flight per wait)
       float mx = m_run;
       if (kvalid >= 128) {
+        uint32_t sb[32];
+        float m0 = m_run, m1 = m_run, m2 = m_run, m3 = m_run;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 4; c += 2) {
           tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
+          tmem_ld32(tmem + lane_off + s_col + c * 32 + 32, sb);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; i += 2)
-            mx = fmax3(mx, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
+          for (int i = 0; i < 32; i += 4) {
+            m0 = fmax3(m0, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
+            m1 = fmax3(m1, __uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3]));
+            m2 = fmax3(m2, __uint_as_float(sb[i]), __uint_as_float(sb[i + 1]));
+            m3 = fmax3(m3, __uint_as_float(sb[i + 2]), __uint_as_float(sb[i + 3]));
+          }
         }
+        mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
       } else {
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
@@ -216,30 +225,22 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
       // the previous PV must have consumed P before it is overwritten
       if (j >= 1) fold_pv(j - 1);
       // pass 2: p = exp2(s log2e - m log2e), row sum, bf16 P into swizzled smem
-      float rs = 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
-        tmem_wait_ld();
+      float rs0 = 0.f, rs1 = 0.f, rs2 = 0.f, rs3 = 0.f;
+      auto emit = [&](int c, const uint32_t (&v)[32], bool full) {
         uint32_t pk[16];
-        if (kvalid >= 128) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float p0 = ex2(fmaf(__uint_as_float(sr[2 * i]), kLog2e, -mscaled));
-            const float p1 = ex2(fmaf(__uint_as_float(sr[2 * i + 1]), kLog2e, -mscaled));
-            rs += p0 + p1;
-            pk[i] = pack_bf16x2(p0, p1);
+        for (int i = 0; i < 16; ++i) {
+          float p0, p1;
+          if (full) {
+            p0 = ex2(fmaf(__uint_as_float(v[2 * i]), kLog2e, -mscaled));
+            p1 = ex2(fmaf(__uint_as_float(v[2 * i + 1]), kLog2e, -mscaled));
+          } else {
+            p0 = (c * 32 + 2 * i < kvalid) ? ex2(fmaf(__uint_as_float(v[2 * i]), kLog2e, -mscaled)) : 0.f;
+            p1 = (c * 32 + 2 * i + 1 < kvalid)
+                     ? ex2(fmaf(__uint_as_float(v[2 * i + 1]), kLog2e, -mscaled)) : 0.f;
           }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float p0 = (c * 32 + 2 * i < kvalid)
-                                 ? ex2(fmaf(__uint_as_float(sr[2 * i]), kLog2e, -mscaled)) : 0.f;
-            const float p1 = (c * 32 + 2 * i + 1 < kvalid)
-                                 ? ex2(fmaf(__uint_as_float(sr[2 * i + 1]), kLog2e, -mscaled)) : 0.f;
-            rs += p0 + p1;
-            pk[i] = pack_bf16x2(p0, p1);
-          }
+          if (i & 1) { rs2 += p0; rs3 += p1; } else { rs0 += p0; rs1 += p1; }
+          pk[i] = pack_bf16x2(p0, p1);
         }
         // 32 keys = 4 chunks of 16 B; block = c / 2, chunk-in-row = (c % 2) * 4 + u
 #pragma unroll
@@ -249,7 +250,26 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
                                                 ((chunk ^ (r & 7)) << 4));
           *dst = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
+      };
+      if (kvalid >= 128) {
+        uint32_t sb[32];
+#pragma unroll 1
+        for (int c = 0; c < 4; c += 2) {
+          tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
+          tmem_ld32(tmem + lane_off + s_col + c * 32 + 32, sb);
+          tmem_wait_ld();
+          emit(c, sr, true);
+          emit(c + 1, sb, true);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
+          tmem_wait_ld();
+          emit(c, sr, false);
+        }
       }
+      const float rs = (rs0 + rs1) + (rs2 + rs3);
       tc_fence_before();
       fence_proxy_async_smem();
       __syncwarp();
