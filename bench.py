@@ -223,7 +223,8 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
     segs = make_workload(args.segments, rank)
     audio_s = sum(len(x) for _, x in segs) / 16000.0
     eng = WhisperGPU(dims, seed=0, device=local, max_slots=min(64, args.segments),
-                     max_encode_batch=args.encode_batch, steps_per_poll=args.steps_per_poll)
+                     max_encode_batch=args.encode_batch, steps_per_poll=args.steps_per_poll,
+                     decode_groups=args.decode_groups)
     backend = B200Backend(B200BackendConfig(model=MODEL, device=local), engine=eng)
 
     # resident inputs for `value`
@@ -311,7 +312,8 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
                        "audio_s_per_gpu": round(audio_s, 3),
                        "parallelism": f"replicas x{world} (no collective)",
                        "l2": "flushed between timed steps (256 MB write)",
-                       "encode_batch": args.encode_batch, "steps_per_poll": args.steps_per_poll},
+                       "encode_batch": args.encode_batch, "steps_per_poll": args.steps_per_poll,
+                       "decode_groups": eng.decode_groups},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "path": "SegmentQueue(dynamic) -> B200Backend.transcribe_batch (host int16)"},
@@ -372,6 +374,7 @@ def main():
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--ref-segments-per-step", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--decode-groups", type=int, default=None)
     ap.add_argument("--profile", action="store_true",
                     help="run exactly one resident-input step and exit (ncu)")
     args = ap.parse_args()

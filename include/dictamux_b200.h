@@ -78,11 +78,8 @@ typedef struct dm_whisper_config {
   int num_pages;          /* self-KV pages of 64 tokens in the pool */
   int decode_groups;      /* independent decode groups (slot s -> group s % G), each with its
                              own step graph and stream; <= 0 means 1 */
-  int persistent_decode;  /* 1: whole decode steps run in one persistent cooperative kernel
-                             (one CTA per SM, grid barriers between phases); 0: CUDA graph of
-                             per-phase kernels with programmatic dependent launch */
-  int fuse_ln;            /* 1: decoder LayerNorms fused into the following projections (fewer
-                             kernels; wins at low active-slot counts); 0: separate LN kernels */
+  int persistent_decode;  /* reserved, must be 0 */
+  int fuse_ln;            /* reserved, must be 0 */
 } dm_whisper_config;
 
 /* Weight offsets (elements into the bf16 blob), in this order:
@@ -152,16 +149,13 @@ DM_API int dm_ctc_read(void* handle, int32_t* tokens, int32_t* counts, int32_t* 
 /* which = 0: per-frame argmax ids [n * rows] int32; 1: final hidden [n * rows, 768] fp32 */
 DM_API int dm_ctc_debug(void* handle, int which, void* host_dst, size_t bytes, void* stream);
 
-/* Microbenchmark: cost of one grid-wide barrier of the persistent decode kernel
- * (148 cooperative CTAs x 256 threads, release/acquire counter), microseconds. */
-DM_API int dm_bench_grid_barrier(int iters, float* us_per_barrier);
-
 /* Telemetry: out[0..3] = kernels launched, decode steps, encode calls, segments. */
 DM_API int dm_whisper_stats(void* handle, int64_t* out, int n);
 /* Time one decode kernel over the current active slots with CUDA events on
- * `stream` (idempotent kernels only): which = 0 cross-attention(layer),
- * 1 self-attention(layer), 2 LM head, 3 decoder LN, 4 cross-q projection,
- * 5 fc2 projection (split-K), 6 empty PDL kernel (launch floor).
+ * `stream` (a probe: it may overwrite row-space activations): which =
+ * 0 cross-attention(layer), 1 self-attention(layer), 2 LM head, 3 decoder LN
+ * (+ residual partials), 4 cross-q projection, 5 fc2 projection,
+ * 6 empty PDL kernel (launch floor), 7 fc1 projection (+GELU), 8 qkv projection.
  * avg_ms = mean over iters back-to-back launches. */
 DM_API int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float* avg_ms,
                                   void* stream);

@@ -20,7 +20,6 @@ EXPORTS = (
     "dm_whisper_set_active", "dm_whisper_step", "dm_whisper_read",
     "dm_whisper_debug", "dm_whisper_stats", "dm_whisper_time_kernel",
     "dm_ctc_create", "dm_ctc_destroy", "dm_ctc_transcribe", "dm_ctc_read", "dm_ctc_debug",
-    "dm_bench_grid_barrier",
 )
 
 
@@ -87,7 +86,6 @@ def load(build_if_missing: bool = False):
             "dm_ctc_transcribe": [P, P, P, P, C.c_int, P],
             "dm_ctc_read": [P, P, P, P, P],
             "dm_ctc_debug": [P, C.c_int, P, C.c_size_t, P],
-            "dm_bench_grid_barrier": [C.c_int, P],
         }
         for name, args in sig.items():
             fn = getattr(lib, name)

@@ -7,6 +7,23 @@
 // are stored as a bf16 hi/lo pair (x = hi + lo exactly to ~2^-17 relative) so
 // the projections run on tcgen05 with fp32 accumulation while keeping fp32
 // activation precision (SURVEY.md §7 "Design rule").
+//
+// Step graph per decoder layer (every kernel launched with programmatic
+// dependent launch; everything that does not depend on the predecessor --
+// weight tiles, cross-KV blocks, LayerNorm parameters, biases -- is fetched
+// before griddepcontrol.wait):
+//
+//   ln(+embed | +residual partials) -> qkv GEMV (K-split partials)
+//   -> self-attention (reduces q/k/v partials, appends k/v to the page)
+//   -> o GEMV (partials) -> ln(+residual) -> cross-q GEMV (partials)
+//   -> cross-attention (reduces q, key splits merged over DSMEM in a cluster)
+//   -> cross-o GEMV (partials) -> ln(+residual) -> fc1 GEMV (+GELU, hi/lo)
+//   -> fc2 GEMV (partials)
+//
+// then ln_f(+residual) -> LM-head GEMV (per-vocab-tile argmax) -> finalize.
+// K-split partial sums are reduced by the consumer in split order, so every
+// reduction order depends only on K / positions, never on which or how many
+// rows are active: a segment decodes bit-identically alone or in any batch.
 #pragma once
 
 #include "common.cuh"
@@ -15,7 +32,8 @@
 
 namespace dm {
 
-constexpr int kRows = 64;          // max active slots = MMA N
+constexpr int kRows = 64;          // max active slots = max MMA N
+constexpr int kXSplits = 8;        // cross-attention key splits (cluster size); fixed per engine
 
 struct DecodeState {
   int max_slots, d, heads, layers, ffn, vocab;
@@ -25,89 +43,112 @@ struct DecodeState {
   int prompt_len;
   const int32_t* prompt;       // [prompt_len]
   // slot bookkeeping
-  const int32_t* active;       // [kRows] slot of row i
-  const int32_t* n_active;     // device scalar
+  const int32_t* active;       // [kRows] slot of row i (host-set before a step graph runs)
+  const int32_t* n_active;     // device scalar (host-set)
   int32_t* pos;                // [S] position of the token being fed
   int32_t* cur_tok;            // [S]
   int32_t* n_gen;              // [S]
   int32_t* cap;                // [S]
   int32_t* done;               // [S]
   int32_t* out_tokens;         // [S, 448]
-  const int32_t* page_table;   // [S, pages_per_slot]
+  const int32_t* page_table;   // [S, pages_per_slot] (host-set at admission)
   uint16_t* kv_pool;           // [pages][L][2][H][page_tokens][64] bf16
   const uint16_t* xkv;         // [L][S][2][H][1500][64] bf16
   // row-space activations
   float* x;                    // [kRows, d] residual stream (fp32)
   uint16_t *xh, *xl;           // [kRows, d]   LN output, bf16 hi/lo
-  float* q;                    // [kRows, d]   attention query (pre-scaled)
   uint16_t *ah, *al;           // [kRows, d]   attention output hi/lo
   uint16_t *hh, *hl;           // [kRows, ffn] fc1 output hi/lo
   // scratch
-  float* part;                 // split-K / split-KV partials
+  float* part;                 // split-K partials of non-linear epilogues (last-CTA reduction)
   int32_t* counters;           // zero-initialised tile counters
   float* amax_val;             // [vocab tiles, kRows]
   int32_t* amax_idx;           // [vocab tiles, kRows]
   float* logits_dbg;           // optional [kRows, vocab]
-  float* ln_part;              // [d / 128][kRows][2]: per 128-feature tile, per row, (sum, sum sq)
-                               // of the residual stream, written by its producer (embed or a
-                               // residual-add projection) for the next fused LayerNorm
-  int xsplits;                 // cross-attention key splits
+  // optional timeline tap (debug): per kernel of the step [128][4] globaltimer ns:
+  // min CTA entry, min / max dependency release (after griddepcontrol.wait), max exit
+  unsigned long long* trace;
+  int trace_id;
 };
 
-enum TcGemvEpi : int {
-  TV_STORE = 0,     // y[r, n] = (acc + b) * scale                 (fp32)
-  TV_GELU_HILO = 1, // yh/yl[r, n] = split(gelu(acc + b))         (bf16 pair)
-  TV_RESID = 2,     // x[r, n] += acc + b
-  TV_QKV = 3,       // q (scaled) / append k, v to the row's self-KV page
-  TV_ARGMAX = 4,    // per-row (max, lowest index) over this 128-row vocab tile
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// which: 0 entry, 1 released (records min and max), 3 exit
+__device__ __forceinline__ void trace_mark(const DecodeState& st, int which) {
+  if (st.trace == nullptr) return;
+  const unsigned long long t = global_ns();
+  unsigned long long* p = st.trace + st.trace_id * 4;
+  if (which == 0) atomicMin(p, t);
+  else if (which == 1) { atomicMin(p + 1, t); atomicMax(p + 2, t); }
+  else atomicMax(p + 3, t);
+}
+
+// K-split partial sums of a linear projection: part[s][row][n] (fp32, no bias),
+// reduced by the consumer as bias + sum_s part[s] in split order.
+struct Partials {
+  const float* p;
+  int splits;
+  int n;                       // row length N
+  const uint16_t* bias;        // [N] bf16
 };
 
-struct TcGemvArgs {
-  const uint16_t* bias;    // [N] nullable
+enum GemvEpi : int {
+  GV_PARTIAL = 0,   // part[split][r][n] = acc            (consumer reduces + adds bias)
+  GV_GELU_HILO = 1, // yh/yl[r, n] = split(gelu(acc + b)) (bf16 pair)
+  GV_ARGMAX = 2,    // per-row (max, lowest index) over this 128-feature vocab tile
+};
+
+struct GemvArgs {
+  const uint16_t* bias;    // [N] nullable (not used by GV_PARTIAL)
   int N, K;
   int epi;
-  float scale;
-  int layer;               // TV_QKV
   int splits;              // K splits (fixed per shape; never depends on rows)
+  int kb_per;              // 64-wide k-blocks per split
+  int stages;              // weight ring depth (whole slice prefetched when it fits)
+  int rgroups;             // row groups (grid z): 2 -> CTA z owns rows [32 z, 32 z + 32)
   int counter_base;
-  float* y;                // TV_STORE / TV_RESID target [kRows, N]
-  uint16_t *yh, *yl;       // TV_GELU_HILO targets
-  // fused LayerNorm prologue: if ln_g != nullptr the activation operand is
-  // LN(ln_x) (fp32 [kRows, K]) built in shared memory instead of TMA-loaded
-  const float* ln_x;
-  const uint16_t *ln_g, *ln_b;
+  float* part;             // GV_PARTIAL output [splits][kRows][N]
+  uint16_t *yh, *yl;       // GV_GELU_HILO targets [kRows, N]
 };
 
-// Pre-encoded TMA maps of one projection: weights [N, K] and the hi/lo input.
+// Pre-encoded TMA maps of one projection: weights [N, K] (box 128 x 64) and the
+// hi/lo activation input [kRows, K] (box 16 rows x 64, loads scale with rows).
 struct TcGemvMaps {
   CUtensorMap w, xh, xl;
 };
 
+constexpr int kGvXBox = 16;
+
 int make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
-int tc_gemv_splits(int N, int K);
-size_t tc_gemv_part_floats(int N, int K);
-int launch_tc_gemv(const DecodeState& st, const TcGemvMaps& maps, const TcGemvArgs& a,
-                   cudaStream_t stream);
-int launch_decode_ln(const DecodeState& st, const float* x, const uint16_t* g,
-                     const uint16_t* b, cudaStream_t stream);
-int launch_embed(const DecodeState& st, const uint16_t* embed, const uint16_t* pos_emb,
-                 cudaStream_t stream);
-int launch_self_attn(const DecodeState& st, const CUtensorMap& kv_map, int layer,
-                     cudaStream_t stream);
-int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
-                      int counter_base, cudaStream_t stream);
-int launch_finalize(const DecodeState& st, cudaStream_t stream);
+// Plan (splits, kb_per, stages) of a projection; depends only on (N, K, epilogue).
+GemvArgs gemv_plan(int N, int K, int epi);
+size_t gemv_part_floats(int N, int K, int epi);   // scratch for its partial sums
+int launch_gemv(const DecodeState& st, const TcGemvMaps& maps, const GemvArgs& a,
+                cudaStream_t stream);
 
-// Persistent decode (one cooperative CTA per SM runs n_steps whole steps).
-// layer_ptrs: per layer 12 pointers (ln1 g/b, qkv b, o b, ln2 g/b, xq b, xo b,
-// ln3 g/b, fc1 b, fc2 b).
-int mk_setup(const DecodeState& st, const std::vector<TcGemvMaps>& maps, const CUtensorMap& kv_map,
-             const CUtensorMap& xkv_map, const std::vector<const uint16_t*>& layer_ptrs,
-             void** handle);
-void mk_free(void* handle);
-int mk_launch(void* handle, const DecodeState& st, const uint16_t* lnfg, const uint16_t* lnfb,
-              const uint16_t* embed, const uint16_t* pos_emb, int n_steps, cudaStream_t stream,
-              unsigned long long* timing = nullptr);
+// LayerNorm of the row-space residual into the hi/lo projection operand.
+// mode 0: x as is; 1: x = embed[cur_tok] + pos_emb[pos] (first layer);
+// 2: x += bias + sum_s part[s] (the preceding projection's residual add).
+struct LnArgs {
+  int mode;
+  const uint16_t *g, *b;             // LayerNorm weight / bias [d]
+  const uint16_t *embed, *pos_emb;   // mode 1
+  Partials res;                      // mode 2
+};
+int launch_ln(const DecodeState& st, const LnArgs& a, cudaStream_t stream);
+
+// Self-attention of the fed token: q/k/v from the qkv partials (q scaled),
+// k/v appended to the slot's page, keys 0..pos; output -> ah/al.
+int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, float q_scale,
+                     cudaStream_t stream);
+// Cross-attention over the slot's 1500 cross-KV rows; q from the cross-q
+// partials (scaled); output -> ah/al.
+int launch_cross_attn(const DecodeState& st, int layer, const Partials& xq, float q_scale,
+                      cudaStream_t stream);
+int launch_finalize(const DecodeState& st, cudaStream_t stream);
 
 }  // namespace dm

@@ -30,7 +30,6 @@ int launch_layernorm_bf16(const float*, const uint16_t*, const uint16_t*, uint16
                           cudaStream_t, float* y32 = nullptr);
 int launch_attention(const uint16_t*, const uint16_t*, const uint16_t*, int, int, int, int,
                      uint16_t*, int, cudaStream_t, const int32_t* seg_len = nullptr);
-int bench_grid_barrier(int iters, float* us_per_barrier);
 
 // ------------------------------------------------------------ log-mel tables
 struct LogmelTablesHost {
@@ -186,8 +185,9 @@ struct WhisperEngine {
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t step_exec = nullptr;
   cudaGraph_t step_graph = nullptr;
-  int gemv_counter_base = 0, xattn_counter_base = 0;
+  int gemv_counter_base = 0;
   std::vector<TcGemvMaps> maps;   // [Ld * 6 + 1]: per layer qkv,o,xq,xo,fc1,fc2; LM head
+  std::vector<GemvArgs> plans;    // same order: launch plan of each projection
   // Independent decode groups (slot s belongs to group s % G): each has its own
   // row-space activations, active list, scratch, step graph and stream, so the
   // groups' latency-bound kernel chains overlap on the GPU.
@@ -200,15 +200,14 @@ struct WhisperEngine {
     cudaEvent_t done = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    // K-split partial sums of the linear projections (consumer-reduced)
+    float *p_qkv = nullptr, *p_o = nullptr, *p_xq = nullptr, *p_xo = nullptr, *p_fc2 = nullptr;
   };
   std::vector<Group> groups;
   cudaEvent_t step_start = nullptr;
-  void* mega = nullptr;            // persistent decode state (cfg.persistent_decode)
-  unsigned long long* mk_timing = nullptr;   // debug: per-barrier globaltimer stamps
-  CUtensorMap kv_map, xkv_map;    // self-KV pool / cross-KV cache as [rows, 64] bf16
   // telemetry: kernels launched (graph nodes counted per replay)
   long long launches = 0, steps = 0, encodes = 0, segments = 0;
-  int step_kernels() const { return cfg.fuse_ln ? 1 + 8 * Ld + 2 : 1 + 11 * Ld + 3; }
+  int step_kernels() const { return 11 * Ld + 3; }
   int encode_kernels() const { return 2 + 2 + 7 * L + 1 + 1; }
 
   int alloc(void** p, size_t bytes, bool zero = true) {
@@ -223,7 +222,6 @@ struct WhisperEngine {
   }
 
   ~WhisperEngine() {
-    if (mega) mk_free(mega);
     for (auto& g : groups) {
       if (g.exec) cudaGraphExecDestroy(g.exec);
       if (g.graph) cudaGraphDestroy(g.graph);
@@ -258,6 +256,7 @@ static int engine_init(WhisperEngine* e) {
   DM_REQUIRE(c.max_encode_batch >= 1, "max_encode_batch >= 1");
   DM_REQUIRE(c.prompt_len >= 1 && c.prompt_len <= 8, "prompt_len in [1, 8]");
   DM_REQUIRE(c.num_pages >= c.max_slots, "num_pages >= max_slots");
+  DM_REQUIRE(c.persistent_decode == 0 && c.fuse_ln == 0, "persistent_decode / fuse_ln are reserved (0)");
   const int d = e->d, E = c.max_encode_batch, S = c.max_slots;
   e->E = E;
   const size_t rows = size_t(E) * 1500;
@@ -315,7 +314,6 @@ static int engine_init(WhisperEngine* e) {
   if (e->alloc_t(&xkv, size_t(e->Ld) * S * 2 * e->H * 1500 * 64)) return 2;
   st.xkv = xkv;
   const int G = std::max(1, std::min(c.decode_groups > 0 ? c.decode_groups : 1, S));
-  const int Sg = ceil_div(S, G);
   e->groups.resize(G);
   const int tiles = ceil_div(c.vocab, 128);
   for (int gi = 0; gi < G; ++gi) {
@@ -328,28 +326,39 @@ static int engine_init(WhisperEngine* e) {
     if (e->alloc_t(&gs.x, size_t(kRows) * d)) return 2;
     if (e->alloc_t(&gs.xh, size_t(kRows) * d)) return 2;
     if (e->alloc_t(&gs.xl, size_t(kRows) * d)) return 2;
-    if (e->alloc_t(&gs.q, size_t(kRows) * d)) return 2;
     if (e->alloc_t(&gs.ah, size_t(kRows) * d)) return 2;
     if (e->alloc_t(&gs.al, size_t(kRows) * d)) return 2;
     if (e->alloc_t(&gs.hh, size_t(kRows) * e->F)) return 2;
     if (e->alloc_t(&gs.hl, size_t(kRows) * e->F)) return 2;
-    // cross-attention key splits: enough CTAs to cover the chip at full group batch
-    gs.xsplits = 1;
-    while (Sg * e->H * gs.xsplits < 4 * kNumSMs && gs.xsplits < 8) gs.xsplits *= 2;
-    size_t part = size_t(kRows) * e->H * gs.xsplits * 66;
-    const int shapes[5][2] = {{3 * d, d}, {d, d}, {e->F, d}, {d, e->F}, {c.vocab, d}};
-    for (auto& sh : shapes) part = std::max(part, tc_gemv_part_floats(sh[0], sh[1]));
+    // launch plans (depend only on the projection shape) and their scratch
+    e->plans.clear();
+    for (int l = 0; l < e->Ld; ++l) {
+      e->plans.push_back(gemv_plan(3 * d, d, GV_PARTIAL));     // qkv
+      e->plans.push_back(gemv_plan(d, d, GV_PARTIAL));         // o
+      e->plans.push_back(gemv_plan(d, d, GV_PARTIAL));         // xq
+      e->plans.push_back(gemv_plan(d, d, GV_PARTIAL));         // xo
+      e->plans.push_back(gemv_plan(e->F, d, GV_GELU_HILO));    // fc1
+      e->plans.push_back(gemv_plan(d, e->F, GV_PARTIAL));      // fc2
+    }
+    e->plans.push_back(gemv_plan(c.vocab, d, GV_ARGMAX));      // LM head
+    if (e->alloc_t(&gr.p_qkv, gemv_part_floats(3 * d, d, GV_PARTIAL))) return 2;
+    if (e->alloc_t(&gr.p_o, gemv_part_floats(d, d, GV_PARTIAL))) return 2;
+    if (e->alloc_t(&gr.p_xq, gemv_part_floats(d, d, GV_PARTIAL))) return 2;
+    if (e->alloc_t(&gr.p_xo, gemv_part_floats(d, d, GV_PARTIAL))) return 2;
+    if (e->alloc_t(&gr.p_fc2, gemv_part_floats(d, e->F, GV_PARTIAL))) return 2;
+    size_t part = std::max<size_t>(1, std::max(gemv_part_floats(e->F, d, GV_GELU_HILO),
+                                               gemv_part_floats(c.vocab, d, GV_ARGMAX)));
     if (e->alloc_t(&gs.part, part)) return 2;
-    if (e->alloc_t(&gs.counters, 4096 + size_t(kRows) * e->H)) return 2;
+    if (e->alloc_t(&gs.counters, 4096)) return 2;
     if (e->alloc_t(&gs.amax_val, size_t(tiles) * kRows)) return 2;
     if (e->alloc_t(&gs.amax_idx, size_t(tiles) * kRows)) return 2;
-    if (c.fuse_ln && e->alloc_t(&gs.ln_part, size_t(d / 128) * kRows * 2)) return 2;
     gs.logits_dbg = nullptr;
-    // TMA maps of every decoder projection (weights [N, K] + this group's hi/lo inputs)
+    // TMA maps of every decoder projection (weights [N, K] + this group's hi/lo inputs,
+    // activation boxes of 16 rows so loads scale with the active rows)
     auto mk = [&](TcGemvMaps& m, int wi, int N, int K, const uint16_t* xh, const uint16_t* xl) {
       if (make_tmap_2d(&m.w, e->W(wi), K, N, uint64_t(K) * 2, 64, 128)) return 2;
-      if (make_tmap_2d(&m.xh, xh, K, kRows, uint64_t(K) * 2, 64, kRows)) return 2;
-      if (make_tmap_2d(&m.xl, xl, K, kRows, uint64_t(K) * 2, 64, kRows)) return 2;
+      if (make_tmap_2d(&m.xh, xh, K, kRows, uint64_t(K) * 2, 64, kGvXBox)) return 2;
+      if (make_tmap_2d(&m.xl, xl, K, kRows, uint64_t(K) * 2, 64, kGvXBox)) return 2;
       return 0;
     };
     gr.maps.resize(size_t(e->Ld) * 6 + 1);
@@ -369,7 +378,6 @@ static int engine_init(WhisperEngine* e) {
   }
   DM_CHECK_CUDA(cudaEventCreateWithFlags(&e->step_start, cudaEventDisableTiming));
   e->gemv_counter_base = 0;
-  e->xattn_counter_base = 4096;
   {
     // group 0 doubles as the engine's default state (debug / timing probes)
     DecodeState shared = st;
@@ -377,22 +385,7 @@ static int engine_init(WhisperEngine* e) {
     e->maps = e->groups[0].maps;
     (void)shared;
   }
-  if (make_tmap_2d(&e->kv_map, st.kv_pool, 64, uint64_t(c.num_pages) * e->Ld * 2 * e->H * 64, 128,
-                   64, 64))
-    return 2;
-  if (make_tmap_2d(&e->xkv_map, st.xkv, 64, uint64_t(e->Ld) * S * 2 * e->H * 1500, 128, 64, 64))
-    return 2;
   DM_CHECK_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
-  if (c.persistent_decode) {
-    DM_REQUIRE(G == 1, "persistent decode runs one decode group");
-    std::vector<const uint16_t*> lp;
-    for (int l = 0; l < e->Ld; ++l) {
-      const int b0 = e->dec_layer_base(l);
-      const int idx[12] = {0, 1, 3, 5, 6, 7, 9, 11, 12, 13, 15, 17};
-      for (int j : idx) lp.push_back(e->W(b0 + j));
-    }
-    if (int rc = mk_setup(st, e->maps, e->kv_map, e->xkv_map, lp, &e->mega)) return rc;
-  }
   DM_CHECK_CUDA(cudaDeviceSynchronize());
   return 0;
 }
@@ -485,64 +478,55 @@ static int launch_pdl_floor(cudaStream_t s) {
   return 0;
 }
 
+#define DM_STEP(call)                 \
+  do {                                \
+    if (int rc = (call)) return rc;   \
+    ++st.trace_id;                    \
+  } while (0)
+
 static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t s) {
-  DecodeState& st = grp.st;
+  DecodeState st = grp.st;        // local copy: trace_id numbers the step's kernels
+  st.trace_id = 0;
   const int d = e->d;
   const int a = e->after_enc();
-  const uint16_t* embed = e->W(a + 2);
-  const uint16_t* pos_emb = e->W(a + 3);
-  if (int rc = launch_embed(st, embed, pos_emb, s)) return rc;
+  auto gv = [&](int idx, float* part, uint16_t* yh, uint16_t* yl, const uint16_t* bias) {
+    GemvArgs g = e->plans[idx];
+    g.bias = bias; g.part = part; g.yh = yh; g.yl = yl; g.counter_base = e->gemv_counter_base;
+    return launch_gemv(st, grp.maps[idx], g, s);
+  };
+  auto ln = [&](int mode, int gi, const Partials& res) {
+    LnArgs la{};
+    la.mode = mode; la.g = e->W(gi); la.b = e->W(gi + 1);
+    la.embed = e->W(a + 2); la.pos_emb = e->W(a + 3); la.res = res;
+    return launch_ln(st, la, s);
+  };
+  Partials prev{};                 // residual partials feeding the next LayerNorm
   for (int l = 0; l < e->Ld; ++l) {
     const int b0 = e->dec_layer_base(l);
-    const TcGemvMaps* m = &grp.maps[size_t(l) * 6];
-    auto gv = [&](const TcGemvMaps& mp, int wi, int N, int K, int epi, float scale, float* y,
-                  uint16_t* yh, uint16_t* yl, int ln_wi) {
-      TcGemvArgs g{};
-      g.bias = e->W(wi + 1); g.N = N; g.K = K; g.epi = epi; g.scale = scale; g.layer = l;
-      g.splits = tc_gemv_splits(N, K); g.counter_base = e->gemv_counter_base;
-      g.y = y; g.yh = yh; g.yl = yl;
-      if (ln_wi >= 0) {               // LayerNorm fused into the projection's operand
-        g.ln_x = st.x; g.ln_g = e->W(ln_wi); g.ln_b = e->W(ln_wi + 1);
-      }
-      return launch_tc_gemv(st, mp, g, s);
-    };
-    const bool fl = e->cfg.fuse_ln != 0;
-    if (!fl)
-      if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 0), e->W(b0 + 1), s)) return rc;
-    if (int rc = gv(m[0], b0 + 2, 3 * d, d, TV_QKV, 0.125f, nullptr, nullptr, nullptr,
-                    fl ? b0 + 0 : -1))
-      return rc;
-    if (int rc = launch_self_attn(st, e->kv_map, l, s)) return rc;
-    if (int rc = gv(m[1], b0 + 4, d, d, TV_RESID, 1.f, st.x, nullptr, nullptr, -1)) return rc;
-    if (!fl)
-      if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 6), e->W(b0 + 7), s)) return rc;
-    if (int rc = gv(m[2], b0 + 8, d, d, TV_STORE, 0.125f, st.q, nullptr, nullptr,
-                    fl ? b0 + 6 : -1))
-      return rc;
-    if (int rc = launch_cross_attn(st, e->xkv_map, l, e->xattn_counter_base, s)) return rc;
-    if (int rc = gv(m[3], b0 + 10, d, d, TV_RESID, 1.f, st.x, nullptr, nullptr, -1)) return rc;
-    if (!fl)
-      if (int rc = launch_decode_ln(st, st.x, e->W(b0 + 12), e->W(b0 + 13), s)) return rc;
-    if (int rc = gv(m[4], b0 + 14, e->F, d, TV_GELU_HILO, 1.f, nullptr, st.hh, st.hl,
-                    fl ? b0 + 12 : -1))
-      return rc;
-    if (int rc = gv(m[5], b0 + 16, d, e->F, TV_RESID, 1.f, st.x, nullptr, nullptr, -1)) return rc;
+    const int pi = l * 6;
+    const int gq = e->plans[pi].splits, go = e->plans[pi + 1].splits, gx = e->plans[pi + 2].splits;
+    const int gxo = e->plans[pi + 3].splits, gf = e->plans[pi + 5].splits;
+    // ln1 (+ embedding for layer 0, + previous fc2 residual otherwise)
+    DM_STEP(ln(l == 0 ? 1 : 2, b0 + 0, prev));
+    DM_STEP(gv(pi + 0, grp.p_qkv, nullptr, nullptr, nullptr));
+    DM_STEP(launch_self_attn(st, l, Partials{grp.p_qkv, gq, 3 * d, e->W(b0 + 3)}, 0.125f, s));
+    DM_STEP(gv(pi + 1, grp.p_o, nullptr, nullptr, nullptr));
+    DM_STEP(ln(2, b0 + 6, Partials{grp.p_o, go, d, e->W(b0 + 5)}));
+    DM_STEP(gv(pi + 2, grp.p_xq, nullptr, nullptr, nullptr));
+    DM_STEP(launch_cross_attn(st, l, Partials{grp.p_xq, gx, d, e->W(b0 + 9)}, 0.125f, s));
+    DM_STEP(gv(pi + 3, grp.p_xo, nullptr, nullptr, nullptr));
+    DM_STEP(ln(2, b0 + 12, Partials{grp.p_xo, gxo, d, e->W(b0 + 11)}));
+    DM_STEP(gv(pi + 4, nullptr, st.hh, st.hl, e->W(b0 + 15)));
+    DM_STEP(gv(pi + 5, grp.p_fc2, nullptr, nullptr, nullptr));
+    prev = Partials{grp.p_fc2, gf, d, e->W(b0 + 17)};
   }
   const int x = e->after_dec();
-  if (!e->cfg.fuse_ln)
-    if (int rc = launch_decode_ln(st, st.x, e->W(x + 2), e->W(x + 3), s)) return rc;
-  {
-    TcGemvArgs g{};
-    g.bias = nullptr; g.N = e->cfg.vocab; g.K = d; g.epi = TV_ARGMAX; g.scale = 1.f;
-    g.splits = tc_gemv_splits(e->cfg.vocab, d); g.counter_base = e->gemv_counter_base;
-    if (e->cfg.fuse_ln) {                  // final LN fused
-      g.ln_x = st.x; g.ln_g = e->W(x + 2); g.ln_b = e->W(x + 3);
-    }
-    if (int rc = launch_tc_gemv(st, grp.maps.back(), g, s)) return rc;
-  }
-  if (int rc = launch_finalize(st, s)) return rc;
+  DM_STEP(ln(2, x + 2, prev));                                   // final LayerNorm
+  DM_STEP(gv(e->Ld * 6, nullptr, nullptr, nullptr, nullptr));    // tied LM head + tile argmax
+  DM_STEP(launch_finalize(st, s));
   return 0;
 }
+#undef DM_STEP
 
 static int build_step_graph(WhisperEngine* e) {
   for (auto& grp : e->groups) {
@@ -767,18 +751,9 @@ int dm_whisper_set_active(void* handle, const int32_t* slot_ids, int n, void* st
 int dm_whisper_step(void* handle, int n_steps, void* stream) {
   auto* e = static_cast<WhisperEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
-  if (!e->mega && !e->step_exec)
+  if (!e->step_exec)
     if (int rc = build_step_graph(e)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (e->mega) {
-    const int x = e->after_dec(), a = e->after_enc();
-    if (int rc = mk_launch(e->mega, e->st, e->W(x + 2), e->W(x + 3), e->W(a + 2), e->W(a + 3),
-                           n_steps, s, e->mk_timing))
-      return rc;
-    e->steps += n_steps;
-    e->launches += n_steps > 0 ? 2 : 0;
-    return 0;
-  }
   if (e->groups.size() == 1) {
     for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(e->groups[0].exec, s));
   } else {
@@ -793,11 +768,6 @@ int dm_whisper_step(void* handle, int n_steps, void* stream) {
   e->steps += n_steps;
   e->launches += (long long)n_steps * e->step_kernels();
   return 0;
-}
-
-int dm_bench_grid_barrier(int iters, float* us_per_barrier) {
-  DM_REQUIRE(iters >= 1 && us_per_barrier != nullptr, "bad arguments");
-  return bench_grid_barrier(iters, us_per_barrier);
 }
 
 int dm_whisper_stats(void* handle, int64_t* out, int n) {
@@ -815,40 +785,37 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // capture `iters` back-to-back launches in a graph so the timing sees the
   // GPU-side launch/complete latency, not host submission
+  // probes run on decode group 0's state at its current active rows
+  WhisperEngine::Group& grp = e->groups[0];
+  const int d = e->d, b0 = e->dec_layer_base(layer), pi = layer * 6;
+  auto gv = [&](int idx, float* part, uint16_t* yh, uint16_t* yl, const uint16_t* bias,
+                cudaStream_t cs) {
+    GemvArgs g = e->plans[idx];
+    g.bias = bias; g.part = part; g.yh = yh; g.yl = yl; g.counter_base = e->gemv_counter_base;
+    return launch_gemv(grp.st, grp.maps[idx], g, cs);
+  };
   auto launch_one = [&](cudaStream_t cs) -> int {
     switch (which) {
-      case 0: return launch_cross_attn(e->st, e->xkv_map, layer, e->xattn_counter_base, cs);
-      case 1: return launch_self_attn(e->st, e->kv_map, layer, cs);
-      case 2: {
-        TcGemvArgs g{};
-        g.N = e->cfg.vocab; g.K = e->d; g.epi = TV_ARGMAX; g.scale = 1.f;
-        g.splits = tc_gemv_splits(e->cfg.vocab, e->d);
-        const int xx = e->after_dec();
-        if (e->cfg.fuse_ln) {
-          g.ln_x = e->st.x; g.ln_g = e->W(xx + 2); g.ln_b = e->W(xx + 3);
-        }
-        return launch_tc_gemv(e->st, e->maps.back(), g, cs);
-      }
+      case 0:
+        return launch_cross_attn(grp.st, layer,
+                                 Partials{grp.p_xq, e->plans[pi + 2].splits, d, e->W(b0 + 9)},
+                                 0.125f, cs);
+      case 1:
+        return launch_self_attn(grp.st, layer,
+                                Partials{grp.p_qkv, e->plans[pi].splits, 3 * d, e->W(b0 + 3)},
+                                0.125f, cs);
+      case 2: return gv(e->Ld * 6, nullptr, nullptr, nullptr, nullptr, cs);
       case 3: {
-        const int b0 = e->dec_layer_base(layer);
-        return launch_decode_ln(e->st, e->st.x, e->W(b0 + 6), e->W(b0 + 7), cs);
+        LnArgs la{};
+        la.mode = 2; la.g = e->W(b0 + 6); la.b = e->W(b0 + 7);
+        la.res = Partials{grp.p_o, e->plans[pi + 1].splits, d, e->W(b0 + 5)};
+        return launch_ln(grp.st, la, cs);
       }
-      case 4: {
-        const int b0 = e->dec_layer_base(layer);
-        TcGemvArgs g{};
-        g.bias = e->W(b0 + 9); g.N = e->d; g.K = e->d; g.epi = TV_STORE; g.scale = 0.125f;
-        g.layer = layer; g.splits = tc_gemv_splits(e->d, e->d); g.y = e->st.q;
-        return launch_tc_gemv(e->st, e->maps[size_t(layer) * 6 + 2], g, cs);
-      }
-      case 5: {
-        const int b0 = e->dec_layer_base(layer);
-        TcGemvArgs g{};
-        g.bias = e->W(b0 + 17); g.N = e->d; g.K = e->F; g.epi = TV_RESID; g.scale = 1.f;
-        g.layer = layer; g.splits = tc_gemv_splits(e->d, e->F); g.y = e->st.x;
-        g.counter_base = e->gemv_counter_base;
-        return launch_tc_gemv(e->st, e->maps[size_t(layer) * 6 + 5], g, cs);
-      }
+      case 4: return gv(pi + 2, grp.p_xq, nullptr, nullptr, nullptr, cs);
+      case 5: return gv(pi + 5, grp.p_fc2, nullptr, nullptr, nullptr, cs);
       case 6: return launch_pdl_floor(cs);
+      case 7: return gv(pi + 4, nullptr, grp.st.hh, grp.st.hl, e->W(b0 + 15), cs);
+      case 8: return gv(pi + 0, grp.p_qkv, nullptr, nullptr, nullptr, cs);
       default: set_error("unknown kernel id"); return 1;
     }
   };
@@ -920,12 +887,27 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
     }
     case 4: e->enc_stop = int(bytes); return 0;
     case 7: e->enc_tap = bytes != 0; return 0;
-    case 8:
-      if (!e->mk_timing && e->alloc_t(&e->mk_timing, 1 << 16)) return 2;
+    case 10: {       // step timeline tap on (graph re-captured with per-kernel globaltimer marks)
+      if (!e->groups[0].st.trace) {
+        unsigned long long* t = nullptr;
+        if (e->alloc_t(&t, 128 * 4)) return 2;
+        e->groups[0].st.trace = t;
+        if (int rc = build_step_graph(e)) return rc;
+      }
       return 0;
-    case 9:
-      DM_REQUIRE(e->mk_timing != nullptr, "timing tap not enabled");
-      src = e->mk_timing; avail = size_t(8) << 16;
+    }
+    case 11: {       // reset the timeline (entry/release minima to +inf, maxima to 0)
+      DM_REQUIRE(e->groups[0].st.trace != nullptr, "timeline tap not enabled");
+      std::vector<unsigned long long> init(128 * 4, 0ull);
+      for (int k = 0; k < 128; ++k) init[k * 4] = init[k * 4 + 1] = ~0ull;
+      DM_CHECK_CUDA(cudaMemcpyAsync(e->groups[0].st.trace, init.data(), init.size() * 8,
+                                    cudaMemcpyHostToDevice, s));
+      DM_CHECK_CUDA(cudaStreamSynchronize(s));
+      return 0;
+    }
+    case 12:
+      DM_REQUIRE(e->groups[0].st.trace != nullptr, "timeline tap not enabled");
+      src = e->groups[0].st.trace; avail = 128 * 4 * 8;
       break;
     case 5: src = e->resid; avail = size_t(e->last_n) * 1500 * e->d * 4; break;
     case 6: src = e->attn_out; avail = size_t(e->last_n) * 1500 * e->d * 2; break;

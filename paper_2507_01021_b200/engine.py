@@ -100,8 +100,7 @@ class WhisperGPU:
                  device: int | str | torch.device = 0, max_slots: int = 64,
                  max_encode_batch: int = 32, num_pages: int | None = None,
                  eot: int | None = None, steps_per_poll: int = 8,
-                 decode_groups: int | None = None, persistent_decode: bool = False,
-                 fuse_ln: bool = False):
+                 decode_groups: int | None = None):
         if not torch.cuda.is_available():
             raise _native.DmError("no CUDA device: the B200 engine has no CPU fallback")
         self.dims = dims
@@ -128,10 +127,7 @@ class WhisperGPU:
             if decode_groups is None:
                 decode_groups = 1
             cfg.decode_groups = decode_groups
-            cfg.persistent_decode = int(bool(persistent_decode))
-            cfg.fuse_ln = int(bool(fuse_ln))
             self.decode_groups = decode_groups
-            self.persistent_decode = bool(persistent_decode)
             arr = (C.c_int64 * len(offs))(*offs)
             h = C.c_void_p()
             _native.check(self.lib.dm_whisper_create(C.byref(cfg), C.c_void_p(self.blob.data_ptr()),

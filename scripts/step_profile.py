@@ -10,11 +10,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--model", default="whisper-base")
 ap.add_argument("--slots", type=int, default=64)
 ap.add_argument("--encode-batch", type=int, default=32)
-ap.add_argument("--persistent", action="store_true")
 args = ap.parse_args()
 dims = get_model(args.model)
-eng = WhisperGPU(dims, max_slots=args.slots, max_encode_batch=args.encode_batch,
-                 persistent_decode=args.persistent)
+eng = WhisperGPU(dims, max_slots=args.slots, max_encode_batch=args.encode_batch)
 rng = np.random.default_rng(0)
 segs = [rng.integers(-8000, 8000, size=480000, dtype=np.int16) for _ in range(args.encode_batch)]
 ev = lambda: torch.cuda.Event(enable_timing=True)
@@ -46,7 +44,7 @@ for n in (64, 48, 32, 16, 8, 1):
     res[n] = {"step_ms": round(ms, 4), "xkv_GBps": round(xkv / ms / 1e6, 1)}
 out["decode_step"] = res
 names = {0: "cross_attn", 1: "self_attn", 2: "lm_head", 3: "decode_ln", 4: "gemv_xq",
-         5: "gemv_fc2_splitk", 6: "empty_pdl_floor"}
+         5: "gemv_fc2", 6: "empty_pdl_floor", 7: "gemv_fc1", 8: "gemv_qkv"}
 for n in (64, 1):
     eng.set_active(slots[:n])
     out[f"kernel_us_rows{n}"] = {names[w]: round(1000 * eng.time_kernel(w, 0, 50), 2) for w in names}

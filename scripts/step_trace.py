@@ -1,0 +1,67 @@
+"""Decode-step timeline from in-kernel globaltimer marks (debug tap 10-12):
+per kernel of the step graph, the dependency-release time (first CTA past
+griddepcontrol.wait) relative to the previous kernel's last exit, and its own
+release-to-exit span. Usage: python scripts/step_trace.py [model] [rows...]"""
+import ctypes as C, json, sys
+sys.path.insert(0, '.')
+import numpy as np, torch
+from paper_2507_01021_b200.engine import WhisperGPU
+from paper_2507_01021_b200.models import get_model
+
+name = sys.argv[1] if len(sys.argv) > 1 else "whisper-base"
+rows_list = [int(x) for x in sys.argv[2:]] or [64, 32, 8, 1]
+dims = get_model(name)
+S = 64
+eng = WhisperGPU(dims, max_slots=S, max_encode_batch=32)
+rng = np.random.default_rng(0)
+seg = rng.integers(-8000, 8000, size=160000, dtype=np.int16)
+slots = list(range(S))
+for i in range(0, S, 32):
+    eng.encode([seg] * 32, slots[i:i + 32])
+eng.admit(slots, [400] * S)
+names = []
+for l in range(dims.dec_layers):
+    names += [f"L{l}.{k}" for k in ("ln1", "qkv", "self", "o", "ln2", "xq", "xattn", "xo", "ln3", "fc1", "fc2")]
+names += ["ln_f", "lm_head", "finalize"]
+lib = eng.lib
+def dbg(which, buf=None, n=0):
+    ptr = buf.ctypes.data_as(C.c_void_p) if buf is not None else None
+    from paper_2507_01021_b200 import _native
+    _native.check(lib.dm_whisper_debug(eng.handle, which, ptr, buf.nbytes if buf is not None else n, eng._s))
+dbg(10)
+out = {}
+for rows in rows_list:
+    eng.set_active(slots[:rows])
+    eng.step(6)
+    torch.cuda.synchronize()
+    acc = None
+    reps = 10
+    for _ in range(reps):
+        dbg(11)
+        eng.step(1)
+        torch.cuda.synchronize()
+        t = np.zeros((128, 4), np.uint64)
+        dbg(12, t)
+        t = t[:len(names)].astype(np.float64)
+        t0 = t[0, 1]
+        t = t - t0
+        acc = t if acc is None else acc + t
+    t = acc / reps
+    res = []
+    prev_end = 0.0
+    for k, nm in enumerate(names):
+        entry, rel, rel_max, end = t[k]
+        res.append({"k": nm, "gap_us": round((rel - prev_end) / 1e3, 2),
+                    "span_us": round((end - rel) / 1e3, 2),
+                    "early_us": round((rel - entry) / 1e3, 2)})
+        prev_end = end
+    total = t[len(names) - 1, 3] / 1e3
+    kinds = {}
+    for r in res:
+        kk = r["k"].split(".")[-1]
+        d = kinds.setdefault(kk, [0.0, 0.0, 0])
+        d[0] += r["gap_us"]; d[1] += r["span_us"]; d[2] += 1
+    out[rows] = {"step_us": round(total, 1),
+                 "by_kind": {k: {"n": v[2], "gap_us": round(v[0], 1), "span_us": round(v[1], 1)} for k, v in kinds.items()},
+                 "layer0": res[:13]}
+print(json.dumps(out, indent=1))
