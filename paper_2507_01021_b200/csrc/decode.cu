@@ -18,6 +18,8 @@
 #include "decode.cuh"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 namespace dm {

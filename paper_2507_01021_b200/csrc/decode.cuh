@@ -16,7 +16,8 @@
 //   ln(+embed | +residual partials) -> qkv GEMV (K-split partials)
 //   -> self-attention (reduces q/k/v partials, appends k/v to the page)
 //   -> o GEMV (partials) -> ln(+residual) -> cross-q GEMV (partials)
-//   -> cross-attention (reduces q, key splits merged over DSMEM in a cluster)
+//   -> cross-attention (reduces q; the 8 key splits of a (row, head) form a cluster
+//      and merge over DSMEM)
 //   -> cross-o GEMV (partials) -> ln(+residual) -> fc1 GEMV (+GELU, hi/lo)
 //   -> fc2 GEMV (partials)
 //
