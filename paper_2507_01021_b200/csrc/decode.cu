@@ -560,17 +560,24 @@ __device__ __forceinline__ void store_hilo1(const DecodeState& st, int r, int c,
 
 constexpr int kSaThreads = 256;
 constexpr int kSaMaxKeys = 448;
+constexpr int kSaPageBytes = 64 * 128;                         // one page block: 64 keys x 64 dims
+constexpr int kSaPrePages = 2;                                 // pages staged in shared memory
 
-// Self-attention for (row, head): reduces the fed token's q/k/v from the qkv
-// partials, appends k/v (bf16) at `pos` in the slot's page, attends over the
-// cached keys 0..pos-1 plus the fed key (kept in shared memory).
+// Self-attention for (row, head). The fed token's position and the slot's
+// earlier keys/values do not depend on this step's predecessors (positions
+// advance only in the previous step's finalize), so the K and V page blocks
+// of positions 0..min(pos, 128)-1 are bulk-copied into shared memory before
+// the dependency wait (later positions are read from global memory). After it: reduce the fed token's q/k/v from the qkv
+// partials, append k/v (bf16) at `pos`, scores (cached keys read chunk-wise in
+// XOR order -- conflict-free -- plus the fed key), two-pass softmax, P.V.
 __global__ void __launch_bounds__(kSaThreads)
 self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_scale) {
-  __shared__ float qs[64], kc[64], vc[64];
+  extern __shared__ __align__(128) uint8_t sa_smem[];          // [pages][K 8K | V 8K] + bar
+  __shared__ __align__(16) float qs[64];
+  __shared__ float kc[64], vc[64];
   __shared__ float sc[kSaMaxKeys];
   __shared__ float red[8];
   __shared__ float op[8][64];
-  __shared__ int pts[8];
   const int r = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
   if (tid == 0) trace_mark(st, 0);
@@ -578,21 +585,31 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
   if (r >= *st.n_active) return;                 // host-set: safe before the wait
   const int slot = st.active[r];
   const int d = st.d, H = st.heads, L = st.layers;
-  if (tid < st.pages_per_slot) pts[tid] = st.page_table[slot * st.pages_per_slot + tid];
+  const int p = st.pos[slot];                    // final since the previous step
+  const int np = min(ceil_div(p, 64), kSaPrePages);   // staged pages of positions < p
+  const int* pt = st.page_table + slot * st.pages_per_slot;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sa_smem + kSaPrePages * 2 * kSaPageBytes);
+  const size_t kv_off = size_t(H) * 64 * 64;     // k -> v within a (page, layer)
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    fence_barrier_init();
+    if (np > 0) {
+      mbar_arrive_expect_tx(bar, np * 2 * kSaPageBytes);
+      for (int g = 0; g < np; ++g) {
+        const uint16_t* kb = st.kv_pool + ((size_t(pt[g]) * L + layer) * 2 * H + h) * 64 * 64;
+        bulk_load(sa_smem + g * 2 * kSaPageBytes, kb, kSaPageBytes, bar);
+        bulk_load(sa_smem + g * 2 * kSaPageBytes + kSaPageBytes, kb + kv_off, kSaPageBytes, bar);
+      }
+    }
+  }
   float bq = 0.f, bk = 0.f, bv = 0.f;
   if (tid < 64) {
     bq = bf16_to_f32(qkv.bias[h * 64 + tid]);
     bk = bf16_to_f32(qkv.bias[d + h * 64 + tid]);
     bv = bf16_to_f32(qkv.bias[2 * d + h * 64 + tid]);
   }
-  const size_t kv_off = size_t(H) * 64 * 64;     // k -> v within a (page, layer)
-  __syncthreads();
-  auto key_base = [&](int t) -> size_t {
-    return ((size_t(pts[t >> 6]) * L + layer) * 2 * H + h) * 64 * 64 + size_t(t & 63) * 64;
-  };
   pdl_wait();
   if (tid == 0) trace_mark(st, 1);
-  const int p = st.pos[slot];
   if (tid < 64) {
     const int c = h * 64 + tid;
     const float* pp = qkv.p + size_t(r) * qkv.n + c;
@@ -604,7 +621,7 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
       av += __ldcg(ps + 2 * d);
     }
     const uint16_t kb = f32_to_bf16(ak + bk), vb = f32_to_bf16(av + bv);
-    const size_t kbase = key_base(p);
+    const size_t kbase = ((size_t(pt[p >> 6]) * L + layer) * 2 * H + h) * 64 * 64 + size_t(p & 63) * 64;
     st.kv_pool[kbase + tid] = kb;
     st.kv_pool[kbase + kv_off + tid] = vb;
     qs[tid] = (aq + bq) * q_scale;
@@ -612,12 +629,14 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
     vc[tid] = bf16_to_f32(vb);
   }
   __syncthreads();
+  if (np > 0) mbar_wait(bar, 0);
   const int nk = p + 1;
   float mloc = -INFINITY;
   for (int t = tid; t < nk; t += kSaThreads) {
     float s = 0.f;
-    if (t < p) {
-      const uint4* kr = reinterpret_cast<const uint4*>(st.kv_pool + key_base(t));
+    if (t < p && t >= 64 * kSaPrePages) {
+      const uint4* kr = reinterpret_cast<const uint4*>(
+          st.kv_pool + ((size_t(pt[t >> 6]) * L + layer) * 2 * H + h) * 64 * 64 + size_t(t & 63) * 64);
       uint4 w[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) w[j] = __ldg(kr + j);
@@ -629,6 +648,27 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
           s = fmaf(qs[8 * j + 2 * u], __uint_as_float(ws[u] << 16), s);
           s = fmaf(qs[8 * j + 2 * u + 1], __uint_as_float(ws[u] & 0xFFFF0000u), s);
         }
+      }
+    } else if (t < p) {
+      // chunk j of key row t read at chunk (j ^ t) & 7: 4 lanes per 16-byte
+      // bank group; chunk dot products summed in that (position-fixed) order
+      const uint8_t* kr = sa_smem + (t >> 6) * 2 * kSaPageBytes + (t & 63) * 128;
+      const int sw = t & 7;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int cc = j ^ sw;
+        const uint4 w = *reinterpret_cast<const uint4*>(kr + cc * 16);
+        const float4 qa = *reinterpret_cast<const float4*>(qs + 8 * cc);
+        const float4 qb = *reinterpret_cast<const float4*>(qs + 8 * cc + 4);
+        float sj = qa.x * __uint_as_float(w.x << 16);
+        sj = fmaf(qa.y, __uint_as_float(w.x & 0xFFFF0000u), sj);
+        sj = fmaf(qa.z, __uint_as_float(w.y << 16), sj);
+        sj = fmaf(qa.w, __uint_as_float(w.y & 0xFFFF0000u), sj);
+        sj = fmaf(qb.x, __uint_as_float(w.z << 16), sj);
+        sj = fmaf(qb.y, __uint_as_float(w.z & 0xFFFF0000u), sj);
+        sj = fmaf(qb.z, __uint_as_float(w.w << 16), sj);
+        sj = fmaf(qb.w, __uint_as_float(w.w & 0xFFFF0000u), sj);
+        s += sj;
       }
     } else {
 #pragma unroll 8
@@ -646,26 +686,26 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
   }
   const float l = block_sum_fixed(lsum, red);    // (its barrier publishes sc[])
   float o0 = 0.f, o1 = 0.f;
-  for (int t0 = warp; t0 < nk; t0 += 8 * 8) {
-    // 8 keys per batch: all V loads issued before the FMAs
-    uint32_t w[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int t = t0 + 8 * i;
-      w[i] = t < p ? __ldg(reinterpret_cast<const uint32_t*>(st.kv_pool + key_base(t) + kv_off) + lane)
-                   : 0u;
+#pragma unroll 4
+  for (int t = warp; t < nk; t += 8) {
+    float v0, v1;
+    if (t < p) {
+      const uint32_t w =
+          t < 64 * kSaPrePages
+              ? *reinterpret_cast<const uint32_t*>(sa_smem + (t >> 6) * 2 * kSaPageBytes +
+                                                   kSaPageBytes + (t & 63) * 128 + lane * 4)
+              : __ldg(reinterpret_cast<const uint32_t*>(
+                          st.kv_pool + ((size_t(pt[t >> 6]) * L + layer) * 2 * H + h) * 64 * 64 +
+                          kv_off + size_t(t & 63) * 64) + lane);
+      v0 = __uint_as_float(w << 16);
+      v1 = __uint_as_float(w & 0xFFFF0000u);
+    } else {
+      v0 = vc[2 * lane];
+      v1 = vc[2 * lane + 1];
     }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int t = t0 + 8 * i;
-      if (t < nk) {
-        const float v0 = t < p ? __uint_as_float(w[i] << 16) : vc[2 * lane];
-        const float v1 = t < p ? __uint_as_float(w[i] & 0xFFFF0000u) : vc[2 * lane + 1];
-        const float e = sc[t];
-        o0 = fmaf(e, v0, o0);
-        o1 = fmaf(e, v1, o1);
-      }
-    }
+    const float e = sc[t];
+    o0 = fmaf(e, v0, o0);
+    o1 = fmaf(e, v1, o1);
   }
   op[warp][2 * lane] = o0;
   op[warp][2 * lane + 1] = o1;
@@ -683,8 +723,15 @@ int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, floa
                      cudaStream_t stream) {
   DM_REQUIRE(qkv.p != nullptr && qkv.n == 3 * st.d && qkv.bias != nullptr, "self-attn: qkv partials");
   DM_REQUIRE(st.page_tokens == 64 && st.pages_per_slot * 64 <= kSaMaxKeys, "self-attn: page geometry");
-  DM_CHECK_CUDA(launch_pdl(self_attn_kernel, dim3(kRows, st.heads), dim3(kSaThreads), 0, stream,
-                           st, layer, qkv, q_scale));
+  const int smem = kSaPrePages * 2 * kSaPageBytes + 16;
+  static bool attr = false;
+  if (!attr) {
+    DM_CHECK_CUDA(cudaFuncSetAttribute(self_attn_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  DM_CHECK_CUDA(launch_pdl(self_attn_kernel, dim3(kRows, st.heads), dim3(kSaThreads), smem,
+                           stream, st, layer, qkv, q_scale));
   return 0;
 }
 
