@@ -114,32 +114,35 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
       }
     }
   } else if (warp == 1) {
+    // Issue order per tile t: PV_t(j) then S_t(j + 1) as soon as softmax_t(j)
+    // has published P_t(j) (which also frees S_t), so each tile's next scores
+    // never wait on the other tile's softmax.
     constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128);
     constexpr uint32_t idesc_o = umma_idesc_bf16(128, 64);
     mbar_wait(q_full, 0);
+    auto issue_s = [&](int t, int j) {           // S_t = Q_t K_j^T
+      const uint32_t sk = smem_u32(smem + AttnSmemLayout::k + (j % kAttnKS) * kKBytes);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t sq = smem_u32(smem + AttnSmemLayout::q + t * kQBytes);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_bf16_ss(tmem + t * 128, umma_desc_sw128(sq + kk * 32),
+                       umma_desc_sw128(sk + kk * 32), idesc_s, kk != 0);
+        umma_commit(&s_full[t]);
+      }
+      __syncwarp();
+    };
+    mbar_wait(&kv_full[0], 0);
+    issue_s(0, 0);
+    issue_s(1, 0);
     for (int j = 0; j < nb; ++j) {
       const int st = j % kAttnKS;
       const uint32_t ph = j & 1;
-      mbar_wait(&kv_full[st], (j / kAttnKS) & 1);
-      const uint32_t sk = smem_u32(smem + AttnSmemLayout::k + st * kKBytes);
       const uint32_t sv = smem_u32(smem + AttnSmemLayout::v + st * kVBytes);
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {          // S_t = Q_t K_j^T
-        mbar_wait(&s_empty[t], ph ^ 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t sq = smem_u32(smem + AttnSmemLayout::q + t * kQBytes);
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            umma_bf16_ss(tmem + t * 128, umma_desc_sw128(sq + kk * 32),
-                         umma_desc_sw128(sk + kk * 32), idesc_s, kk != 0);
-          umma_commit(&s_full[t]);
-        }
-        __syncwarp();
-      }
-#pragma unroll
       for (int t = 0; t < 2; ++t) {          // PV_t = P_t V_j
-        mbar_wait(&p_full[t], ph);
+        mbar_wait(&p_full[t], ph);           // (softmax_t(j) done: S_t is free as well)
         mbar_wait(&o_empty[t], ph ^ 1);
         tc_fence_after();
         if (elect_one()) {
@@ -155,6 +158,11 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
           if (t == 1) umma_commit(&kv_empty[st]);
         }
         __syncwarp();
+        if (j + 1 < nb) {
+          if (t == 0) mbar_wait(&kv_full[(j + 1) % kAttnKS], ((j + 1) / kAttnKS) & 1);
+          mbar_wait(&s_empty[t], ph);
+          issue_s(t, j + 1);
+        }
       }
     }
   } else {

@@ -10,7 +10,7 @@ from paper_2507_01021_b200.models import get_model
 
 rows = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 which = [int(w) for w in (sys.argv[2] if len(sys.argv) > 2 else "0").split(",")]
-model = sys.argv[3] if len(sys.argv) > 3 else "whisper-base"
+model = sys.argv[3] if len(sys.argv) > 3 and not sys.argv[3].startswith("--") else "whisper-base"
 dims = get_model(model)
 eng = WhisperGPU(dims, max_slots=64, max_encode_batch=32)
 seg = np.random.default_rng(0).integers(-8000, 8000, size=160000, dtype=np.int16)
@@ -19,7 +19,8 @@ for i in range(0, 64, 32):
     eng.encode([seg] * 32, slots[i:i + 32])
 eng.admit(slots, [200] * 64)
 eng.set_active(slots[:rows])
-eng.step(40)
+if "--nostep" not in sys.argv:
+    eng.step(40)
 torch.cuda.synchronize()
 for w in which:
     us = 1000 * eng.time_kernel(w, 0, 5)
