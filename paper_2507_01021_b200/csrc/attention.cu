@@ -114,9 +114,9 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
       }
     }
   } else if (warp == 1) {
-    // Issue order per tile t: PV_t(j) then S_t(j + 1) as soon as softmax_t(j)
-    // has published P_t(j) (which also frees S_t), so each tile's next scores
-    // never wait on the other tile's softmax.
+    // Issue order per tile t: as soon as softmax_t(j) has published P_t(j)
+    // (which also frees S_t): S_t(j + 1), then PV_t(j). Each tile's next
+    // scores neither wait on the other tile's softmax nor queue behind PV.
     constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128);
     constexpr uint32_t idesc_o = umma_idesc_bf16(128, 64);
     mbar_wait(q_full, 0);
@@ -141,9 +141,15 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
       const uint32_t ph = j & 1;
       const uint32_t sv = smem_u32(smem + AttnSmemLayout::v + st * kVBytes);
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {          // PV_t = P_t V_j
-        mbar_wait(&p_full[t], ph);           // (softmax_t(j) done: S_t is free as well)
-        mbar_wait(&o_empty[t], ph ^ 1);
+      for (int t = 0; t < 2; ++t) {
+        mbar_wait(&p_full[t], ph);           // softmax_t(j) done: P_t(j) written, S_t free
+        // S_t(j + 1) first: the tile's next softmax starts while PV_t(j) runs
+        if (j + 1 < nb) {
+          if (t == 0) mbar_wait(&kv_full[(j + 1) % kAttnKS], ((j + 1) / kAttnKS) & 1);
+          mbar_wait(&s_empty[t], ph);
+          issue_s(t, j + 1);
+        }
+        mbar_wait(&o_empty[t], ph ^ 1);      // PV_t = P_t V_j
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sp = smem_u32(smem + AttnSmemLayout::p + t * kPBytes);
@@ -158,11 +164,6 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
           if (t == 1) umma_commit(&kv_empty[st]);
         }
         __syncwarp();
-        if (j + 1 < nb) {
-          if (t == 0) mbar_wait(&kv_full[(j + 1) % kAttnKS], ((j + 1) / kAttnKS) & 1);
-          mbar_wait(&s_empty[t], ph);
-          issue_s(t, j + 1);
-        }
       }
     }
   } else {
