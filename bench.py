@@ -352,7 +352,7 @@ def measure_roofline(eng, dims, args) -> dict:
     if tf.exists():     # dram read+write of one ncu --set full capture (64 rows), scaled to rows
         t = _j.loads(tf.read_text())
         traffic = (t["dram_bytes_read"] + t["dram_bytes_write"]) * rows / t["rows"]
-    return {"kernel": "dec_attn_kernel<cross> (decode K6)", "bound": "hbm", "achieved": achieved,
+    return {"kernel": "cross_attn_kernel (decode K6)", "bound": "hbm", "achieved": achieved,
             "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
             "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/r01_xattn_traffic.json)",
             "timing": "CUDA events on the engine stream around a graph of 20 back-to-back launches "
