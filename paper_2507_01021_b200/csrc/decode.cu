@@ -584,6 +584,9 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
   pdl_trigger();
   if (r >= *st.n_active) return;                 // host-set: safe before the wait
   const int slot = st.active[r];
+  // a slot that finished (EOT / cap) in an earlier step stays in the active
+  // list until the host's next poll; its outputs are never read again
+  if (st.done[slot]) return;
   const int d = st.d, H = st.heads, L = st.layers;
   const int p = st.pos[slot];                    // final since the previous step
   const int np = min(ceil_div(p, 64), kSaPrePages);   // staged pages of positions < p
@@ -757,6 +760,7 @@ cross_attn_kernel(const DecodeState st, int layer, const Partials xq, float q_sc
   pdl_trigger();
   if (r >= *st.n_active) return;                 // whole cluster (same row) leaves together
   const int slot = st.active[r];
+  if (st.done[slot]) return;                     // finished in an earlier step (see self-attn)
   const int d = st.d, H = st.heads;
   const int k0 = sp * kXaKeys, nk = min(1500, k0 + kXaKeys) - k0;
   uint8_t* Ks = xa_smem;

@@ -141,8 +141,45 @@ __global__ void fill_normal_kernel(uint16_t* dst, uint64_t n, uint64_t key, floa
   }
 }
 
+// ------------------------------------------------------------ upload ring
+// Pinned host chunks for the small stream-ordered uploads (slot ids, page
+// table, admission args, active lists). A chunk is reused only after the copy
+// that read it has executed (its event), so no call has to drain the stream.
+struct UploadRing {
+  static constexpr int kN = 16;
+  static constexpr size_t kChunk = 16 * 1024;
+  uint8_t* host = nullptr;
+  cudaEvent_t ev[kN] = {};
+  bool used[kN] = {};
+  int next = 0;
+  int init() {
+    DM_CHECK_CUDA(cudaMallocHost(&host, kN * kChunk));
+    for (int i = 0; i < kN; ++i) DM_CHECK_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    return 0;
+  }
+  ~UploadRing() {
+    for (int i = 0; i < kN; ++i)
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    if (host) cudaFreeHost(host);
+  }
+  // copy `bytes` from host memory to `dev` in stream order
+  int upload(void* dev, const void* src, size_t bytes, cudaStream_t s) {
+    DM_REQUIRE(bytes <= kChunk, "upload larger than a staging chunk");
+    const int i = next;
+    next = (next + 1) % kN;
+    if (used[i]) DM_CHECK_CUDA(cudaEventSynchronize(ev[i]));
+    std::memcpy(host + i * kChunk, src, bytes);
+    DM_CHECK_CUDA(cudaMemcpyAsync(dev, host + i * kChunk, bytes, cudaMemcpyHostToDevice, s));
+    DM_CHECK_CUDA(cudaEventRecord(ev[i], s));
+    used[i] = true;
+    return 0;
+  }
+};
+
 // ------------------------------------------------------------ Whisper engine
 struct WhisperEngine {
+  UploadRing ring;
+  int32_t* admit_args_dev = nullptr;   // [2 * max_slots]
   dm_whisper_config cfg;
   int d, H, L, Ld, F, nm, Cp;
   // weights
@@ -280,6 +317,8 @@ static int engine_init(WhisperEngine* e) {
   if (e->alloc_t(&e->enc_out, rows * d, false)) return 2;
   if (e->alloc_t(&e->slot_dev, E)) return 2;
   DM_CHECK_CUDA(cudaMallocHost(&e->slot_host, sizeof(int32_t) * E));
+  if (int rc = e->ring.init()) return rc;
+  if (e->alloc_t(&e->admit_args_dev, size_t(2) * S)) return 2;
   DM_CHECK_CUDA(cudaMallocHost(&e->staging, sizeof(int32_t) * (64 * 65 + 4096 + 256)));
 
   // decode state
@@ -637,10 +676,7 @@ int dm_whisper_encode(void* handle, const int16_t* pcm, const int64_t* offsets,
   for (int i = 0; i < n; ++i)
     DM_REQUIRE(slot_ids[i] >= 0 && slot_ids[i] < e->cfg.max_slots, "slot id out of range");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  DM_CHECK_CUDA(cudaStreamSynchronize(s));   // slot_host staging reuse
-  std::memcpy(e->slot_host, slot_ids, sizeof(int32_t) * n);
-  DM_CHECK_CUDA(cudaMemcpyAsync(e->slot_dev, e->slot_host, sizeof(int32_t) * n,
-                                cudaMemcpyHostToDevice, s));
+  if (int rc = e->ring.upload(e->slot_dev, slot_ids, sizeof(int32_t) * n, s)) return rc;
   e->last_n = n;
   e->encodes += 1;
   e->segments += n;
@@ -679,7 +715,7 @@ int dm_whisper_admit(void* handle, const int32_t* slot_ids, const int32_t* caps,
     set_error("self-KV page pool exhausted");
     return 3;
   }
-  DM_CHECK_CUDA(cudaStreamSynchronize(s));   // staging reuse
+  std::vector<int32_t> args(size_t(2) * n);
   for (int i = 0; i < n; ++i) {
     const int slot = slot_ids[i];
     const int np = ceil_div(e->cfg.prompt_len + caps[i], 64);
@@ -692,18 +728,16 @@ int dm_whisper_admit(void* handle, const int32_t* slot_ids, const int32_t* caps,
       e->page_table_host[size_t(slot) * 7 + p] = page;
     }
     e->slot_pages[slot] = np;
-    e->staging[2 * i] = slot;
-    e->staging[2 * i + 1] = caps[i];
+    args[2 * i] = slot;
+    args[2 * i + 1] = caps[i];
   }
-  DM_CHECK_CUDA(cudaMemcpyAsync(e->page_table_dev, e->page_table_host.data(),
-                                sizeof(int32_t) * e->page_table_host.size(),
-                                cudaMemcpyHostToDevice, s));
-  int32_t* args = e->staging + 4096;
-  std::memcpy(args, e->staging, sizeof(int32_t) * 2 * n);
-  admit_kernel<<<ceil_div(n, 64), 64, 0, s>>>(e->st, args, n);
+  if (int rc = e->ring.upload(e->page_table_dev, e->page_table_host.data(),
+                              sizeof(int32_t) * e->page_table_host.size(), s))
+    return rc;
+  if (int rc = e->ring.upload(e->admit_args_dev, args.data(), sizeof(int32_t) * 2 * n, s)) return rc;
+  admit_kernel<<<ceil_div(n, 64), 64, 0, s>>>(e->st, e->admit_args_dev, n);
   DM_CHECK_LAUNCH();
   e->launches += 1;
-  DM_CHECK_CUDA(cudaStreamSynchronize(s));   // host table / staging consumed
   return 0;
 }
 
@@ -725,26 +759,24 @@ int dm_whisper_set_active(void* handle, const int32_t* slot_ids, int n, void* st
   DM_REQUIRE(e != nullptr, "null handle");
   DM_REQUIRE(n >= 0 && n <= e->cfg.max_slots, "bad n");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  DM_CHECK_CUDA(cudaStreamSynchronize(s));
   const int G = int(e->groups.size());
-  // staging layout per group: [count, slots...] at stride kRows + 1
-  for (int g = 0; g < G; ++g) e->staging[g * (kRows + 1)] = 0;
+  // per group: [count, slots...]; uploads are stream-ordered after any step
+  // graph already queued, which still sees the previous active list
+  std::vector<int32_t> rows(size_t(G) * (kRows + 1), 0);
   for (int i = 0; i < n; ++i) {
     DM_REQUIRE(slot_ids[i] >= 0 && slot_ids[i] < e->cfg.max_slots, "slot id out of range");
     const int g = slot_ids[i] % G;
-    int32_t* row = e->staging + g * (kRows + 1);
+    int32_t* row = rows.data() + g * (kRows + 1);
     DM_REQUIRE(row[0] < kRows, "too many active slots in one decode group");
     row[1 + row[0]++] = slot_ids[i];
   }
   for (int g = 0; g < G; ++g) {
-    int32_t* row = e->staging + g * (kRows + 1);
-    DM_CHECK_CUDA(cudaMemcpyAsync(e->groups[g].n_active_dev, row, sizeof(int32_t),
-                                  cudaMemcpyHostToDevice, s));
+    int32_t* row = rows.data() + g * (kRows + 1);
+    if (int rc = e->ring.upload(e->groups[g].n_active_dev, row, sizeof(int32_t), s)) return rc;
     if (row[0])
-      DM_CHECK_CUDA(cudaMemcpyAsync(e->groups[g].active_dev, row + 1, sizeof(int32_t) * row[0],
-                                    cudaMemcpyHostToDevice, s));
+      if (int rc = e->ring.upload(e->groups[g].active_dev, row + 1, sizeof(int32_t) * row[0], s))
+        return rc;
   }
-  DM_CHECK_CUDA(cudaStreamSynchronize(s));
   return 0;
 }
 

@@ -133,13 +133,19 @@ class WhisperGPU:
             _native.check(self.lib.dm_whisper_create(C.byref(cfg), C.c_void_p(self.blob.data_ptr()),
                                                      arr, len(offs), C.byref(h)))
             self.handle = h
-            # pinned staging for PCM uploads + device buffers
-            self._pcm_host = torch.empty(max_encode_batch * N_SAMPLES, dtype=torch.int16,
-                                         pin_memory=True)
-            self._pcm_dev = torch.empty(max_encode_batch * N_SAMPLES, dtype=torch.int16,
-                                        device=self.device)
-            self._meta_host = torch.empty(3 * max_encode_batch, dtype=torch.int64, pin_memory=True)
-            self._meta_dev = torch.empty(3 * max_encode_batch, dtype=torch.int64, device=self.device)
+            # double-buffered pinned staging for PCM uploads + device buffers: the
+            # host copy of encode batch k + 1 overlaps the GPU work of batch k
+            self._pcm_host = [torch.empty(max_encode_batch * N_SAMPLES, dtype=torch.int16,
+                                          pin_memory=True) for _ in range(2)]
+            self._pcm_dev = [torch.empty(max_encode_batch * N_SAMPLES, dtype=torch.int16,
+                                         device=self.device) for _ in range(2)]
+            self._meta_host = [torch.empty(3 * max_encode_batch, dtype=torch.int64,
+                                           pin_memory=True) for _ in range(2)]
+            self._meta_dev = [torch.empty(3 * max_encode_batch, dtype=torch.int64,
+                                          device=self.device) for _ in range(2)]
+            self._up_done = [torch.cuda.Event() for _ in range(2)]
+            self._up_used = [False, False]
+            self._up_next = 0
             self._done = np.zeros(max_slots, np.int32)
             self._ngen = np.zeros(max_slots, np.int32)
             self._tokens = np.zeros(max_slots * MAX_TOKENS, np.int32)
@@ -172,20 +178,33 @@ class WhisperGPU:
         """Register a device int16 buffer that ResidentPCM jobs index into."""
         self._resident = pcm_dev
 
+    def _stage(self) -> int:
+        """Next staging buffer; waits only for the copy that last read it."""
+        b = self._up_next
+        self._up_next ^= 1
+        if self._up_used[b]:
+            self._up_done[b].synchronize()
+        return b
+
     def upload_segments(self, segs: Sequence[np.ndarray]):
         """Trim (pad_or_trim's truncation; padding is implicit in the kernel)
-        and copy PCM to the device. Returns (pcm, offsets, lengths) pointers."""
+        and copy PCM to the device (stream-ordered, double-buffered). Returns
+        (pcm, offsets, lengths) device pointers."""
         n = len(segs)
+        b = self._stage()
+        mh, md = self._meta_host[b], self._meta_dev[b]
         if n and all(isinstance(s, ResidentPCM) for s in segs):
-            meta = self._meta_host.numpy()
+            meta = mh.numpy()
             meta[:n] = [s.offset for s in segs]
             meta[n:].view(np.int32)[:n] = [min(s.length, N_SAMPLES) for s in segs]
             with torch.cuda.stream(self.stream):
-                self._meta_dev.copy_(self._meta_host, non_blocking=True)
-            self.stream.synchronize()
-            return (C.c_void_p(self._resident.data_ptr()), C.c_void_p(self._meta_dev.data_ptr()),
-                    C.c_void_p(self._meta_dev.data_ptr() + 8 * n))
-        host = self._pcm_host.numpy()
+                md.copy_(mh, non_blocking=True)
+                self._up_done[b].record(self.stream)
+            self._up_used[b] = True
+            return (C.c_void_p(self._resident.data_ptr()), C.c_void_p(md.data_ptr()),
+                    C.c_void_p(md.data_ptr() + 8 * n))
+        ph, pd = self._pcm_host[b], self._pcm_dev[b]
+        host = ph.numpy()
         offs, lens = [], []
         pos = 0
         for s in segs:
@@ -197,19 +216,18 @@ class WhisperGPU:
             offs.append(pos)
             lens.append(k)
             pos += k
-        meta = self._meta_host.numpy()
+        meta = mh.numpy()
         meta[:n] = offs
         meta32 = meta[n:].view(np.int32)     # lengths packed after offsets
         meta32[:n] = lens
         with torch.cuda.stream(self.stream):
             if pos:
-                self._pcm_dev[:pos].copy_(self._pcm_host[:pos], non_blocking=True)
-            self._meta_dev.copy_(self._meta_host, non_blocking=True)
+                pd[:pos].copy_(ph[:pos], non_blocking=True)
+            md.copy_(mh, non_blocking=True)
+            self._up_done[b].record(self.stream)
+        self._up_used[b] = True
         self.h2d_bytes += 2 * pos + 12 * n
-        pcm = C.c_void_p(self._pcm_dev.data_ptr())
-        offp = C.c_void_p(self._meta_dev.data_ptr())
-        lenp = C.c_void_p(self._meta_dev.data_ptr() + 8 * n)
-        return pcm, offp, lenp
+        return C.c_void_p(pd.data_ptr()), C.c_void_p(md.data_ptr()), C.c_void_p(md.data_ptr() + 8 * n)
 
     def encode(self, segs: Sequence[np.ndarray], slots: Sequence[int]) -> None:
         pcm, offp, lenp = self.upload_segments(segs)
