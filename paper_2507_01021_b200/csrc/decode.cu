@@ -31,6 +31,33 @@ __device__ __forceinline__ void split_hilo(float v, uint16_t& hi, uint16_t& lo) 
   lo = f32_to_bf16(v - bf16_to_f32(hi));
 }
 
+// Sum of up to kMaxSplits K-split partials p[s * stride] in split order. All
+// loads are issued before the first add (a runtime-trip loop would serialise
+// one L2 round trip per split on the consumer's critical path).
+constexpr int kMaxSplits = 8;
+__device__ __forceinline__ float sum_splits(const float* p, size_t stride, int splits) {
+  float v[kMaxSplits];
+#pragma unroll
+  for (int s = 0; s < kMaxSplits; ++s) v[s] = s < splits ? __ldcg(p + s * stride) : 0.f;
+  float a = v[0];
+#pragma unroll
+  for (int s = 1; s < kMaxSplits; ++s)
+    if (s < splits) a += v[s];
+  return a;
+}
+__device__ __forceinline__ float4 sum_splits4(const float* p, size_t stride, int splits) {
+  float4 v[kMaxSplits];
+#pragma unroll
+  for (int s = 0; s < kMaxSplits; ++s)
+    v[s] = s < splits ? __ldcg(reinterpret_cast<const float4*>(p + s * stride))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 a = v[0];
+#pragma unroll
+  for (int s = 1; s < kMaxSplits; ++s)
+    if (s < splits) { a.x += v[s].x; a.y += v[s].y; a.z += v[s].z; a.w += v[s].w; }
+  return a;
+}
+
 // ------------------------------------------------------------ cluster / bulk-copy PTX
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
@@ -115,7 +142,7 @@ constexpr int kSmemOptin = 232448;             // 227 KB per CTA (sm_100)
 
 __host__ __device__ constexpr int gemv_smem_bytes(int kb_per, int stages, int epi, int rgroups) {
   return 1024 + kb_per * 2 * (kGvXBytes / rgroups) + stages * kGvWBytes +
-         (epi == GV_ARGMAX ? kGvTr : 0) + kGvMisc;
+         (epi != GV_PARTIAL ? kGvTr : 0) + kGvMisc;
 }
 
 template <int EPI, bool SPLIT>
@@ -128,8 +155,8 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
   const int kb_per = a.kb_per, NS = a.stages;
   uint8_t* xs = smem;                                        // [kb][hi | lo], RG rows each
   uint8_t* ws = xs + kb_per * 2 * (kRows / int(gridDim.z)) * 128;   // [stage] 16K
-  float* tr = reinterpret_cast<float*>(ws + NS * kGvWBytes); // GV_ARGMAX
-  uint8_t* misc = reinterpret_cast<uint8_t*>(tr) + (EPI == GV_ARGMAX ? kGvTr : 0);
+  float* tr = reinterpret_cast<float*>(ws + NS * kGvWBytes); // GV_ARGMAX / GELU staging
+  uint8_t* misc = reinterpret_cast<uint8_t*>(tr) + (EPI != GV_PARTIAL ? kGvTr : 0);
   uint64_t* wfull = reinterpret_cast<uint64_t*>(misc);
   uint64_t* wempty = wfull + kGvMaxStages;
   uint64_t* xfull = wempty + kGvMaxStages;
@@ -169,7 +196,7 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 128);
+  if (warp == 1) tmem_alloc(tmem_slot, 256);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -194,17 +221,21 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
       trace_mark(st, 1);
       mbar_arrive_expect_tx(xfull, kb_per * 2 * G * kGvXBox * 128);
       for (int i = 0; i < kb_per; ++i) {
-        uint8_t* xb = xs + i * 2 * XB;
+        uint8_t* xb = xs + i * 2 * XB;          // [hi: Np rows | lo: Np rows], 128 B rows
         for (int g = 0; g < G; ++g) {
           tma_load_2d(xb + g * kGvXBox * 128, &txh, xfull, (kb0 + i) * 64, r0 + g * kGvXBox);
-          tma_load_2d(xb + XB + g * kGvXBox * 128, &txl, xfull, (kb0 + i) * 64, r0 + g * kGvXBox);
+          tma_load_2d(xb + (Np + g * kGvXBox) * 128, &txl, xfull, (kb0 + i) * 64, r0 + g * kGvXBox);
         }
       }
       for (int q = pre; q < total; ++q) issue_w(q);
     }
   } else if (warp == 1) {
-    const uint32_t idesc = umma_idesc_bf16(128, Np);
+    // one MMA per k-step: B = [x_hi rows ; x_lo rows] (N = 2 Np), so the
+    // weight tile (the A operand, the smem-read-bound side at small N) is read
+    // once for both halves; D columns [0, Np) hold W.x_hi, [Np, 2 Np) W.x_lo
+    const uint32_t idesc = umma_idesc_bf16(128, 2 * Np);
     mbar_wait(xfull, 0);
+    if (lane == 0) trace_mark(st, 4);
     int wi = 0, it = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
       const int buf = it & 1;
@@ -216,14 +247,11 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
         tc_fence_after();
         if (elect_one()) {
           const uint32_t sw = smem_u32(ws + s * kGvWBytes);
-          const uint32_t sh = smem_u32(xs + i * 2 * XB), sl = sh + XB;
+          const uint32_t sh = smem_u32(xs + i * 2 * XB);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            umma_bf16_ss(tmem + buf * 64, umma_desc_sw128(sw + k * 32),
+          for (int k = 0; k < 4; ++k)
+            umma_bf16_ss(tmem + buf * 128, umma_desc_sw128(sw + k * 32),
                          umma_desc_sw128(sh + k * 32), idesc, (i | k) != 0);
-            umma_bf16_ss(tmem + buf * 64, umma_desc_sw128(sw + k * 32),
-                         umma_desc_sw128(sl + k * 32), idesc, 1);
-          }
           umma_commit(&wempty[s]);
           if (i == kb_per - 1) umma_commit(&tm_full[buf]);
         }
@@ -250,18 +278,29 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
       const int buf = it & 1;
       mbar_wait(&tm_full[buf], (it >> 1) & 1);
       tc_fence_after();
+      if (et == 0) trace_mark(st, 5);
       float v0[32], v1[32];
       {
+        // row r: W.x_hi (column r) + W.x_lo (column Np + r)
+        const uint32_t base = tmem + (uint32_t(quad * 32) << 16) + buf * 128;
         uint32_t rr[32];
-        tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + buf * 64, rr);
+        tmem_ld32(base, rr);
         tmem_wait_ld();
 #pragma unroll
         for (int i = 0; i < 32; ++i) v0[i] = __uint_as_float(rr[i]);
+        tmem_ld32(base + Np, rr);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v0[i] += __uint_as_float(rr[i]);
         if (Np > 32) {
-          tmem_ld32(tmem + (uint32_t(quad * 32) << 16) + buf * 64 + 32, rr);
+          tmem_ld32(base + 32, rr);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) v1[i] = __uint_as_float(rr[i]);
+          tmem_ld32(base + Np + 32, rr);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v1[i] += __uint_as_float(rr[i]);
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v1[i] = 0.f;
@@ -318,11 +357,18 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
         if (nvalid) {
           uint16_t* __restrict__ yh = a.yh + size_t(r0) * a.N + n;
           uint16_t* __restrict__ yl = a.yl + size_t(r0) * a.N + n;
+          // stage the rows in this thread's smem column (conflict-free), then
+          // one compact loop over the active rows (no unrolled erf copies)
+          float* col = tr + f;
 #pragma unroll
-          for (int i = 0; i < 64; ++i) {
-            if (i >= R) break;
+          for (int i = 0; i < 32; ++i) {
+            col[i * 129] = v0[i];
+            col[(32 + i) * 129] = v1[i];
+          }
+#pragma unroll 1
+          for (int i = 0; i < R; ++i) {
             uint16_t hi, lo;
-            split_hilo(gelu_erf((i < 32 ? v0[i] : v1[i - 32]) + b), hi, lo);
+            split_hilo(gelu_erf(col[i * 129] + b), hi, lo);
             yh[size_t(i) * a.N] = hi;
             yl[size_t(i) * a.N] = lo;
           }
@@ -362,12 +408,13 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
       }
     }
   }
+  if (warp >= 2 && lane == 0) trace_mark(st, 6);
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) trace_mark(st, 3);
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 128);
+    tmem_dealloc(tmem, 256);
   }
 }
 
@@ -378,11 +425,18 @@ GemvArgs gemv_plan(int N, int K, int epi) {
   a.epi = epi;
   const int KB = K / 64;
   if (epi == GV_PARTIAL) {
-    // largest divisor of KB that is <= 4: activation slice <= 64 KB and the
-    // whole weight slice of a tile prefetched before the dependency wait
+    // largest divisor of KB that is <= 2: the whole weight slice of a tile is
+    // prefetched before the dependency wait, and the per-CTA MMA time (bound
+    // by reading the weight tile from smem) stays short
     a.kb_per = 1;
-    for (int k = 1; k <= 4 && k <= KB; ++k)
+    for (int k = 1; k <= 2 && k <= KB; ++k)
       if (KB % k == 0) a.kb_per = k;
+    // ... but at most 8 partial sums for the consumer to reduce
+    while (KB / a.kb_per > 8 && a.kb_per < KB) {
+      int k = a.kb_per + 1;
+      while (KB % k) ++k;
+      a.kb_per = k;
+    }
   } else {
     // non-linear epilogue: as few K splits as fit (<= 8 k-blocks per CTA)
     a.kb_per = KB;
@@ -493,11 +547,8 @@ __global__ void __launch_bounds__(320) ln_kernel(const DecodeState st, const LnA
     reinterpret_cast<float4*>(xr)[t] = x;
   } else if (MODE == 2) {
     x = __ldcg(reinterpret_cast<const float4*>(xr) + t);
-    float4 acc = __ldcg(reinterpret_cast<const float4*>(a.res.p + size_t(r) * a.res.n) + t);
-    for (int s = 1; s < a.res.splits; ++s) {
-      const float4 q = __ldcg(reinterpret_cast<const float4*>(a.res.p + (size_t(s) * kRows + r) * a.res.n) + t);
-      acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
-    }
+    const float4 acc = sum_splits4(a.res.p + size_t(r) * a.res.n + 4 * t,
+                                   size_t(kRows) * a.res.n, a.res.splits);
     x.x += acc.x + rb.x; x.y += acc.y + rb.y; x.z += acc.z + rb.z; x.w += acc.w + rb.w;
     reinterpret_cast<float4*>(xr)[t] = x;
   } else {
@@ -521,7 +572,8 @@ __global__ void __launch_bounds__(320) ln_kernel(const DecodeState st, const LnA
 
 int launch_ln(const DecodeState& st, const LnArgs& a, cudaStream_t stream) {
   DM_REQUIRE(st.d % 128 == 0 && st.d / 4 <= 320, "LayerNorm: d must be a multiple of 128, <= 1280");
-  DM_REQUIRE(a.mode != 2 || (a.res.p != nullptr && a.res.splits >= 1 && a.res.n == st.d),
+  DM_REQUIRE(a.mode != 2 || (a.res.p != nullptr && a.res.splits >= 1 &&
+                             a.res.splits <= kMaxSplits && a.res.n == st.d),
              "LayerNorm: residual partials missing");
   const dim3 grid(kRows), block(st.d / 4);
   switch (a.mode) {
@@ -616,13 +668,10 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
   if (tid < 64) {
     const int c = h * 64 + tid;
     const float* pp = qkv.p + size_t(r) * qkv.n + c;
-    float aq = __ldcg(pp), ak = __ldcg(pp + d), av = __ldcg(pp + 2 * d);
-    for (int s = 1; s < qkv.splits; ++s) {
-      const float* ps = pp + size_t(s) * kRows * qkv.n;
-      aq += __ldcg(ps);
-      ak += __ldcg(ps + d);
-      av += __ldcg(ps + 2 * d);
-    }
+    const size_t sstr = size_t(kRows) * qkv.n;
+    const float aq = sum_splits(pp, sstr, qkv.splits);
+    const float ak = sum_splits(pp + d, sstr, qkv.splits);
+    const float av = sum_splits(pp + 2 * d, sstr, qkv.splits);
     const uint16_t kb = f32_to_bf16(ak + bk), vb = f32_to_bf16(av + bv);
     const size_t kbase = ((size_t(pt[p >> 6]) * L + layer) * 2 * H + h) * 64 * 64 + size_t(p & 63) * 64;
     st.kv_pool[kbase + tid] = kb;
@@ -724,7 +773,8 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
 
 int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, float q_scale,
                      cudaStream_t stream) {
-  DM_REQUIRE(qkv.p != nullptr && qkv.n == 3 * st.d && qkv.bias != nullptr, "self-attn: qkv partials");
+  DM_REQUIRE(qkv.p != nullptr && qkv.n == 3 * st.d && qkv.bias != nullptr &&
+                 qkv.splits >= 1 && qkv.splits <= kMaxSplits, "self-attn: qkv partials");
   DM_REQUIRE(st.page_tokens == 64 && st.pages_per_slot * 64 <= kSaMaxKeys, "self-attn: page geometry");
   const int smem = kSaPrePages * 2 * kSaPageBytes + 16;
   static bool attr = false;
@@ -760,7 +810,8 @@ cross_attn_kernel(const DecodeState st, int layer, const Partials xq, float q_sc
   pdl_trigger();
   if (r >= *st.n_active) return;                 // whole cluster (same row) leaves together
   const int slot = st.active[r];
-  if (st.done[slot]) return;                     // finished in an earlier step (see self-attn)
+  // (no done-slot early exit here: it would put a dependent load in front of
+  // the K/V prefetch of every CTA)
   const int d = st.d, H = st.heads;
   const int k0 = sp * kXaKeys, nk = min(1500, k0 + kXaKeys) - k0;
   uint8_t* Ks = xa_smem;
@@ -788,8 +839,7 @@ cross_attn_kernel(const DecodeState st, int layer, const Partials xq, float q_sc
   if (tid == 0) trace_mark(st, 1);
   if (tid < 64) {
     const float* pp = xq.p + size_t(r) * xq.n + h * 64 + tid;
-    float a = __ldcg(pp);
-    for (int s = 1; s < xq.splits; ++s) a += __ldcg(pp + size_t(s) * kRows * xq.n);
+    const float a = sum_splits(pp, size_t(kRows) * xq.n, xq.splits);
     qs[tid] = (a + bq) * q_scale;
   }
   __syncthreads();
@@ -874,7 +924,8 @@ cross_attn_kernel(const DecodeState st, int layer, const Partials xq, float q_sc
 
 int launch_cross_attn(const DecodeState& st, int layer, const Partials& xq, float q_scale,
                       cudaStream_t stream) {
-  DM_REQUIRE(xq.p != nullptr && xq.n == st.d && xq.bias != nullptr, "cross-attn: q partials");
+  DM_REQUIRE(xq.p != nullptr && xq.n == st.d && xq.bias != nullptr && xq.splits >= 1 &&
+                 xq.splits <= kMaxSplits, "cross-attn: q partials");
   static bool attr = false;
   if (!attr) {
     DM_CHECK_CUDA(cudaFuncSetAttribute(cross_attn_kernel,

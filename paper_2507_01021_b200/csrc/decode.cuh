@@ -66,8 +66,9 @@ struct DecodeState {
   float* amax_val;             // [vocab tiles, kRows]
   int32_t* amax_idx;           // [vocab tiles, kRows]
   float* logits_dbg;           // optional [kRows, vocab]
-  // optional timeline tap (debug): per kernel of the step [128][4] globaltimer ns:
-  // min CTA entry, min / max dependency release (after griddepcontrol.wait), max exit
+  // optional timeline tap (debug): per kernel of the step [128][8] globaltimer ns:
+  // min CTA entry, min / max dependency release (after griddepcontrol.wait), max exit,
+  // then kernel-specific max stamps 4..7 (GEMV: operand landed, MMA done, stores issued)
   unsigned long long* trace;
   int trace_id;
 };
@@ -77,14 +78,14 @@ __device__ __forceinline__ unsigned long long global_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// which: 0 entry, 1 released (records min and max), 3 exit
+// which: 0 entry, 1 released (records min and max), 3 exit, 4..7 max stamps
 __device__ __forceinline__ void trace_mark(const DecodeState& st, int which) {
   if (st.trace == nullptr) return;
   const unsigned long long t = global_ns();
-  unsigned long long* p = st.trace + st.trace_id * 4;
+  unsigned long long* p = st.trace + st.trace_id * 8;
   if (which == 0) atomicMin(p, t);
   else if (which == 1) { atomicMin(p + 1, t); atomicMax(p + 2, t); }
-  else atomicMax(p + 3, t);
+  else atomicMax(p + which, t);
 }
 
 // K-split partial sums of a linear projection: part[s][row][n] (fp32, no bias),

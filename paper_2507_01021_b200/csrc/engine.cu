@@ -922,7 +922,7 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
     case 10: {       // step timeline tap on (graph re-captured with per-kernel globaltimer marks)
       if (!e->groups[0].st.trace) {
         unsigned long long* t = nullptr;
-        if (e->alloc_t(&t, 128 * 4)) return 2;
+        if (e->alloc_t(&t, 128 * 8)) return 2;
         e->groups[0].st.trace = t;
         if (int rc = build_step_graph(e)) return rc;
       }
@@ -930,8 +930,8 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
     }
     case 11: {       // reset the timeline (entry/release minima to +inf, maxima to 0)
       DM_REQUIRE(e->groups[0].st.trace != nullptr, "timeline tap not enabled");
-      std::vector<unsigned long long> init(128 * 4, 0ull);
-      for (int k = 0; k < 128; ++k) init[k * 4] = init[k * 4 + 1] = ~0ull;
+      std::vector<unsigned long long> init(128 * 8, 0ull);
+      for (int k = 0; k < 128; ++k) init[k * 8] = init[k * 8 + 1] = ~0ull;
       DM_CHECK_CUDA(cudaMemcpyAsync(e->groups[0].st.trace, init.data(), init.size() * 8,
                                     cudaMemcpyHostToDevice, s));
       DM_CHECK_CUDA(cudaStreamSynchronize(s));
@@ -939,7 +939,7 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
     }
     case 12:
       DM_REQUIRE(e->groups[0].st.trace != nullptr, "timeline tap not enabled");
-      src = e->groups[0].st.trace; avail = 128 * 4 * 8;
+      src = e->groups[0].st.trace; avail = 128 * 8 * 8;
       break;
     case 5: src = e->resid; avail = size_t(e->last_n) * 1500 * e->d * 4; break;
     case 6: src = e->attn_out; avail = size_t(e->last_n) * 1500 * e->d * 2; break;

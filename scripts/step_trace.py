@@ -40,7 +40,7 @@ for rows in rows_list:
         dbg(11)
         eng.step(1)
         torch.cuda.synchronize()
-        t = np.zeros((128, 4), np.uint64)
+        t = np.zeros((128, 8), np.uint64)
         dbg(12, t)
         t = t[:len(names)].astype(np.float64)
         t0 = t[0, 1]
@@ -50,10 +50,14 @@ for rows in rows_list:
     res = []
     prev_end = 0.0
     for k, nm in enumerate(names):
-        entry, rel, rel_max, end = t[k]
-        res.append({"k": nm, "gap_us": round((rel - prev_end) / 1e3, 2),
-                    "span_us": round((end - rel) / 1e3, 2),
-                    "early_us": round((rel - entry) / 1e3, 2)})
+        entry, rel, rel_max, end = t[k][:4]
+        rec = {"k": nm, "gap_us": round((rel - prev_end) / 1e3, 2),
+               "span_us": round((end - rel) / 1e3, 2),
+               "early_us": round((rel - entry) / 1e3, 2)}
+        for j, lab in ((4, "x_landed"), (5, "mma_done"), (6, "stores")):
+            if t[k][j] > 0 and t[k][j] >= rel:
+                rec[lab + "_us"] = round((t[k][j] - rel) / 1e3, 2)
+        res.append(rec)
         prev_end = end
     total = t[len(names) - 1, 3] / 1e3
     kinds = {}
