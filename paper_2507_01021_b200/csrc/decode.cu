@@ -258,6 +258,12 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
         __syncwarp();
       }
     }
+    // release TMEM as soon as the epilogue has read the last accumulators,
+    // while its global stores are still draining
+    for (int k = it - 2; k < it; ++k)
+      if (k >= 0) mbar_wait(&tm_empty[k & 1], (k >> 1) & 1);
+    tc_fence_after();
+    tmem_dealloc(tmem, 256);
   } else {
     const int quad = warp & 3;
     const int f = quad * 32 + lane;                // feature within the tile
@@ -412,10 +418,6 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) trace_mark(st, 3);
-  if (warp == 1) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 256);
-  }
 }
 
 GemvArgs gemv_plan(int N, int K, int epi) {
