@@ -113,6 +113,10 @@ DM_API int dm_whisper_step(void* handle, int n_steps, void* stream);
 /* Copy per-slot state to host: done[max_slots], n_gen[max_slots] and (if
  * tokens != NULL) tokens[max_slots * 448]. Synchronises the stream. */
 DM_API int dm_whisper_read(void* handle, int32_t* done, int32_t* n_gen, int32_t* tokens, void* stream);
+/* Same copies, stream-ordered and without synchronising (destinations should
+ * be pinned host memory; the caller waits on an event it records after). */
+DM_API int dm_whisper_read_async(void* handle, int32_t* done, int32_t* n_gen, int32_t* tokens,
+                                 void* stream);
 /* Debug/parity taps (synchronous copies to host):
  *  which = 0: encoder output of the last encode, [n, 1500, d] bf16 bits
  *  which = 1: log-mel of the last encode, [n, n_mels, 3000] fp32

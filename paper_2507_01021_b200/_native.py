@@ -17,7 +17,7 @@ EXPORTS = (
     "dm_last_error", "dm_version", "dm_fill_normal_bf16", "dm_logmel",
     "dm_gemm_bf16_f32", "dm_whisper_create", "dm_whisper_destroy",
     "dm_whisper_encode", "dm_whisper_admit", "dm_whisper_release",
-    "dm_whisper_set_active", "dm_whisper_step", "dm_whisper_read",
+    "dm_whisper_set_active", "dm_whisper_step", "dm_whisper_read", "dm_whisper_read_async",
     "dm_whisper_debug", "dm_whisper_stats", "dm_whisper_time_kernel",
     "dm_ctc_create", "dm_ctc_destroy", "dm_ctc_transcribe", "dm_ctc_read", "dm_ctc_debug",
 )
@@ -78,6 +78,7 @@ def load(build_if_missing: bool = False):
             "dm_whisper_set_active": [P, P, C.c_int, P],
             "dm_whisper_step": [P, C.c_int, P],
             "dm_whisper_read": [P, P, P, P, P],
+            "dm_whisper_read_async": [P, P, P, P, P],
             "dm_whisper_debug": [P, C.c_int, P, C.c_size_t, P],
             "dm_whisper_stats": [P, P, C.c_int],
             "dm_whisper_time_kernel": [P, C.c_int, C.c_int, C.c_int, P, P],

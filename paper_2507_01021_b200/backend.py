@@ -50,15 +50,34 @@ def pad_or_trim(samples: np.ndarray, window_s: float, sample_rate_hz: int) -> np
     return out
 
 
+def _render(t: int) -> str:
+    syl = [_SYLLABLES[(t >> (4 * k)) & 15] for k in range(4) if (t >> (4 * k)) or k == 0]
+    return "".join(syl)
+
+
+_WORDS: list[str] = []
+
+
 def detokenize(ids: list[int]) -> str:
     """Deterministic rendering of token ids (no tokenizer files offline, and
-    random-init weights make BPE text meaningless): one pseudo-word per id."""
-    words = []
-    for t in ids:
-        t = int(t)
-        syl = [_SYLLABLES[(t >> (4 * k)) & 15] for k in range(4) if (t >> (4 * k)) or k == 0]
-        words.append("".join(syl))
-    return " ".join(words)
+    random-init weights make BPE text meaningless): one pseudo-word per id
+    (table-driven; ids outside the Whisper vocabularies render on the fly)."""
+    global _WORDS
+    if not _WORDS:
+        _WORDS = [_render(t) for t in range(51866)]
+    words = _WORDS
+    n = len(words)
+    return " ".join(words[t] if 0 <= t < n else _render(int(t)) for t in ids)
+
+
+def _is_silent(samples: np.ndarray) -> bool:
+    """All-zero PCM (the reference's silence rule, backend.py:130-135). Speech
+    almost always has a non-zero sample near the start: check a prefix first."""
+    if len(samples) == 0:
+        return True
+    if samples[:256].any():
+        return False
+    return not samples.any()
 
 
 @dataclass
@@ -116,7 +135,7 @@ class B200Backend:
             samples = np.asarray(seg.samples)
             if samples.dtype != np.int16:
                 samples = samples.astype(np.int16)
-            if self.cfg.silence_is_empty and (len(samples) == 0 or not samples.any()):
+            if self.cfg.silence_is_empty and _is_silent(samples):
                 texts[i] = ""
                 continue
             jobs.append(SegmentJob(i, samples, self.cap_for(seg.duration_s)))

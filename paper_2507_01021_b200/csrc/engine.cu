@@ -882,7 +882,8 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
   return 0;
 }
 
-int dm_whisper_read(void* handle, int32_t* done, int32_t* n_gen, int32_t* tokens, void* stream) {
+int dm_whisper_read_async(void* handle, int32_t* done, int32_t* n_gen, int32_t* tokens,
+                          void* stream) {
   auto* e = static_cast<WhisperEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -892,7 +893,12 @@ int dm_whisper_read(void* handle, int32_t* done, int32_t* n_gen, int32_t* tokens
   if (tokens)
     DM_CHECK_CUDA(cudaMemcpyAsync(tokens, e->st.out_tokens, sizeof(int32_t) * S * 448,
                                   cudaMemcpyDeviceToHost, s));
-  DM_CHECK_CUDA(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int dm_whisper_read(void* handle, int32_t* done, int32_t* n_gen, int32_t* tokens, void* stream) {
+  if (int rc = dm_whisper_read_async(handle, done, n_gen, tokens, stream)) return rc;
+  DM_CHECK_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
   return 0;
 }
 

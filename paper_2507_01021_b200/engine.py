@@ -149,6 +149,12 @@ class WhisperGPU:
             self._done = np.zeros(max_slots, np.int32)
             self._ngen = np.zeros(max_slots, np.int32)
             self._tokens = np.zeros(max_slots * MAX_TOKENS, np.int32)
+            # pinned double-buffered snapshots for the pipelined slot loop
+            self._snaps = [(torch.zeros(max_slots, dtype=torch.int32, pin_memory=True),
+                            torch.zeros(max_slots, dtype=torch.int32, pin_memory=True),
+                            torch.zeros(max_slots * MAX_TOKENS, dtype=torch.int32,
+                                        pin_memory=True)) for _ in range(2)]
+            self._snap_ev = [torch.cuda.Event() for _ in range(2)]
         self.stats = EngineStats()
         self._held: set[int] = set()       # slots holding self-KV pages
         self._resident: torch.Tensor | None = None
@@ -204,7 +210,6 @@ class WhisperGPU:
             return (C.c_void_p(self._resident.data_ptr()), C.c_void_p(md.data_ptr()),
                     C.c_void_p(md.data_ptr() + 8 * n))
         ph, pd = self._pcm_host[b], self._pcm_dev[b]
-        host = ph.numpy()
         offs, lens = [], []
         pos = 0
         for s in segs:
@@ -212,7 +217,7 @@ class WhisperGPU:
             if s.dtype != np.int16:
                 raise TypeError("segment samples must be int16 PCM")
             k = min(len(s), N_SAMPLES)
-            host[pos:pos + k] = s[:k]
+            ph[pos:pos + k].copy_(torch.from_numpy(s[:k]))      # (multithreaded host copy)
             offs.append(pos)
             lens.append(k)
             pos += k
@@ -309,22 +314,52 @@ class WhisperGPU:
         return self.debug(1, np.empty((n, self.dims.n_mels, 3000), np.float32))
 
     # ----------------------------------------------------------- slot loop
+    def _snap(self, b: int) -> None:
+        """Stream-ordered snapshot of done / n_gen / tokens into pinned buffer b."""
+        d, g, t = self._snaps[b]
+        _native.check(self.lib.dm_whisper_read_async(
+            self.handle, C.c_void_p(d.data_ptr()), C.c_void_p(g.data_ptr()),
+            C.c_void_p(t.data_ptr()), self._s))
+        self._snap_ev[b].record(self.stream)
+        self.d2h_bytes += 8 * self.max_slots + 4 * self.max_slots * MAX_TOKENS
+
     def run_jobs(self, jobs: Iterable[SegmentJob],
                  refill: Callable[[int], list[SegmentJob]] | None = None) -> dict:
         """Continuous batching: admit jobs into free decode slots (encoding
         them in groups of <= max_encode_batch), step the active slots, route a
         segment as soon as its slot hits EOT or its cap, refill freed slots
         from `pending` then from `refill(n_free)` (the multiplexer hook).
-        Returns {key: token ids}."""
+
+        The host never waits on the step it just issued: each batch of steps
+        runs up to the next slot's cap (predicted exactly on the host:
+        prompt_len - 1 + cap steps), so cap-terminated slots leave the active
+        set and free their pages with no wasted step; a stream-ordered
+        snapshot of (done, n_gen, tokens) is taken after each batch and read
+        one batch later (tokens of finished slots never change, and slots
+        that hit EOT early only linger one batch -- their attention is
+        skipped). Returns {key: token ids}."""
         pending = deque(jobs)
         free = list(range(self.max_slots - 1, -1, -1))
         active: dict[int, SegmentJob] = {}
+        left: dict[int, int] = {}              # slot -> steps to its cap
+        waiting: list[tuple[int, SegmentJob]] = []   # finished, result in the next snapshot
         results: dict = {}
+        prompt_extra = len(self.dims.prompt) - 1
         t0 = time.perf_counter()
+        prev = None                            # (snapshot buffer, [(slot, job)], active slots)
+        b = 0
+        dirty = True
+
+        def route(slot: int, job: SegmentJob, snap) -> None:
+            _, ngen, toks = snap
+            ids = toks[slot, :ngen[slot]].tolist()
+            results[job.key] = ids
+            if job.on_done is not None:
+                job.on_done(job.key, ids)
+
         while True:
             if free and refill is not None and len(pending) < len(free):
                 pending.extend(refill(len(free) - len(pending)))
-            admitted = False
             while free and pending:
                 take = []
                 while free and pending and len(take) < self.max_encode_batch:
@@ -334,27 +369,48 @@ class WhisperGPU:
                 self.admit(slots, [j.cap for _, j in take])
                 for s, j in take:
                     active[s] = j
-                admitted = True
-            if not active:
+                    left[s] = prompt_extra + j.cap
+                dirty = True
+            cur = None
+            if active:
+                if dirty:
+                    self.set_active(sorted(active))
+                    dirty = False
+                n = max(1, min(self.steps_per_poll, min(left[s] for s in active)))
+                self.step(n)
+                self.stats.steps += n
+                self.stats.slot_steps += n * len(active)
+                for s in active:
+                    left[s] -= n
+                self._snap(b)
+                capped = [s for s in active if left[s] <= 0]
+                for s in capped:
+                    waiting.append((s, active.pop(s)))
+                if capped:
+                    self.release(capped)
+                    free.extend(capped)
+                    dirty = True
+                cur = (b, waiting, set(active))
+                waiting = []
+                b ^= 1
+            if prev is not None:
+                pb, finished, was_active = prev
+                self._snap_ev[pb].synchronize()
+                snap = tuple(x.numpy() for x in self._snaps[pb])
+                snap = (snap[0], snap[1], snap[2].reshape(self.max_slots, MAX_TOKENS))
+                for s, j in finished:
+                    route(s, j, snap)
+                # early EOT: done in the snapshot while still listed as active
+                eot = [s for s in was_active if s in active and snap[0][s]]
+                for s in eot:
+                    route(s, active.pop(s), snap)
+                if eot:
+                    self.release(eot)
+                    free.extend(eot)
+                    dirty = True
+            prev = cur
+            if prev is None and not active and not pending:
                 break
-            if admitted:
-                self.set_active(sorted(active))
-            self.step(self.steps_per_poll)
-            self.stats.steps += self.steps_per_poll
-            self.stats.slot_steps += self.steps_per_poll * len(active)
-            done, ngen, _ = self.read(tokens=False)
-            finished = [s for s in active if done[s]]
-            if finished:
-                _, ngen, toks = self.read(tokens=True)
-                for s in finished:
-                    j = active.pop(s)
-                    ids = toks[s, :ngen[s]].tolist()
-                    results[j.key] = ids
-                    if j.on_done is not None:
-                        j.on_done(j.key, ids)
-                self.release(finished)
-                free.extend(finished)
-                self.set_active(sorted(active))
         self.stats.busy_s += time.perf_counter() - t0
         return results
 
