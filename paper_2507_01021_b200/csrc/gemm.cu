@@ -36,10 +36,11 @@ struct TileGeom {
   int MT, NT, tiles, KB, cpb;   // cpb = channel blocks per conv tap
 };
 
-template <int BN>
+template <int BN, int MODE>
 __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, const GemmArgs& g,
                                                int b, int t, int row_valid, int n0,
-                                               uint32_t (&r)[32]) {
+                                               uint32_t (&r)[32], const float4* pre = nullptr,
+                                               const uint4* bpre = nullptr) {
   float v[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
@@ -47,7 +48,7 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, const GemmArgs
     const uint4* bp = reinterpret_cast<const uint4*>(e.bias + n0);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      uint4 w = __ldg(bp + i);
+      uint4 w = bpre ? bpre[i] : __ldg(bp + i);
       uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -58,7 +59,7 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, const GemmArgs
   }
   if (!row_valid) return;
   const int N = g.N;
-  switch (e.mode) {
+  switch (MODE) {
     case EPI_GELU_BF16:
     case EPI_GELU_F32:
     case EPI_CONV1:
@@ -69,11 +70,11 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, const GemmArgs
     default:
       break;
   }
-  switch (e.mode) {
+  switch (MODE) {
     case EPI_STORE_BF16:
     case EPI_GELU_BF16:
     case EPI_CONV1: {
-      size_t row = (e.mode == EPI_CONV1) ? size_t(b) * (g.T + 2) + t + 1
+      size_t row = (MODE == EPI_CONV1) ? size_t(b) * (g.T + 2) + t + 1
                                          : size_t(b) * g.T + t;
       uint4* dst = reinterpret_cast<uint4*>(static_cast<uint16_t*>(e.out) +
                                             row * e.ldo + n0);
@@ -112,8 +113,8 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, const GemmArgs
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
         float4 o = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        if (e.mode == EPI_RESID_F32) {
-          float4 rr = dst[i];
+        if (MODE == EPI_RESID_F32) {
+          float4 rr = pre ? pre[i] : dst[i];
           o.x += rr.x; o.y += rr.y; o.z += rr.z; o.w += rr.w;
         }
         dst[i] = o;
@@ -218,7 +219,7 @@ struct GemmSmem {
   static constexpr int kBytes = STAGES * kStageBytes + 1024 /*align*/ + 256 /*bars*/;
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int MODE>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
                     const __grid_constant__ CUtensorMap tmap_b, const GemmArgs g,
@@ -326,17 +327,52 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
       const int b = mb / geo.MT, mt = mb % geo.MT;
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
-      mbar_wait(&tmem_full[as], aphase);
-      tc_fence_after();
       const int t = mt * kBM + quad * 32 + lane;
       const int row_valid = t < g.T;
+      // fp32 residual of this thread's row segment: independent of the MMA, so
+      // it is fetched before waiting for the accumulator (BN = 128: 64 floats)
+      constexpr int kPre = BN == 128 ? BN / 8 : 1;
+      float4 res[kPre];
+      const bool pre = BN == 128 && MODE == EPI_RESID_F32 && row_valid &&
+                       nt * BN + (chalf + 1) * (BN / 2) <= g.N;
+      if (pre) {
+        const float4* src = reinterpret_cast<const float4*>(
+            static_cast<const float*>(g.epi.out) + (size_t(b) * g.T + t) * g.epi.ldo + nt * BN +
+            chalf * (BN / 2));
+#pragma unroll
+        for (int i = 0; i < kPre; ++i) res[i] = __ldcs(src + i);
+      }
+      // (and the bias of this thread's columns)
+      uint4 bias_pre[BN == 128 ? 8 : 1];
+      const bool bpre = BN == 128 && g.epi.bias != nullptr && nt * BN + (chalf + 1) * (BN / 2) <= g.N;
+      if (bpre) {
+        const uint4* bp = reinterpret_cast<const uint4*>(g.epi.bias + nt * BN + chalf * (BN / 2));
+#pragma unroll
+        for (int i = 0; i < (BN == 128 ? 8 : 1); ++i) bias_pre[i] = __ldg(bp + i);
+      }
+      mbar_wait(&tmem_full[as], aphase);
+      tc_fence_after();
+      if (BN == 128) {
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = chalf * (BN / 2) + cc * 32;
+          const int n0 = nt * BN + c;
+          uint32_t r[32];
+          tmem_ld32(tmem_base + (uint32_t(quad * 32) << 16) + as * BN + c, r);
+          tmem_wait_ld();
+          if (n0 < g.N)
+            epilogue_chunk<BN, MODE>(g.epi, g, b, t, row_valid, n0, r, pre ? res + cc * 8 : nullptr,
+                               bpre ? bias_pre + cc * 4 : nullptr);
+        }
+      } else {
 #pragma unroll 1
-      for (int c = chalf * (BN / 2); c < (chalf + 1) * (BN / 2); c += 32) {
-        const int n0 = nt * BN + c;
-        uint32_t r[32];
-        tmem_ld32(tmem_base + (uint32_t(quad * 32) << 16) + as * BN + c, r);
-        tmem_wait_ld();
-        if (n0 < g.N) epilogue_chunk<BN>(g.epi, g, b, t, row_valid, n0, r);
+        for (int c = chalf * (BN / 2); c < (chalf + 1) * (BN / 2); c += 32) {
+          const int n0 = nt * BN + c;
+          uint32_t r[32];
+          tmem_ld32(tmem_base + (uint32_t(quad * 32) << 16) + as * BN + c, r);
+          tmem_wait_ld();
+          if (n0 < g.N) epilogue_chunk<BN, MODE>(g.epi, g, b, t, row_valid, n0, r);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -381,8 +417,8 @@ static int make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t*
   return 0;
 }
 
-template <int BN, int STAGES>
-static int launch_bn(const GemmArgs& g, cudaStream_t stream) {
+template <int BN, int STAGES, int MODE>
+static int launch_bn_mode(const GemmArgs& g, cudaStream_t stream) {
   CUtensorMap ma, mb;
   if (g.a_mode == A_FLAT) {
     cuuint64_t dims[3] = {cuuint64_t(g.K), cuuint64_t(g.T), cuuint64_t(g.Bt)};
@@ -417,14 +453,30 @@ static int launch_bn(const GemmArgs& g, cudaStream_t stream) {
   const int smem = GemmSmem<BN, STAGES>::kBytes;
   static bool attr = false;
   if (!attr) {
-    DM_CHECK_CUDA(cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, STAGES>,
+    DM_CHECK_CUDA(cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, STAGES, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr = true;
   }
   int grid = geo.tiles < kNumSMs ? geo.tiles : kNumSMs;
-  gemm_tcgen05_kernel<BN, STAGES><<<grid, kGemmThreads, smem, stream>>>(ma, mb, g, geo);
+  gemm_tcgen05_kernel<BN, STAGES, MODE><<<grid, kGemmThreads, smem, stream>>>(ma, mb, g, geo);
   DM_CHECK_LAUNCH();
   return 0;
+}
+
+// The epilogue mode is a template parameter: each instantiation carries only
+// its own epilogue (register pressure and I-cache footprint of one mode).
+template <int BN, int STAGES>
+static int launch_bn(const GemmArgs& g, cudaStream_t stream) {
+  switch (g.epi.mode) {
+#define DM_GEMM_MODE(m) \
+  case m: return launch_bn_mode<BN, STAGES, m>(g, stream);
+    DM_GEMM_MODE(EPI_STORE_BF16) DM_GEMM_MODE(EPI_GELU_BF16) DM_GEMM_MODE(EPI_CONV1)
+    DM_GEMM_MODE(EPI_CONV2_POS) DM_GEMM_MODE(EPI_RESID_F32) DM_GEMM_MODE(EPI_QKV)
+    DM_GEMM_MODE(EPI_XKV) DM_GEMM_MODE(EPI_STORE_F32) DM_GEMM_MODE(EPI_W2V_PROJ)
+    DM_GEMM_MODE(EPI_CTC_ARGMAX) DM_GEMM_MODE(EPI_GELU_F32)
+#undef DM_GEMM_MODE
+    default: DM_REQUIRE(false, "unknown GEMM epilogue");
+  }
 }
 
 int make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
@@ -468,7 +520,10 @@ int launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   DM_REQUIRE((reinterpret_cast<uintptr_t>(g.A) & 15) == 0 &&
                  (reinterpret_cast<uintptr_t>(g.W) & 15) == 0,
              "operands must be 16-byte aligned");
-  if (g.grouped) return launch_bn<64, 8>(g, stream);
+  if (g.grouped) {
+    DM_REQUIRE(g.epi.mode == EPI_W2V_POS, "grouped GEMM: wav2vec2 pos-conv epilogue only");
+    return launch_bn_mode<64, 8, EPI_W2V_POS>(g, stream);
+  }
   if (g.N % 256 == 0 && g.N >= 1024) return launch_bn<256, 4>(g, stream);
   return launch_bn<128, 6>(g, stream);
 }
