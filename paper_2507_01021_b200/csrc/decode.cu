@@ -216,7 +216,17 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
         ++wi;
       };
       const int pre = total < NS ? total : NS;
-      for (int q = 0; q < pre; ++q) issue_w(q);     // weights never depend on the predecessor
+      if (total <= NS) {
+        // whole weight slice resident: one barrier for all of it, so the MMA
+        // warp needs a single wait instead of one handshake per k-block
+        mbar_arrive_expect_tx(&wfull[0], total * kGvWBytes);
+        for (int q = 0; q < total; ++q)
+          tma_load_2d(ws + q * kGvWBytes, &tw, &wfull[0], (kb0 + q % kb_per) * 64,
+                      (int(blockIdx.x) + (q / kb_per) * int(gridDim.x)) * 128);
+        wi = total;
+      } else {
+        for (int q = 0; q < pre; ++q) issue_w(q);   // weights never depend on the predecessor
+      }
       pdl_wait();
       trace_mark(st, 1);
       mbar_arrive_expect_tx(xfull, kb_per * 2 * G * kGvXBox * 128);
@@ -234,10 +244,35 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
     // weight tile (the A operand, the smem-read-bound side at small N) is read
     // once for both halves; D columns [0, Np) hold W.x_hi, [Np, 2 Np) W.x_lo
     const uint32_t idesc = umma_idesc_bf16(128, 2 * Np);
+    const int my_tiles = (tiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1;
+    const bool resident = my_tiles * kb_per <= NS;
     mbar_wait(xfull, 0);
     if (lane == 0) trace_mark(st, 4);
     int wi = 0, it = 0;
-    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+    if (resident) {
+      // all operands landed after two waits: issue every MMA back to back
+      mbar_wait(&wfull[0], 0);
+      tc_fence_after();
+      for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
+        const int buf = it & 1;
+        mbar_wait(&tm_empty[buf], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t d = tmem + buf * 128;
+          for (int i = 0; i < kb_per; ++i) {
+            const uint64_t aw = umma_desc_sw128(smem_u32(ws + (it * kb_per + i) * kGvWBytes));
+            const uint64_t bx = umma_desc_sw128(smem_u32(xs + i * 2 * XB));
+#pragma unroll
+            for (int k = 0; k < 4; ++k)      // +32 B per k-step = +2 in the address field
+              umma_bf16_ss(d, aw + 2 * k, bx + 2 * k, idesc, (i | k) != 0);
+          }
+          trace_mark(st, 7);
+          umma_commit(&tm_full[buf]);
+        }
+        __syncwarp();
+      }
+    }
+    for (int tile = resident ? tiles : int(blockIdx.x); tile < tiles; tile += gridDim.x, ++it) {
       const int buf = it & 1;
       mbar_wait(&tm_empty[buf], ((it >> 1) & 1) ^ 1);
       tc_fence_after();
@@ -253,7 +288,10 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
             umma_bf16_ss(tmem + buf * 128, umma_desc_sw128(sw + k * 32),
                          umma_desc_sw128(sh + k * 32), idesc, (i | k) != 0);
           umma_commit(&wempty[s]);
-          if (i == kb_per - 1) umma_commit(&tm_full[buf]);
+          if (i == kb_per - 1) {
+            trace_mark(st, 7);
+            umma_commit(&tm_full[buf]);
+          }
         }
         __syncwarp();
       }
@@ -371,7 +409,7 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
             col[i * 129] = v0[i];
             col[(32 + i) * 129] = v1[i];
           }
-#pragma unroll 1
+#pragma unroll 4
           for (int i = 0; i < R; ++i) {
             uint16_t hi, lo;
             split_hilo(gelu_erf(col[i * 129] + b), hi, lo);
@@ -446,9 +484,9 @@ GemvArgs gemv_plan(int N, int K, int epi) {
       if (KB % s == 0 && KB / s <= 8) { a.kb_per = KB / s; break; }
   }
   a.splits = KB / a.kb_per;
-  // fc1-style projections (non-linear, unsplit): two row groups of 32 so each
-  // CTA holds its whole weight slice plus half the activation rows
-  a.rgroups = (epi == GV_GELU_HILO && a.splits == 1) ? 2 : 1;
+  // fc1-style projections (non-linear, unsplit): four row groups of 16 so each
+  // CTA holds its whole weight slice plus a quarter of the activation rows
+  a.rgroups = (epi == GV_GELU_HILO && a.splits == 1) ? 4 : 1;
   const int tiles = ceil_div(N, 128);
   const int gx = std::max(1, std::min(tiles, kNumSMs / a.splits));
   const int per_cta = ceil_div(tiles, gx) * a.kb_per;
@@ -485,7 +523,7 @@ int launch_gemv(const DecodeState& st, const TcGemvMaps& maps, const GemvArgs& a
                 cudaStream_t stream) {
   DM_REQUIRE(a.K % 64 == 0 && a.kb_per >= 1 && a.splits * a.kb_per * 64 == a.K, "bad K split");
   DM_REQUIRE(a.stages >= 1 && a.stages <= kGvMaxStages, "bad weight ring depth");
-  DM_REQUIRE(a.rgroups == 1 || a.rgroups == 2, "GEMV row groups: 1 or 2");
+  DM_REQUIRE(a.rgroups == 1 || a.rgroups == 2 || a.rgroups == 4, "GEMV row groups: 1, 2 or 4");
   DM_REQUIRE(a.rgroups == 1 || (a.epi != GV_ARGMAX && a.splits == 1), "row groups: linear / fc1 only");
   DM_REQUIRE(gemv_smem_bytes(a.kb_per, a.stages, a.epi, a.rgroups) <= kSmemOptin,
              "GEMV slice exceeds smem");

@@ -110,7 +110,7 @@ struct GemvArgs {
   int splits;              // K splits (fixed per shape; never depends on rows)
   int kb_per;              // 64-wide k-blocks per split
   int stages;              // weight ring depth (whole slice prefetched when it fits)
-  int rgroups;             // row groups (grid z): 2 -> CTA z owns rows [32 z, 32 z + 32)
+  int rgroups;             // row groups (grid z): CTA z owns rows [z * 64 / rgroups, +64 / rgroups)
   int counter_base;
   float* part;             // GV_PARTIAL output [splits][kRows][N]
   uint16_t *yh, *yl;       // GV_GELU_HILO targets [kRows, N]

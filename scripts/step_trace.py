@@ -54,7 +54,7 @@ for rows in rows_list:
         rec = {"k": nm, "gap_us": round((rel - prev_end) / 1e3, 2),
                "span_us": round((end - rel) / 1e3, 2),
                "early_us": round((rel - entry) / 1e3, 2)}
-        for j, lab in ((4, "x_landed"), (5, "mma_done"), (6, "stores")):
+        for j, lab in ((4, "x_landed"), (7, "mma_issued"), (5, "mma_done"), (6, "stores")):
             if t[k][j] > 0 and t[k][j] >= rel:
                 rec[lab + "_us"] = round((t[k][j] - rel) / 1e3, 2)
         res.append(rec)
