@@ -828,9 +828,9 @@ int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, floa
   return 0;
 }
 
-constexpr int kXaThreads = 256;
+constexpr int kXaThreads = 192;                               // one key per thread
 constexpr int kXaKeys = 192;                                  // ceil(1500 / 8 / 64) * 64
-constexpr int kXaSmem = 2 * kXaKeys * 128 + 64;   // K, V blocks + 3 mbarriers
+constexpr int kXaSmem = 1024 + 2 * kXaKeys * 128 + 64;   // (align) K, V blocks + 3 mbarriers
 static_assert(kXSplits * kXaKeys >= 1500 && (kXSplits - 1) * kXaKeys < 1500, "key splits");
 
 // Cross-attention for (row, head, key split). The split's K and V blocks
@@ -840,9 +840,11 @@ static_assert(kXSplits * kXaKeys >= 1500 && (kXSplits - 1) * kXaKeys < 1500, "ke
 // o[64]) into rank 0's shared memory (DSMEM stores + a release arrive on rank
 // 0's mbarrier) and leaves; rank 0 merges them in split order.
 __global__ void __launch_bounds__(kXaThreads)
-cross_attn_kernel(const DecodeState st, int layer, const Partials xq, float q_scale) {
-  extern __shared__ __align__(128) uint8_t xa_smem[];
-  __shared__ float qs[64], sc[kXaKeys], red[8], op[8][64];
+cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, int layer,
+                  const Partials xq, float q_scale) {
+  extern __shared__ uint8_t xa_raw[];
+  uint8_t* xa_smem = xa_raw + ((1024 - (smem_u32(xa_raw) & 1023)) & 1023);   // TMA swizzle atoms
+  __shared__ float qs[64], sc[kXaKeys], red[8], op[kXaThreads / 32][64];
   __shared__ float rml[kXSplits][2], ro[kXSplits][64];     // rank 0: pushed split results
   const int r = blockIdx.x, h = blockIdx.y, sp = blockIdx.z, tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
@@ -864,13 +866,18 @@ cross_attn_kernel(const DecodeState st, int layer, const Partials xq, float q_sc
     mbar_init(barV, 1);
     mbar_init(barM, kXSplits);
     fence_barrier_init();
-    const uint16_t* kg =
-        st.xkv + ((((size_t(layer) * st.max_slots + slot) * 2 + 0) * H + h) * 1500 + k0) * 64;
-    const uint16_t* vg = kg + size_t(H) * 1500 * 64;
-    mbar_arrive_expect_tx(barK, nk * 128);
-    bulk_load(Ks, kg, nk * 128, barK);           // cross-KV never depends on the predecessor
-    mbar_arrive_expect_tx(barV, nk * 128);
-    bulk_load(Vs, vg, nk * 128, barV);
+    // K and V of the split: 3 TMA boxes of 64 keys each (128B-swizzled rows;
+    // keys past the slot's 1500 are masked), cross-KV never depends on the
+    // predecessor
+    tma_prefetch_desc(&tm);
+    const int row_k = (((layer * st.max_slots + slot) * 2 + 0) * H + h) * 1500 + k0;
+    const int row_v = row_k + H * 1500;
+    mbar_arrive_expect_tx(barK, 3 * 64 * 128);
+#pragma unroll
+    for (int bx = 0; bx < 3; ++bx) tma_load_2d(Ks + bx * 64 * 128, &tm, barK, 0, row_k + bx * 64);
+    mbar_arrive_expect_tx(barV, 3 * 64 * 128);
+#pragma unroll
+    for (int bx = 0; bx < 3; ++bx) tma_load_2d(Vs + bx * 64 * 128, &tm, barV, 0, row_v + bx * 64);
   }
   __syncthreads();
   cluster_arrive_relaxed();                      // rank 0's barM is initialised
@@ -883,30 +890,31 @@ cross_attn_kernel(const DecodeState st, int layer, const Partials xq, float q_sc
     qs[tid] = (a + bq) * q_scale;
   }
   __syncthreads();
+  float q[64];                                   // (broadcast reads)
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float4 v = *reinterpret_cast<const float4*>(qs + 4 * j);
+    q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
+  }
   mbar_wait(barK, 0);
   float mloc = -INFINITY;
   if (tid < nk) {
-    // lane reads its key row chunk by chunk in XOR order (conflict-free: 4
-    // lanes per 16-byte chunk column); chunk dot products summed in that order
-    const uint8_t* kr = Ks + tid * 128;
+    // key row tid, logical chunk j at physical chunk j ^ (tid & 7) (the TMA
+    // 128B swizzle): conflict-free, q in registers, dims summed in order
+    const uint8_t* kr = Ks + (tid >> 6) * 64 * 128 + (tid & 63) * 128;
     const int sw = tid & 7;
     float s = 0.f;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int c = j ^ sw;
-      const uint4 w = *reinterpret_cast<const uint4*>(kr + c * 16);
-      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-      const float4 qa = *reinterpret_cast<const float4*>(qs + 8 * c);
-      const float4 qb = *reinterpret_cast<const float4*>(qs + 8 * c + 4);
-      float sj = qa.x * __uint_as_float(ws[0] << 16);
-      sj = fmaf(qa.y, __uint_as_float(ws[0] & 0xFFFF0000u), sj);
-      sj = fmaf(qa.z, __uint_as_float(ws[1] << 16), sj);
-      sj = fmaf(qa.w, __uint_as_float(ws[1] & 0xFFFF0000u), sj);
-      sj = fmaf(qb.x, __uint_as_float(ws[2] << 16), sj);
-      sj = fmaf(qb.y, __uint_as_float(ws[2] & 0xFFFF0000u), sj);
-      sj = fmaf(qb.z, __uint_as_float(ws[3] << 16), sj);
-      sj = fmaf(qb.w, __uint_as_float(ws[3] & 0xFFFF0000u), sj);
-      s += sj;
+      const uint4 w = *reinterpret_cast<const uint4*>(kr + ((j ^ sw) << 4));
+      s = fmaf(q[8 * j + 0], __uint_as_float(w.x << 16), s);
+      s = fmaf(q[8 * j + 1], __uint_as_float(w.x & 0xFFFF0000u), s);
+      s = fmaf(q[8 * j + 2], __uint_as_float(w.y << 16), s);
+      s = fmaf(q[8 * j + 3], __uint_as_float(w.y & 0xFFFF0000u), s);
+      s = fmaf(q[8 * j + 4], __uint_as_float(w.z << 16), s);
+      s = fmaf(q[8 * j + 5], __uint_as_float(w.z & 0xFFFF0000u), s);
+      s = fmaf(q[8 * j + 6], __uint_as_float(w.w << 16), s);
+      s = fmaf(q[8 * j + 7], __uint_as_float(w.w & 0xFFFF0000u), s);
     }
     sc[tid] = s;
     mloc = s;
@@ -920,9 +928,11 @@ cross_attn_kernel(const DecodeState st, int layer, const Partials xq, float q_sc
   const float l = block_sum_fixed(e, red);       // (its barrier publishes sc[])
   mbar_wait(barV, 0);
   float o0 = 0.f, o1 = 0.f;
+  const int vch = lane >> 2, vwo = (lane & 3) * 4;     // dims (2 lane, 2 lane + 1)
 #pragma unroll 4
-  for (int t = warp; t < nk; t += 8) {
-    const uint32_t w = *reinterpret_cast<const uint32_t*>(Vs + t * 128 + lane * 4);
+  for (int t = warp; t < nk; t += kXaThreads / 32) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(
+        Vs + (t >> 6) * 64 * 128 + (t & 63) * 128 + ((vch ^ (t & 7)) << 4) + vwo);
     const float pe = sc[t];
     o0 = fmaf(pe, __uint_as_float(w << 16), o0);
     o1 = fmaf(pe, __uint_as_float(w & 0xFFFF0000u), o1);
@@ -934,7 +944,7 @@ cross_attn_kernel(const DecodeState st, int layer, const Partials xq, float q_sc
   if (tid < 64) {
     float a = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) a += op[w][tid];
+    for (int w = 0; w < kXaThreads / 32; ++w) a += op[w][tid];
     st_dsmem_f32(dsmem_addr(&ro[sp][tid], 0), a);
     if (tid == 0) {
       st_dsmem_f32(dsmem_addr(&rml[sp][0], 0), m);
@@ -962,8 +972,8 @@ cross_attn_kernel(const DecodeState st, int layer, const Partials xq, float q_sc
   if (tid == 0) trace_mark(st, 3);
 }
 
-int launch_cross_attn(const DecodeState& st, int layer, const Partials& xq, float q_scale,
-                      cudaStream_t stream) {
+int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
+                      const Partials& xq, float q_scale, cudaStream_t stream) {
   DM_REQUIRE(xq.p != nullptr && xq.n == st.d && xq.bias != nullptr && xq.splits >= 1 &&
                  xq.splits <= kMaxSplits, "cross-attn: q partials");
   static bool attr = false;
@@ -973,8 +983,8 @@ int launch_cross_attn(const DecodeState& st, int layer, const Partials& xq, floa
     attr = true;
   }
   DM_CHECK_CUDA(launch_pdl_cluster(cross_attn_kernel, dim3(kRows, st.heads, kXSplits),
-                                   dim3(kXaThreads), dim3(1, 1, kXSplits), kXaSmem, stream, st,
-                                   layer, xq, q_scale));
+                                   dim3(kXaThreads), dim3(1, 1, kXSplits), kXaSmem, stream,
+                                   xkv_map, st, layer, xq, q_scale));
   return 0;
 }
 

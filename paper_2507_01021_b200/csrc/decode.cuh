@@ -149,8 +149,9 @@ int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, floa
                      cudaStream_t stream);
 // Cross-attention over the slot's 1500 cross-KV rows; q from the cross-q
 // partials (scaled); output -> ah/al.
-int launch_cross_attn(const DecodeState& st, int layer, const Partials& xq, float q_scale,
-                      cudaStream_t stream);
+// xkv_map: the cross-KV cache as [rows, 64] bf16, box 64 x 64, 128B swizzle.
+int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
+                      const Partials& xq, float q_scale, cudaStream_t stream);
 int launch_finalize(const DecodeState& st, cudaStream_t stream);
 
 }  // namespace dm

@@ -225,6 +225,7 @@ struct WhisperEngine {
   int gemv_counter_base = 0;
   std::vector<TcGemvMaps> maps;   // [Ld * 6 + 1]: per layer qkv,o,xq,xo,fc1,fc2; LM head
   std::vector<GemvArgs> plans;    // same order: launch plan of each projection
+  CUtensorMap xkv_map;            // cross-KV cache as [rows, 64] bf16 (box 64 x 64, 128B swizzle)
   // Independent decode groups (slot s belongs to group s % G): each has its own
   // row-space activations, active list, scratch, step graph and stream, so the
   // groups' latency-bound kernel chains overlap on the GPU.
@@ -424,6 +425,8 @@ static int engine_init(WhisperEngine* e) {
     e->maps = e->groups[0].maps;
     (void)shared;
   }
+  if (make_tmap_2d(&e->xkv_map, st.xkv, 64, uint64_t(e->Ld) * S * 2 * e->H * 1500, 128, 64, 64))
+    return 2;
   DM_CHECK_CUDA(cudaStreamCreateWithFlags(&e->cap_stream, cudaStreamNonBlocking));
   DM_CHECK_CUDA(cudaDeviceSynchronize());
   return 0;
@@ -552,7 +555,7 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
     DM_STEP(gv(pi + 1, grp.p_o, nullptr, nullptr, nullptr));
     DM_STEP(ln(2, b0 + 6, Partials{grp.p_o, go, d, e->W(b0 + 5)}));
     DM_STEP(gv(pi + 2, grp.p_xq, nullptr, nullptr, nullptr));
-    DM_STEP(launch_cross_attn(st, l, Partials{grp.p_xq, gx, d, e->W(b0 + 9)}, 0.125f, s));
+    DM_STEP(launch_cross_attn(st, e->xkv_map, l, Partials{grp.p_xq, gx, d, e->W(b0 + 9)}, 0.125f, s));
     DM_STEP(gv(pi + 3, grp.p_xo, nullptr, nullptr, nullptr));
     DM_STEP(ln(2, b0 + 12, Partials{grp.p_xo, gxo, d, e->W(b0 + 11)}));
     DM_STEP(gv(pi + 4, nullptr, st.hh, st.hl, e->W(b0 + 15)));
@@ -829,7 +832,7 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
   auto launch_one = [&](cudaStream_t cs) -> int {
     switch (which) {
       case 0:
-        return launch_cross_attn(grp.st, layer,
+        return launch_cross_attn(grp.st, e->xkv_map, layer,
                                  Partials{grp.p_xq, e->plans[pi + 2].splits, d, e->W(b0 + 9)},
                                  0.125f, cs);
       case 1:
