@@ -325,9 +325,11 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
 
 
 def measure_roofline(eng, dims, args) -> dict:
-    """Cross-attention (decode, K6) is the dominant HBM stream: per launch it
-    reads every active slot's K and V for one layer: n_active * 2 * 1500 * d
-    bf16 (L*2*1500*d*2 B per segment per step)."""
+    """Cross-attention (decode, K6; cross-o projection fused in its tail) is
+    the dominant HBM stream: per launch it reads every active slot's K and V
+    for one layer: n_active * 2 * 1500 * d bf16 (SURVEY.md §8(d):
+    L*2*1500*d*2 B per segment per step). The 2*d*d B cross-o weight slices
+    (L2-resident across the batch) are not counted."""
     import json as _j
     peaks = _j.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -352,7 +354,7 @@ def measure_roofline(eng, dims, args) -> dict:
     if tf.exists():     # dram read+write of one ncu --set full capture (64 rows), scaled to rows
         t = _j.loads(tf.read_text())
         traffic = (t["dram_bytes_read"] + t["dram_bytes_write"]) * rows / t["rows"]
-    return {"kernel": "cross_attn_kernel (decode K6)", "bound": "hbm", "achieved": achieved,
+    return {"kernel": "cross_attn_kernel (decode K6, + cross-o tail)", "bound": "hbm", "achieved": achieved,
             "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
             "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/r01_xattn_traffic.json)",
             "timing": "CUDA events on the engine stream around a graph of 20 back-to-back launches "

@@ -45,15 +45,16 @@ __device__ __forceinline__ float sum_splits(const float* p, size_t stride, int s
     if (s < splits) a += v[s];
   return a;
 }
+template <int MAXS = kMaxSplits>
 __device__ __forceinline__ float4 sum_splits4(const float* p, size_t stride, int splits) {
-  float4 v[kMaxSplits];
+  float4 v[MAXS];
 #pragma unroll
-  for (int s = 0; s < kMaxSplits; ++s)
+  for (int s = 0; s < MAXS; ++s)
     v[s] = s < splits ? __ldcg(reinterpret_cast<const float4*>(p + s * stride))
                       : make_float4(0.f, 0.f, 0.f, 0.f);
   float4 a = v[0];
 #pragma unroll
-  for (int s = 1; s < kMaxSplits; ++s)
+  for (int s = 1; s < MAXS; ++s)
     if (s < splits) { a.x += v[s].x; a.y += v[s].y; a.z += v[s].z; a.w += v[s].w; }
   return a;
 }
@@ -587,8 +588,8 @@ __global__ void __launch_bounds__(320) ln_kernel(const DecodeState st, const LnA
     reinterpret_cast<float4*>(xr)[t] = x;
   } else if (MODE == 2) {
     x = __ldcg(reinterpret_cast<const float4*>(xr) + t);
-    const float4 acc = sum_splits4(a.res.p + size_t(r) * a.res.n + 4 * t,
-                                   size_t(kRows) * a.res.n, a.res.splits);
+    const float4 acc = sum_splits4<kMaxHeads>(a.res.p + size_t(r) * a.res.n + 4 * t,
+                                              size_t(kRows) * a.res.n, a.res.splits);
     x.x += acc.x + rb.x; x.y += acc.y + rb.y; x.z += acc.z + rb.z; x.w += acc.w + rb.w;
     reinterpret_cast<float4*>(xr)[t] = x;
   } else {
@@ -613,7 +614,7 @@ __global__ void __launch_bounds__(320) ln_kernel(const DecodeState st, const LnA
 int launch_ln(const DecodeState& st, const LnArgs& a, cudaStream_t stream) {
   DM_REQUIRE(st.d % 128 == 0 && st.d / 4 <= 320, "LayerNorm: d must be a multiple of 128, <= 1280");
   DM_REQUIRE(a.mode != 2 || (a.res.p != nullptr && a.res.splits >= 1 &&
-                             a.res.splits <= kMaxSplits && a.res.n == st.d),
+                             a.res.splits <= kMaxHeads && a.res.n == st.d),
              "LayerNorm: residual partials missing");
   const dim3 grid(kRows), block(st.d / 4);
   switch (a.mode) {
@@ -830,22 +831,45 @@ int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, floa
 
 constexpr int kXaThreads = 192;                               // one key per thread
 constexpr int kXaKeys = 192;                                  // ceil(1500 / 8 / 64) * 64
-constexpr int kXaSmem = 1024 + 2 * kXaKeys * 128 + 64;   // (align) K, V blocks + 3 mbarriers
+constexpr int kXaSmem = 1024 + 2 * kXaKeys * 128 + 64;   // (align) K, V blocks + mbarriers
+constexpr int kXaPush = 64 + 4;                          // o[64], max, sum (+pad): floats per split
 static_assert(kXSplits * kXaKeys >= 1500 && (kXSplits - 1) * kXaKeys < 1500, "key splits");
 
-// Cross-attention for (row, head, key split). The split's K and V blocks
-// (contiguous in the slot's cross-KV cache) are bulk-copied into shared
-// memory before the dependency wait; after it only q is read. The 8 key
-// splits of a (row, head) form a cluster: every split pushes its (max, sum,
-// o[64]) into rank 0's shared memory (DSMEM stores + a release arrive on rank
-// 0's mbarrier) and leaves; rank 0 merges them in split order.
-__global__ void __launch_bounds__(kXaThreads)
+// async store into another CTA's shared memory, completing `bytes` on that CTA's mbarrier
+__device__ __forceinline__ void st_async_v4(uint32_t addr, float4 v, uint32_t bar) {
+  asm volatile(
+      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+          addr),
+      "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
+      "r"(__float_as_uint(v.w)), "r"(bar)
+      : "memory");
+}
+
+// Cross-attention + cross-o projection for (row, head, key split)
+// (modeling_whisper.py:398-406, encoder_attn of the decoder layer; q·64^-½ at
+// :310). The split's K and V blocks (contiguous in the slot's cross-KV cache)
+// are TMA-loaded into shared memory before the dependency wait; after it only
+// q is read. The 8 key splits of a (row, head) form a cluster:
+//   1. scores (one key per thread), two-pass softmax, P.V over the split;
+//   2. every split st.async's (o[64], max, sum) into every rank's shared
+//      memory (completion on that rank's mbarrier: no cluster-wide fence) and
+//      each rank merges the 8 splits in split order (identical on all ranks);
+//   3. rank s computes output features [s*d/8, +d/8) of Wo[:, h*64 .. +64].o_h
+//      -- its 16*d-byte weight slice is bulk-copied into the dead K buffer as
+//      soon as the scores are done -- and stores them as head h's partial.
+// The cross-o GEMV launch of the unfused chain disappears; every reduction
+// order depends only on d and key positions, never on the batch.
+__global__ void __launch_bounds__(kXaThreads, 4)
 cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, int layer,
-                  const Partials xq, float q_scale) {
+                  const Partials xq, float q_scale, const uint16_t* __restrict__ wo_pack,
+                  float* __restrict__ part_o) {
   extern __shared__ uint8_t xa_raw[];
   uint8_t* xa_smem = xa_raw + ((1024 - (smem_u32(xa_raw) & 1023)) & 1023);   // TMA swizzle atoms
-  __shared__ float qs[64], sc[kXaKeys], red[8], op[kXaThreads / 32][64];
-  __shared__ float rml[kXSplits][2], ro[kXSplits][64];     // rank 0: pushed split results
+  __shared__ __align__(16) float qs[64];
+  __shared__ __align__(16) float oh[64];
+  __shared__ __align__(16) float push[kXSplits][kXaPush];   // split results (pushed by every rank)
+  __shared__ __align__(16) float mine[kXaPush];
+  __shared__ float sc[kXaKeys], red[8], op[kXaThreads / 32][64];
   const int r = blockIdx.x, h = blockIdx.y, sp = blockIdx.z, tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
   if (tid == 0) trace_mark(st, 0);
@@ -854,17 +878,20 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
   const int slot = st.active[r];
   // (no done-slot early exit here: it would put a dependent load in front of
   // the K/V prefetch of every CTA)
-  const int d = st.d, H = st.heads;
+  const int d = st.d, H = st.heads, d8 = d / 8;
   const int k0 = sp * kXaKeys, nk = min(1500, k0 + kXaKeys) - k0;
   uint8_t* Ks = xa_smem;
   uint8_t* Vs = xa_smem + kXaKeys * 128;
+  const uint16_t* Wo = reinterpret_cast<const uint16_t*>(Ks);   // [d/8][64], after the scores
   uint64_t* barK = reinterpret_cast<uint64_t*>(xa_smem + 2 * kXaKeys * 128);
   uint64_t* barV = barK + 1;
-  uint64_t* barM = barK + 2;                     // rank 0: split results landed
+  uint64_t* barW = barK + 2;
+  uint64_t* barM = barK + 3;                     // the 8 split results landed (st.async)
   if (tid == 0) {
     mbar_init(barK, 1);
     mbar_init(barV, 1);
-    mbar_init(barM, kXSplits);
+    mbar_init(barW, 1);
+    mbar_init(barM, 1);
     fence_barrier_init();
     // K and V of the split: 3 TMA boxes of 64 keys each (128B-swizzled rows;
     // keys past the slot's 1500 are masked), cross-KV never depends on the
@@ -878,9 +905,10 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     mbar_arrive_expect_tx(barV, 3 * 64 * 128);
 #pragma unroll
     for (int bx = 0; bx < 3; ++bx) tma_load_2d(Vs + bx * 64 * 128, &tm, barV, 0, row_v + bx * 64);
+    mbar_arrive_expect_tx(barM, kXSplits * kXaPush * 4);
   }
   __syncthreads();
-  cluster_arrive_relaxed();                      // rank 0's barM is initialised
+  cluster_arrive_relaxed();                      // every rank's barM is initialised
   const float bq = tid < 64 ? bf16_to_f32(xq.bias[h * 64 + tid]) : 0.f;
   pdl_wait();
   if (tid == 0) trace_mark(st, 1);
@@ -919,7 +947,13 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     sc[tid] = s;
     mloc = s;
   }
-  const float m = block_max(mloc, red);
+  const float m = block_max(mloc, red);          // (its barrier retires every K read)
+  if (tid == 0) {
+    // the K buffer is dead: fetch this rank's cross-o slice into it
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(barW, 16 * d);
+    bulk_load(Ks, wo_pack + size_t(h * kXSplits + sp) * d8 * 64, 16 * d, barW);
+  }
   float e = 0.f;
   if (tid < nk) {
     e = exp2f((sc[tid] - m) * kLog2e);
@@ -940,42 +974,75 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
   op[warp][2 * lane] = o0;
   op[warp][2 * lane + 1] = o1;
   __syncthreads();
-  cluster_wait();                                // (all ranks arrived long ago)
+  // 2. push (o, max, sum) to every rank; merge the 8 splits in split order
   if (tid < 64) {
     float a = 0.f;
 #pragma unroll
     for (int w = 0; w < kXaThreads / 32; ++w) a += op[w][tid];
-    st_dsmem_f32(dsmem_addr(&ro[sp][tid], 0), a);
-    if (tid == 0) {
-      st_dsmem_f32(dsmem_addr(&rml[sp][0], 0), m);
-      st_dsmem_f32(dsmem_addr(&rml[sp][1], 0), l);
-    }
+    mine[tid] = a;
+  } else if (tid == 64) {
+    mine[64] = m;
+    mine[65] = l;
+    mine[66] = 0.f;
+    mine[67] = 0.f;
   }
   __syncthreads();
-  if (tid == 0) mbar_arrive_remote(dsmem_addr(barM, 0));
-  if (sp == 0) {
-    mbar_wait_cluster(barM, 0);
-    if (tid < 64) {
-      float M = -INFINITY;
+  cluster_wait();                                // (all ranks arrived long ago)
+  if (tid < kXSplits * (kXaPush / 4)) {          // 8 ranks x 17 float4 chunks
+    const int dst = tid / (kXaPush / 4), ch = tid % (kXaPush / 4);
+    st_async_v4(dsmem_addr(&push[sp][4 * ch], dst), *reinterpret_cast<const float4*>(&mine[4 * ch]),
+                dsmem_addr(barM, dst));
+  }
+  mbar_wait(barM, 0);
+  if (tid < 64) {
+    float M = -INFINITY;
 #pragma unroll
-      for (int s = 0; s < kXSplits; ++s) M = fmaxf(M, rml[s][0]);
-      float Ls = 0.f, O = 0.f;
+    for (int s = 0; s < kXSplits; ++s) M = fmaxf(M, push[s][64]);
+    float Ls = 0.f, O = 0.f;
 #pragma unroll
-      for (int s = 0; s < kXSplits; ++s) {
-        const float f = exp2f((rml[s][0] - M) * kLog2e);
-        Ls += rml[s][1] * f;
-        O += ro[s][tid] * f;
-      }
-      store_hilo1(st, r, h * 64 + tid, O / Ls);
+    for (int s = 0; s < kXSplits; ++s) {
+      const float f = exp2f((push[s][64] - M) * kLog2e);
+      Ls += push[s][65] * f;
+      O += push[s][tid] * f;
     }
+    oh[tid] = O / Ls;
+  }
+  __syncthreads();
+  // 3. output features sp*d/8 + n of Wo[:, h*64 .. +64] . o_h: 8 lanes per
+  // feature (16-byte chunk each, conflict-free), xor tree over the 8 lanes
+  mbar_wait(barW, 0);
+  const int ch = tid & 7;
+  float ov[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) ov[j] = oh[ch * 8 + j];
+  float* dst = part_o + (size_t(h) * kRows + r) * d + sp * d8;
+  for (int n = tid >> 3; n < d8; n += kXaThreads / 8) {     // (warp-uniform: d/8 % 4 == 0)
+    const uint4 w = *reinterpret_cast<const uint4*>(Wo + n * 64 + ch * 8);
+    float acc = ov[0] * __uint_as_float(w.x << 16);
+    acc = fmaf(ov[1], __uint_as_float(w.x & 0xFFFF0000u), acc);
+    acc = fmaf(ov[2], __uint_as_float(w.y << 16), acc);
+    acc = fmaf(ov[3], __uint_as_float(w.y & 0xFFFF0000u), acc);
+    acc = fmaf(ov[4], __uint_as_float(w.z << 16), acc);
+    acc = fmaf(ov[5], __uint_as_float(w.z & 0xFFFF0000u), acc);
+    acc = fmaf(ov[6], __uint_as_float(w.w << 16), acc);
+    acc = fmaf(ov[7], __uint_as_float(w.w & 0xFFFF0000u), acc);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    if (ch == 0) dst[n] = acc;
   }
   if (tid == 0) trace_mark(st, 3);
 }
 
 int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
-                      const Partials& xq, float q_scale, cudaStream_t stream) {
+                      const Partials& xq, float q_scale, const uint16_t* wo_pack, float* part_o,
+                      cudaStream_t stream) {
   DM_REQUIRE(xq.p != nullptr && xq.n == st.d && xq.bias != nullptr && xq.splits >= 1 &&
                  xq.splits <= kMaxSplits, "cross-attn: q partials");
+  DM_REQUIRE(wo_pack != nullptr && part_o != nullptr, "cross-attn: cross-o operands");
+  DM_REQUIRE(st.d % 64 == 0, "cross-attn: d must be a multiple of 64");
+  DM_REQUIRE(16 * st.d <= kXaKeys * 128 && st.heads <= kMaxHeads,
+             "cross-attn: the cross-o slice must fit the K buffer");
   static bool attr = false;
   if (!attr) {
     DM_CHECK_CUDA(cudaFuncSetAttribute(cross_attn_kernel,
@@ -984,7 +1051,24 @@ int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int lay
   }
   DM_CHECK_CUDA(launch_pdl_cluster(cross_attn_kernel, dim3(kRows, st.heads, kXSplits),
                                    dim3(kXaThreads), dim3(1, 1, kXSplits), kXaSmem, stream,
-                                   xkv_map, st, layer, xq, q_scale));
+                                   xkv_map, st, layer, xq, q_scale, wo_pack, part_o));
+  return 0;
+}
+
+__global__ void repack_xo_kernel(const uint16_t* __restrict__ wo, uint16_t* __restrict__ out, int d) {
+  // wo [d, d] ([out, in]) -> out [H][8][d/8][64]: the (head h, split s) slice =
+  // output features s*d/8 .. +d/8 x input dims h*64 .. +64, contiguous
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d * d) return;
+  const int d8 = d / 8;
+  const int j = i % 64, n = (i / 64) % d8, s = (i / (64 * d8)) % kXSplits, h = i / (64 * d);
+  out[i] = wo[size_t(s * d8 + n) * d + h * 64 + j];
+}
+
+int repack_xo(const uint16_t* wo, uint16_t* out, int d, int H, cudaStream_t stream) {
+  DM_REQUIRE(d == H * 64 && d % 32 == 0, "repack_xo: d = 64 * heads");
+  repack_xo_kernel<<<ceil_div(d * d, 256), 256, 0, stream>>>(wo, out, d);
+  DM_CHECK_LAUNCH();
   return 0;
 }
 

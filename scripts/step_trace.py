@@ -21,7 +21,7 @@ for i in range(0, S, 32):
 eng.admit(slots, [400] * S)
 names = []
 for l in range(dims.dec_layers):
-    names += [f"L{l}.{k}" for k in ("ln1", "qkv", "self", "o", "ln2", "xq", "xattn", "xo", "ln3", "fc1", "fc2")]
+    names += [f"L{l}.{k}" for k in ("ln1", "qkv", "self", "o", "ln2", "xq", "xattn", "ln3", "fc1", "fc2")]
 names += ["ln_f", "lm_head", "finalize"]
 lib = eng.lib
 def dbg(which, buf=None, n=0):
@@ -67,5 +67,5 @@ for rows in rows_list:
         d[0] += r["gap_us"]; d[1] += r["span_us"]; d[2] += 1
     out[rows] = {"step_us": round(total, 1),
                  "by_kind": {k: {"n": v[2], "gap_us": round(v[0], 1), "span_us": round(v[1], 1)} for k, v in kinds.items()},
-                 "layer0": res[:13]}
+                 "layer0": res[:12]}
 print(json.dumps(out, indent=1))
