@@ -269,6 +269,7 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
 
     # dominant decode kernel: cross-attention over a full slot set, CUDA events
     roof = measure_roofline(eng, dims, args)
+    stages = measure_stages(eng, dims, segs, offs, pcm_dev)
 
     # e2e through the public API (host PCM -> results)
     def e2e_once():
@@ -317,11 +318,109 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "path": "SegmentQueue(dynamic) -> B200Backend.transcribe_batch (host int16)"},
-            "roofline": roof, "cpu_baseline": cpu, "clocks": clocks.summary(),
+            "roofline": roof, "stages": stages, "cpu_baseline": cpu, "clocks": clocks.summary(),
             "gpu_launches": launches // args.steps,
             "gpu_launches_note": "kernels per timed step (C-ABI counter; graph nodes per replay)",
         }
         print(json.dumps(line), flush=True)
+
+
+def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
+    """Per-stage throughput as a fraction of its roofline (north star: log-mel
+    and decode on HBM GB/s, encoder on dense bf16 TFLOP/s), each timed live
+    with CUDA events on the engine stream, L2 flushed before every timed call.
+
+      log-mel : dm_logmel over the first E workload segments; algorithmic bytes
+                = true int16 PCM (2 n) + the fp32 [n_mels, 3000] features
+                (SURVEY.md §8(d)).
+      encoder : dm_whisper_encode of the same E segments (log-mel -> conv stem
+                -> layers -> cross-KV); algorithmic FLOPs = E x (encoder +
+                cross-KV) per segment, SURVEY.md §8(d).
+      decode  : one greedy step with all 64 slots active (same E segments
+                replicated); algorithmic bytes = decoder weights + every active
+                slot's cross-KV + its self-KV up to the fed position."""
+    import ctypes as C
+    import json as _j
+    import torch
+    from paper_2507_01021_b200.engine import ResidentPCM
+    peaks = _j.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    tc = float(peaks.get("bf16_tflops", 2250.0))
+    dev = pcm_dev.device
+    E = eng.max_encode_batch
+    sub = [(uid, x, int(o)) for (uid, x), o in zip(segs[:E], offs[:E])]
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def ev_ms(fn, reps=5):
+        out = []
+        for _ in range(reps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize(dev)
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(eng.stream)
+            fn()
+            b.record(eng.stream)
+            torch.cuda.synchronize(dev)
+            out.append(a.elapsed_time(b))
+        return statistics.median(out)
+
+    # log-mel (K1)
+    nm = dims.n_mels
+    offs_d = torch.tensor([o for _, _, o in sub], dtype=torch.int64, device=dev)
+    lens_d = torch.tensor([len(x) for _, x, _ in sub], dtype=torch.int32, device=dev)
+    mel = torch.empty(E, nm, 3000, dtype=torch.float32, device=dev)
+    from paper_2507_01021_b200 import _native
+    lm = lambda: _native.check(eng.lib.dm_logmel(C.c_void_p(pcm_dev.data_ptr()),
+                                                C.c_void_p(offs_d.data_ptr()),
+                                                C.c_void_p(lens_d.data_ptr()), E, nm,
+                                                C.c_void_p(mel.data_ptr()), eng._s))
+    lm()
+    lm_ms = ev_ms(lm)
+    lm_bytes = sum(2 * min(len(x), 480000) for _, x, _ in sub) + E * nm * 3000 * 4
+    # encoder (K2-K5)
+    d, L, Ld, F = dims.d_model, dims.enc_layers, dims.dec_layers, dims.ffn
+    enc_flop = (2 * nm * 3 * d * 3000 + 2 * 3 * d * d * 1500
+                + L * (8 * d * d * 1500 + 4 * 1500 * 1500 * d + 4 * d * F * 1500)
+                + 4 * Ld * d * d * 1500)
+    jobs = [ResidentPCM(o, len(x)) for _, x, o in sub]
+    slots = list(range(E))
+    en = lambda: eng.encode(jobs, slots)
+    en()
+    en_ms = ev_ms(en)
+    # decode step at 64 rows (K6)
+    S = eng.max_slots
+    for i in range(E, S, E):
+        eng.encode(jobs[:min(E, S - i)], list(range(i, min(S, i + E))))
+    allslots = list(range(S))
+    eng.admit(allslots, [400] * S)
+    eng.set_active(allslots)
+    eng.step(8)                       # past the prompt: positions 7..
+    torch.cuda.synchronize(dev)
+    pos = 8
+    st_ms = ev_ms(lambda: eng.step(1), reps=9)
+    eng.release(allslots)
+    eng.set_active([])
+    torch.cuda.synchronize(dev)
+    w_bytes = 2 * (Ld * (4 * d * d + 2 * d * d + 2 * d * F) + dims.vocab * d)
+    x_bytes = S * Ld * 2 * 1500 * d * 2
+    kv_bytes = S * Ld * 2 * d * 2 * (pos + 5)
+    st_bytes = w_bytes + x_bytes + kv_bytes
+    return {
+        "logmel": {"bound": "hbm", "achieved": lm_bytes / (lm_ms / 1e3) / 1e9, "peak": hbm,
+                   "unit": "GB/s", "frac": lm_bytes / (lm_ms / 1e3) / 1e9 / hbm,
+                   "ms": lm_ms, "bytes": lm_bytes, "segments": E,
+                   "note": "FFT+mel is ~27 MFLOP/segment: the kernel sits at the FP32 ridge"},
+        "encoder": {"bound": "tensor", "achieved": E * enc_flop / (en_ms / 1e3) / 1e12, "peak": tc,
+                    "unit": "TFLOP/s", "frac": E * enc_flop / (en_ms / 1e3) / 1e12 / tc,
+                    "ms": en_ms, "flop": E * enc_flop, "segments": E,
+                    "note": "whole dm_whisper_encode (log-mel + conv stem + layers + LN + cross-KV)"},
+        "decode_step": {"bound": "hbm", "achieved": st_bytes / (st_ms / 1e3) / 1e9, "peak": hbm,
+                        "unit": "GB/s", "frac": st_bytes / (st_ms / 1e3) / 1e9 / hbm,
+                        "ms": st_ms, "bytes": st_bytes, "rows": S,
+                        "note": "one CUDA-graph step: weights + cross-KV + self-KV, 64 active slots"},
+        "peak_source": "MEASURED_PEAKS.json (hbm_gbs burst copy, bf16_tflops burst)" if peaks else "fallback",
+    }
 
 
 def measure_roofline(eng, dims, args) -> dict:

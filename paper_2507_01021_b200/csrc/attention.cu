@@ -18,7 +18,7 @@
 namespace dm {
 
 constexpr int kAttnThreads = 320;    // w0 TMA, w1 MMA, w2..5 softmax tile A, w6..9 tile B
-constexpr int kAttnKS = 2;           // K/V ring depth
+constexpr int kAttnKS = 4;           // K/V ring depth (TMA lookahead of 3 key blocks)
 constexpr int kQBytes = 128 * 128;   // 128 rows x 64 bf16
 constexpr int kKBytes = 128 * 128;
 constexpr int kVBytes = 2 * 64 * 128;  // two 64-key boxes of [64 dims x 64 keys]
@@ -142,13 +142,14 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
       const uint32_t sv = smem_u32(smem + AttnSmemLayout::v + st * kVBytes);
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
-        mbar_wait(&p_full[t], ph);           // softmax_t(j) done: P_t(j) written, S_t free
-        // S_t(j + 1) first: the tile's next softmax starts while PV_t(j) runs
+        // S_t(j + 1) as soon as softmax_t(j) has read S_t(j) out of TMEM (before
+        // it finishes P_t(j)): the tile's next scores overlap its own exp/pack
         if (j + 1 < nb) {
           if (t == 0) mbar_wait(&kv_full[(j + 1) % kAttnKS], ((j + 1) / kAttnKS) & 1);
           mbar_wait(&s_empty[t], ph);
           issue_s(t, j + 1);
         }
+        mbar_wait(&p_full[t], ph);           // softmax_t(j) done: P_t(j) written
         mbar_wait(&o_empty[t], ph ^ 1);      // PV_t = P_t V_j
         tc_fence_after();
         if (elect_one()) {
@@ -260,6 +261,13 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
           *dst = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
       };
+      // S_t is released right after its last TMEM load (the MMA warp then
+      // issues S_t(j + 1) while this warp still computes P from registers)
+      auto release_s = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[t]);
+      };
       if (kvalid >= 128) {
         uint32_t sb[32];
 #pragma unroll 1
@@ -267,6 +275,7 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
           tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
           tmem_ld32(tmem + lane_off + s_col + c * 32 + 32, sb);
           tmem_wait_ld();
+          if (c == 2) release_s();
           emit(c, sr, true);
           emit(c + 1, sb, true);
         }
@@ -275,17 +284,14 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
         for (int c = 0; c < 4; ++c) {
           tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
           tmem_wait_ld();
+          if (c == 3) release_s();
           emit(c, sr, false);
         }
       }
       const float rs = (rs0 + rs1) + (rs2 + rs3);
-      tc_fence_before();
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_empty[t]);
-        mbar_arrive(&p_full[t]);
-      }
+      if (lane == 0) mbar_arrive(&p_full[t]);
       l_run = l_run * alpha + rs;
       m_run = mx;
       alpha_prev = alpha;

@@ -634,13 +634,21 @@ int dm_logmel(const int16_t* pcm, const int64_t* offsets, const int32_t* lengths
   DM_REQUIRE(pcm && offsets && lengths && out, "null pointer");
   const LogmelTables* tab = nullptr;
   if (int rc = get_logmel_tables(n_mels, &tab)) return rc;
-  uint32_t* segmax = nullptr;
-  DM_CHECK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&segmax), sizeof(uint32_t) * n,
-                                static_cast<cudaStream_t>(stream)));
-  int rc = launch_logmel(pcm, offsets, lengths, n, n_mels, tab, out, nullptr, segmax,
-                         static_cast<cudaStream_t>(stream));
-  cudaFreeAsync(segmax, static_cast<cudaStream_t>(stream));
-  return rc;
+  // per-segment max scratch: grown once, reused (no per-call allocation on the stream)
+  static uint32_t* segmax = nullptr;
+  static int segmax_n = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (segmax_n < n) {
+    DM_CHECK_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    if (segmax) cudaFree(segmax);
+    segmax = nullptr;
+    segmax_n = 0;
+    DM_CHECK_CUDA(cudaMalloc(reinterpret_cast<void**>(&segmax), sizeof(uint32_t) * n));
+    segmax_n = n;
+  }
+  return launch_logmel(pcm, offsets, lengths, n, n_mels, tab, out, nullptr, segmax,
+                       static_cast<cudaStream_t>(stream));
 }
 
 int dm_gemm_bf16_f32(const uint16_t* A, const uint16_t* Wt, const uint16_t* bias, float* out,

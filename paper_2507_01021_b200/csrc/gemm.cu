@@ -10,6 +10,7 @@
 
 #include <cudaTypedefs.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "gemm.cuh"
@@ -211,28 +212,41 @@ __device__ __forceinline__ void epilogue_chunk(const Epilogue& e, const GemmArgs
   }
 }
 
-template <int BN, int STAGES>
+// fp32 residual tiles (EPI_RESID_F32, BN = 128) are TMA-loaded by the
+// producer into a 64 KB shared buffer -- four 32-column boxes, 128B-swizzled
+// -- as soon as the epilogue has taken the previous tile's residual into
+// registers, so the epilogue never waits on a global load.
+template <int BN, int STAGES, int MODE>
+constexpr bool kResTma = BN == 128 && STAGES == 5 && MODE == EPI_RESID_F32;
+
+template <int BN, int STAGES, int MODE>
 struct GemmSmem {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kBytes = STAGES * kStageBytes + 1024 /*align*/ + 256 /*bars*/;
+  static constexpr int kResBytes = kResTma<BN, STAGES, MODE> ? kBM * BN * 4 : 0;
+  static constexpr int kBytes = STAGES * kStageBytes + kResBytes + 1024 /*align*/ + 256 /*bars*/;
 };
 
 template <int BN, int STAGES, int MODE>
 __global__ void __launch_bounds__(kGemmThreads, 1)
 gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
-                    const __grid_constant__ CUtensorMap tmap_b, const GemmArgs g,
+                    const __grid_constant__ CUtensorMap tmap_b,
+                    const __grid_constant__ CUtensorMap tmap_r, const GemmArgs g,
                     const TileGeom geo) {
-  using S = GemmSmem<BN, STAGES>;
+  using S = GemmSmem<BN, STAGES, MODE>;
+  constexpr bool RT = kResTma<BN, STAGES, MODE>;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStageBytes);
+  uint8_t* rbuf = smem + STAGES * S::kStageBytes;                     // [4 boxes][128 rows][128 B]
+  uint64_t* full = reinterpret_cast<uint64_t*>(rbuf + S::kResBytes);
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;      // [2]
   uint64_t* tmem_empty = tmem_full + 2;      // [2]
-  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* res_full = tmem_empty + 2;
+  uint64_t* res_empty = res_full + 1;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(res_empty + 1);
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
@@ -248,6 +262,9 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
       mbar_init(&tmem_full[s], 1);
       mbar_init(&tmem_empty[s], kEpiWarps);   // one arrive per epilogue warp
     }
+    mbar_init(res_full, 1);
+    mbar_init(res_empty, kEpiWarps);
+    if (RT) tma_prefetch_desc(&tmap_r);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_base_slot, 2 * BN);
@@ -261,10 +278,20 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
     if (elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < geo.tiles; tile += gridDim.x) {
+      int it = 0;
+      for (int tile = blockIdx.x; tile < geo.tiles; tile += gridDim.x, ++it) {
         const int nt = tile % geo.NT;
         const int mb = tile / geo.NT;
         const int b = mb / geo.MT, mt = mb % geo.MT;
+        if (RT) {
+          // this tile's residual, once the epilogue holds the previous one in registers
+          mbar_wait(res_empty, (it & 1) ^ 1);
+          mbar_arrive_expect_tx(res_full, S::kResBytes);
+#pragma unroll
+          for (int j = 0; j < BN / 32; ++j)
+            tma_load_2d(rbuf + j * (kBM * 128), &tmap_r, res_full, nt * BN + j * 32,
+                        b * g.T + mt * kBM);
+        }
         for (int kb = 0; kb < geo.KB; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * S::kStageBytes;
@@ -335,7 +362,20 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
       float4 res[kPre];
       const bool pre = BN == 128 && MODE == EPI_RESID_F32 && row_valid &&
                        nt * BN + (chalf + 1) * (BN / 2) <= g.N;
-      if (pre) {
+      if (RT) {
+        // rows quad*32 + lane, columns chalf*64 .. +64 = boxes 2*chalf, 2*chalf + 1;
+        // 16-byte chunk q of row r sits at chunk q ^ (r & 7) (conflict-free)
+        mbar_wait(res_full, it & 1);
+        const int tr = quad * 32 + lane;
+#pragma unroll
+        for (int i = 0; i < kPre; ++i) {
+          const int box = chalf * 2 + i / 8, q = i % 8;
+          res[i] = *reinterpret_cast<const float4*>(rbuf + box * (kBM * 128) + tr * 128 +
+                                                    ((q ^ (tr & 7)) << 4));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(res_empty);
+      } else if (pre) {
         const float4* src = reinterpret_cast<const float4*>(
             static_cast<const float*>(g.epi.out) + (size_t(b) * g.T + t) * g.epi.ldo + nt * BN +
             chalf * (BN / 2));
@@ -419,7 +459,20 @@ static int make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t*
 
 template <int BN, int STAGES, int MODE>
 static int launch_bn_mode(const GemmArgs& g, cudaStream_t stream) {
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mr;
+  std::memset(&mr, 0, sizeof(mr));
+  if (kResTma<BN, STAGES, MODE>) {
+    // fp32 residual [rows, N] (row stride ldo), boxes of 32 columns x 128 rows, 128B swizzle
+    DM_REQUIRE(g.a_mode == A_FLAT && g.Bt == 1 && g.epi.ldo % 4 == 0, "residual TMA: flat rows");
+    cuuint64_t dims[2] = {cuuint64_t(g.N), cuuint64_t(g.T)};
+    cuuint64_t str[1] = {cuuint64_t(g.epi.ldo) * 4};
+    cuuint32_t box[2] = {32, kBM};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode(&mr, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, g.epi.out, dims, str, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DM_REQUIRE(r == CUDA_SUCCESS, "residual tensor map: CUresult " + std::to_string(int(r)));
+  }
   if (g.a_mode == A_FLAT) {
     cuuint64_t dims[3] = {cuuint64_t(g.K), cuuint64_t(g.T), cuuint64_t(g.Bt)};
     cuuint64_t str[2] = {cuuint64_t(g.lda) * 2, cuuint64_t(g.a_bstride) * 2};
@@ -450,7 +503,7 @@ static int launch_bn_mode(const GemmArgs& g, cudaStream_t stream) {
   geo.tiles = g.Bt * geo.MT * geo.NT;
   geo.KB = ceil_div(g.K, kBK);
   geo.cpb = g.grouped ? 1 : (g.C > 0 ? g.C / kBK : 1);
-  const int smem = GemmSmem<BN, STAGES>::kBytes;
+  const int smem = GemmSmem<BN, STAGES, MODE>::kBytes;
   static bool attr = false;
   if (!attr) {
     DM_CHECK_CUDA(cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, STAGES, MODE>,
@@ -458,7 +511,7 @@ static int launch_bn_mode(const GemmArgs& g, cudaStream_t stream) {
     attr = true;
   }
   int grid = geo.tiles < kNumSMs ? geo.tiles : kNumSMs;
-  gemm_tcgen05_kernel<BN, STAGES, MODE><<<grid, kGemmThreads, smem, stream>>>(ma, mb, g, geo);
+  gemm_tcgen05_kernel<BN, STAGES, MODE><<<grid, kGemmThreads, smem, stream>>>(ma, mb, mr, g, geo);
   DM_CHECK_LAUNCH();
   return 0;
 }
@@ -525,6 +578,8 @@ int launch_gemm(const GemmArgs& g, cudaStream_t stream) {
     return launch_bn_mode<64, 8, EPI_W2V_POS>(g, stream);
   }
   if (g.N % 256 == 0 && g.N >= 1024) return launch_bn<256, 4>(g, stream);
+  if (g.epi.mode == EPI_RESID_F32 && g.a_mode == A_FLAT && g.Bt == 1)
+    return launch_bn_mode<128, 5, EPI_RESID_F32>(g, stream);     // + 64 KB residual buffer
   return launch_bn<128, 6>(g, stream);
 }
 
