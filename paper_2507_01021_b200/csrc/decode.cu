@@ -563,9 +563,16 @@ __device__ __forceinline__ float block_sum_fixed(float v, float* red) {
   return s;
 }
 
+// MODE 2 brings the residual row and every partial row into shared memory
+// with one bulk copy each, all issued by one thread onto one mbarrier: a
+// single L2 round trip however many partials there are (per-thread loads
+// issue in groups of ~6 -- the SASS scoreboard limit -- so 8-20 partials would
+// cost 2-4 dependent round trips).
 template <int MODE>
 __global__ void __launch_bounds__(320) ln_kernel(const DecodeState st, const LnArgs a) {
+  extern __shared__ __align__(16) float ln_rows[];      // MODE 2: [1 + splits][d]
   __shared__ float red[16];
+  __shared__ __align__(8) uint64_t ln_bar;
   const int r = blockIdx.x, t = threadIdx.x, d = st.d;
   if (t == 0) trace_mark(st, 0);
   pdl_trigger();
@@ -575,6 +582,10 @@ __global__ void __launch_bounds__(320) ln_kernel(const DecodeState st, const LnA
   float4 rb = make_float4(0.f, 0.f, 0.f, 0.f);
   if (MODE == 2 && a.res.bias) rb = bf16x4_to_f32(__ldg(reinterpret_cast<const uint2*>(a.res.bias) + t));
   const int slot = r < R ? st.active[r] : 0;
+  if (MODE == 2 && t == 0) {
+    mbar_init(&ln_bar, 1);
+    fence_barrier_init();
+  }
   pdl_wait();
   if (t == 0) trace_mark(st, 1);
   if (r >= R) return;
@@ -587,17 +598,30 @@ __global__ void __launch_bounds__(320) ln_kernel(const DecodeState st, const LnA
     x = make_float4(e.x + pe.x, e.y + pe.y, e.z + pe.z, e.w + pe.w);
     reinterpret_cast<float4*>(xr)[t] = x;
   } else if (MODE == 2) {
-    x = __ldcg(reinterpret_cast<const float4*>(xr) + t);
-    const float4 acc = sum_splits4<kMaxHeads>(a.res.p + size_t(r) * a.res.n + 4 * t,
-                                              size_t(kRows) * a.res.n, a.res.splits);
+    const int ns = a.res.splits;
+    if (t == 0) {
+      mbar_arrive_expect_tx(&ln_bar, uint32_t(ns + 1) * d * 4);
+      bulk_load(ln_rows, xr, d * 4, &ln_bar);
+      for (int s = 0; s < ns; ++s)
+        bulk_load(ln_rows + (s + 1) * d, a.res.p + (size_t(s) * kRows + r) * a.res.n, d * 4, &ln_bar);
+    }
+    mbar_wait(&ln_bar, 0);
+    x = reinterpret_cast<const float4*>(ln_rows)[t];
+    float4 acc = reinterpret_cast<const float4*>(ln_rows + d)[t];
+    for (int s = 1; s < ns; ++s) {
+      const float4 v = reinterpret_cast<const float4*>(ln_rows + (s + 1) * d)[t];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
     x.x += acc.x + rb.x; x.y += acc.y + rb.y; x.z += acc.z + rb.z; x.w += acc.w + rb.w;
     reinterpret_cast<float4*>(xr)[t] = x;
   } else {
     x = __ldcg(reinterpret_cast<const float4*>(xr) + t);
   }
+  if (t == 0) trace_mark(st, 4);
   const float mean = block_sum_fixed((x.x + x.y) + (x.z + x.w), red) / d;
   const float c0 = x.x - mean, c1 = x.y - mean, c2 = x.z - mean, c3 = x.w - mean;
   const float var = block_sum_fixed((c0 * c0 + c1 * c1) + (c2 * c2 + c3 * c3), red) / d;
+  if (t == 0) trace_mark(st, 5);
   const float rstd = rsqrtf(var + 1e-5f);
   uint16_t h[4], l[4];
   split_hilo(c0 * rstd * gm.x + bt.x, h[0], l[0]);
@@ -620,7 +644,17 @@ int launch_ln(const DecodeState& st, const LnArgs& a, cudaStream_t stream) {
   switch (a.mode) {
     case 0: DM_CHECK_CUDA(launch_pdl(ln_kernel<0>, grid, block, 0, stream, st, a)); break;
     case 1: DM_CHECK_CUDA(launch_pdl(ln_kernel<1>, grid, block, 0, stream, st, a)); break;
-    case 2: DM_CHECK_CUDA(launch_pdl(ln_kernel<2>, grid, block, 0, stream, st, a)); break;
+    case 2: {
+      const int smem = (a.res.splits + 1) * st.d * 4;
+      static bool attr = false;
+      if (!attr) {
+        DM_CHECK_CUDA(cudaFuncSetAttribute(ln_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (kMaxHeads + 1) * 1280 * 4));
+        attr = true;
+      }
+      DM_CHECK_CUDA(launch_pdl(ln_kernel<2>, grid, block, smem, stream, st, a));
+      break;
+    }
     default: DM_REQUIRE(false, "LayerNorm: unknown mode");
   }
   return 0;
@@ -722,7 +756,9 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
     vc[tid] = bf16_to_f32(vb);
   }
   __syncthreads();
+  if (tid == 0) trace_mark(st, 4);
   if (np > 0) mbar_wait(bar, 0);
+  if (tid == 0) trace_mark(st, 5);
   const int nk = p + 1;
   float mloc = -INFINITY;
   for (int t = tid; t < nk; t += kSaThreads) {
@@ -778,6 +814,7 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
     lsum += e;
   }
   const float l = block_sum_fixed(lsum, red);    // (its barrier publishes sc[])
+  if (tid == 0) trace_mark(st, 6);
   float o0 = 0.f, o1 = 0.f;
 #pragma unroll 4
   for (int t = warp; t < nk; t += 8) {
@@ -803,6 +840,7 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
   op[warp][2 * lane] = o0;
   op[warp][2 * lane + 1] = o1;
   __syncthreads();
+  if (tid == 0) trace_mark(st, 7);
   if (tid < 64) {
     float a = 0.f;
 #pragma unroll

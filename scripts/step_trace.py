@@ -54,7 +54,13 @@ for rows in rows_list:
         rec = {"k": nm, "gap_us": round((rel - prev_end) / 1e3, 2),
                "span_us": round((end - rel) / 1e3, 2),
                "early_us": round((rel - entry) / 1e3, 2)}
-        for j, lab in ((4, "x_landed"), (7, "mma_issued"), (5, "mma_done"), (6, "stores")):
+        kind = nm.split(".")[-1]
+        labs = {"self": ((4, "qkv_ready"), (5, "pages_landed"), (6, "softmax_done"), (7, "pv_done")),
+                "ln1": ((4, "loaded"), (5, "stats_done")), "ln2": ((4, "loaded"), (5, "stats_done")),
+                "ln3": ((4, "loaded"), (5, "stats_done")), "ln_f": ((4, "loaded"), (5, "stats_done")),
+                "xattn": (),
+                }.get(kind, ((4, "x_landed"), (7, "mma_issued"), (5, "mma_done"), (6, "stores")))
+        for j, lab in labs:
             if t[k][j] > 0 and t[k][j] >= rel:
                 rec[lab + "_us"] = round((t[k][j] - rel) / 1e3, 2)
         res.append(rec)
