@@ -208,12 +208,13 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
       const int my_tiles = (tiles - 1 - int(blockIdx.x)) / int(gridDim.x) + 1;
       const int total = my_tiles * kb_per;
       int wi = 0;
+      const uint64_t keep = l2_policy_evict_last();      // weights: re-read every step
       auto issue_w = [&](int q) {
         const int s = wi % NS;
         mbar_wait(&wempty[s], ((wi / NS) & 1) ^ 1);
         mbar_arrive_expect_tx(&wfull[s], kGvWBytes);
-        tma_load_2d(ws + s * kGvWBytes, &tw, &wfull[s], (kb0 + q % kb_per) * 64,
-                    (int(blockIdx.x) + (q / kb_per) * int(gridDim.x)) * 128);
+        tma_load_2d_hint(ws + s * kGvWBytes, &tw, &wfull[s], (kb0 + q % kb_per) * 64,
+                         (int(blockIdx.x) + (q / kb_per) * int(gridDim.x)) * 128, keep);
         ++wi;
       };
       const int pre = total < NS ? total : NS;
@@ -222,8 +223,8 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
         // warp needs a single wait instead of one handshake per k-block
         mbar_arrive_expect_tx(&wfull[0], total * kGvWBytes);
         for (int q = 0; q < total; ++q)
-          tma_load_2d(ws + q * kGvWBytes, &tw, &wfull[0], (kb0 + q % kb_per) * 64,
-                      (int(blockIdx.x) + (q / kb_per) * int(gridDim.x)) * 128);
+          tma_load_2d_hint(ws + q * kGvWBytes, &tw, &wfull[0], (kb0 + q % kb_per) * 64,
+                           (int(blockIdx.x) + (q / kb_per) * int(gridDim.x)) * 128, keep);
         wi = total;
       } else {
         for (int q = 0; q < pre; ++q) issue_w(q);   // weights never depend on the predecessor
@@ -937,12 +938,15 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     tma_prefetch_desc(&tm);
     const int row_k = (((layer * st.max_slots + slot) * 2 + 0) * H + h) * 1500 + k0;
     const int row_v = row_k + H * 1500;
+    const uint64_t stream = l2_policy_evict_first();     // read once per step
     mbar_arrive_expect_tx(barK, 3 * 64 * 128);
 #pragma unroll
-    for (int bx = 0; bx < 3; ++bx) tma_load_2d(Ks + bx * 64 * 128, &tm, barK, 0, row_k + bx * 64);
+    for (int bx = 0; bx < 3; ++bx)
+      tma_load_2d_hint(Ks + bx * 64 * 128, &tm, barK, 0, row_k + bx * 64, stream);
     mbar_arrive_expect_tx(barV, 3 * 64 * 128);
 #pragma unroll
-    for (int bx = 0; bx < 3; ++bx) tma_load_2d(Vs + bx * 64 * 128, &tm, barV, 0, row_v + bx * 64);
+    for (int bx = 0; bx < 3; ++bx)
+      tma_load_2d_hint(Vs + bx * 64 * 128, &tm, barV, 0, row_v + bx * 64, stream);
     mbar_arrive_expect_tx(barM, kXSplits * kXaPush * 4);
   }
   __syncthreads();
