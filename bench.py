@@ -224,7 +224,7 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
     audio_s = sum(len(x) for _, x in segs) / 16000.0
     eng = WhisperGPU(dims, seed=0, device=local, max_slots=min(64, args.segments),
                      max_encode_batch=args.encode_batch, steps_per_poll=args.steps_per_poll,
-                     decode_groups=args.decode_groups)
+                     decode_groups=args.decode_groups, first_encode_batch=args.first_encode_batch)
     backend = B200Backend(B200BackendConfig(model=MODEL, device=local), engine=eng)
 
     # resident inputs for `value`
@@ -313,7 +313,8 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
                        "audio_s_per_gpu": round(audio_s, 3),
                        "parallelism": f"replicas x{world} (no collective)",
                        "l2": "flushed between timed steps (256 MB write)",
-                       "encode_batch": args.encode_batch, "steps_per_poll": args.steps_per_poll,
+                       "encode_batch": args.encode_batch, "first_encode_batch": args.first_encode_batch,
+                       "steps_per_poll": args.steps_per_poll,
                        "decode_groups": eng.decode_groups},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
@@ -476,6 +477,9 @@ def main():
     ap.add_argument("--ref-segments-per-step", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--decode-groups", type=int, default=None)
+    ap.add_argument("--first-encode-batch", type=int, default=8,
+                    help="segments in the first encode group of an idle engine (the GPU starts "
+                         "while the host stages the rest)")
     ap.add_argument("--profile", action="store_true",
                     help="run exactly one resident-input step and exit (ncu)")
     args = ap.parse_args()

@@ -100,7 +100,7 @@ class WhisperGPU:
                  device: int | str | torch.device = 0, max_slots: int = 64,
                  max_encode_batch: int = 32, num_pages: int | None = None,
                  eot: int | None = None, steps_per_poll: int = 8,
-                 decode_groups: int | None = None):
+                 decode_groups: int | None = None, first_encode_batch: int = 8):
         if not torch.cuda.is_available():
             raise _native.DmError("no CUDA device: the B200 engine has no CPU fallback")
         self.dims = dims
@@ -109,6 +109,7 @@ class WhisperGPU:
         self.max_slots = max_slots
         self.max_encode_batch = max_encode_batch
         self.steps_per_poll = steps_per_poll
+        self.first_encode_batch = first_encode_batch
         self.eot = dims.eot if eot is None else eot
         with torch.cuda.device(self.device):
             self.stream = torch.cuda.Stream(self.device)
@@ -362,7 +363,11 @@ class WhisperGPU:
                 pending.extend(refill(len(free) - len(pending)))
             while free and pending:
                 take = []
-                while free and pending and len(take) < self.max_encode_batch:
+                # an idle engine starts with a small group: the GPU begins
+                # while the host still stages the rest of the PCM
+                lim = self.max_encode_batch if (active or waiting or prev) else min(
+                    self.max_encode_batch, self.first_encode_batch)
+                while free and pending and len(take) < lim:
                     take.append((free.pop(), pending.popleft()))
                 slots = [s for s, _ in take]
                 self.encode([j.samples for _, j in take], slots)
