@@ -577,7 +577,10 @@ int launch_gemm(const GemmArgs& g, cudaStream_t stream) {
     DM_REQUIRE(g.epi.mode == EPI_W2V_POS, "grouped GEMM: wav2vec2 pos-conv epilogue only");
     return launch_bn_mode<64, 8, EPI_W2V_POS>(g, stream);
   }
-  if (g.N % 256 == 0 && g.N >= 1024) return launch_bn<256, 4>(g, stream);
+  // wide N, or long K (fc2, the stride-2 conv): 128 x 256 tiles cut the per-SM
+  // operand stream (bytes per FLOP (128 + BN) / (128 BN)); with a long K the
+  // epilogue's global traffic overlaps the next tile's mainloop
+  if (g.N % 256 == 0 && (g.N >= 1024 || g.K >= 1536)) return launch_bn<256, 4>(g, stream);
   if (g.epi.mode == EPI_RESID_F32 && g.a_mode == A_FLAT && g.Bt == 1)
     return launch_bn_mode<128, 5, EPI_RESID_F32>(g, stream);     // + 64 KB residual buffer
   return launch_bn<128, 6>(g, stream);
