@@ -704,7 +704,7 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
   __shared__ __align__(16) float qs[64];
   __shared__ float kc[64], vc[64];
   __shared__ float sc[kSaMaxKeys];
-  __shared__ float red[8];
+  __shared__ float redm[8], reds[8];
   __shared__ float op[8][64];
   const int r = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
@@ -807,14 +807,28 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
     sc[t] = s;
     mloc = fmaxf(mloc, s);
   }
-  const float m = block_max(mloc, red);
+  // block max / sum with one barrier each (separate per-warp slots; same
+  // reduction order as block_max / block_sum_fixed)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
+  if (lane == 0) redm[warp] = mloc;
+  __syncthreads();
+  float m = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < kSaThreads / 32; ++w) m = fmaxf(m, redm[w]);
   float lsum = 0.f;
   for (int t = tid; t < nk; t += kSaThreads) {
     const float e = exp2f((sc[t] - m) * kLog2e);
     sc[t] = e;
     lsum += e;
   }
-  const float l = block_sum_fixed(lsum, red);    // (its barrier publishes sc[])
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+  if (lane == 0) reds[warp] = lsum;
+  __syncthreads();                               // (also publishes sc[])
+  float l = 0.f;
+#pragma unroll
+  for (int w = 0; w < kSaThreads / 32; ++w) l += reds[w];
   if (tid == 0) trace_mark(st, 6);
   float o0 = 0.f, o1 = 0.f;
 #pragma unroll 4
@@ -907,8 +921,8 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
   __shared__ __align__(16) float qs[64];
   __shared__ __align__(16) float oh[64];
   __shared__ __align__(16) float push[kXSplits][kXaPush];   // split results (pushed by every rank)
-  __shared__ __align__(16) float mine[kXaPush];
-  __shared__ float sc[kXaKeys], red[8], op[kXaThreads / 32][64];
+  __shared__ float sc[kXaKeys], redm[8], reds[8];
+  __shared__ __align__(16) float op[kXaThreads / 32][64];
   const int r = blockIdx.x, h = blockIdx.y, sp = blockIdx.z, tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
   if (tid == 0) trace_mark(st, 0);
@@ -989,7 +1003,15 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     sc[tid] = s;
     mloc = s;
   }
-  const float m = block_max(mloc, red);          // (its barrier retires every K read)
+  // block max and sum with one barrier each (separate per-warp slots, so no
+  // trailing barrier; same reduction order as block_max / block_sum_fixed)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
+  if (lane == 0) redm[warp] = mloc;
+  __syncthreads();                               // (also retires every K read)
+  float m = -INFINITY;
+#pragma unroll
+  for (int w = 0; w < kXaThreads / 32; ++w) m = fmaxf(m, redm[w]);
   if (tid == 0) {
     // the K buffer is dead: fetch this rank's cross-o slice into it
     fence_proxy_async_smem();
@@ -1001,7 +1023,14 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     e = exp2f((sc[tid] - m) * kLog2e);
     sc[tid] = e;
   }
-  const float l = block_sum_fixed(e, red);       // (its barrier publishes sc[])
+  float es = e;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+  if (lane == 0) reds[warp] = es;
+  __syncthreads();                               // (also publishes sc[])
+  float l = 0.f;
+#pragma unroll
+  for (int w = 0; w < kXaThreads / 32; ++w) l += reds[w];
   mbar_wait(barV, 0);
   float o0 = 0.f, o1 = 0.f;
   const int vch = lane >> 2, vwo = (lane & 3) * 4;     // dims (2 lane, 2 lane + 1)
@@ -1016,24 +1045,22 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
   op[warp][2 * lane] = o0;
   op[warp][2 * lane + 1] = o1;
   __syncthreads();
-  // 2. push (o, max, sum) to every rank; merge the 8 splits in split order
-  if (tid < 64) {
-    float a = 0.f;
-#pragma unroll
-    for (int w = 0; w < kXaThreads / 32; ++w) a += op[w][tid];
-    mine[tid] = a;
-  } else if (tid == 64) {
-    mine[64] = m;
-    mine[65] = l;
-    mine[66] = 0.f;
-    mine[67] = 0.f;
-  }
-  __syncthreads();
+  // 2. push (o, max, sum) to every rank; merge the 8 splits in split order.
+  // Thread (rank dst, chunk ch) sums dims 4ch..4ch+3 over the warps itself
+  // and st.async's them (8 ranks x 16 chunks + 8 (max, sum) stores)
   cluster_wait();                                // (all ranks arrived long ago)
-  if (tid < kXSplits * (kXaPush / 4)) {          // 8 ranks x 17 float4 chunks
-    const int dst = tid / (kXaPush / 4), ch = tid % (kXaPush / 4);
-    st_async_v4(dsmem_addr(&push[sp][4 * ch], dst), *reinterpret_cast<const float4*>(&mine[4 * ch]),
-                dsmem_addr(barM, dst));
+  if (tid < kXSplits * 16) {
+    const int dst = tid >> 4, ch = tid & 15;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < kXaThreads / 32; ++w) {
+      const float4 v = *reinterpret_cast<const float4*>(&op[w][4 * ch]);
+      a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+    }
+    st_async_v4(dsmem_addr(&push[sp][4 * ch], dst), a, dsmem_addr(barM, dst));
+  } else if (tid < kXSplits * 16 + kXSplits) {
+    const int dst = tid - kXSplits * 16;
+    st_async_v4(dsmem_addr(&push[sp][64], dst), make_float4(m, l, 0.f, 0.f), dsmem_addr(barM, dst));
   }
   mbar_wait(barM, 0);
   if (tid < 64) {
