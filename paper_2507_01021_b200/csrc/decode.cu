@@ -569,10 +569,23 @@ __device__ __forceinline__ float block_sum_fixed(float v, float* red) {
 // single L2 round trip however many partials there are (per-thread loads
 // issue in groups of ~6 -- the SASS scoreboard limit -- so 8-20 partials would
 // cost 2-4 dependent round trips).
+// block_sum_fixed without the trailing barrier: the caller gives each
+// reduction its own per-warp slots (same order: xor tree, then warps 0..n-1)
+__device__ __forceinline__ float block_sum_once(float v, float* slots) {
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) slots[warp] = v;
+  __syncthreads();
+  float s = 0.f;
+  for (int w = 0; w < nw; ++w) s += slots[w];
+  return s;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(320) ln_kernel(const DecodeState st, const LnArgs a) {
   extern __shared__ __align__(16) float ln_rows[];      // MODE 2: [1 + splits][d]
-  __shared__ float red[16];
+  __shared__ float red[20];                              // two reductions' per-warp slots
   __shared__ __align__(8) uint64_t ln_bar;
   const int r = blockIdx.x, t = threadIdx.x, d = st.d;
   if (t == 0) trace_mark(st, 0);
@@ -619,9 +632,9 @@ __global__ void __launch_bounds__(320) ln_kernel(const DecodeState st, const LnA
     x = __ldcg(reinterpret_cast<const float4*>(xr) + t);
   }
   if (t == 0) trace_mark(st, 4);
-  const float mean = block_sum_fixed((x.x + x.y) + (x.z + x.w), red) / d;
+  const float mean = block_sum_once((x.x + x.y) + (x.z + x.w), red) / d;
   const float c0 = x.x - mean, c1 = x.y - mean, c2 = x.z - mean, c3 = x.w - mean;
-  const float var = block_sum_fixed((c0 * c0 + c1 * c1) + (c2 * c2 + c3 * c3), red) / d;
+  const float var = block_sum_once((c0 * c0 + c1 * c1) + (c2 * c2 + c3 * c3), red + 10) / d;
   if (t == 0) trace_mark(st, 5);
   const float rstd = rsqrtf(var + 1e-5f);
   uint16_t h[4], l[4];
