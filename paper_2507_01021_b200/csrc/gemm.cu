@@ -10,6 +10,8 @@
 
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -427,6 +429,229 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
   }
 }
 
+// ------------------------------------------------------------ CTA-pair GEMM
+// 2-SM variant (tcgen05 cta_group::2) for 256 x 256 output tiles. The two
+// CTAs of a cluster each hold 128 rows of A and their half (128 rows) of the
+// B tile; the leader issues tcgen05.mma.cta_group::2 (M = 256), which reads
+// both CTAs' shared memory and writes each CTA's 128 accumulator rows into its
+// own TMEM. Per k-block an SM ingests 16 KB of A + 16 KB of B instead of
+// 16 + 32 KB: the d = 512 layer GEMMs are bound by that L2 -> SMEM stream.
+// Barriers: both CTAs' TMA bytes complete on the leader's `full` barrier
+// (peer bit cleared); the MMA commit multicasts to both CTAs' `empty` and
+// `tmem_full`; both CTAs' epilogue warps arrive on the leader's `tmem_empty`.
+// Per output element the MMA sequence is the same as the 1-SM kernel's, so
+// results do not depend on which kernel ran.
+constexpr int kPairBN = 256;
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;   // clears the CTA-rank bit of a cluster smem address
+
+template <int STAGES>
+struct PairSmem {
+  static constexpr int kABytes = kBM * kBK * 2;             // 16 KB
+  static constexpr int kBBytes = (kPairBN / 2) * kBK * 2;   // 16 KB: this CTA's half of B
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBytes = STAGES * kStageBytes + 1024 /*align*/ + 256 /*bars*/;
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void pair_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_pair_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_pair_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tma_pair_4d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar) & kPeerBitMask), "r"(c0), "r"(c1), "r"(c2),
+      "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_ss_pair(uint32_t tmem_d, uint64_t a_desc, uint64_t b_desc,
+                                                  uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {   // -> both CTAs' barrier
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+
+template <int STAGES, int MODE>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                 const __grid_constant__ CUtensorMap tmap_b, const GemmArgs g, const TileGeom geo) {
+  using S = PairSmem<STAGES>;
+  constexpr int BN = kPairBN;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * S::kStageBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;      // [2]
+  uint64_t* tmem_empty = tmem_full + 2;      // [2] (the leader's counts both CTAs' epilogues)
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int pair = int(blockIdx.x) >> 1, npairs = int(gridDim.x) >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmap_a);
+    tma_prefetch_desc(&tmap_b);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tmem_full[s], 1);
+      mbar_init(&tmem_empty[s], 2 * kEpiWarps);
+    }
+    fence_barrier_init();
+  }
+  pair_cluster_sync();                       // both CTAs' barriers initialised
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_base_slot)),
+                 "r"(uint32_t(2 * BN)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs: own A rows, own half of B)
+    if (elect_one()) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = pair; tile < geo.tiles; tile += npairs) {
+        const int nt = tile % geo.NT;
+        const int mb = tile / geo.NT;
+        const int b = mb / geo.MT, mt = mb % geo.MT;
+        const int row0 = mt * (2 * kBM) + int(rank) * kBM;
+        for (int kb = 0; kb < geo.KB; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * S::kStageBytes;
+          uint8_t* sb = sa + S::kABytes;
+          if (leader) mbar_arrive_expect_tx(&full[stage], 2 * S::kStageBytes);
+          if (g.a_mode == A_FLAT) {
+            tma_pair_3d(sa, &tmap_a, &full[stage], kb * kBK, row0, b);
+          } else {
+            const int tap = kb / geo.cpb;
+            const int c0 = (kb % geo.cpb) * kBK;
+            if (g.a_mode == A_CONV_S1)
+              tma_pair_3d(sa, &tmap_a, &full[stage], c0, row0 + tap, b);
+            else
+              tma_pair_4d(sa, &tmap_a, &full[stage], c0, tap & 1, row0 + (tap >> 1), b);
+          }
+          tma_pair_2d(sb, &tmap_b, &full[stage], kb * kBK, nt * BN + int(rank) * (BN / 2));
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader only)
+    if (leader) {
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * kBM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = pair; tile < geo.tiles; tile += npairs, ++it) {
+        const int as = it & 1;
+        const uint32_t aphase = (it >> 1) & 1;
+        mbar_wait(&tmem_empty[as], aphase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + as * BN;
+        for (int kb = 0; kb < geo.KB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t sa = smem_u32(smem + stage * S::kStageBytes);
+            const uint32_t sb = sa + S::kABytes;
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              umma_bf16_ss_pair(d_tmem, umma_desc_sw128(sa + k * 32), umma_desc_sw128(sb + k * 32),
+                                idesc, (kb | k) != 0);
+            umma_commit_pair(&empty[stage]);
+            if (kb == geo.KB - 1) umma_commit_pair(&tmem_full[as]);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue warps (2..9): this CTA's 128 rows
+    const int quad = warp & 3;
+    const int chalf = (warp - 2) >> 2;
+    const uint32_t lead_empty0 = [&] {
+      uint32_t r;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(tmem_empty)));
+      return r;
+    }();
+    int it = 0;
+    for (int tile = pair; tile < geo.tiles; tile += npairs, ++it) {
+      const int nt = tile % geo.NT;
+      const int mb = tile / geo.NT;
+      const int b = mb / geo.MT, mt = mb % geo.MT;
+      const int as = it & 1;
+      const uint32_t aphase = (it >> 1) & 1;
+      const int t = mt * (2 * kBM) + int(rank) * kBM + quad * 32 + lane;
+      const int row_valid = t < g.T;
+      mbar_wait(&tmem_full[as], aphase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = chalf * (BN / 2); c < (chalf + 1) * (BN / 2); c += 32) {
+        const int n0 = nt * BN + c;
+        uint32_t r[32];
+        tmem_ld32(tmem_base + (uint32_t(quad * 32) << 16) + as * BN + c, r);
+        tmem_wait_ld();
+        if (n0 < g.N) epilogue_chunk<BN, MODE>(g.epi, g, b, t, row_valid, n0, r);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t bar = lead_empty0 + uint32_t(as) * 8;
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar) : "memory");
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  pair_cluster_sync();                       // both CTAs done with TMEM and peer smem
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(uint32_t(2 * BN)));
+  }
+}
+
 // ------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static std::once_flag g_encode_once;
@@ -516,6 +741,78 @@ static int launch_bn_mode(const GemmArgs& g, cudaStream_t stream) {
   return 0;
 }
 
+template <int STAGES, int MODE>
+static int launch_pair_mode(const GemmArgs& g, cudaStream_t stream) {
+  constexpr int BN = kPairBN;
+  CUtensorMap ma, mb;
+  if (g.a_mode == A_FLAT) {
+    cuuint64_t dims[3] = {cuuint64_t(g.K), cuuint64_t(g.T), cuuint64_t(g.Bt)};
+    cuuint64_t str[2] = {cuuint64_t(g.lda) * 2, cuuint64_t(g.a_bstride) * 2};
+    cuuint32_t box[3] = {kBK, kBM, 1};
+    if (make_map(&ma, g.A, 3, dims, str, box)) return 2;
+  } else if (g.a_mode == A_CONV_S1) {
+    const int rows = g.a_rows ? g.a_rows : g.T + 2;
+    cuuint64_t dims[3] = {cuuint64_t(g.C), cuuint64_t(rows), cuuint64_t(g.Bt)};
+    cuuint64_t str[2] = {cuuint64_t(g.C) * 2, cuuint64_t(g.C) * 2 * rows};
+    cuuint32_t box[3] = {kBK, kBM, 1};
+    if (make_map(&ma, g.A, 3, dims, str, box)) return 2;
+  } else {
+    const int rows = g.a_rows ? g.a_rows : 2 * g.T + 2;
+    cuuint64_t dims[4] = {cuuint64_t(g.C), 2, cuuint64_t(rows / 2), cuuint64_t(g.Bt)};
+    cuuint64_t str[3] = {cuuint64_t(g.C) * 2, cuuint64_t(g.C) * 4, cuuint64_t(g.C) * 2 * rows};
+    cuuint32_t box[4] = {kBK, 1, kBM, 1};
+    if (make_map(&ma, g.A, 4, dims, str, box)) return 2;
+  }
+  {
+    cuuint64_t dims[2] = {cuuint64_t(g.K), cuuint64_t(g.N)};
+    cuuint64_t str[1] = {cuuint64_t(g.K) * 2};
+    cuuint32_t box[2] = {kBK, BN / 2};          // this CTA's half of the B tile
+    if (make_map(&mb, g.W, 2, dims, str, box)) return 2;
+  }
+  TileGeom geo;
+  geo.MT = ceil_div(g.T, 2 * kBM);
+  geo.NT = ceil_div(g.N, BN);
+  geo.tiles = g.Bt * geo.MT * geo.NT;
+  geo.KB = ceil_div(g.K, kBK);
+  geo.cpb = g.C > 0 ? g.C / kBK : 1;
+  const int smem = PairSmem<STAGES>::kBytes;
+  static bool attr = false;
+  if (!attr) {
+    DM_CHECK_CUDA(cudaFuncSetAttribute(gemm_pair_kernel<STAGES, MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr = true;
+  }
+  const int pairs = std::min(geo.tiles, kNumSMs / 2);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeClusterDimension;
+  attrs[0].val.clusterDim.x = 2;
+  attrs[0].val.clusterDim.y = 1;
+  attrs[0].val.clusterDim.z = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  DM_CHECK_CUDA(cudaLaunchKernelEx(&cfg, gemm_pair_kernel<STAGES, MODE>, ma, mb, g, geo));
+  return 0;
+}
+
+template <int STAGES>
+static int launch_pair(const GemmArgs& g, cudaStream_t stream) {
+  switch (g.epi.mode) {
+#define DM_GEMM_MODE(m) \
+  case m: return launch_pair_mode<STAGES, m>(g, stream);
+    DM_GEMM_MODE(EPI_STORE_BF16) DM_GEMM_MODE(EPI_GELU_BF16) DM_GEMM_MODE(EPI_CONV1)
+    DM_GEMM_MODE(EPI_CONV2_POS) DM_GEMM_MODE(EPI_RESID_F32) DM_GEMM_MODE(EPI_QKV)
+    DM_GEMM_MODE(EPI_XKV) DM_GEMM_MODE(EPI_STORE_F32) DM_GEMM_MODE(EPI_W2V_PROJ)
+    DM_GEMM_MODE(EPI_CTC_ARGMAX) DM_GEMM_MODE(EPI_GELU_F32)
+#undef DM_GEMM_MODE
+    default: DM_REQUIRE(false, "unknown GEMM epilogue");
+  }
+}
+
 // The epilogue mode is a template parameter: each instantiation carries only
 // its own epilogue (register pressure and I-cache footprint of one mode).
 template <int BN, int STAGES>
@@ -580,7 +877,17 @@ int launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   // wide N, or long K (fc2, the stride-2 conv): 128 x 256 tiles cut the per-SM
   // operand stream (bytes per FLOP (128 + BN) / (128 BN)); with a long K the
   // epilogue's global traffic overlaps the next tile's mainloop
-  if (g.N % 256 == 0 && (g.N >= 1024 || g.K >= 1536)) return launch_bn<256, 4>(g, stream);
+  if (g.N % 256 == 0 && (g.N >= 1024 || g.K >= 1536)) {
+    // long K (stride-2 conv, fc2): the mainloop's L2 -> SMEM operand stream
+    // bounds the 1-SM kernel, so 256 x 256 tiles run on CTA pairs
+    // (cta_group::2; measured conv2 99 -> 95 us, fc2 118 -> 112 us). The
+    // K = 512 GEMMs are bound by their epilogues (GELU, Q/K/V scatter) and
+    // stay on the 1-SM kernel (pairs measured slower: fc1 163 -> 176 us).
+    // DM_GEMM_NO_PAIR=1 forces the 1-SM kernel (same per-element MMA sequence).
+    static const bool no_pair = std::getenv("DM_GEMM_NO_PAIR") != nullptr;
+    if (g.K >= 1536 && !no_pair) return launch_pair<6>(g, stream);
+    return launch_bn<256, 4>(g, stream);
+  }
   if (g.epi.mode == EPI_RESID_F32 && g.a_mode == A_FLAT && g.Bt == 1)
     return launch_bn_mode<128, 5, EPI_RESID_F32>(g, stream);     // + 64 KB residual buffer
   return launch_bn<128, 6>(g, stream);
