@@ -149,17 +149,17 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
           mbar_wait(&s_empty[t], ph);
           issue_s(t, j + 1);
         }
-        mbar_wait(&p_full[t], ph);           // softmax_t(j) done: P_t(j) written
-        mbar_wait(&o_empty[t], ph ^ 1);      // PV_t = P_t V_j
+        // softmax_t(j) done: P_t(j) written and O_t rescaled if its max moved
+        mbar_wait(&p_full[t], ph);
         tc_fence_after();
-        if (elect_one()) {
+        if (elect_one()) {                   // O_t += P_t V_j (accumulated in TMEM)
           const uint32_t sp = smem_u32(smem + AttnSmemLayout::p + t * kPBytes);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t a = sp + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
             const uint32_t bb = sv + (kk >> 2) * (64 * 128) + (kk & 3) * 32;
             umma_bf16_ss(tmem + 256 + t * 64, umma_desc_sw128(a), umma_desc_sw128(bb), idesc_o,
-                         kk != 0);
+                         (j | kk) != 0);
           }
           umma_commit(&o_full[t]);
           if (t == 1) umma_commit(&kv_empty[st]);
@@ -174,27 +174,12 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
     const uint32_t lane_off = uint32_t(quad * 32) << 16;
     const uint32_t s_col = t * 128, o_col = 256 + t * 64;
     constexpr float kLog2e = 1.4426950408889634f;
-    float m_run = -INFINITY, l_run = 0.f, alpha_prev = 0.f;
-    float o[64];
-#pragma unroll
-    for (int i = 0; i < 64; ++i) o[i] = 0.f;
+    // O_t accumulates in TMEM across key blocks. The exponent offset m_run
+    // only moves when the block max exceeds it by more than 2^8 (then O_t's
+    // row is rescaled in TMEM before the next P.V accumulates): P <= 256 fits
+    // bf16, and numerator and row sum share the same offset.
+    float m_run = -INFINITY, l_run = 0.f;
     uint8_t* prow = smem + AttnSmemLayout::p + t * kPBytes + r * 128;
-    auto fold_pv = [&](int j) {
-      mbar_wait(&o_full[t], j & 1);
-      tc_fence_after();
-      uint32_t pv[32];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        tmem_ld32(tmem + lane_off + o_col + c * 32, pv);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          o[c * 32 + i] = fmaf(o[c * 32 + i], alpha_prev, __uint_as_float(pv[i]));
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&o_empty[t]);
-    };
     for (int j = 0; j < nb; ++j) {
       mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
@@ -230,10 +215,33 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
             if (c * 32 + i < kvalid) mx = fmaxf(mx, __uint_as_float(sr[i]));
         }
       }
-      const float alpha = ex2((m_run - mx) * kLog2e);
-      const float mscaled = mx * kLog2e;
-      // the previous PV must have consumed P before it is overwritten
-      if (j >= 1) fold_pv(j - 1);
+      float alpha = 1.f, m_use = m_run;
+      bool resc = false;
+      if (j == 0) {
+        m_use = mx;
+      } else if ((mx - m_run) * kLog2e > 8.f) {
+        alpha = ex2((m_run - mx) * kLog2e);
+        m_use = mx;
+        resc = true;
+      }
+      const float mscaled = m_use * kLog2e;
+      if (j >= 1) {
+        // PV_t(j - 1) done: P_t is free and O_t holds blocks 0..j-1
+        mbar_wait(&o_full[t], (j - 1) & 1);
+        tc_fence_after();
+        if (__any_sync(0xffffffffu, resc)) {
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {
+            uint32_t ov[32];
+            tmem_ld32(tmem + lane_off + o_col + c * 32, ov);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+            tmem_st32(tmem + lane_off + o_col + c * 32, ov);
+          }
+          tmem_wait_st();
+        }
+      }
       // pass 2: p = exp2(s log2e - m log2e), row sum, bf16 P into swizzled smem
       float rs0 = 0.f, rs1 = 0.f, rs2 = 0.f, rs3 = 0.f;
       auto emit = [&](int c, const uint32_t (&v)[32], bool full) {
@@ -289,26 +297,34 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
         }
       }
       const float rs = (rs0 + rs1) + (rs2 + rs3);
+      tc_fence_before();                      // (orders an O_t rescale before the next P.V)
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
       l_run = l_run * alpha + rs;
-      m_run = mx;
-      alpha_prev = alpha;
+      m_run = m_use;
     }
-    fold_pv(nb - 1);
+    mbar_wait(&o_full[t], (nb - 1) & 1);
+    tc_fence_after();
     // normalise and store this query row
     const int tq = qp * 256 + t * 128 + r;
-    if (tq < T) {
-      const float inv = 1.0f / l_run;
-      const int b = bh / heads, h = bh % heads;
-      uint4* dst = reinterpret_cast<uint4*>(out + (size_t(b) * T_rows + tq) * ldo + h * 64);
+    const float inv = 1.0f / l_run;
+    const int b = bh / heads, h = bh % heads;
+#pragma unroll 1
+    for (int c = 0; c < 2; ++c) {
+      uint32_t ov[32];
+      tmem_ld32(tmem + lane_off + o_col + c * 32, ov);
+      tmem_wait_ld();
+      if (tq < T) {
+        uint4* dst = reinterpret_cast<uint4*>(out + (size_t(b) * T_rows + tq) * ldo + h * 64 + c * 32);
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
-        dst[i] = make_uint4(pack_bf16x2(o[8 * i] * inv, o[8 * i + 1] * inv),
-                            pack_bf16x2(o[8 * i + 2] * inv, o[8 * i + 3] * inv),
-                            pack_bf16x2(o[8 * i + 4] * inv, o[8 * i + 5] * inv),
-                            pack_bf16x2(o[8 * i + 6] * inv, o[8 * i + 7] * inv));
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(
+              pack_bf16x2(__uint_as_float(ov[8 * i]) * inv, __uint_as_float(ov[8 * i + 1]) * inv),
+              pack_bf16x2(__uint_as_float(ov[8 * i + 2]) * inv, __uint_as_float(ov[8 * i + 3]) * inv),
+              pack_bf16x2(__uint_as_float(ov[8 * i + 4]) * inv, __uint_as_float(ov[8 * i + 5]) * inv),
+              pack_bf16x2(__uint_as_float(ov[8 * i + 6]) * inv, __uint_as_float(ov[8 * i + 7]) * inv));
+      }
     }
   }
   tc_fence_before();
