@@ -329,24 +329,19 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
       {
         // row r: W.x_hi (column r) + W.x_lo (column Np + r)
         const uint32_t base = tmem + (uint32_t(quad * 32) << 16) + buf * 128;
-        uint32_t rr[32];
-        tmem_ld32(base, rr);
+        // hi and lo columns in flight together, one wait
+        uint32_t ra[32], rb[32];
+        tmem_ld32(base, ra);
+        tmem_ld32(base + Np, rb);
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v0[i] = __uint_as_float(rr[i]);
-        tmem_ld32(base + Np, rr);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) v0[i] += __uint_as_float(rr[i]);
+        for (int i = 0; i < 32; ++i) v0[i] = __uint_as_float(ra[i]) + __uint_as_float(rb[i]);
         if (Np > 32) {
-          tmem_ld32(base + 32, rr);
+          tmem_ld32(base + 32, ra);
+          tmem_ld32(base + Np + 32, rb);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v1[i] = __uint_as_float(rr[i]);
-          tmem_ld32(base + Np + 32, rr);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v1[i] += __uint_as_float(rr[i]);
+          for (int i = 0; i < 32; ++i) v1[i] = __uint_as_float(ra[i]) + __uint_as_float(rb[i]);
         } else {
 #pragma unroll
           for (int i = 0; i < 32; ++i) v1[i] = 0.f;
