@@ -76,3 +76,40 @@ def test_tcgen05_gemm_matches_fp32(native_lib, M, N, K):
     torch.cuda.synchronize()
     err = (out.cpu() - ref).abs().max().item()
     assert err <= 1e-3 * (K ** 0.5), err
+
+
+_PAIR_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from paper_2507_01021_b200 import _native
+_native.load()
+g = torch.Generator().manual_seed(5)
+M, N, K = 1000, 512, 2048
+A = torch.randn(M, K, generator=g).bfloat16().cuda()
+W = torch.randn(N, K, generator=g).bfloat16().cuda()
+b = torch.randn(N, generator=g).bfloat16().cuda()
+out = torch.empty(M, N, device="cuda")
+_native.call("dm_gemm_bf16_f32", A.data_ptr(), W.data_ptr(), b.data_ptr(), out.data_ptr(), M, N, K, None)
+torch.cuda.synchronize()
+np.save(sys.argv[2], out.cpu().numpy())
+"""
+
+
+def test_cta_pair_gemm_bitwise_equals_single_sm(native_lib, tmp_path):
+    """Long-K GEMMs run on CTA pairs (tcgen05 cta_group::2, M = 256); the
+    single-SM kernel (DM_GEMM_NO_PAIR=1) issues the same per-element MMA
+    sequence, so the two must agree bit for bit (batch invariance does not
+    depend on which kernel a shape selects)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = str(Path(__file__).resolve().parent.parent)
+    outs = []
+    for env_extra, name in (({}, "pair.npy"), ({"DM_GEMM_NO_PAIR": "1"}, "single.npy")):
+        env = dict(os.environ, **env_extra)
+        path = tmp_path / name
+        subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root, str(path)], env=env, check=True,
+                       timeout=300)
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
