@@ -450,13 +450,13 @@ def measure_roofline(eng, dims, args) -> dict:
     bytes_per_launch = rows * 2 * 1500 * dims.d_model * 2
     achieved = bytes_per_launch / (ms / 1000.0) / 1e9
     traffic = None
-    tf = ROOT / "profiles" / "r01_xattn_traffic_v8.json"
+    tf = ROOT / "profiles" / "r01_xattn_traffic_v10.json"
     if tf.exists():     # dram read+write of one ncu --set full capture (64 rows), scaled to rows
         t = _j.loads(tf.read_text())
         traffic = (t["dram_bytes_read"] + t["dram_bytes_write"]) * rows / t["rows"]
     return {"kernel": "cross_attn_kernel (decode K6, + cross-o tail)", "bound": "hbm", "achieved": achieved,
             "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-            "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/r01_xattn_traffic_v8.json)",
+            "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/r01_xattn_traffic_v10.json)",
             "timing": "CUDA events on the engine stream around a graph of 20 back-to-back launches "
                       "per decoder layer at a full 64-row batch, after the timed region",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback",
