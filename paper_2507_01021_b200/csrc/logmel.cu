@@ -117,6 +117,8 @@ struct LogmelSmem {
   float2 tw25[25];
   float2 tw400[kBins];
   float window[kFFT];
+  int mstart[128], mcount[128], mwoff[128];
+  float mw[1024];
 };
 
 __global__ void __launch_bounds__(kLogmelThreads)
@@ -152,12 +154,41 @@ logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offse
   for (int i = tid; i < kFFT; i += kLogmelThreads) s.window[i] = tab->window[i];
   // Samples of the padded + reflected window [f0*160-200, f0*160-200+kSpan).
   const int base = f0 * kHop - kFFT / 2;
-  for (int i = tid; i < kSpan; i += kLogmelThreads) {
-    int j = base + i;
-    if (j < 0) j = -j;                                   // reflect at start
-    if (j >= kWindow) j = 2 * (kWindow - 1) - j;         // reflect at end
-    s.samples[i] = (j < n) ? float(x[j]) * (1.0f / 32768.0f) : 0.0f;
+  if (base >= 0 && base + kSpan <= n) {
+    // interior span: 16-byte loads (8 samples each) from the first aligned
+    // address, the unaligned head and tail sample by sample
+    const int16_t* src = x + base;
+    const int head = int(((16 - (reinterpret_cast<uintptr_t>(src) & 15)) & 15) >> 1);
+    const int nv = (kSpan - head) >> 3;
+    const uint4* v = reinterpret_cast<const uint4*>(src + head);
+    for (int i = tid; i < nv; i += kLogmelThreads) {
+      const uint4 w = __ldg(v + i);
+      float* d = s.samples + head + 8 * i;
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        d[2 * u] = float(int16_t(ws[u] & 0xFFFFu)) * (1.0f / 32768.0f);
+        d[2 * u + 1] = float(int16_t(ws[u] >> 16)) * (1.0f / 32768.0f);
+      }
+    }
+    const int tail0 = head + 8 * nv;
+    if (tid < head) s.samples[tid] = float(src[tid]) * (1.0f / 32768.0f);
+    if (tid < kSpan - tail0) s.samples[tail0 + tid] = float(src[tail0 + tid]) * (1.0f / 32768.0f);
+  } else {
+    for (int i = tid; i < kSpan; i += kLogmelThreads) {
+      int j = base + i;
+      if (j < 0) j = -j;                                   // reflect at start
+      if (j >= kWindow) j = 2 * (kWindow - 1) - j;         // reflect at end
+      s.samples[i] = (j < n) ? float(x[j]) * (1.0f / 32768.0f) : 0.0f;
+    }
   }
+  // sparse mel bank into shared memory (read by every (mel, frame) task)
+  for (int i = tid; i < n_mels; i += kLogmelThreads) {
+    s.mstart[i] = tab->mel_start[i];
+    s.mcount[i] = tab->mel_count[i];
+    s.mwoff[i] = tab->mel_woff[i];
+  }
+  for (int i = tid; i < 1024; i += kLogmelThreads) s.mw[i] = tab->mel_w[i];
   __syncthreads();
 
   // Stage A: per (frame, q): 8-point DFT over p of z[25p+q], twiddle W200^{q k1}.
@@ -226,10 +257,10 @@ logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offse
   for (int t = tid; t < n_mels * kFPB; t += kLogmelThreads) {
     int m = t / kFPB, fr = t % kFPB;
     if (fr >= nfr) continue;
-    int k0 = tab->mel_start[m], cnt = tab->mel_count[m], wo = tab->mel_woff[m];
+    const int k0 = s.mstart[m], cnt = s.mcount[m], wo = s.mwoff[m];
     const float* pw = power + fr * kBins + k0;
     float acc = 0.f;
-    for (int i = 0; i < cnt; ++i) acc = fmaf(tab->mel_w[wo + i], pw[i], acc);
+    for (int i = 0; i < cnt; ++i) acc = fmaf(s.mw[wo + i], pw[i], acc);
     float v = log10f(fmaxf(acc, 1e-10f));
     outb[size_t(m) * kFrames + f0 + fr] = v;
     lmax = fmaxf(lmax, v);
