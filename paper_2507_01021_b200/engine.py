@@ -147,6 +147,13 @@ class WhisperGPU:
             self._up_done = [torch.cuda.Event() for _ in range(2)]
             self._up_used = [False, False]
             self._up_next = 0
+            # H2D uploads run on their own stream so the next group's copy
+            # overlaps the current group's encode; buffer b is rewritten only
+            # after the encode that read it (_enc_done[b])
+            self.copy_stream = torch.cuda.Stream(self.device)
+            self._enc_done = [torch.cuda.Event() for _ in range(2)]
+            self._enc_used = [False, False]
+            self._last_buf = 0
             self._done = np.zeros(max_slots, np.int32)
             self._ngen = np.zeros(max_slots, np.int32)
             self._tokens = np.zeros(max_slots * MAX_TOKENS, np.int32)
@@ -199,14 +206,18 @@ class WhisperGPU:
         (pcm, offsets, lengths) device pointers."""
         n = len(segs)
         b = self._stage()
+        self._last_buf = b
         mh, md = self._meta_host[b], self._meta_dev[b]
         if n and all(isinstance(s, ResidentPCM) for s in segs):
             meta = mh.numpy()
             meta[:n] = [s.offset for s in segs]
             meta[n:].view(np.int32)[:n] = [min(s.length, N_SAMPLES) for s in segs]
-            with torch.cuda.stream(self.stream):
+            with torch.cuda.stream(self.copy_stream):
+                if self._enc_used[b]:
+                    self.copy_stream.wait_event(self._enc_done[b])
                 md.copy_(mh, non_blocking=True)
-                self._up_done[b].record(self.stream)
+                self._up_done[b].record(self.copy_stream)
+            self.stream.wait_event(self._up_done[b])
             self._up_used[b] = True
             return (C.c_void_p(self._resident.data_ptr()), C.c_void_p(md.data_ptr()),
                     C.c_void_p(md.data_ptr() + 8 * n))
@@ -226,11 +237,14 @@ class WhisperGPU:
         meta[:n] = offs
         meta32 = meta[n:].view(np.int32)     # lengths packed after offsets
         meta32[:n] = lens
-        with torch.cuda.stream(self.stream):
+        with torch.cuda.stream(self.copy_stream):
+            if self._enc_used[b]:
+                self.copy_stream.wait_event(self._enc_done[b])
             if pos:
                 pd[:pos].copy_(ph[:pos], non_blocking=True)
             md.copy_(mh, non_blocking=True)
-            self._up_done[b].record(self.stream)
+            self._up_done[b].record(self.copy_stream)
+        self.stream.wait_event(self._up_done[b])
         self._up_used[b] = True
         self.h2d_bytes += 2 * pos + 12 * n
         return C.c_void_p(pd.data_ptr()), C.c_void_p(md.data_ptr()), C.c_void_p(md.data_ptr() + 8 * n)
@@ -239,6 +253,9 @@ class WhisperGPU:
         pcm, offp, lenp = self.upload_segments(segs)
         _native.check(self.lib.dm_whisper_encode(self.handle, pcm, offp, lenp, len(segs),
                                                  self._i32(slots), self._s))
+        b = self._last_buf
+        self._enc_done[b].record(self.stream)     # buffer b free for the upload after next
+        self._enc_used[b] = True
         self.stats.encode_calls += 1
         self.stats.segments_encoded += len(segs)
 
