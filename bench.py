@@ -477,9 +477,10 @@ def main():
     ap.add_argument("--ref-segments-per-step", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--decode-groups", type=int, default=None)
-    ap.add_argument("--first-encode-batch", type=int, default=8,
-                    help="segments in the first encode group of an idle engine (the GPU starts "
-                         "while the host stages the rest)")
+    ap.add_argument("--first-encode-batch", type=int, default=32,
+                    help="segments in the first encode group of an idle engine (smaller: the GPU "
+                         "starts while the host stages the rest; with uploads on a side copy "
+                         "stream 8..32 measure the same e2e, 32 the best resident value)")
     ap.add_argument("--profile", action="store_true",
                     help="run exactly one resident-input step and exit (ncu)")
     args = ap.parse_args()
