@@ -30,6 +30,7 @@ constexpr int kWindow = 480000;
 constexpr int kFrames = 3000;
 constexpr int kBins = 201;
 constexpr int kFPB = 32;                               // frames per CTA
+static_assert(kFrames % 4 == 0 && kFPB % 4 == 0, "float4 frame groups");
 constexpr int kSpan = (kFPB - 1) * kHop + kFFT;        // 5360 samples
 constexpr int kLogmelThreads = 256;
 
@@ -288,20 +289,35 @@ logmel_normalize_kernel(float* __restrict__ out, const uint32_t* __restrict__ se
   const int nfr = min(kFPB, kFrames - f0);
   const float floor_v = ordered_to_float(segmax[b]) - 8.0f;
   float* outb = out + size_t(b) * n_mels * kFrames;
-  for (int t = threadIdx.x; t < n_mels * kFPB; t += blockDim.x) {
-    int m = t / kFPB, fr = t % kFPB;
+  // 4 frames per float4 (rows of 3000 floats are 16-byte aligned, nfr % 4 == 0)
+  for (int t = threadIdx.x; t < n_mels * (kFPB / 4); t += blockDim.x) {
+    const int m = t / (kFPB / 4), fr = 4 * (t % (kFPB / 4));
     if (fr >= nfr) continue;
-    float v = outb[size_t(m) * kFrames + f0 + fr];
-    v = (fmaxf(v, floor_v) + 4.0f) / 4.0f;
-    outb[size_t(m) * kFrames + f0 + fr] = v;
-    tile[m][fr] = v;
+    float4* p = reinterpret_cast<float4*>(outb + size_t(m) * kFrames + f0 + fr);
+    float4 v = *p;
+    v.x = (fmaxf(v.x, floor_v) + 4.0f) / 4.0f;
+    v.y = (fmaxf(v.y, floor_v) + 4.0f) / 4.0f;
+    v.z = (fmaxf(v.z, floor_v) + 4.0f) / 4.0f;
+    v.w = (fmaxf(v.w, floor_v) + 4.0f) / 4.0f;
+    *p = v;
+    tile[m][fr] = v.x;
+    tile[m][fr + 1] = v.y;
+    tile[m][fr + 2] = v.z;
+    tile[m][fr + 3] = v.w;
   }
   if (mel_t == nullptr) return;
   __syncthreads();
+  // time-major bf16 rows: 8 mels per 16-byte store
   uint16_t* dst = mel_t + (size_t(b) * (kFrames + 2) + f0 + 1) * ldt;
-  for (int t = threadIdx.x; t < n_mels * nfr; t += blockDim.x) {
-    int fr = t / n_mels, m = t % n_mels;
-    dst[size_t(fr) * ldt + m] = f32_to_bf16(tile[m][fr]);
+  const int mc = n_mels / 8;
+  for (int t = threadIdx.x; t < mc * nfr; t += blockDim.x) {
+    const int fr = t / mc, m0 = 8 * (t % mc);
+    uint4 w;
+    w.x = pack_bf16x2(tile[m0][fr], tile[m0 + 1][fr]);
+    w.y = pack_bf16x2(tile[m0 + 2][fr], tile[m0 + 3][fr]);
+    w.z = pack_bf16x2(tile[m0 + 4][fr], tile[m0 + 5][fr]);
+    w.w = pack_bf16x2(tile[m0 + 6][fr], tile[m0 + 7][fr]);
+    *reinterpret_cast<uint4*>(dst + size_t(fr) * ldt + m0) = w;
   }
 }
 
