@@ -184,65 +184,37 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
       mbar_wait(&s_full[t], j & 1);
       tc_fence_after();
       const int kvalid = T - j * 128;                     // < 128 only on the tail block
-      uint32_t sr[32];
-      // pass 1: row max (3-input max, independent accumulators, two TMEM
-      // loads in flight per wait)
-      float mx = m_run;
-      if (kvalid >= 128) {
-        uint32_t sb[32];
-        float m0 = m_run, m1 = m_run, m2 = m_run, m3 = m_run;
+      float alpha = 1.f, m_use = m_run, mscaled = 0.f;
+      // exponent offset for this block (and O_t rescale when it moves)
+      auto offset = [&](float mx) {
+        bool resc = false;
+        if (j == 0) {
+          m_use = mx;
+        } else if ((mx - m_run) * kLog2e > 8.f) {
+          alpha = ex2((m_run - mx) * kLog2e);
+          m_use = mx;
+          resc = true;
+        }
+        mscaled = m_use * kLog2e;
+        if (j >= 1) {
+          // PV_t(j - 1) done: P_t is free and O_t holds blocks 0..j-1
+          mbar_wait(&o_full[t], (j - 1) & 1);
+          tc_fence_after();
+          if (__any_sync(0xffffffffu, resc)) {
 #pragma unroll 1
-        for (int c = 0; c < 4; c += 2) {
-          tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
-          tmem_ld32(tmem + lane_off + s_col + c * 32 + 32, sb);
-          tmem_wait_ld();
+            for (int c = 0; c < 2; ++c) {
+              uint32_t ov[32];
+              tmem_ld32(tmem + lane_off + o_col + c * 32, ov);
+              tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; i += 4) {
-            m0 = fmax3(m0, __uint_as_float(sr[i]), __uint_as_float(sr[i + 1]));
-            m1 = fmax3(m1, __uint_as_float(sr[i + 2]), __uint_as_float(sr[i + 3]));
-            m2 = fmax3(m2, __uint_as_float(sb[i]), __uint_as_float(sb[i + 1]));
-            m3 = fmax3(m3, __uint_as_float(sb[i + 2]), __uint_as_float(sb[i + 3]));
+              for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
+              tmem_st32(tmem + lane_off + o_col + c * 32, ov);
+            }
+            tmem_wait_st();
           }
         }
-        mx = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-      } else {
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (c * 32 + i < kvalid) mx = fmaxf(mx, __uint_as_float(sr[i]));
-        }
-      }
-      float alpha = 1.f, m_use = m_run;
-      bool resc = false;
-      if (j == 0) {
-        m_use = mx;
-      } else if ((mx - m_run) * kLog2e > 8.f) {
-        alpha = ex2((m_run - mx) * kLog2e);
-        m_use = mx;
-        resc = true;
-      }
-      const float mscaled = m_use * kLog2e;
-      if (j >= 1) {
-        // PV_t(j - 1) done: P_t is free and O_t holds blocks 0..j-1
-        mbar_wait(&o_full[t], (j - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, resc)) {
-#pragma unroll 1
-          for (int c = 0; c < 2; ++c) {
-            uint32_t ov[32];
-            tmem_ld32(tmem + lane_off + o_col + c * 32, ov);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) ov[i] = __float_as_uint(__uint_as_float(ov[i]) * alpha);
-            tmem_st32(tmem + lane_off + o_col + c * 32, ov);
-          }
-          tmem_wait_st();
-        }
-      }
-      // pass 2: p = exp2(s log2e - m log2e), row sum, bf16 P into swizzled smem
+      };
+      // p = exp2(s log2e - m log2e), row sum, bf16 P into swizzled smem
       float rs0 = 0.f, rs1 = 0.f, rs2 = 0.f, rs3 = 0.f;
       auto emit = [&](int c, const uint32_t (&v)[32], bool full) {
         uint32_t pk[16];
@@ -269,25 +241,45 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
           *dst = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
       };
-      // S_t is released right after its last TMEM load (the MMA warp then
-      // issues S_t(j + 1) while this warp still computes P from registers)
-      auto release_s = [&]() {
+      auto release_s = [&]() {                   // the MMA warp may issue S_t(j + 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&s_empty[t]);
       };
       if (kvalid >= 128) {
-        uint32_t sb[32];
-#pragma unroll 1
-        for (int c = 0; c < 4; c += 2) {
-          tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
-          tmem_ld32(tmem + lane_off + s_col + c * 32 + 32, sb);
-          tmem_wait_ld();
-          if (c == 2) release_s();
-          emit(c, sr, true);
-          emit(c + 1, sb, true);
+        // the whole S row in registers with one wait; S_t is released at once
+        uint32_t s0[32], s1[32], s2[32], s3[32];
+        tmem_ld32(tmem + lane_off + s_col, s0);
+        tmem_ld32(tmem + lane_off + s_col + 32, s1);
+        tmem_ld32(tmem + lane_off + s_col + 64, s2);
+        tmem_ld32(tmem + lane_off + s_col + 96, s3);
+        tmem_wait_ld();
+        release_s();
+        float m0 = m_run, m1 = m_run, m2 = m_run, m3 = m_run;
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          m0 = fmax3(m0, __uint_as_float(s0[i]), __uint_as_float(s0[i + 1]));
+          m1 = fmax3(m1, __uint_as_float(s1[i]), __uint_as_float(s1[i + 1]));
+          m2 = fmax3(m2, __uint_as_float(s2[i]), __uint_as_float(s2[i + 1]));
+          m3 = fmax3(m3, __uint_as_float(s3[i]), __uint_as_float(s3[i + 1]));
         }
+        offset(fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)));
+        emit(0, s0, true);
+        emit(1, s1, true);
+        emit(2, s2, true);
+        emit(3, s3, true);
       } else {
+        uint32_t sr[32];
+        float mx = m_run;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (c * 32 + i < kvalid) mx = fmaxf(mx, __uint_as_float(sr[i]));
+        }
+        offset(mx);
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
           tmem_ld32(tmem + lane_off + s_col + c * 32, sr);
