@@ -392,6 +392,19 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
 #pragma unroll
         for (int i = 0; i < (BN == 128 ? 8 : 1); ++i) bias_pre[i] = __ldg(bp + i);
       }
+      // BN = 256: bias of this thread's first 32-column chunk, fetched before
+      // the accumulator wait (later chunks are fetched one chunk ahead)
+      uint4 bias_c[4];
+      const bool wide_bias = BN != 128 && g.epi.bias != nullptr;
+      auto load_bias4 = [&](int c, uint4 (&dst)[4]) {
+        const int n0 = nt * BN + c;
+        if (wide_bias && n0 + 32 <= g.N) {
+          const uint4* bp = reinterpret_cast<const uint4*>(g.epi.bias + n0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dst[i] = __ldg(bp + i);
+        }
+      };
+      if (BN != 128) load_bias4(chalf * (BN / 2), bias_c);
       mbar_wait(&tmem_full[as], aphase);
       tc_fence_after();
       if (BN == 128) {
@@ -410,10 +423,16 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
 #pragma unroll 1
         for (int c = chalf * (BN / 2); c < (chalf + 1) * (BN / 2); c += 32) {
           const int n0 = nt * BN + c;
+          uint4 bias_n[4];
+          if (c + 32 < (chalf + 1) * (BN / 2)) load_bias4(c + 32, bias_n);
           uint32_t r[32];
           tmem_ld32(tmem_base + (uint32_t(quad * 32) << 16) + as * BN + c, r);
           tmem_wait_ld();
-          if (n0 < g.N) epilogue_chunk<BN, MODE>(g.epi, g, b, t, row_valid, n0, r);
+          if (n0 < g.N)
+            epilogue_chunk<BN, MODE>(g.epi, g, b, t, row_valid, n0, r, nullptr,
+                                     (wide_bias && n0 + 32 <= g.N) ? bias_c : nullptr);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) bias_c[i] = bias_n[i];
         }
       }
       tc_fence_before();
@@ -624,15 +643,33 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a,
       const uint32_t aphase = (it >> 1) & 1;
       const int t = mt * (2 * kBM) + int(rank) * kBM + quad * 32 + lane;
       const int row_valid = t < g.T;
+      // bias one 32-column chunk ahead (the first before the accumulator wait)
+      uint4 bias_c[4];
+      const bool has_bias = g.epi.bias != nullptr;
+      auto load_bias4 = [&](int c, uint4 (&dst)[4]) {
+        const int n0 = nt * BN + c;
+        if (has_bias && n0 + 32 <= g.N) {
+          const uint4* bp = reinterpret_cast<const uint4*>(g.epi.bias + n0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dst[i] = __ldg(bp + i);
+        }
+      };
+      load_bias4(chalf * (BN / 2), bias_c);
       mbar_wait(&tmem_full[as], aphase);
       tc_fence_after();
 #pragma unroll 1
       for (int c = chalf * (BN / 2); c < (chalf + 1) * (BN / 2); c += 32) {
         const int n0 = nt * BN + c;
+        uint4 bias_n[4];
+        if (c + 32 < (chalf + 1) * (BN / 2)) load_bias4(c + 32, bias_n);
         uint32_t r[32];
         tmem_ld32(tmem_base + (uint32_t(quad * 32) << 16) + as * BN + c, r);
         tmem_wait_ld();
-        if (n0 < g.N) epilogue_chunk<BN, MODE>(g.epi, g, b, t, row_valid, n0, r);
+        if (n0 < g.N)
+          epilogue_chunk<BN, MODE>(g.epi, g, b, t, row_valid, n0, r, nullptr,
+                                   (has_bias && n0 + 32 <= g.N) ? bias_c : nullptr);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) bias_c[i] = bias_n[i];
       }
       tc_fence_before();
       __syncwarp();
