@@ -115,7 +115,7 @@ static cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 
   cfg.stream = stream;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   attr[1].id = cudaLaunchAttributeClusterDimension;
   attr[1].val.clusterDim.x = cluster.x;
   attr[1].val.clusterDim.y = cluster.y;
@@ -591,9 +591,16 @@ __global__ void __launch_bounds__(320) ln_kernel(const DecodeState st, const LnA
   float4 rb = make_float4(0.f, 0.f, 0.f, 0.f);
   if (MODE == 2 && a.res.bias) rb = bf16x4_to_f32(__ldg(reinterpret_cast<const uint2*>(a.res.bias) + t));
   const int slot = r < R ? st.active[r] : 0;
-  if (MODE == 2 && t == 0) {
-    mbar_init(&ln_bar, 1);
-    fence_barrier_init();
+  if (MODE == 2) {
+    if (t == 0) {
+      mbar_init(&ln_bar, 1);
+      fence_barrier_init();
+    }
+    // every thread polls ln_bar after the wait: it must be initialised first
+    // (without this barrier a warp that runs ahead of warp 0 -- common when
+    // the SM is shared with another stream's CTAs -- waits on stale shared
+    // memory and the CTA faults)
+    __syncthreads();
   }
   pdl_wait();
   if (t == 0) trace_mark(st, 1);

@@ -3,6 +3,7 @@
 // the decode step (captured once as a CUDA graph, replayed per step), and the
 // K7 slot / self-KV page allocator.
 
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -249,10 +250,17 @@ struct WhisperEngine {
   int step_kernels() const { return 10 * Ld + 3; }
   int encode_kernels() const { return 2 + 2 + 7 * L + 1 + 1; }
 
+  // debug (DM_GUARD=1 at create): every allocation gets a 64 KB 0xA5 tail
+  // guard; dm_whisper_debug(13) reports the allocations whose guard changed
+  static constexpr size_t kGuard = 64 * 1024;
+  bool guard = std::getenv("DM_GUARD") != nullptr;
+  std::vector<size_t> alloc_bytes;
   int alloc(void** p, size_t bytes, bool zero = true) {
-    DM_CHECK_CUDA(cudaMalloc(p, bytes));
+    DM_CHECK_CUDA(cudaMalloc(p, bytes + (guard ? kGuard : 0)));
     allocs.push_back(*p);
+    alloc_bytes.push_back(bytes);
     if (zero) DM_CHECK_CUDA(cudaMemset(*p, 0, bytes));
+    if (guard) DM_CHECK_CUDA(cudaMemset(static_cast<uint8_t*>(*p) + bytes, 0xA5, kGuard));
     return 0;
   }
   template <class T>
@@ -966,6 +974,30 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
       DM_REQUIRE(e->groups[0].st.trace != nullptr, "timeline tap not enabled");
       src = e->groups[0].st.trace; avail = 128 * 8 * 8;
       break;
+    case 13: {       // guard check: host_dst int32[bytes/4] = {n_bad, (index, first bad offset, KB)...}
+      DM_REQUIRE(e->guard, "engine created without DM_GUARD=1");
+      DM_CHECK_CUDA(cudaStreamSynchronize(s));
+      std::vector<uint8_t> g(WhisperEngine::kGuard);
+      auto* out = static_cast<int32_t*>(host_dst);
+      const int cap = int(bytes / 4);
+      int nbad = 0;
+      for (size_t i = 0; i < e->allocs.size(); ++i) {
+        DM_CHECK_CUDA(cudaMemcpy(g.data(), static_cast<uint8_t*>(e->allocs[i]) + e->alloc_bytes[i],
+                                 g.size(), cudaMemcpyDeviceToHost));
+        for (size_t k = 0; k < g.size(); ++k)
+          if (g[k] != 0xA5) {
+            if (3 + 3 * nbad < cap) {
+              out[1 + 3 * nbad] = int(i);
+              out[2 + 3 * nbad] = int(k);
+              out[3 + 3 * nbad] = int(e->alloc_bytes[i] / 1024);
+            }
+            ++nbad;
+            break;
+          }
+      }
+      if (cap > 0) out[0] = nbad;
+      return 0;
+    }
     case 5: src = e->resid; avail = size_t(e->last_n) * 1500 * e->d * 4; break;
     case 6: src = e->attn_out; avail = size_t(e->last_n) * 1500 * e->d * 2; break;
     default: DM_REQUIRE(false, "unknown debug tap");

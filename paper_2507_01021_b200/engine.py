@@ -100,7 +100,8 @@ class WhisperGPU:
                  device: int | str | torch.device = 0, max_slots: int = 64,
                  max_encode_batch: int = 32, num_pages: int | None = None,
                  eot: int | None = None, steps_per_poll: int = 8,
-                 decode_groups: int | None = None, first_encode_batch: int = 8):
+                 decode_groups: int | None = None, first_encode_batch: int = 8,
+                 overlap_encode: bool = False, decode_priority: int = 0):
         if not torch.cuda.is_available():
             raise _native.DmError("no CUDA device: the B200 engine has no CPU fallback")
         self.dims = dims
@@ -110,9 +111,13 @@ class WhisperGPU:
         self.max_encode_batch = max_encode_batch
         self.steps_per_poll = steps_per_poll
         self.first_encode_batch = first_encode_batch
+        self.overlap_encode = overlap_encode
         self.eot = dims.eot if eot is None else eot
         with torch.cuda.device(self.device):
-            self.stream = torch.cuda.Stream(self.device)
+            # run_jobs(overlap_encode) encodes on enc_stream so a new group's
+            # encode overlaps the decode of the groups already admitted
+            self.stream = torch.cuda.Stream(self.device, priority=decode_priority)
+            self.enc_stream = torch.cuda.Stream(self.device)
             self.man = whisper_manifest(dims, seed, init_std)
             self.blob = materialize_weights(self.man, self.device, self.stream)
             offs = whisper_offsets(self.man, dims)
@@ -200,10 +205,11 @@ class WhisperGPU:
             self._up_done[b].synchronize()
         return b
 
-    def upload_segments(self, segs: Sequence[np.ndarray]):
+    def upload_segments(self, segs: Sequence[np.ndarray], stream=None):
         """Trim (pad_or_trim's truncation; padding is implicit in the kernel)
         and copy PCM to the device (stream-ordered, double-buffered). Returns
         (pcm, offsets, lengths) device pointers."""
+        stream = self.stream if stream is None else stream
         n = len(segs)
         b = self._stage()
         self._last_buf = b
@@ -217,7 +223,7 @@ class WhisperGPU:
                     self.copy_stream.wait_event(self._enc_done[b])
                 md.copy_(mh, non_blocking=True)
                 self._up_done[b].record(self.copy_stream)
-            self.stream.wait_event(self._up_done[b])
+            stream.wait_event(self._up_done[b])
             self._up_used[b] = True
             return (C.c_void_p(self._resident.data_ptr()), C.c_void_p(md.data_ptr()),
                     C.c_void_p(md.data_ptr() + 8 * n))
@@ -244,17 +250,20 @@ class WhisperGPU:
                 pd[:pos].copy_(ph[:pos], non_blocking=True)
             md.copy_(mh, non_blocking=True)
             self._up_done[b].record(self.copy_stream)
-        self.stream.wait_event(self._up_done[b])
+        stream.wait_event(self._up_done[b])
         self._up_used[b] = True
         self.h2d_bytes += 2 * pos + 12 * n
         return C.c_void_p(pd.data_ptr()), C.c_void_p(md.data_ptr()), C.c_void_p(md.data_ptr() + 8 * n)
 
-    def encode(self, segs: Sequence[np.ndarray], slots: Sequence[int]) -> None:
-        pcm, offp, lenp = self.upload_segments(segs)
+    def encode(self, segs: Sequence[np.ndarray], slots: Sequence[int], stream=None) -> None:
+        """Encode into the slots' cross-KV cache on `stream` (default: the
+        decode stream, so a following admit/step/debug is ordered after it)."""
+        stream = self.stream if stream is None else stream
+        pcm, offp, lenp = self.upload_segments(segs, stream)
         _native.check(self.lib.dm_whisper_encode(self.handle, pcm, offp, lenp, len(segs),
-                                                 self._i32(slots), self._s))
+                                                 self._i32(slots), C.c_void_p(stream.cuda_stream)))
         b = self._last_buf
-        self._enc_done[b].record(self.stream)     # buffer b free for the upload after next
+        self._enc_done[b].record(stream)          # buffer b free for the upload after next
         self._enc_used[b] = True
         self.stats.encode_calls += 1
         self.stats.segments_encoded += len(segs)
@@ -270,6 +279,7 @@ class WhisperGPU:
 
     def reset(self) -> None:
         """Drop every slot (after a failed run): free pages, empty active set."""
+        self.enc_stream.synchronize()
         self.stream.synchronize()
         if self._held:
             self.release(sorted(self._held))
@@ -355,8 +365,21 @@ class WhisperGPU:
         snapshot of (done, n_gen, tokens) is taken after each batch and read
         one batch later (tokens of finished slots never change, and slots
         that hit EOT early only linger one batch -- their attention is
-        skipped). Returns {key: token ids}."""
+        skipped). Returns {key: token ids}.
+
+        With overlap_encode (experimental), encodes run on
+        enc_stream and a group is admitted (decode stream waits on its encode
+        event) once the host sees its event complete -- or at once when
+        nothing is decoding -- so the groups already admitted decode while the
+        next group encodes; the jobs of one call are then taken longest cap
+        first. Outputs are batch-invariant bit for bit either way."""
+        overlap = self.overlap_encode
+        jobs = list(jobs)
+        if overlap:
+            jobs.sort(key=lambda j: -j.cap)
+            self.enc_stream.wait_stream(self.stream)   # encodes after prior work
         pending = deque(jobs)
+        encoding: deque = deque()              # (event, [(slot, job)]) in flight on enc_stream
         free = list(range(self.max_slots - 1, -1, -1))
         active: dict[int, SegmentJob] = {}
         left: dict[int, int] = {}              # slot -> steps to its cap
@@ -382,13 +405,27 @@ class WhisperGPU:
                 take = []
                 # an idle engine starts with a small group: the GPU begins
                 # while the host still stages the rest of the PCM
-                lim = self.max_encode_batch if (active or waiting or prev) else min(
+                lim = self.max_encode_batch if (active or waiting or prev or encoding) else min(
                     self.max_encode_batch, self.first_encode_batch)
                 while free and pending and len(take) < lim:
                     take.append((free.pop(), pending.popleft()))
                 slots = [s for s, _ in take]
+                if overlap:
+                    self.encode([j.samples for _, j in take], slots, self.enc_stream)
+                    ev = torch.cuda.Event()
+                    ev.record(self.enc_stream)
+                    encoding.append((ev, take))
+                    continue
                 self.encode([j.samples for _, j in take], slots)
                 self.admit(slots, [j.cap for _, j in take])
+                for s, j in take:
+                    active[s] = j
+                    left[s] = prompt_extra + j.cap
+                dirty = True
+            while encoding and (not active or encoding[0][0].query()):
+                ev, take = encoding.popleft()
+                self.stream.wait_event(ev)
+                self.admit([s for s, _ in take], [j.cap for _, j in take])
                 for s, j in take:
                     active[s] = j
                     left[s] = prompt_extra + j.cap
@@ -431,7 +468,7 @@ class WhisperGPU:
                     free.extend(eot)
                     dirty = True
             prev = cur
-            if prev is None and not active and not pending:
+            if prev is None and not active and not pending and not encoding:
                 break
         self.stats.busy_s += time.perf_counter() - t0
         return results
