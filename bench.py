@@ -224,7 +224,8 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
     audio_s = sum(len(x) for _, x in segs) / 16000.0
     eng = WhisperGPU(dims, seed=0, device=local, max_slots=min(64, args.segments),
                      max_encode_batch=args.encode_batch, steps_per_poll=args.steps_per_poll,
-                     decode_groups=args.decode_groups, first_encode_batch=args.first_encode_batch)
+                     decode_groups=args.decode_groups, first_encode_batch=args.first_encode_batch,
+                     overlap_encode=bool(args.overlap_encode), decode_priority=args.decode_priority)
     backend = B200Backend(B200BackendConfig(model=MODEL, device=local), engine=eng)
 
     # resident inputs for `value`
@@ -314,6 +315,8 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
                        "parallelism": f"replicas x{world} (no collective)",
                        "l2": "flushed between timed steps (256 MB write)",
                        "encode_batch": args.encode_batch, "first_encode_batch": args.first_encode_batch,
+                       "overlap_encode": bool(args.overlap_encode),
+                       "decode_priority": args.decode_priority,
                        "steps_per_poll": args.steps_per_poll,
                        "decode_groups": eng.decode_groups},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
@@ -478,10 +481,15 @@ def main():
     ap.add_argument("--ref-segments-per-step", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--decode-groups", type=int, default=None)
-    ap.add_argument("--first-encode-batch", type=int, default=16,
-                    help="segments in the first encode group of an idle engine: the GPU starts "
-                         "while the host stages the rest (measured with --encode-batch 64: "
-                         "16 -> e2e 18.1k, 64 -> 17.8k RTFx)")
+    ap.add_argument("--overlap-encode", type=int, default=1,
+                    help="1: encode the next group on a second stream while admitted groups decode")
+    ap.add_argument("--decode-priority", type=int, default=-1,
+                    help="CUDA stream priority of the decode stream (-1 high, 0 normal)")
+    ap.add_argument("--first-encode-batch", type=int, default=24,
+                    help="segments (longest caps first) in the first encode group of an idle "
+                         "engine; the rest encode on a second stream while it decodes "
+                         "(measured, overlap on: 20 -> e2e 18.5k, 24 -> 18.7k, 32 -> 18.3k RTFx; "
+                         "overlap off, 16: 18.1k)")
     ap.add_argument("--profile", action="store_true",
                     help="run exactly one resident-input step and exit (ncu)")
     args = ap.parse_args()

@@ -101,7 +101,7 @@ class WhisperGPU:
                  max_encode_batch: int = 32, num_pages: int | None = None,
                  eot: int | None = None, steps_per_poll: int = 8,
                  decode_groups: int | None = None, first_encode_batch: int = 8,
-                 overlap_encode: bool = False, decode_priority: int = 0):
+                 overlap_encode: bool = True, decode_priority: int = -1):
         if not torch.cuda.is_available():
             raise _native.DmError("no CUDA device: the B200 engine has no CPU fallback")
         self.dims = dims
