@@ -126,3 +126,42 @@ def test_eot_releases_slot(native_lib):
     assert got == want
     assert got[0] == []
     gpu.close()
+
+
+def test_overlapped_encode_matches_serial(native_lib):
+    """run_jobs with the next encode group on a second stream (overlap_encode,
+    longest caps first) returns the same tokens as the serial order, over
+    several groups joining a running decode batch."""
+    from paper_2507_01021_b200.engine import SegmentJob, WhisperGPU
+    gpu = WhisperGPU(WHISPER_TINY, seed=0, init_std=0.05, max_slots=24, max_encode_batch=6,
+                     first_encode_batch=4)
+    durs = [3.0, 28.0, 9.0, 15.0, 4.5, 30.0, 12.0, 6.0, 21.0, 7.0, 18.0, 25.0,
+            3.5, 11.0, 27.0, 5.0, 16.0, 8.0, 29.0, 10.0]
+    segs = _segments(len(durs), durs, seed=7)
+    caps = [max(1, int(np.ceil(d * 1.5))) for d in durs]
+    jobs = lambda: [SegmentJob(i, s, c) for i, (s, c) in enumerate(zip(segs, caps))]
+    gpu.overlap_encode = False
+    serial = gpu.run_jobs(jobs())
+    gpu.overlap_encode = True
+    for _ in range(3):
+        assert gpu.run_jobs(jobs()) == serial
+    assert [len(serial[i]) for i in range(len(durs))] == caps
+
+
+def test_decode_under_concurrent_stream_load(native_lib):
+    """Decode steps sharing the SMs with another stream's kernels give the same
+    tokens (regression: the LayerNorm kernel polled an mbarrier before thread 0
+    had initialised it, which faulted once another stream's CTAs shared the SM)."""
+    from paper_2507_01021_b200.engine import WhisperGPU
+    gpu = WhisperGPU(WHISPER_TINY, seed=0, init_std=0.05, max_slots=16, max_encode_batch=8)
+    segs = _segments(16, [5.0 + i for i in range(16)], seed=8)
+    caps = [40] * 16
+    alone = gpu.transcribe_ids(segs, caps)
+    side = torch.cuda.Stream()
+    a = torch.randn(4096, 4096, device="cuda", dtype=torch.bfloat16)
+    for _ in range(3):
+        with torch.cuda.stream(side):
+            for _ in range(100):
+                a = torch.tanh(a @ a * 1e-3)
+        assert gpu.transcribe_ids(segs, caps) == alone
+    torch.cuda.synchronize()
