@@ -92,6 +92,8 @@ class B200BackendConfig:
     window_s: float = 30.0
     silence_is_empty: bool = True
     steps_per_poll: int = 8
+    overlap_encode: bool = True         # next encode group on a second stream while others decode
+    first_encode_batch: int = 8         # first group of an idle engine (longest caps first)
 
     def __post_init__(self) -> None:
         get_model(self.model)
@@ -110,7 +112,8 @@ class B200Backend:
         self.engine = engine or WhisperGPU(
             dims, seed=self.cfg.seed, init_std=self.cfg.init_std, device=self.cfg.device,
             max_slots=self.cfg.max_slots, max_encode_batch=self.cfg.max_encode_batch,
-            steps_per_poll=self.cfg.steps_per_poll)
+            steps_per_poll=self.cfg.steps_per_poll, overlap_encode=self.cfg.overlap_encode,
+            first_encode_batch=self.cfg.first_encode_batch)
         self._device_lock = threading.Lock()
 
     def cap_for(self, duration_s: float) -> int:
