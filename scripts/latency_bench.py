@@ -123,12 +123,15 @@ def main():
     ap.add_argument("--max-batch", type=int, default=64)
     ap.add_argument("--starvation-ms", type=float, default=100.0)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--overlap-encode", type=int, default=1,
+                    help="1: new arrivals encode on a second stream while admitted slots decode")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
     dims = get_model(args.model)
     t = time.time()
     engines = [WhisperGPU(dims, device=g, max_slots=args.slots, max_encode_batch=args.encode_batch,
-                          steps_per_poll=4) for g in range(args.gpus)]
+                          steps_per_poll=4, overlap_encode=bool(args.overlap_encode))
+               for g in range(args.gpus)]
     init_s = time.time() - t
     users = {f"u{i:03d}": user_session(args.seed, f"u{i:03d}", args.session_s)
              for i in range(args.users)}
