@@ -1,28 +1,40 @@
 #!/usr/bin/env python
-"""Benchmark: audio-seconds transcribed per second (RTFx) on B200.
+"""Benchmark: audio-seconds transcribed per second (RTFx) on B200, with the
+p50/p95 per-segment latency of 64 concurrent users in the same line.
 
-Workload (BASELINE.json configs[1], the config the metric is quoted on that
-fits one GPU): whisper-base random-init (seed 0), 64 synthetic segments per
-GPU with durations uniform in [3, 30] s (loadgen-style speech = uniform int16
-noise in [-8000, 8000), per-user PCG64 seeded by blake2s(f"{seed}:u{id}")),
-dynamic batching (max_batch 64, target_audio_s 64*30 -> one batch), greedy
-cap ceil(3.75 * duration) tokens (the sim text rate), continuous-batching
-decode slots. One "step" = the whole hot path over that batch: log-mel ->
-encoder -> cross-KV -> greedy decode of every segment to EOT/cap.
+Workload (BASELINE.json configs[2], cfg3 -- the largest configuration that
+fits one GPU): whisper-large-v3 random-init bf16 (seed 0), 64 synthetic
+segments per GPU with durations uniform in [3, 30] s (loadgen-style speech =
+uniform int16 noise in [-8000, 8000), per-user PCG64 seeded by
+blake2s(f"{seed}:u{id}"), loadgen.py:50-53,97-98), continuous batching
+(the reference's continuous policy, min_batch 32, max_batch 64) over 64
+decode slots, greedy cap ceil(3.75 * duration) tokens (the sim text rate).
+One "step" = the whole hot path over those 64 segments: log-mel -> encoder
+-> cross-KV -> greedy decode of every segment to EOT/cap.
 
-  value : inputs (int16 PCM) already resident in HBM when the timed region
-          starts; CUDA events on the engine stream, max over ranks.
-  e2e   : the public API a user calls — SegmentQueue (dynamic policy) ->
-          B200Backend.transcribe_batch(batch) with host numpy PCM: pinned
-          staging + H2D, kernels, D2H token reads, detokenisation.
+  value   : inputs (int16 PCM) already resident in HBM when the timed region
+            starts; CUDA events on the engine stream, max over ranks.
+  e2e     : the public API a user calls -- the reference's own SegmentQueue
+            (continuous policy) -> B200Backend.transcribe_batch(batch) with
+            host numpy PCM: pinned staging + H2D, kernels, D2H token reads,
+            detokenisation.
+  latency : 64 live users speaking in real time into the reference's
+            SegmentQueue, one GpuConsumer per GPU (iteration-level
+            admission); p50/p95 endpoint -> delivery by nearest rank
+            (report.py:17-26), next to one user alone through the
+            reference's own SequentialJobRunner (server.py:142-206).
+  stages  : log-mel (HBM), encoder (bf16 tensor), decode step at 64 rows
+            (HBM), each as a fraction of MEASURED_PEAKS.json.
+  roofline: the dominant kernel (decode cross-attention + cross-o tail).
 
-N GPUs (torchrun): one process per GPU, each with its own 64 segments (weak
-scaling, no data-path collective: segments are independent);
-torch.distributed (nccl) only for the barrier and the max-over-ranks time.
+N GPUs: `--gpus N` launches N ranks itself (torch.distributed.run) unless
+already under torchrun; one process per GPU, each with its own 64 segments
+(weak scaling, no data-path collective: segments are independent, SURVEY.md
+§8(e)); torch.distributed only for the barrier and the max-over-ranks time.
 
-`--impl reference` times the CPU oracle (the reference path has no compiled
-implementation: faster-whisper/CTranslate2 are absent) on
-the host cores with all threads, rank 0 only.
+`--impl reference` times the reference path's CPU restatement (oracle/,
+faster-whisper/CTranslate2 are absent) on the host cores
+with all threads, rank 0 only, on the same model and workload.
 """
 
 from __future__ import annotations
@@ -32,6 +44,7 @@ import hashlib
 import json
 import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -46,7 +59,8 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "audio-seconds transcribed/sec (RTFx)"
 UNIT = "audio_s/s"
-MODEL = "whisper-base"
+MODEL = "whisper-large-v3"
+REF = ROOT / "baseline" / "_ref"
 
 
 # ---------------------------------------------------------------- workload
@@ -69,6 +83,16 @@ def make_workload(n: int, rank: int = 0, seed: int = 0, lo: float = 3.0, hi: flo
 
 def token_cap(duration_s: float) -> int:
     return max(1, min(444, math.ceil(3.75 * duration_s)))
+
+
+def reference_scheduler():
+    """The reference's own scheduler module (unmodified, baseline/_ref), or None."""
+    if not (REF / "dictamux").exists():
+        return None
+    if str(REF) not in sys.path:
+        sys.path.insert(0, str(REF))
+    import dictamux.scheduler as rs
+    return rs
 
 
 # ---------------------------------------------------------------- clocks
@@ -131,6 +155,8 @@ def max_over_ranks(x: float, world: int, device=None) -> float:
         return x
     import torch
     import torch.distributed as dist
+    if dist.get_backend() != "nccl":
+        device = None                 # gloo (--share-devices): reduce on the host
     t = torch.tensor([x], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -142,20 +168,57 @@ def barrier(world: int):
         dist.barrier()
 
 
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: start N ranks on this node."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={_free_port()}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def pick_device(local: int, world: int, share: bool) -> tuple[int, str]:
+    """(CUDA device, process-group backend) of this rank. Fewer visible GPUs
+    than ranks is an error unless --share-devices (a plumbing check of the
+    N-rank path on a 1-GPU lease: ranks never wait on each other's kernels,
+    and the barrier/max-over-ranks runs on gloo)."""
+    import torch
+    n = torch.cuda.device_count()
+    if n == 0:
+        raise SystemExit("bench.py: no CUDA device (the B200 path has no CPU fallback)")
+    if world > n:
+        if not share:
+            raise SystemExit(f"bench.py: --gpus {world} but only {n} CUDA device(s) visible")
+        return local % n, "gloo"
+    return local, "nccl"
+
+
 # ---------------------------------------------------------------- CPU oracle
-def cpu_oracle_rtfx(segs, dims_name: str, threads: int, budget_s: float = 20.0) -> dict:
+def _oracle_for(dims, blob=None, man=None, threads=None):
+    from oracle.weights import load_all_f32, load_all_f32_from_bits
+    from oracle.whisper import WhisperOracle
+    from paper_2507_01021_b200.weights import whisper_manifest
+    man = man or whisper_manifest(dims, 0, 0.02)
+    w = load_all_f32_from_bits(man, blob) if blob is not None else load_all_f32(man, threads)
+    return WhisperOracle(dims, seed=0, weights=w)
+
+
+def cpu_oracle_rtfx(orc, segs, threads: int, budget_s: float = 20.0) -> dict:
     """Time the CPU restatement (oracle/) of the full path on a bounded sample."""
     import torch
     from oracle.logmel import log_mel_batch
-    from oracle.whisper import WhisperOracle
-    from paper_2507_01021_b200.models import get_model
     torch.set_num_threads(threads)
-    dims = get_model(dims_name)
-    orc = WhisperOracle(dims, seed=0)
     audio, wall, used = 0.0, 0.0, 0
     for uid, x in segs:
         t0 = time.perf_counter()
-        mel = log_mel_batch([x], dims.n_mels)
+        mel = log_mel_batch([x], orc.dims.n_mels)
         enc = orc.encode(mel)
         orc.greedy(enc[0], token_cap(len(x) / 16000.0))
         wall += time.perf_counter() - t0
@@ -176,57 +239,73 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def workload_name(segments: int) -> str:
+    return (f"cfg3: {MODEL} random-init bf16 (seed 0), {segments} segments/GPU x U[3,30] s "
+            f"synthetic speech, continuous batching (min_batch 32, max_batch 64) over 64 decode "
+            f"slots, greedy cap ceil(3.75*dur)")
+
+
 # ---------------------------------------------------------------- arms
 def run_reference(args, rank: int, world: int) -> None:
+    """The reference path's CPU implementation (the oracle port: the
+    reference's faster-whisper/CTranslate2 path is absent) on this host's
+    cores. Each timed step = one segment of the same workload (rotating),
+    transcribed end to end; warm-up steps run the shortest segment with cap 4."""
     if rank != 0:
         return
+    from paper_2507_01021_b200.models import get_model
     threads = len(os.sched_getaffinity(0))
+    dims = get_model(MODEL)
+    t0 = time.perf_counter()
+    orc = _oracle_for(dims, threads=threads)
+    init_s = time.perf_counter() - t0
     segs = make_workload(args.segments, 0)
-    per_step = max(1, args.ref_segments_per_step)
+    import torch
+    torch.set_num_threads(threads)
+    short = min(segs, key=lambda s: len(s[1]))
+    for _ in range(args.warmup):
+        from oracle.logmel import log_mel_batch
+        orc.greedy(orc.encode(log_mel_batch([short[1]], dims.n_mels))[0], 4)
     times, audios = [], []
-    idx = 0
-    for it in range(args.warmup + args.steps):
-        sample = [segs[(idx + j) % len(segs)] for j in range(per_step)]
-        idx += per_step
-        r = cpu_oracle_rtfx(sample, MODEL, threads, budget_s=1e9)
-        if it >= args.warmup:
-            times.append(r["wall_s"])
-            audios.append(r["audio_s"])
+    for it in range(args.steps):
+        r = cpu_oracle_rtfx(orc, [segs[(it * 7) % len(segs)]], threads, budget_s=1e9)
+        times.append(r["wall_s"])
+        audios.append(r["audio_s"])
     value = sum(audios) / sum(times)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * sum(times) / len(times), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"cfg2: {MODEL} random-init, {args.segments} x U[3,30] s "
-                               f"synthetic segments, greedy cap ceil(3.75*dur)",
-                   "model": MODEL, "sample_per_step": f"{per_step} segments (rotating)"},
+        "config": {"workload": workload_name(args.segments), "model": MODEL,
+                   "sample_per_step": "1 workload segment (rotating, stride 7) end to end",
+                   "weights_init_s": round(init_s, 1)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{per_step} segments per step x {args.steps} steps, "
-                                   f"oracle/ (torch fp32 CPU) on {cpu_model()}"},
+                         "sample": f"{args.steps} workload segments ({sum(audios):.1f} audio-s), "
+                                   f"one per step, full path (log-mel + encode + greedy) in "
+                                   f"oracle/ (torch fp32 CPU, {threads} threads) on {cpu_model()}"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def run_b200(args, rank: int, world: int, local: int) -> None:
+def run_b200(args, rank: int, world: int, device: int) -> None:
     import torch
     from paper_2507_01021_b200.backend import B200Backend, B200BackendConfig
     from paper_2507_01021_b200.engine import ResidentPCM, SegmentJob, WhisperGPU
     from paper_2507_01021_b200.models import get_model
-    from paper_2507_01021_b200.multiplex import BatchingPolicy, SegmentQueue
-    from paper_2507_01021_b200.types import make_segment
+    from paper_2507_01021_b200.types import batch_of, make_segment
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    torch.cuda.set_device(device)
+    dev = torch.device("cuda", device)
     dims = get_model(MODEL)
     segs = make_workload(args.segments, rank)
     audio_s = sum(len(x) for _, x in segs) / 16000.0
-    eng = WhisperGPU(dims, seed=0, device=local, max_slots=min(64, args.segments),
+    eng = WhisperGPU(dims, seed=0, device=device, max_slots=min(64, args.segments),
                      max_encode_batch=args.encode_batch, steps_per_poll=args.steps_per_poll,
-                     decode_groups=args.decode_groups, first_encode_batch=args.first_encode_batch,
+                     first_encode_batch=args.first_encode_batch,
                      overlap_encode=bool(args.overlap_encode), decode_priority=args.decode_priority)
-    backend = B200Backend(B200BackendConfig(model=MODEL, device=local), engine=eng)
+    backend = B200Backend(B200BackendConfig(model=MODEL, device=device), engine=eng)
 
     # resident inputs for `value`
     flat = np.concatenate([x for _, x in segs])
@@ -259,7 +338,7 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
     for _ in range(args.warmup):
         timed(lambda: eng.run_jobs(res_jobs()))
     c0 = eng.counters()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(device)
     with clocks:
         step_ms = [timed(lambda: eng.run_jobs(res_jobs()))[0] for _ in range(args.steps)]
     c1 = eng.counters()
@@ -268,18 +347,20 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
     value = world * audio_s / (ms_max / 1000.0)
     launches = c1["launches"] - c0["launches"]
 
-    # dominant decode kernel: cross-attention over a full slot set, CUDA events
-    roof = measure_roofline(eng, dims, args)
-    stages = measure_stages(eng, dims, segs, offs, pcm_dev)
+    # e2e through the public API (host PCM -> results): the reference's own
+    # SegmentQueue + continuous policy forms the batch (our mirror types when
+    # the reference package is absent)
+    rs = reference_scheduler()
 
-    # e2e through the public API (host PCM -> results)
     def e2e_once():
-        q = SegmentQueue()
-        for i, (uid, x) in enumerate(segs):
-            q.enqueue_segment(make_segment(uid, x, session_id=uid, endpoint_time=0.0), 0.0)
-        pol = BatchingPolicy(kind="dynamic", max_batch=len(segs), max_wait_ms=200.0,
-                             target_audio_s=len(segs) * 30.0)
-        batch = q.try_form_batch(pol, 0.0)
+        if rs is not None:
+            q = rs.SegmentQueue()
+            for uid, x in segs:
+                q.enqueue_segment(make_segment(uid, x, session_id=uid, endpoint_time=0.0), 0.0)
+            pol = rs.BatchingPolicy(kind="continuous", min_batch=32, max_batch=len(segs))
+            batch = q.try_form_batch(pol, 0.0)
+        else:
+            batch = batch_of([make_segment(uid, x, session_id=uid) for uid, x in segs])
         assert batch is not None and len(batch.entries) == len(segs)
         res = backend.transcribe_batch(batch)
         assert len(res) == len(segs) and not any(r.is_error for r in res)
@@ -293,10 +374,18 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
     e2e_ms_max = max_over_ranks(statistics.mean(e2e_ms), world, dev)
     e2e_value = world * audio_s / (e2e_ms_max / 1000.0)
 
+    stages = measure_stages(eng, dims, segs, offs, pcm_dev) if not args.no_stages else None
+    roof = measure_roofline(eng, dims) if not args.no_stages else None
+
+    latency = None
+    if args.latency_users > 0 and world == 1:
+        latency = measure_latency(eng, dims, args, rs)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
-        r = cpu_oracle_rtfx(segs, MODEL, threads, budget_s=args.cpu_budget_s)
+        orc = _oracle_for(dims, blob=eng.blob.cpu().numpy().view(np.uint16), man=eng.man)
+        r = cpu_oracle_rtfx(orc, segs, threads, budget_s=args.cpu_budget_s)
         cpu = {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"first {r['segments']} of the {args.segments} workload segments "
                          f"({r['audio_s']:.1f} audio-s, {r['wall_s']:.1f} s wall), full path "
@@ -307,9 +396,7 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"cfg2: {MODEL} random-init (seed 0), {args.segments} "
-                                   f"segments/GPU x U[3,30] s synthetic speech, dynamic batching "
-                                   f"(one batch), greedy cap ceil(3.75*dur), 64 decode slots",
+            "config": {"workload": workload_name(args.segments),
                        "model": MODEL, "segments_per_gpu": args.segments,
                        "audio_s_per_gpu": round(audio_s, 3),
                        "parallelism": f"replicas x{world} (no collective)",
@@ -317,16 +404,22 @@ def run_b200(args, rank: int, world: int, local: int) -> None:
                        "encode_batch": args.encode_batch, "first_encode_batch": args.first_encode_batch,
                        "overlap_encode": bool(args.overlap_encode),
                        "decode_priority": args.decode_priority,
-                       "steps_per_poll": args.steps_per_poll,
-                       "decode_groups": eng.decode_groups},
+                       "steps_per_poll": args.steps_per_poll},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
-                    "path": "SegmentQueue(dynamic) -> B200Backend.transcribe_batch (host int16)"},
-            "roofline": roof, "stages": stages, "cpu_baseline": cpu, "clocks": clocks.summary(),
-            "gpu_launches": launches // args.steps,
+                    "path": ("reference SegmentQueue(continuous, min_batch 32) -> "
+                             if rs is not None else "Batch -> ")
+                            + "B200Backend.transcribe_batch (host int16)"},
+            "latency": latency, "roofline": roof, "stages": stages, "cpu_baseline": cpu,
+            "clocks": clocks.summary(), "gpu_launches": launches // args.steps,
             "gpu_launches_note": "kernels per timed step (C-ABI counter; graph nodes per replay)",
         }
         print(json.dumps(line), flush=True)
+
+
+def _peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    return json.loads(p.read_text()) if p.exists() else {}
 
 
 def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
@@ -335,19 +428,19 @@ def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
     with CUDA events on the engine stream, L2 flushed before every timed call.
 
       log-mel : dm_logmel over the first E workload segments; algorithmic bytes
-                = true int16 PCM (2 n) + the fp32 [n_mels, 3000] features
+                = true int16 PCM (2 n) + the [n_mels, 3000] features written
                 (SURVEY.md §8(d)).
       encoder : dm_whisper_encode of the same E segments (log-mel -> conv stem
                 -> layers -> cross-KV); algorithmic FLOPs = E x (encoder +
                 cross-KV) per segment, SURVEY.md §8(d).
-      decode  : one greedy step with all 64 slots active (same E segments
+      decode  : one greedy step with all 64 slots active (the E segments
                 replicated); algorithmic bytes = decoder weights + every active
                 slot's cross-KV + its self-KV up to the fed position."""
     import ctypes as C
-    import json as _j
     import torch
+    from paper_2507_01021_b200 import _native
     from paper_2507_01021_b200.engine import ResidentPCM
-    peaks = _j.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peaks = _peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     tc = float(peaks.get("bf16_tflops", 2250.0))
     dev = pcm_dev.device
@@ -374,7 +467,6 @@ def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
     offs_d = torch.tensor([o for _, _, o in sub], dtype=torch.int64, device=dev)
     lens_d = torch.tensor([len(x) for _, x, _ in sub], dtype=torch.int32, device=dev)
     mel = torch.empty(E, nm, 3000, dtype=torch.float32, device=dev)
-    from paper_2507_01021_b200 import _native
     lm = lambda: _native.check(eng.lib.dm_logmel(C.c_void_p(pcm_dev.data_ptr()),
                                                 C.c_void_p(offs_d.data_ptr()),
                                                 C.c_void_p(lens_d.data_ptr()), E, nm,
@@ -391,7 +483,7 @@ def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
     slots = list(range(E))
     en = lambda: eng.encode(jobs, slots)
     en()
-    en_ms = ev_ms(en)
+    en_ms = ev_ms(en, reps=3)
     # decode step at 64 rows (K6)
     S = eng.max_slots
     for i in range(E, S, E):
@@ -413,8 +505,7 @@ def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
     return {
         "logmel": {"bound": "hbm", "achieved": lm_bytes / (lm_ms / 1e3) / 1e9, "peak": hbm,
                    "unit": "GB/s", "frac": lm_bytes / (lm_ms / 1e3) / 1e9 / hbm,
-                   "ms": lm_ms, "bytes": lm_bytes, "segments": E,
-                   "note": "FFT+mel is ~27 MFLOP/segment: the kernel sits at the FP32 ridge"},
+                   "ms": lm_ms, "bytes": lm_bytes, "segments": E},
         "encoder": {"bound": "tensor", "achieved": E * enc_flop / (en_ms / 1e3) / 1e12, "peak": tc,
                     "unit": "TFLOP/s", "frac": E * enc_flop / (en_ms / 1e3) / 1e12 / tc,
                     "ms": en_ms, "flop": E * enc_flop, "segments": E,
@@ -427,17 +518,19 @@ def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
     }
 
 
-def measure_roofline(eng, dims, args) -> dict:
+def measure_roofline(eng, dims) -> dict:
     """Cross-attention (decode, K6; cross-o projection fused in its tail) is
-    the dominant HBM stream: per launch it reads every active slot's K and V
-    for one layer: n_active * 2 * 1500 * d bf16 (SURVEY.md §8(d):
-    L*2*1500*d*2 B per segment per step). The 2*d*d B cross-o weight slices
-    (L2-resident across the batch) are not counted."""
-    import json as _j
-    peaks = _j.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    the dominant kernel: per launch it streams every active slot's K and V of
+    one layer, n_active * 2 * 1500 * d bf16 (SURVEY.md §8(d):
+    L*2*1500*d*2 B per segment per step; 491.5 MB per launch at 64 rows on
+    large-v3). Timed with CUDA events around a graph of one launch per decoder
+    layer (launch i runs layer i % L, so every launch reads a different
+    layer's cross-KV from HBM, PDL-chained as inside the step graph) at 64
+    active rows. The 2*d*d B cross-o weight slices (L2-resident) are not counted."""
+    import torch
+    peaks = _peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
     S = eng.max_slots
-    # fill all slots with a resident segment so the kernel runs at full batch
     seg = np.random.default_rng(0).integers(-8000, 8000, size=160000, dtype=np.int16)
     slots = list(range(S))
     for i in range(0, S, eng.max_encode_batch):
@@ -446,25 +539,49 @@ def measure_roofline(eng, dims, args) -> dict:
     eng.admit(slots, [8] * S)
     eng.set_active(slots)
     eng.step(1)                      # q for the cross-attention
-    ms = statistics.mean(eng.time_kernel(0, layer=l, iters=20) for l in range(dims.dec_layers))
+    L = dims.dec_layers
+    runs = [eng.time_kernel(0, layer=-1, iters=2 * L) for _ in range(5)]
+    ms = statistics.median(runs)
     eng.release(slots)
     eng.set_active([])
-    rows = sum(1 for s in slots if s % eng.decode_groups == 0)     # decode group 0's rows
-    bytes_per_launch = rows * 2 * 1500 * dims.d_model * 2
+    torch.cuda.synchronize(eng.device)
+    bytes_per_launch = S * 2 * 1500 * dims.d_model * 2
     achieved = bytes_per_launch / (ms / 1000.0) / 1e9
     traffic = None
-    tf = ROOT / "profiles" / "r01_xattn_traffic_v10.json"
-    if tf.exists():     # dram read+write of one ncu --set full capture (64 rows), scaled to rows
-        t = _j.loads(tf.read_text())
-        traffic = (t["dram_bytes_read"] + t["dram_bytes_write"]) * rows / t["rows"]
-    return {"kernel": "cross_attn_kernel (decode K6, + cross-o tail)", "bound": "hbm", "achieved": achieved,
-            "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-            "traffic_unit": "bytes per launch (ncu dram__bytes_read+write, profiles/r01_xattn_traffic_v10.json)",
-            "timing": "CUDA events on the engine stream around a graph of 20 back-to-back launches "
-                      "per decoder layer at a full 64-row batch, after the timed region",
+    tf = ROOT / "profiles" / "r02_xattn_traffic_large_v3.json"
+    if tf.exists():     # dram read+write of one ncu --set full capture, scaled to rows
+        t = json.loads(tf.read_text())
+        traffic = (t["dram_bytes_read"] + t["dram_bytes_write"]) * S / t["rows"]
+    return {"kernel": "cross_attn_kernel (decode K6, + cross-o tail)", "bound": "hbm",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic,
+            "traffic_unit": f"bytes per launch (ncu dram__bytes_read+write, {tf.name})",
+            "timing": f"CUDA events on the engine stream around a graph of {2 * L} launches, "
+                      f"launch i = decoder layer i % {L}, 64 active rows (median of 5)",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback",
             "bytes_per_launch": bytes_per_launch, "avg_launch_ms": ms,
             "per_unit": "2*1500*d*2 B per active slot per layer"}
+
+
+def measure_latency(eng, dims, args, rs) -> dict | None:
+    """p50/p95 per-segment latency of `latency_users` live users (cfg3) on
+    this GPU vs one user alone through the reference's SequentialJobRunner."""
+    if rs is None:
+        return {"unavailable": "reference package not installed in baseline/_ref"}
+    sys.path.insert(0, str(ROOT / "scripts"))
+    import latency_bench as lb
+    users = {f"u{i:03d}": lb.user_session(args.seed, f"u{i:03d}", args.latency_session_s)
+             for i in range(args.latency_users)}
+    policy = rs.BatchingPolicy(kind="continuous", min_batch=32, max_batch=64,
+                               starvation_flush_ms=args.starvation_ms)
+    mux = lb.run_multiplexed([eng], users, policy, rs)
+    seq = lb.run_sequential_reference([eng], users["u000"], 64, MODEL)
+    return {"users": args.latency_users, "session_s": args.latency_session_s,
+            "policy": {"kind": "continuous", "min_batch": 32, "max_batch": 64,
+                       "starvation_flush_ms": args.starvation_ms},
+            "multiplexed": mux, "sequential_single_user": seq,
+            "p95_below_sequential": mux["p95_ms"] < seq["p95_ms"],
+            "percentile": "nearest rank (report.py:17-26)"}
 
 
 def main():
@@ -475,37 +592,42 @@ def main():
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--segments", type=int, default=64)
     ap.add_argument("--encode-batch", type=int, default=64,
-                    help="segments per encoder launch (64: the whole cfg2 batch in one encode)")
+                    help="segments per encoder launch (64: the rest of the batch in one encode)")
     ap.add_argument("--steps-per-poll", type=int, default=8)
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
-    ap.add_argument("--ref-segments-per-step", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--decode-groups", type=int, default=None)
+    ap.add_argument("--no-stages", action="store_true")
     ap.add_argument("--overlap-encode", type=int, default=1,
                     help="1: encode the next group on a second stream while admitted groups decode")
     ap.add_argument("--decode-priority", type=int, default=-1,
                     help="CUDA stream priority of the decode stream (-1 high, 0 normal)")
     ap.add_argument("--first-encode-batch", type=int, default=24,
-                    help="segments (longest caps first) in the first encode group of an idle "
-                         "engine; the rest encode on a second stream while it decodes "
-                         "(measured, overlap on: 20 -> e2e 18.5k, 24 -> 18.7k, 32 -> 18.3k RTFx; "
-                         "overlap off, 16: 18.1k)")
+                    help="segments (longest caps first) in the first encode group of an idle engine")
+    ap.add_argument("--latency-users", type=int, default=64,
+                    help="live users for the latency block (0: skip)")
+    ap.add_argument("--latency-session-s", type=float, default=30.0)
+    ap.add_argument("--starvation-ms", type=float, default=100.0)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--share-devices", action="store_true",
+                    help="allow more ranks than visible GPUs (plumbing check; gloo barrier)")
     ap.add_argument("--profile", action="store_true",
                     help="run exactly one resident-input step and exit (ncu)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.impl == "reference":
+        run_reference(args, rank, world)    # rank 0 alone; no process group needed
+        return
+    device, backend = pick_device(local, world, args.share_devices)
     if world > 1:
         import torch
         import torch.distributed as dist
-        if args.impl == "b200":
-            torch.cuda.set_device(local)
-            dist.init_process_group("nccl")
-        else:
-            dist.init_process_group("gloo")
-    if args.impl == "reference":
-        run_reference(args, rank, world)
-    else:
-        run_b200(args, rank, world, local)
+        torch.cuda.set_device(device)
+        dist.init_process_group(backend)
+    run_b200(args, rank, world, device)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()

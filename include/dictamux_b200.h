@@ -160,7 +160,9 @@ DM_API int dm_whisper_stats(void* handle, int64_t* out, int n);
  * 0 cross-attention(layer), 1 self-attention(layer), 2 LM head, 3 decoder LN
  * (+ residual partials), 4 cross-q projection, 5 fc2 projection,
  * 6 empty PDL kernel (launch floor), 7 fc1 projection (+GELU), 8 qkv projection.
- * avg_ms = mean over iters back-to-back launches. */
+ * avg_ms = mean over iters back-to-back launches. layer < 0: launch i runs
+ * decoder layer i % dec_layers (each launch streams a different layer's
+ * cross-KV / weights, as inside a decode step). */
 DM_API int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float* avg_ms,
                                   void* stream);
 

@@ -76,5 +76,68 @@ def blob_bits(man: Manifest) -> np.ndarray:
     return out
 
 
-def load_all_f32(man: Manifest) -> dict[str, np.ndarray]:
-    return {t.name: tensor_f32(man, t.name) for t in man.tensors}
+def load_all_f32(man: Manifest, threads: int | None = None) -> dict[str, np.ndarray]:
+    """Every tensor as fp32. Large normal-init tensors are generated in
+    chunks on a thread pool (numpy's elementwise kernels release the GIL):
+    large-v3 is 1.6 B values."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    threads = threads or len(os.sched_getaffinity(0))
+    out = {t.name: np.empty(t.numel, np.float32) for t in man.tensors}
+    chunk = 1 << 22
+    work = []
+    for t in man.tensors:
+        if t.init == "normal" and t.numel > chunk:
+            work += [(t, s0) for s0 in range(0, t.numel, chunk)]
+        else:
+            work.append((t, None))
+
+    def run(item):
+        t, s0 = item
+        if s0 is None:
+            out[t.name][:] = bf16_bits_to_f32(tensor_bits(man, t))
+            return
+        n = min(chunk, t.numel - s0)
+        part = TensorSpec(t.name, (n,), t.init, t.std, t.mean,
+                          [(max(a - s0, 0), min(b - s0, n)) for a, b in t.zero_ranges
+                           if b > s0 and a < s0 + n])
+        part.tid = t.tid
+        bits = tensor_bits_range(man, part, s0, n)
+        out[t.name][s0:s0 + n] = bf16_bits_to_f32(bits)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(run, work))
+    return {t.name: out[t.name].reshape(t.shape) for t in man.tensors}
+
+
+def tensor_bits_range(man: Manifest, spec: TensorSpec, start: int, n: int) -> np.ndarray:
+    """bf16 bits of elements [start, start + n) of a normal-init tensor
+    (spec.zero_ranges relative to start)."""
+    key = np.uint64(tensor_key(man.seed, spec.tid))
+    scale = np.float32(normal_scale(spec.std))
+    mean = np.float32(spec.mean)
+    idx = np.arange(start, start + n, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        h = _splitmix64_np(idx + key)
+    m = np.uint64(0xFFFF)
+    s = ((h & m) + ((h >> np.uint64(16)) & m)
+         + ((h >> np.uint64(32)) & m) + (h >> np.uint64(48)))
+    z = (s.astype(np.int64) - 131070).astype(np.float32)
+    v = (z * scale) + mean
+    u = v.view(np.uint32)
+    rnd = ((u >> np.uint32(16)) & np.uint32(1)) + np.uint32(0x7FFF)
+    out = ((u + rnd) >> np.uint32(16)).astype(np.uint16)
+    for a, b in spec.zero_ranges:
+        out[a:b] = 0
+    return out
+
+
+def load_all_f32_from_bits(man: Manifest, bits: np.ndarray) -> dict[str, np.ndarray]:
+    """The same fp32 tensors sliced out of a flat bf16 blob (uint16) -- e.g.
+    the device blob read back, whose bytes `tests/test_gpu_kernels.py`
+    checks against `tensor_bits` -- to skip regenerating billions of values
+    on the host for large-v3."""
+    out = {}
+    for t in man.tensors:
+        out[t.name] = bf16_bits_to_f32(bits[t.offset:t.offset + t.numel]).reshape(t.shape)
+    return out

@@ -143,7 +143,16 @@ class B200Backend:
                 continue
             jobs.append(SegmentJob(i, samples, self.cap_for(seg.duration_s)))
         with self._device_lock:
-            ids = self.engine.run_jobs(jobs) if jobs else {}
+            try:
+                ids = self.engine.run_jobs(jobs) if jobs else {}
+            except BaseException:
+                # free every slot's pages and drain both streams so the next
+                # batch starts clean; the caller turns the raise into per-entry
+                # error rows (scheduler.py:258-275, server.py:187-199)
+                try:
+                    self.engine.reset()
+                finally:
+                    raise
         for i, toks in ids.items():
             texts[i] = detokenize(toks)
         elapsed_ms = (time.monotonic() - started) * 1000.0

@@ -405,13 +405,7 @@ int launch_attention(const uint16_t* q, const uint16_t* k, const uint16_t* vt, i
   DM_REQUIRE(t_pad % 128 == 0 && t_pad >= T, "t_pad must be a multiple of 128 >= T");
   CUtensorMap mq, mk, mv;
   if (make_attn_maps(q, k, vt, n_seg * heads, t_pad, &mq, &mk, &mv)) return 2;
-  static bool attr = false;
-  if (!attr) {
-    DM_CHECK_CUDA(cudaFuncSetAttribute(attn_tcgen05_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       AttnSmemLayout::total));
-    attr = true;
-  }
+  DM_SMEM_ATTR(attn_tcgen05_kernel, AttnSmemLayout::total);
   dim3 grid(ceil_div(T, 256), n_seg * heads);
   attn_tcgen05_kernel<<<grid, kAttnThreads, AttnSmemLayout::total, stream>>>(
       mq, mk, mv, T, t_pad, heads, out, ldo, seg_len);

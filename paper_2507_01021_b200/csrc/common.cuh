@@ -38,6 +38,31 @@ const char* last_error();
 // Launch-error check after a <<<>>> launch.
 #define DM_CHECK_LAUNCH() DM_CHECK_CUDA(cudaGetLastError())
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device setting:
+// raise it once per (kernel, current device) (engine.cu keeps the set), so
+// engines on several GPUs in one process each get it.
+cudaError_t set_max_smem(const void* fn, int bytes);
+#define DM_SMEM_ATTR(fn, bytes) \
+  DM_CHECK_CUDA(::dm::set_max_smem(reinterpret_cast<const void*>(fn), int(bytes)))
+
+// Every handle remembers the device it was created on; each C-ABI entry point
+// makes it current for the call (the caller's thread may have another one).
+struct DeviceScope {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceScope(int dev) {
+    err = cudaGetDevice(&prev);
+    if (err == cudaSuccess && prev != dev) err = cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DeviceScope() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+#define DM_ON_DEVICE(dev)                \
+  ::dm::DeviceScope _dm_dev_scope(dev);  \
+  DM_CHECK_CUDA(_dm_dev_scope.err)
+
 constexpr int kNumSMs = 148;
 
 __host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }

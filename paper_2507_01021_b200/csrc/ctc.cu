@@ -198,6 +198,7 @@ __global__ void repack_posconv_kernel(const uint16_t* __restrict__ w, uint16_t* 
 
 // ============================================================ engine
 struct CtcEngine {
+  int device = 0;
   dm_ctc_config cfg;
   const uint16_t* w = nullptr;
   std::vector<int64_t> off;
@@ -434,6 +435,10 @@ int dm_ctc_create(const dm_ctc_config* cfg, const uint16_t* weights, const int64
   DM_REQUIRE(cfg && weights && offsets && handle, "null argument");
   DM_REQUIRE(n_offsets == 17 + 12 * cfg->layers + 2, "CTC offset table has the wrong length");
   auto* e = new CtcEngine();
+  if (cudaGetDevice(&e->device) != cudaSuccess) {
+    delete e;
+    DM_CHECK_CUDA(cudaGetLastError());
+  }
   e->cfg = *cfg;
   e->w = weights;
   e->off.assign(offsets, offsets + n_offsets);
@@ -446,6 +451,8 @@ int dm_ctc_create(const dm_ctc_config* cfg, const uint16_t* weights, const int64
 }
 
 int dm_ctc_destroy(void* handle) {
+  if (!handle) return 0;
+  DM_ON_DEVICE(static_cast<CtcEngine*>(handle)->device);
   delete static_cast<CtcEngine*>(handle);
   return 0;
 }
@@ -454,6 +461,7 @@ int dm_ctc_transcribe(void* handle, const int16_t* pcm, const int64_t* offsets,
                       const int32_t* lengths, int n, void* stream) {
   auto* e = static_cast<CtcEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
+  DM_ON_DEVICE(e->device);
   DM_REQUIRE(n >= 1 && n <= e->cfg.max_batch, "n must be in [1, max_batch]");
   std::vector<int> lens(n);
   for (int i = 0; i < n; ++i) {
@@ -476,6 +484,7 @@ int dm_ctc_read(void* handle, int32_t* tokens, int32_t* counts, int32_t* rows_pe
                 void* stream) {
   auto* e = static_cast<CtcEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
+  DM_ON_DEVICE(e->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (rows_per_segment) *rows_per_segment = e->last_R6;
   if (counts)
@@ -491,6 +500,7 @@ int dm_ctc_read(void* handle, int32_t* tokens, int32_t* counts, int32_t* rows_pe
 int dm_ctc_debug(void* handle, int which, void* host_dst, size_t bytes, void* stream) {
   auto* e = static_cast<CtcEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
+  DM_ON_DEVICE(e->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const void* src = nullptr;
   size_t avail = 0;

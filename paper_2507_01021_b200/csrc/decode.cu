@@ -501,12 +501,7 @@ size_t gemv_part_floats(int N, int K, int epi) {
 template <int EPI, bool SPLIT>
 static int launch_gv(const DecodeState& st, const TcGemvMaps& maps, const GemvArgs& a,
                      cudaStream_t stream) {
-  static bool attr = false;
-  if (!attr) {
-    DM_CHECK_CUDA(cudaFuncSetAttribute(gemv_kernel<EPI, SPLIT>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemOptin));
-    attr = true;
-  }
+  DM_SMEM_ATTR((gemv_kernel<EPI, SPLIT>), kSmemOptin);
   const int tiles = ceil_div(a.N, 128);
   const int gx = std::max(1, std::min(tiles, kNumSMs / a.splits));
   DM_CHECK_CUDA(launch_pdl(gemv_kernel<EPI, SPLIT>, dim3(gx, a.splits, a.rgroups),
@@ -662,12 +657,7 @@ int launch_ln(const DecodeState& st, const LnArgs& a, cudaStream_t stream) {
     case 1: DM_CHECK_CUDA(launch_pdl(ln_kernel<1>, grid, block, 0, stream, st, a)); break;
     case 2: {
       const int smem = (a.res.splits + 1) * st.d * 4;
-      static bool attr = false;
-      if (!attr) {
-        DM_CHECK_CUDA(cudaFuncSetAttribute(ln_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (kMaxHeads + 1) * 1280 * 4));
-        attr = true;
-      }
+      DM_SMEM_ATTR(ln_kernel<2>, (kMaxHeads + 1) * 1280 * 4);
       DM_CHECK_CUDA(launch_pdl(ln_kernel<2>, grid, block, smem, stream, st, a));
       break;
     }
@@ -886,12 +876,7 @@ int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, floa
                  qkv.splits >= 1 && qkv.splits <= kMaxSplits, "self-attn: qkv partials");
   DM_REQUIRE(st.page_tokens == 64 && st.pages_per_slot * 64 <= kSaMaxKeys, "self-attn: page geometry");
   const int smem = kSaPrePages * 2 * kSaPageBytes + 16;
-  static bool attr = false;
-  if (!attr) {
-    DM_CHECK_CUDA(cudaFuncSetAttribute(self_attn_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  DM_SMEM_ATTR(self_attn_kernel, smem);
   DM_CHECK_CUDA(launch_pdl(self_attn_kernel, dim3(kRows, st.heads), dim3(kSaThreads), smem,
                            stream, st, layer, qkv, q_scale));
   return 0;
@@ -1127,12 +1112,7 @@ int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int lay
   DM_REQUIRE(st.d % 64 == 0, "cross-attn: d must be a multiple of 64");
   DM_REQUIRE(16 * st.d <= kXaKeys * 128 && st.heads <= kMaxHeads,
              "cross-attn: the cross-o slice must fit the K buffer");
-  static bool attr = false;
-  if (!attr) {
-    DM_CHECK_CUDA(cudaFuncSetAttribute(cross_attn_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kXaSmem));
-    attr = true;
-  }
+  DM_SMEM_ATTR(cross_attn_kernel, kXaSmem);
   DM_CHECK_CUDA(launch_pdl_cluster(cross_attn_kernel, dim3(kRows, st.heads, kXSplits),
                                    dim3(kXaThreads), dim3(1, 1, kXSplits), kXaSmem, stream,
                                    xkv_map, st, layer, xq, q_scale, wo_pack, part_o));

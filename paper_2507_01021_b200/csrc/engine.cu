@@ -23,6 +23,20 @@ static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 const char* last_error() { return g_err.c_str(); }
 
+cudaError_t set_max_smem(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> raised;   // (kernel, device) -> bytes
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  int& have = raised[std::make_pair(fn, dev)];
+  if (have >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+
 // forward decls (logmel.cu / attention.cu)
 struct LogmelTables;
 int launch_logmel(const int16_t*, const int64_t*, const int32_t*, int, int,
@@ -179,6 +193,7 @@ struct UploadRing {
 
 // ------------------------------------------------------------ Whisper engine
 struct WhisperEngine {
+  int device = 0;                      // the CUDA device of every buffer/stream below
   UploadRing ring;
   int32_t* admit_args_dev = nullptr;   // [2 * max_slots]
   dm_whisper_config cfg;
@@ -643,18 +658,21 @@ int dm_logmel(const int16_t* pcm, const int64_t* offsets, const int32_t* lengths
   const LogmelTables* tab = nullptr;
   if (int rc = get_logmel_tables(n_mels, &tab)) return rc;
   // per-segment max scratch: grown once, reused (no per-call allocation on the stream)
-  static uint32_t* segmax = nullptr;
-  static int segmax_n = 0;
+  // (one buffer per device: the caller's current device owns the stream)
+  static std::map<int, std::pair<uint32_t*, int>> scratch;
   static std::mutex mu;
+  int dev = 0;
+  DM_CHECK_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(mu);
-  if (segmax_n < n) {
+  auto& sc = scratch[dev];
+  if (sc.second < n) {
     DM_CHECK_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
-    if (segmax) cudaFree(segmax);
-    segmax = nullptr;
-    segmax_n = 0;
-    DM_CHECK_CUDA(cudaMalloc(reinterpret_cast<void**>(&segmax), sizeof(uint32_t) * n));
-    segmax_n = n;
+    if (sc.first) cudaFree(sc.first);
+    sc = {nullptr, 0};
+    DM_CHECK_CUDA(cudaMalloc(reinterpret_cast<void**>(&sc.first), sizeof(uint32_t) * n));
+    sc.second = n;
   }
+  uint32_t* segmax = sc.first;
   return launch_logmel(pcm, offsets, lengths, n, n_mels, tab, out, nullptr, segmax,
                        static_cast<cudaStream_t>(stream));
 }
@@ -674,6 +692,10 @@ int dm_whisper_create(const dm_whisper_config* cfg, const uint16_t* weights,
   DM_REQUIRE(n_offsets == expect, "offset table has " + std::to_string(n_offsets) +
                                       " entries, expected " + std::to_string(expect));
   auto* e = new WhisperEngine();
+  if (cudaGetDevice(&e->device) != cudaSuccess) {
+    delete e;
+    DM_CHECK_CUDA(cudaGetLastError());
+  }
   e->cfg = *cfg;
   e->w = weights;
   e->off.assign(offsets, offsets + n_offsets);
@@ -691,6 +713,8 @@ int dm_whisper_create(const dm_whisper_config* cfg, const uint16_t* weights,
 }
 
 int dm_whisper_destroy(void* handle) {
+  if (!handle) return 0;
+  DM_ON_DEVICE(static_cast<WhisperEngine*>(handle)->device);
   delete static_cast<WhisperEngine*>(handle);
   return 0;
 }
@@ -699,6 +723,7 @@ int dm_whisper_encode(void* handle, const int16_t* pcm, const int64_t* offsets,
                       const int32_t* lengths, int n, const int32_t* slot_ids, void* stream) {
   auto* e = static_cast<WhisperEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
+  DM_ON_DEVICE(e->device);
   DM_REQUIRE(n >= 1 && n <= e->E, "n must be in [1, max_encode_batch]");
   for (int i = 0; i < n; ++i)
     DM_REQUIRE(slot_ids[i] >= 0 && slot_ids[i] < e->cfg.max_slots, "slot id out of range");
@@ -727,6 +752,7 @@ int dm_whisper_admit(void* handle, const int32_t* slot_ids, const int32_t* caps,
                      void* stream) {
   auto* e = static_cast<WhisperEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
+  DM_ON_DEVICE(e->device);
   DM_REQUIRE(n >= 0 && n <= e->cfg.max_slots, "bad n");
   if (n == 0) return 0;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -771,6 +797,7 @@ int dm_whisper_admit(void* handle, const int32_t* slot_ids, const int32_t* caps,
 int dm_whisper_release(void* handle, const int32_t* slot_ids, int n) {
   auto* e = static_cast<WhisperEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
+  DM_ON_DEVICE(e->device);
   for (int i = 0; i < n; ++i) {
     const int slot = slot_ids[i];
     DM_REQUIRE(slot >= 0 && slot < e->cfg.max_slots, "slot id out of range");
@@ -784,6 +811,7 @@ int dm_whisper_release(void* handle, const int32_t* slot_ids, int n) {
 int dm_whisper_set_active(void* handle, const int32_t* slot_ids, int n, void* stream) {
   auto* e = static_cast<WhisperEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
+  DM_ON_DEVICE(e->device);
   DM_REQUIRE(n >= 0 && n <= e->cfg.max_slots, "bad n");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int G = int(e->groups.size());
@@ -810,6 +838,7 @@ int dm_whisper_set_active(void* handle, const int32_t* slot_ids, int n, void* st
 int dm_whisper_step(void* handle, int n_steps, void* stream) {
   auto* e = static_cast<WhisperEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
+  DM_ON_DEVICE(e->device);
   if (!e->step_exec)
     if (int rc = build_step_graph(e)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -832,6 +861,7 @@ int dm_whisper_step(void* handle, int n_steps, void* stream) {
 int dm_whisper_stats(void* handle, int64_t* out, int n) {
   auto* e = static_cast<WhisperEngine*>(handle);
   DM_REQUIRE(e != nullptr && out != nullptr && n >= 4, "need 4 outputs");
+  DM_ON_DEVICE(e->device);
   out[0] = e->launches; out[1] = e->steps; out[2] = e->encodes; out[3] = e->segments;
   return 0;
 }
@@ -840,20 +870,24 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
                            void* stream) {
   auto* e = static_cast<WhisperEngine*>(handle);
   DM_REQUIRE(e != nullptr && avg_ms != nullptr && iters >= 1, "bad arguments");
-  DM_REQUIRE(layer >= 0 && layer < e->Ld, "layer out of range");
+  DM_ON_DEVICE(e->device);
+  // layer < 0: launch i runs decoder layer i % Ld (every launch streams another
+  // layer's weights / cross-KV, as inside a step); else every launch runs `layer`
+  DM_REQUIRE(layer < e->Ld, "layer out of range");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // capture `iters` back-to-back launches in a graph so the timing sees the
   // GPU-side launch/complete latency, not host submission
   // probes run on decode group 0's state at its current active rows
   WhisperEngine::Group& grp = e->groups[0];
-  const int d = e->d, b0 = e->dec_layer_base(layer), pi = layer * 6;
+  const int d = e->d;
   auto gv = [&](int idx, float* part, uint16_t* yh, uint16_t* yl, const uint16_t* bias,
                 cudaStream_t cs) {
     GemvArgs g = e->plans[idx];
     g.bias = bias; g.part = part; g.yh = yh; g.yl = yl; g.counter_base = e->gemv_counter_base;
     return launch_gemv(grp.st, grp.maps[idx], g, cs);
   };
-  auto launch_one = [&](cudaStream_t cs) -> int {
+  auto launch_one = [&](int layer, cudaStream_t cs) -> int {
+    const int b0 = e->dec_layer_base(layer), pi = layer * 6;
     switch (which) {
       case 0:
         return launch_cross_attn(grp.st, e->xkv_map, layer,
@@ -880,7 +914,8 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
   };
   DM_CHECK_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
   int rc = 0;
-  for (int i = 0; i < iters && rc == 0; ++i) rc = launch_one(e->cap_stream);
+  for (int i = 0; i < iters && rc == 0; ++i)
+    rc = launch_one(layer < 0 ? i % e->Ld : layer, e->cap_stream);
   cudaGraph_t g = nullptr;
   cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &g);
   if (rc) {
@@ -913,6 +948,7 @@ int dm_whisper_read_async(void* handle, int32_t* done, int32_t* n_gen, int32_t* 
                           void* stream) {
   auto* e = static_cast<WhisperEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
+  DM_ON_DEVICE(e->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int S = e->cfg.max_slots;
   if (done) DM_CHECK_CUDA(cudaMemcpyAsync(done, e->st.done, sizeof(int32_t) * S, cudaMemcpyDeviceToHost, s));
@@ -932,6 +968,7 @@ int dm_whisper_read(void* handle, int32_t* done, int32_t* n_gen, int32_t* tokens
 int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void* stream) {
   auto* e = static_cast<WhisperEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
+  DM_ON_DEVICE(e->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const void* src = nullptr;
   size_t avail = 0;

@@ -766,12 +766,7 @@ static int launch_bn_mode(const GemmArgs& g, cudaStream_t stream) {
   geo.KB = ceil_div(g.K, kBK);
   geo.cpb = g.grouped ? 1 : (g.C > 0 ? g.C / kBK : 1);
   const int smem = GemmSmem<BN, STAGES, MODE>::kBytes;
-  static bool attr = false;
-  if (!attr) {
-    DM_CHECK_CUDA(cudaFuncSetAttribute(gemm_tcgen05_kernel<BN, STAGES, MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  DM_SMEM_ATTR((gemm_tcgen05_kernel<BN, STAGES, MODE>), smem);
   int grid = geo.tiles < kNumSMs ? geo.tiles : kNumSMs;
   gemm_tcgen05_kernel<BN, STAGES, MODE><<<grid, kGemmThreads, smem, stream>>>(ma, mb, mr, g, geo);
   DM_CHECK_LAUNCH();
@@ -813,12 +808,7 @@ static int launch_pair_mode(const GemmArgs& g, cudaStream_t stream) {
   geo.KB = ceil_div(g.K, kBK);
   geo.cpb = g.C > 0 ? g.C / kBK : 1;
   const int smem = PairSmem<STAGES>::kBytes;
-  static bool attr = false;
-  if (!attr) {
-    DM_CHECK_CUDA(cudaFuncSetAttribute(gemm_pair_kernel<STAGES, MODE>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  DM_SMEM_ATTR((gemm_pair_kernel<STAGES, MODE>), smem);
   const int pairs = std::min(geo.tiles, kNumSMs / 2);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);

@@ -329,14 +329,8 @@ int launch_logmel(const int16_t* pcm, const int64_t* offsets, const int32_t* len
   DM_REQUIRE(n_mels == 80 || n_mels == 128, "n_mels must be 80 or 128");
   DM_REQUIRE(n_segments >= 0, "n_segments < 0");
   if (n_segments == 0) return 0;
-  static bool attr_set = false;
   const size_t smem = logmel_smem_bytes();
-  if (!attr_set) {
-    DM_CHECK_CUDA(cudaFuncSetAttribute(logmel_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       int(smem)));
-    attr_set = true;
-  }
+  DM_SMEM_ATTR(logmel_kernel, int(smem));
   DM_CHECK_CUDA(cudaMemsetAsync(segmax, 0, sizeof(uint32_t) * n_segments, stream));
   dim3 grid(ceil_div(kFrames, kFPB), n_segments);
   logmel_kernel<<<grid, kLogmelThreads, smem, stream>>>(pcm, offsets, lengths, tables,

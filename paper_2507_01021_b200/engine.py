@@ -367,7 +367,7 @@ class WhisperGPU:
         that hit EOT early only linger one batch -- their attention is
         skipped). Returns {key: token ids}.
 
-        With overlap_encode (experimental), encodes run on
+        With overlap_encode, encodes run on
         enc_stream and a group is admitted (decode stream waits on its encode
         event) once the host sees its event complete -- or at once when
         nothing is decoding -- so the groups already admitted decode while the
@@ -381,6 +381,12 @@ class WhisperGPU:
         pending = deque(jobs)
         encoding: deque = deque()              # (event, [(slot, job)]) in flight on enc_stream
         free = list(range(self.max_slots - 1, -1, -1))
+        # Slots freed while the decode stream may still read their cross-KV
+        # (capped slots leave the active set after their last batch is queued;
+        # early-EOT slots are found one batch late): an encode on enc_stream
+        # into such a slot must first wait for the decode work queued so far
+        # (write-after-read on xkv[slot]). Clean slots are handed out first.
+        unfenced: set[int] = set()
         active: dict[int, SegmentJob] = {}
         left: dict[int, int] = {}              # slot -> steps to its cap
         waiting: list[tuple[int, SegmentJob]] = []   # finished, result in the next snapshot
@@ -407,10 +413,17 @@ class WhisperGPU:
                 # while the host still stages the rest of the PCM
                 lim = self.max_encode_batch if (active or waiting or prev or encoding) else min(
                     self.max_encode_batch, self.first_encode_batch)
+                if unfenced:
+                    free.sort(key=lambda s: (s not in unfenced, -s))   # pop() takes clean, low ids first
                 while free and pending and len(take) < lim:
                     take.append((free.pop(), pending.popleft()))
                 slots = [s for s, _ in take]
                 if overlap:
+                    if unfenced.intersection(slots):
+                        fence = torch.cuda.Event()
+                        fence.record(self.stream)         # after every batch issued so far
+                        self.enc_stream.wait_event(fence)
+                        unfenced.clear()
                     self.encode([j.samples for _, j in take], slots, self.enc_stream)
                     ev = torch.cuda.Event()
                     ev.record(self.enc_stream)
@@ -448,6 +461,7 @@ class WhisperGPU:
                 if capped:
                     self.release(capped)
                     free.extend(capped)
+                    unfenced.update(capped)
                     dirty = True
                 cur = (b, waiting, set(active))
                 waiting = []
@@ -466,6 +480,7 @@ class WhisperGPU:
                 if eot:
                     self.release(eot)
                     free.extend(eot)
+                    unfenced.update(eot)
                     dirty = True
             prev = cur
             if prev is None and not active and not pending and not encoding:

@@ -7,18 +7,18 @@ import bench
 from paper_2507_01021_b200.backend import B200Backend, B200BackendConfig
 from paper_2507_01021_b200.engine import WhisperGPU
 from paper_2507_01021_b200.models import get_model
-from paper_2507_01021_b200.multiplex import BatchingPolicy, SegmentQueue
 from paper_2507_01021_b200.types import make_segment
 
+rs = bench.reference_scheduler()
 segs = bench.make_workload(64, 0)
-eng = WhisperGPU(get_model("whisper-base"), max_slots=64, max_encode_batch=32)
-backend = B200Backend(B200BackendConfig(model="whisper-base"), engine=eng)
+eng = WhisperGPU(get_model(bench.MODEL), max_slots=64, max_encode_batch=64, first_encode_batch=24)
+backend = B200Backend(B200BackendConfig(model=bench.MODEL), engine=eng)
 
 def once():
-    q = SegmentQueue()
+    q = rs.SegmentQueue()
     for uid, x in segs:
         q.enqueue_segment(make_segment(uid, x, session_id=uid, endpoint_time=0.0), 0.0)
-    pol = BatchingPolicy(kind="dynamic", max_batch=64, max_wait_ms=200.0, target_audio_s=64 * 30.0)
+    pol = rs.BatchingPolicy(kind="continuous", min_batch=32, max_batch=64)
     batch = q.try_form_batch(pol, 0.0)
     return backend.transcribe_batch(batch)
 

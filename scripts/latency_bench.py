@@ -1,9 +1,10 @@
 #!/usr/bin/env python
 """Per-segment latency under concurrent users (BASELINE.json cfg3/cfg4):
 p50/p95 of endpoint -> delivery, multiplexed (GpuConsumer per GPU, continuous
-batching, shared SegmentQueue) vs the single-user sequential-batch baseline
-(the reference's SequentialJobRunner discipline, server.py:142-206: a session
-is transcribed as one job after it ends, chunked by max_batch).
+batching, the reference's own SegmentQueue) vs the single-user
+sequential-batch baseline run through the reference's own
+SequentialJobRunner (server.py:142-206: a session is transcribed as one job
+after it ends, chunked by max_batch) with B200Backend as its backend.
 
 Users speak in real time: speech spans U[2, 12] s of loadgen-style noise
 (uniform int16 in [-8000, 8000), loadgen.py:97-98) separated by U[0.5, 3] s
@@ -28,12 +29,21 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
+REF = ROOT / "baseline" / "_ref"
 
 from paper_2507_01021_b200.backend import B200Backend, B200BackendConfig  # noqa: E402
 from paper_2507_01021_b200.engine import WhisperGPU  # noqa: E402
-from paper_2507_01021_b200.models import default_token_cap, get_model  # noqa: E402
-from paper_2507_01021_b200.multiplex import BatchingPolicy, Multiplexer  # noqa: E402
-from paper_2507_01021_b200.types import batch_of, make_segment  # noqa: E402
+from paper_2507_01021_b200.models import get_model  # noqa: E402
+from paper_2507_01021_b200.multiplex import Multiplexer  # noqa: E402
+from paper_2507_01021_b200.types import make_segment  # noqa: E402
+
+
+def reference_modules():
+    if str(REF) not in sys.path:
+        sys.path.insert(0, str(REF))
+    import dictamux.scheduler as rs
+    import dictamux.server as rsv
+    return rs, rsv
 
 
 def percentile(xs, q):
@@ -55,14 +65,14 @@ def user_session(seed, uid, session_s):
     return segs
 
 
-def run_multiplexed(engines, users, policy):
+def run_multiplexed(engines, users, policy, rs):
     lock = threading.Lock()
     delivered = {}
 
     def router(r):
         with lock:
             delivered[r.segment_id] = (time.monotonic(), r)
-    mux = Multiplexer(engines, policy, router, poll_interval_ms=2.0)
+    mux = Multiplexer(engines, policy, rs.SegmentQueue(), router, poll_interval_ms=2.0)
     mux.start()
     t0 = time.monotonic() + 0.5
     endpoints = {}
@@ -94,21 +104,39 @@ def run_multiplexed(engines, users, policy):
             "consumer_segments": [c.segments_done for c in mux.consumers]}
 
 
-def run_sequential_single_user(engine, segs, max_batch, dims_name):
-    """One user alone, sequential-batch discipline: the session is one job
-    submitted at its end, transcribed in max_batch chunks (server.py:171-202)."""
-    be = B200Backend(B200BackendConfig(model=dims_name), engine=engine)
-    session_end = segs[-1][0]
+def run_sequential_reference(engines, segs, max_batch, dims_name):
+    """One user alone through the reference's SequentialJobRunner
+    (server.py:142-206) with B200Backend: the user speaks in real time, the
+    session is submitted as one job when it ends, and each segment's latency
+    is its delivery time minus its endpoint."""
+    rs, rsv = reference_modules()
+    be = B200Backend(B200BackendConfig(model=dims_name), engine=engines[0])
+    done, lock = {}, threading.Lock()
+
+    def route(r):
+        with lock:
+            done[r.segment_id] = (time.monotonic(), r.status)
+    runner = rsv.SequentialJobRunner(be, max_batch, route)
+    runner.start()
     t0 = time.monotonic()
-    job = [make_segment(f"seq:{k}", x) for k, (_, x) in enumerate(segs)]
-    lat = []
-    for i in range(0, len(job), max_batch):
-        chunk = job[i:i + max_batch]
-        be.transcribe_batch(batch_of(chunk))
-        done = time.monotonic() - t0
-        for k in range(i, i + len(chunk)):
-            lat.append((session_end - segs[k][0] + done) * 1000.0)
-    return {"segments": len(segs), "p50_ms": percentile(lat, 0.5), "p95_ms": percentile(lat, 0.95)}
+    job, endpoints = [], {}
+    for k, (end_s, x) in enumerate(segs):
+        now = time.monotonic()
+        if t0 + end_s > now:
+            time.sleep(t0 + end_s - now)
+        sid = f"seq:{k:04d}"
+        endpoints[sid] = time.monotonic()
+        job.append(make_segment(sid, x, session_id="seq", endpoint_time=endpoints[sid] * 1000.0))
+    runner.submit(job)
+    deadline = time.monotonic() + 600
+    while len(done) < len(job) and time.monotonic() < deadline:
+        time.sleep(0.005)
+    runner.shutdown()
+    lat = [(done[s][0] - endpoints[s]) * 1000.0 for s in endpoints if s in done]
+    return {"segments": len(segs), "delivered": len(done),
+            "errors": sum(1 for _, st in done.values() if st != "ok"),
+            "p50_ms": percentile(lat, 0.5), "p95_ms": percentile(lat, 0.95),
+            "runner": "dictamux.server.SequentialJobRunner (unmodified reference)"}
 
 
 def main():
@@ -138,10 +166,11 @@ def main():
     # warm-up (graph capture, first encodes)
     for eng in engines:
         eng.transcribe_ids([users["u000"][0][1]] * 2, [4, 4])
-    policy = BatchingPolicy(kind="continuous", min_batch=args.min_batch, max_batch=args.max_batch,
-                            starvation_flush_ms=args.starvation_ms)
-    mux = run_multiplexed(engines, users, policy)
-    seq = run_sequential_single_user(engines[0], users["u000"], args.max_batch, args.model)
+    rs, _ = reference_modules()
+    policy = rs.BatchingPolicy(kind="continuous", min_batch=args.min_batch, max_batch=args.max_batch,
+                               starvation_flush_ms=args.starvation_ms)
+    mux = run_multiplexed(engines, users, policy, rs)
+    seq = run_sequential_reference(engines, users["u000"], args.max_batch, args.model)
     out = {"metric": "p50/p95 per-segment latency (endpoint -> delivery)", "unit": "ms",
            "model": args.model, "users": args.users, "session_s": args.session_s,
            "gpus": args.gpus, "policy": vars(policy), "engine_init_s": round(init_s, 1),

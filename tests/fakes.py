@@ -1,5 +1,6 @@
 """Host-side test doubles (no GPU): a FakeEngine with WhisperGPU.run_jobs
-semantics (slot-limited continuous batching, a job finishes after `cap`
+semantics (slot-limited continuous batching, slots keep their pages after a
+failure until reset(), a job finishes after `cap`
 steps, tokens derived from the audio bytes so identical audio -> identical
 ids regardless of batch mates)."""
 
@@ -20,6 +21,7 @@ class FakeEngine:
         self.step_s = step_s
         self.admitted = []
         self.resets = 0
+        self.held = set()          # slots holding self-KV pages, like WhisperGPU
         self.max_active = 0
         self.lock = threading.Lock()
 
@@ -30,6 +32,8 @@ class FakeEngine:
 
     def run_jobs(self, jobs, refill=None):
         import time
+        if self.held:      # the real engine refuses to admit into a slot that kept its pages
+            raise RuntimeError("slot already holds pages (release it first)")
         pending = deque(jobs)
         active = {}
         results = {}
@@ -42,6 +46,7 @@ class FakeEngine:
                 if j.key in self.fail_on:
                     raise RuntimeError(f"injected failure on {j.key}")
                 active[j.key] = [j, 0]
+                self.held.add(j.key)
                 self.admitted.append(j.key)
             self.max_active = max(self.max_active, len(active))
             if not active:
@@ -53,6 +58,7 @@ class FakeEngine:
                 j, n = active[key]
                 if n >= j.cap:
                     del active[key]
+                    self.held.discard(key)
                     ids = self.ids_for(j.samples, j.cap)
                     results[key] = ids
                     if j.on_done:
@@ -61,6 +67,7 @@ class FakeEngine:
 
     def reset(self):
         self.resets += 1
+        self.held.clear()
 
     def close(self):
         pass

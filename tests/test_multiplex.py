@@ -1,6 +1,7 @@
-"""Queue semantics mirrored from the reference (pkg/tests/test_scheduler.py)
-and the per-GPU continuous-batching consumers (conservation, iteration-level
-admission, failure isolation) with fake engines on the host."""
+"""The per-GPU continuous-batching consumers (conservation, iteration-level
+admission, failure isolation, multi-engine sharding) on the reference's OWN
+SegmentQueue / BatchingPolicy (pkg/src/dictamux/scheduler.py, installed in
+baseline/_ref), with fake engines on the host."""
 
 from __future__ import annotations
 
@@ -12,53 +13,24 @@ from collections import Counter
 import numpy as np
 import pytest
 
+import refdmx
 from fakes import FakeEngine
-from paper_2507_01021_b200.multiplex import (CONTINUOUS, DYNAMIC, BatchingPolicy,
-                                             DuplicateSegmentError, GpuConsumer, Multiplexer,
-                                             QueueClosedError, SegmentQueue)
-from paper_2507_01021_b200.types import make_segment
+from paper_2507_01021_b200.multiplex import GpuConsumer, Multiplexer
+
+pytestmark = pytest.mark.skipif(not refdmx.AVAILABLE, reason="reference not installed in baseline/_ref")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _ref():
+    global rb, rs, rv
+    rb, rs, rv = refdmx.load()
 
 
 def seg(sid, dur=1.0, session="s", val=None):
     n = int(dur * 16000)
     rng = np.random.default_rng(abs(hash(sid)) % (2 ** 32))
     x = rng.integers(-8000, 8000, size=n, dtype=np.int16) if val is None else np.full(n, val, np.int16)
-    return make_segment(sid, x, session_id=session)
-
-
-def test_fifo_tiebreak_duplicates_closed():
-    q = SegmentQueue()
-    q.enqueue_segment(seg("b"), 5.0)
-    q.enqueue_segment(seg("a"), 5.0)
-    q.enqueue_segment(seg("c"), 1.0)
-    b = q.force_batch(BatchingPolicy(max_batch=8, target_audio_s=1e9), 10.0)
-    assert [e.segment.segment_id for e in b.entries] == ["c", "a", "b"]
-    with pytest.raises(DuplicateSegmentError):
-        q.enqueue_segment(seg("a"), 11.0)
-    q.close()
-    with pytest.raises(QueueClosedError):
-        q.enqueue_segment(seg("z"), 12.0)
-
-
-def test_dynamic_and_continuous_triggers():
-    q = SegmentQueue()
-    dyn = BatchingPolicy(kind=DYNAMIC, max_batch=3, max_wait_ms=100.0, target_audio_s=10.0)
-    q.enqueue_segment(seg("a", 2.0), 0.0)
-    assert q.try_form_batch(dyn, 50.0) is None
-    assert q.try_form_batch(dyn, 100.0) is not None           # wait trigger
-    for i in range(3):
-        q.enqueue_segment(seg(f"d{i}", 1.0), 200.0)
-    b = q.try_form_batch(dyn, 200.0)                          # depth trigger
-    assert b is not None and len(b.entries) == 3
-    cont = BatchingPolicy(kind=CONTINUOUS, max_batch=4, min_batch=2, starvation_flush_ms=500.0)
-    q.enqueue_segment(seg("x"), 300.0)
-    assert q.try_form_batch(cont, 301.0) is None
-    assert q.try_form_batch(cont, 800.0) is not None           # starvation flush
-    # dynamic cut at target audio
-    for i in range(4):
-        q.enqueue_segment(seg(f"t{i}", 4.0), 900.0)
-    b = q.force_batch(BatchingPolicy(kind=DYNAMIC, max_batch=8, target_audio_s=10.0), 901.0)
-    assert len(b.entries) == 2
+    return refdmx.ref_segment(rv, sid, x, session=session)
 
 
 def run_mux(n_gpus, segs, engines_kw=None, policy=None):
@@ -69,8 +41,8 @@ def run_mux(n_gpus, segs, engines_kw=None, policy=None):
         with lock:
             routed.append(r)
     engines = [FakeEngine(**(engines_kw or {})) for _ in range(n_gpus)]
-    mux = Multiplexer(engines, policy or BatchingPolicy(kind=CONTINUOUS, max_batch=4, min_batch=1),
-                      router, cap_fn=lambda d: max(1, int(d * 3)), poll_interval_ms=1.0)
+    mux = Multiplexer(engines, policy or rs.BatchingPolicy(kind="continuous", max_batch=4, min_batch=1),
+                      rs.SegmentQueue(), router, cap_fn=lambda d: max(1, int(d * 3)), poll_interval_ms=1.0)
     mux.start()
     for i, s in enumerate(segs):
         mux.queue.enqueue_segment(s, time.monotonic() * 1000.0)
@@ -96,7 +68,7 @@ def test_conservation_every_segment_routed_once(n_gpus):
 
 def test_identical_audio_identical_text_across_gpus():
     base = seg("orig", 1.0)
-    twins = [make_segment(f"twin{i}", base.samples.copy(), session_id="t") for i in range(8)]
+    twins = [refdmx.ref_segment(rv, f"twin{i}", base.samples.copy(), session="t") for i in range(8)]
     routed, _, _ = run_mux(2, twins, {"max_slots": 2})
     assert len({r.text for r in routed}) == 1
 
@@ -131,3 +103,44 @@ def test_iteration_level_admission_refills_free_slots():
     assert engines[0].admitted[0] == "long"
     assert order.index("long") >= 3          # shorts entered freed slots while it decoded
     assert engines[0].max_active == 2
+
+
+def test_failed_run_resets_engine_before_next_batch():
+    """A failure mid-run leaves slots holding pages; the consumer resets the
+    engine, so the NEXT batch is served (not wedged into error rows)."""
+    routed, lock = [], threading.Lock()
+
+    def router(r):
+        with lock:
+            routed.append(r)
+    eng = FakeEngine(max_slots=2, fail_on={"bad"})
+    q = rs.SegmentQueue()
+    c = GpuConsumer(q, rs.BatchingPolicy(kind="continuous", max_batch=2, min_batch=1), eng,
+                    router, cap_fn=lambda d: 2, poll_interval_ms=1.0)
+    c.start()
+    q.enqueue_segment(seg("ok0", 0.5), 0.0)
+    q.enqueue_segment(seg("bad", 0.5), 0.0)
+    t0 = time.time()
+    while len(routed) < 2 and time.time() - t0 < 10:
+        time.sleep(0.005)
+    for i in range(3):
+        q.enqueue_segment(seg(f"w{i}", 0.5), 1.0)
+    while len(routed) < 5 and time.time() - t0 < 10:
+        time.sleep(0.005)
+    c.shutdown()
+    by = {r.segment_id: r.status for r in routed}
+    assert by["bad"] == "error"
+    assert [by[f"w{i}"] for i in range(3)] == ["ok"] * 3
+    assert eng.resets >= 1 and not eng.held
+
+
+def test_refill_policy_keeps_reference_policy_fields():
+    """The refill policy is the reference's own dataclass turned continuous
+    (min_batch 1, max_batch = free slots), other fields preserved."""
+    q = rs.SegmentQueue()
+    pol = rs.BatchingPolicy(kind="dynamic", max_batch=8, max_wait_ms=50.0, target_audio_s=3.0)
+    c = GpuConsumer(q, pol, FakeEngine(), lambda r: None, cap_fn=lambda d: 1)
+    for i in range(5):
+        q.enqueue_segment(seg(f"p{i}", 2.0), 0.0)
+    jobs = c._refill(4)         # continuous: no target_audio cut at 3 s
+    assert len(jobs) == 4
