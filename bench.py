@@ -61,6 +61,7 @@ METRIC = "audio-seconds transcribed/sec (RTFx)"
 UNIT = "audio_s/s"
 MODEL = "whisper-large-v3"
 REF = ROOT / "baseline" / "_ref"
+FP32_PEAK_TFLOPS = 74.4            # 148 SMs x 128 FP32 lanes x 2 (FMA) x 1.965 GHz
 
 
 # ---------------------------------------------------------------- workload
@@ -462,18 +463,25 @@ def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
             out.append(a.elapsed_time(b))
         return statistics.median(out)
 
-    # log-mel (K1)
+    # log-mel (K1) as the encoder consumes it: the bf16 time-major operand
     nm = dims.n_mels
     offs_d = torch.tensor([o for _, _, o in sub], dtype=torch.int64, device=dev)
     lens_d = torch.tensor([len(x) for _, x, _ in sub], dtype=torch.int32, device=dev)
-    mel = torch.empty(E, nm, 3000, dtype=torch.float32, device=dev)
-    lm = lambda: _native.check(eng.lib.dm_logmel(C.c_void_p(pcm_dev.data_ptr()),
-                                                C.c_void_p(offs_d.data_ptr()),
-                                                C.c_void_p(lens_d.data_ptr()), E, nm,
-                                                C.c_void_p(mel.data_ptr()), eng._s))
+    ldt = 64 if nm <= 64 else 128
+    mel = torch.zeros(E, 3002, ldt, dtype=torch.int16, device=dev)
+    segmax = torch.empty(E, dtype=torch.int32, device=dev)
+    lm = lambda: _native.check(eng.lib.dm_logmel_operand(
+        C.c_void_p(pcm_dev.data_ptr()), C.c_void_p(offs_d.data_ptr()),
+        C.c_void_p(lens_d.data_ptr()), E, nm, C.c_void_p(mel.data_ptr()),
+        C.c_void_p(segmax.data_ptr()), eng._s))
     lm()
     lm_ms = ev_ms(lm)
-    lm_bytes = sum(2 * min(len(x), 480000) for _, x, _ in sub) + E * nm * 3000 * 4
+    lm_bytes = sum(2 * min(len(x), 480000) for _, x, _ in sub) + E * nm * 3000 * 2
+    # FP32 work of the frames that are not wholly padding: the 200-point complex
+    # FFT (8 x 25: 25 8-point + 8 25-point DFTs, 400 twiddle products), window,
+    # real-FFT post-processing + power, the sparse mel dot products, log10
+    live_frames = sum(min(3000, (min(len(x), 480000) + 200 + 159) // 160) for _, x, _ in sub)
+    lm_flop = live_frames * 18_000
     # encoder (K2-K5)
     d, L, Ld, F = dims.d_model, dims.enc_layers, dims.dec_layers, dims.ffn
     enc_flop = (2 * nm * 3 * d * 3000 + 2 * 3 * d * d * 1500
@@ -505,7 +513,13 @@ def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
     return {
         "logmel": {"bound": "hbm", "achieved": lm_bytes / (lm_ms / 1e3) / 1e9, "peak": hbm,
                    "unit": "GB/s", "frac": lm_bytes / (lm_ms / 1e3) / 1e9 / hbm,
-                   "ms": lm_ms, "bytes": lm_bytes, "segments": E},
+                   "ms": lm_ms, "bytes": lm_bytes, "segments": E,
+                   "bytes_note": "2 n int16 PCM read + the bf16 [3000, n_mels] encoder operand "
+                                 "written (dm_logmel_operand, the product path)",
+                   "fp32_tflops": lm_flop / (lm_ms / 1e3) / 1e12,
+                   "fp32_frac": lm_flop / (lm_ms / 1e3) / 1e12 / FP32_PEAK_TFLOPS,
+                   "fp32_note": f"~18 kFLOP per non-padding frame ({live_frames} frames) vs "
+                                f"{FP32_PEAK_TFLOPS} TFLOP/s FP32 FMA peak (148 SMs x 128 x 2 x 1.965 GHz)"},
         "encoder": {"bound": "tensor", "achieved": E * enc_flop / (en_ms / 1e3) / 1e12, "peak": tc,
                     "unit": "TFLOP/s", "frac": E * enc_flop / (en_ms / 1e3) / 1e12 / tc,
                     "ms": en_ms, "flop": E * enc_flop, "segments": E,

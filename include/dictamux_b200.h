@@ -62,6 +62,13 @@ DM_API int dm_fill_normal_bf16(uint16_t* dst, uint64_t numel, uint64_t key, floa
  * out: [n, n_mels, 3000] fp32 = Whisper input_features. n_mels in {80,128}. */
 DM_API int dm_logmel(const int16_t* pcm, const int64_t* offsets, const int32_t* lengths, int n,
               int n_mels, float* out, void* stream);
+/* The same features as the encoder consumes them (the engine's product path):
+ * out: [n, 3002, ldt] bf16 time-major (ldt = 64 if n_mels <= 64 else 128),
+ * rows 1..3000 = bf16((max(x, max_seg - 8) + 4) / 4), bit for bit the
+ * rounding of dm_logmel's values; rows 0 and 3001 and channels >= n_mels are
+ * not written (the caller zeroes them once). segmax: [n] uint32 scratch. */
+DM_API int dm_logmel_operand(const int16_t* pcm, const int64_t* offsets, const int32_t* lengths,
+                             int n, int n_mels, uint16_t* out, uint32_t* segmax, void* stream);
 
 /* Test hook for the tcgen05 GEMM: out[M, N] fp32 = A[M, K] . W[N, K]^T (+ bias). */
 DM_API int dm_gemm_bf16_f32(const uint16_t* A, const uint16_t* W, const uint16_t* bias, float* out,
@@ -125,7 +132,11 @@ DM_API int dm_whisper_read_async(void* handle, int32_t* done, int32_t* n_gen, in
  *  which = 4: run only the first `bytes` encoder layers in later encodes
  *  which = 5: fp32 residual stream before the final LN, [n, 1500, d]
  *  which = 6: attention output of the last encoder layer run, [n, 1500, d] bf16
- *  which = 7: (bytes != 0) keep the fp32 encoder output; read it with which = 5 */
+ *  which = 7: (bytes != 0) keep the fp32 encoder output; read it with which = 5
+ *  which = 15: (bytes != 0) also write the fp32 features of later encodes (read with which = 1)
+ *  which = 14: cross-attention kernel of later steps (bytes = 0: by active rows,
+ *              1: always the cluster kernel, 2: always the streaming kernel;
+ *              both compute the same values bit for bit) */
 DM_API int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void* stream);
 
 /* ------------------------------------------------------------ CTC engine (cfg5)
@@ -159,7 +170,8 @@ DM_API int dm_whisper_stats(void* handle, int64_t* out, int n);
  * `stream` (a probe: it may overwrite row-space activations): which =
  * 0 cross-attention(layer), 1 self-attention(layer), 2 LM head, 3 decoder LN
  * (+ residual partials), 4 cross-q projection, 5 fc2 projection,
- * 6 empty PDL kernel (launch floor), 7 fc1 projection (+GELU), 8 qkv projection.
+ * 6 empty PDL kernel (launch floor), 7 fc1 projection (+GELU), 8 qkv projection,
+ * 9 streaming cross-attention (+ cross-o).
  * avg_ms = mean over iters back-to-back launches. layer < 0: launch i runs
  * decoder layer i % dec_layers (each launch streams a different layer's
  * cross-KV / weights, as inside a decode step). */

@@ -14,7 +14,7 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libdictamux_b200.so"
 
 EXPORTS = (
-    "dm_last_error", "dm_version", "dm_fill_normal_bf16", "dm_logmel",
+    "dm_last_error", "dm_version", "dm_fill_normal_bf16", "dm_logmel", "dm_logmel_operand",
     "dm_gemm_bf16_f32", "dm_whisper_create", "dm_whisper_destroy",
     "dm_whisper_encode", "dm_whisper_admit", "dm_whisper_release",
     "dm_whisper_set_active", "dm_whisper_step", "dm_whisper_read", "dm_whisper_read_async",
@@ -68,6 +68,7 @@ def load(build_if_missing: bool = False):
         sig = {
             "dm_fill_normal_bf16": [P, C.c_uint64, C.c_uint64, C.c_float, C.c_float, P],
             "dm_logmel": [P, P, P, C.c_int, C.c_int, P, P],
+            "dm_logmel_operand": [P, P, P, C.c_int, C.c_int, P, P, P],
             "dm_gemm_bf16_f32": [P, P, P, P, C.c_int, C.c_int, C.c_int, P],
             "dm_whisper_create": [C.POINTER(WhisperConfigC), P, P, C.c_int,
                                   C.POINTER(C.c_void_p)],

@@ -1119,6 +1119,279 @@ int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int lay
   return 0;
 }
 
+// ------------------------------------------------------------ streaming cross-attention
+// The same arithmetic as cross_attn_kernel (bit for bit: every per-split
+// reduction, the split merge and the cross-o tail run in the same order), laid
+// out for many active rows: a persistent grid (2 CTAs per SM) pulls
+// (row, head) items from a global ticket counter; per CTA a producer warp
+// streams each item's 8 split K/V blocks (48 KB each) and then its cross-o
+// weight slice through a ring of kXsStages 48 KB stages while 6 consumer
+// warps compute split after split -- no cluster, no per-CTA prologue per
+// split, and the K/V stream never waits for a split's softmax / merge / tail.
+// The step graph uses it when the active rows give at least kXsMinItems
+// (row, head) items (the cluster kernel keeps low-row latency).
+constexpr int kXsStages = 2;
+constexpr int kXsStageBytes = 2 * kXaKeys * 128;                 // K + V of one split
+constexpr int kXsConsumers = kXaThreads;                         // 6 warps, one key per thread
+constexpr int kXsThreads = kXsConsumers + 32;                    // + producer warp
+constexpr int kXsSmem = 1024 + kXsStages * kXsStageBytes + 256;  // (align) ring + barriers
+constexpr int kXsCtasPerSm = 2;
+
+__device__ __forceinline__ int xs_wo_splits_per_stage(int d) {
+  int ws = kXSplits;
+  while (ws > 1 && ws * 16 * d > kXsStageBytes) ws >>= 1;
+  return ws;
+}
+
+__global__ void __launch_bounds__(kXsThreads, kXsCtasPerSm)
+cross_attn_stream_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, int layer,
+                         const Partials xq, float q_scale, const uint16_t* __restrict__ wo_pack,
+                         float* __restrict__ part_o, int* __restrict__ ctr) {
+  extern __shared__ uint8_t xs_raw[];
+  uint8_t* ring = xs_raw + ((1024 - (smem_u32(xs_raw) & 1023)) & 1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kXsStages * kXsStageBytes);
+  uint64_t* empty = full + kXsStages;
+  int* stage_item = reinterpret_cast<int*>(empty + kXsStages);   // [kXsStages]
+  __shared__ __align__(16) float qs[64];
+  __shared__ __align__(16) float oh[64];
+  __shared__ __align__(16) float os[kXSplits][kXaPush];          // per-split (o[64], max, sum)
+  __shared__ float sc[kXaKeys], redm[8], reds[8];
+  __shared__ __align__(16) float op[kXsConsumers / 32][64];
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int d = st.d, H = st.heads, d8 = d / 8;
+  const int ws = xs_wo_splits_per_stage(d), wchunks = kXSplits / ws;
+  if (tid == 0) {
+    trace_mark(st, 0);
+    for (int i = 0; i < kXsStages; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 1);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int items = *st.n_active * H;            // host-set before the graph runs
+  if (warp == kXsConsumers / 32) {
+    // ---------------- producer (one lane): tickets -> TMA into the ring
+    if (lane == 0) {
+      tma_prefetch_desc(&tm);
+      const uint64_t stream = l2_policy_evict_first();
+      int stage = 0;
+      uint32_t ph = 0;
+      auto next_stage = [&](int item) {
+        mbar_wait(empty + stage, ph ^ 1);
+        stage_item[stage] = item;
+      };
+      auto advance = [&]() {
+        if (++stage == kXsStages) { stage = 0; ph ^= 1; }
+      };
+      for (;;) {
+        const int item = atomicAdd(ctr, 1);
+        if (item >= items) {
+          next_stage(-1);                          // end marker for the consumers
+          mbar_arrive(full + stage);
+          break;
+        }
+        const int r = item / H, h = item % H;
+        const int slot = st.active[r];
+        const int row_k0 = (((layer * st.max_slots + slot) * 2 + 0) * H + h) * 1500;
+        for (int sp = 0; sp < kXSplits; ++sp) {
+          next_stage(item);
+          uint8_t* Ks = ring + stage * kXsStageBytes;
+          const int row_k = row_k0 + sp * kXaKeys, row_v = row_k + H * 1500;
+          mbar_arrive_expect_tx(full + stage, kXsStageBytes);
+#pragma unroll
+          for (int bx = 0; bx < 3; ++bx)
+            tma_load_2d_hint(Ks + bx * 64 * 128, &tm, full + stage, 0, row_k + bx * 64, stream);
+#pragma unroll
+          for (int bx = 0; bx < 3; ++bx)
+            tma_load_2d_hint(Ks + kXaKeys * 128 + bx * 64 * 128, &tm, full + stage, 0,
+                             row_v + bx * 64, stream);
+          advance();
+        }
+        for (int c = 0; c < wchunks; ++c) {
+          next_stage(item);
+          mbar_arrive_expect_tx(full + stage, ws * 16 * d);
+          bulk_load(ring + stage * kXsStageBytes,
+                    wo_pack + size_t(h * kXSplits + c * ws) * d8 * 64, ws * 16 * d, full + stage);
+          advance();
+        }
+      }
+      // every ticket of this launch is taken once all CTAs got an out-of-range
+      // one: the last CTA resets the counter for the next launch of the layer
+      __threadfence();
+      if (atomicAdd(ctr + 1, 1) == int(gridDim.x) - 1) {
+        atomicExch(ctr + 1, 0);
+        atomicExch(ctr, 0);
+      }
+    }
+    __syncwarp();
+    pdl_trigger();
+    return;
+  }
+  // ---------------- consumers (6 warps)
+  pdl_wait();
+  if (tid == 0) trace_mark(st, 1);
+  int stage = 0;
+  uint32_t ph = 0;
+  auto advance = [&]() {
+    if (++stage == kXsStages) { stage = 0; ph ^= 1; }
+  };
+  for (;;) {
+    mbar_wait(full + stage, ph);
+    const int item = stage_item[stage];
+    if (item < 0) break;
+    const int r = item / H, h = item % H;
+    if (tid < 64) {
+      const float* pp = xq.p + size_t(r) * xq.n + h * 64 + tid;
+      const float a = sum_splits(pp, size_t(kRows) * xq.n, xq.splits);
+      qs[tid] = (a + bf16_to_f32(xq.bias[h * 64 + tid])) * q_scale;
+    }
+    named_bar_sync(1, kXsConsumers);
+    float q[64];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const float4 v = *reinterpret_cast<const float4*>(qs + 4 * j);
+      q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
+    }
+    for (int sp = 0; sp < kXSplits; ++sp) {
+      if (sp) mbar_wait(full + stage, ph);
+      const uint8_t* Ks = ring + stage * kXsStageBytes;
+      const uint8_t* Vs = Ks + kXaKeys * 128;
+      const int k0 = sp * kXaKeys, nk = min(1500, k0 + kXaKeys) - k0;
+      float mloc = -INFINITY;
+      if (tid < nk) {
+        const uint8_t* kr = Ks + (tid >> 6) * 64 * 128 + (tid & 63) * 128;
+        const int sw = tid & 7;
+        float s = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint4 w = *reinterpret_cast<const uint4*>(kr + ((j ^ sw) << 4));
+          s = fmaf(q[8 * j + 0], __uint_as_float(w.x << 16), s);
+          s = fmaf(q[8 * j + 1], __uint_as_float(w.x & 0xFFFF0000u), s);
+          s = fmaf(q[8 * j + 2], __uint_as_float(w.y << 16), s);
+          s = fmaf(q[8 * j + 3], __uint_as_float(w.y & 0xFFFF0000u), s);
+          s = fmaf(q[8 * j + 4], __uint_as_float(w.z << 16), s);
+          s = fmaf(q[8 * j + 5], __uint_as_float(w.z & 0xFFFF0000u), s);
+          s = fmaf(q[8 * j + 6], __uint_as_float(w.w << 16), s);
+          s = fmaf(q[8 * j + 7], __uint_as_float(w.w & 0xFFFF0000u), s);
+        }
+        sc[tid] = s;
+        mloc = s;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
+      if (lane == 0) redm[warp] = mloc;
+      named_bar_sync(1, kXsConsumers);
+      float m = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < kXsConsumers / 32; ++w) m = fmaxf(m, redm[w]);
+      float e = 0.f;
+      if (tid < nk) {
+        e = exp2f((sc[tid] - m) * kLog2e);
+        sc[tid] = e;
+      }
+      float es = e;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+      if (lane == 0) reds[warp] = es;
+      named_bar_sync(1, kXsConsumers);
+      float l = 0.f;
+#pragma unroll
+      for (int w = 0; w < kXsConsumers / 32; ++w) l += reds[w];
+      float o0 = 0.f, o1 = 0.f;
+      const int vch = lane >> 2, vwo = (lane & 3) * 4;
+#pragma unroll 4
+      for (int t = warp; t < nk; t += kXsConsumers / 32) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(
+            Vs + (t >> 6) * 64 * 128 + (t & 63) * 128 + ((vch ^ (t & 7)) << 4) + vwo);
+        const float pe = sc[t];
+        o0 = fmaf(pe, __uint_as_float(w << 16), o0);
+        o1 = fmaf(pe, __uint_as_float(w & 0xFFFF0000u), o1);
+      }
+      op[warp][2 * lane] = o0;
+      op[warp][2 * lane + 1] = o1;
+      named_bar_sync(1, kXsConsumers);           // every K/V read of the stage is done
+      if (tid == 0) mbar_arrive(empty + stage);
+      advance();
+      if (tid < 16) {
+        // the cluster kernel's push: float4 chunk sums over the warps in order
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int w = 0; w < kXsConsumers / 32; ++w) {
+          const float4 v = *reinterpret_cast<const float4*>(&op[w][4 * tid]);
+          a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+        }
+        *reinterpret_cast<float4*>(&os[sp][4 * tid]) = a;
+      } else if (tid == 16) {
+        os[sp][64] = m;
+        os[sp][65] = l;
+      }
+    }
+    named_bar_sync(1, kXsConsumers);
+    if (tid < 64) {
+      float M = -INFINITY;
+#pragma unroll
+      for (int s = 0; s < kXSplits; ++s) M = fmaxf(M, os[s][64]);
+      float Ls = 0.f, O = 0.f;
+#pragma unroll
+      for (int s = 0; s < kXSplits; ++s) {
+        const float f = exp2f((os[s][64] - M) * kLog2e);
+        Ls += os[s][65] * f;
+        O += os[s][tid] * f;
+      }
+      oh[tid] = O / Ls;
+    }
+    named_bar_sync(1, kXsConsumers);
+    const int ch = tid & 7;
+    float ov[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ov[j] = oh[ch * 8 + j];
+    for (int c = 0; c < wchunks; ++c) {
+      mbar_wait(full + stage, ph);
+      const uint16_t* Wc = reinterpret_cast<const uint16_t*>(ring + stage * kXsStageBytes);
+      for (int si = 0; si < ws; ++si) {
+        const int sp = c * ws + si;
+        const uint16_t* Wo = Wc + size_t(si) * d8 * 64;
+        float* dst = part_o + (size_t(h) * kRows + r) * d + sp * d8;
+        for (int n = tid >> 3; n < d8; n += kXsConsumers / 8) {
+          const uint4 w = *reinterpret_cast<const uint4*>(Wo + n * 64 + ch * 8);
+          float acc = ov[0] * __uint_as_float(w.x << 16);
+          acc = fmaf(ov[1], __uint_as_float(w.x & 0xFFFF0000u), acc);
+          acc = fmaf(ov[2], __uint_as_float(w.y << 16), acc);
+          acc = fmaf(ov[3], __uint_as_float(w.y & 0xFFFF0000u), acc);
+          acc = fmaf(ov[4], __uint_as_float(w.z << 16), acc);
+          acc = fmaf(ov[5], __uint_as_float(w.z & 0xFFFF0000u), acc);
+          acc = fmaf(ov[6], __uint_as_float(w.w << 16), acc);
+          acc = fmaf(ov[7], __uint_as_float(w.w & 0xFFFF0000u), acc);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+          acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+          if (ch == 0) dst[n] = acc;
+        }
+      }
+      named_bar_sync(1, kXsConsumers);
+      if (tid == 0) mbar_arrive(empty + stage);
+      advance();
+    }
+  }
+  if (tid == 0) trace_mark(st, 3);
+}
+
+int launch_cross_attn_stream(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
+                             const Partials& xq, float q_scale, const uint16_t* wo_pack,
+                             float* part_o, int* ctr, cudaStream_t stream) {
+  DM_REQUIRE(xq.p != nullptr && xq.n == st.d && xq.bias != nullptr && xq.splits >= 1 &&
+                 xq.splits <= kMaxSplits, "cross-attn: q partials");
+  DM_REQUIRE(wo_pack != nullptr && part_o != nullptr && ctr != nullptr, "cross-attn: operands");
+  DM_REQUIRE(st.d % 64 == 0 && 16 * st.d <= kXsStageBytes && st.heads <= kMaxHeads,
+             "cross-attn: shapes");
+  DM_SMEM_ATTR(cross_attn_stream_kernel, kXsSmem);
+  DM_CHECK_CUDA(launch_pdl(cross_attn_stream_kernel, dim3(kNumSMs * kXsCtasPerSm),
+                           dim3(kXsThreads), kXsSmem, stream, xkv_map, st, layer, xq, q_scale,
+                           wo_pack, part_o, ctr));
+  return 0;
+}
+
 __global__ void repack_xo_kernel(const uint16_t* __restrict__ wo, uint16_t* __restrict__ out, int d) {
   // wo [d, d] ([out, in]) -> out [H][8][d/8][64]: the (head h, split s) slice =
   // output features s*d/8 .. +d/8 x input dims h*64 .. +64, contiguous

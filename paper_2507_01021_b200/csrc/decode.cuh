@@ -67,12 +67,14 @@ struct DecodeState {
   float* amax_val;             // [vocab tiles, kRows]
   int32_t* amax_idx;           // [vocab tiles, kRows]
   float* logits_dbg;           // optional [kRows, vocab]
-  // optional timeline tap (debug): per kernel of the step [128][8] globaltimer ns:
+  // optional timeline tap (debug): per kernel of the step [kTraceSlots][8] globaltimer ns:
   // min CTA entry, min / max dependency release (after griddepcontrol.wait), max exit,
   // then kernel-specific max stamps 4..7 (GEMV: operand landed, MMA done, stores issued)
   unsigned long long* trace;
   int trace_id;
 };
+
+constexpr int kTraceSlots = 512;   // timeline tap: kernels per step (32 layers x 10 + 3 fits)
 
 __device__ __forceinline__ unsigned long long global_ns() {
   unsigned long long t;
@@ -159,6 +161,14 @@ constexpr int kMaxHeads = 20;   // per-head partial splits a LayerNorm may reduc
 int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
                       const Partials& xq, float q_scale, const uint16_t* wo_pack, float* part_o,
                       cudaStream_t stream);
+// The same computation for many active rows: persistent CTAs pull (row, head)
+// items from ctr[0] (ctr[1] counts finished CTAs; both reset by the last CTA,
+// so each layer needs its own zero-initialised pair) and stream K/V and the
+// cross-o slice through a TMA ring. Bitwise equal to launch_cross_attn.
+constexpr int kXsMinItems = 2 * 148;   // default: stream when rows x heads >= this
+int launch_cross_attn_stream(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
+                             const Partials& xq, float q_scale, const uint16_t* wo_pack,
+                             float* part_o, int* ctr, cudaStream_t stream);
 // [d, d] cross-o weight -> the per-(head, split) contiguous slices the cross-attention loads
 int repack_xo(const uint16_t* wo, uint16_t* out, int d, int H, cudaStream_t stream);
 int launch_finalize(const DecodeState& st, cudaStream_t stream);

@@ -225,6 +225,7 @@ struct WhisperEngine {
   int last_n = 0;
   int enc_stop = 1 << 30;        // debug: run only the first enc_stop layers
   bool enc_tap = false;          // debug: keep the fp32 encoder output (in resid)
+  bool mel_tap = false;          // debug: also write the fp32 [n, n_mels, 3000] features
   // decode
   DecodeState st{};
   int32_t* prompt_dev = nullptr;
@@ -238,6 +239,14 @@ struct WhisperEngine {
   std::vector<void*> allocs;
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t step_exec = nullptr;
+  // cross-attention variant: 0 by active rows (streaming kernel when
+  // rows x heads >= xs_min_items), 1 always the cluster kernel, 2 always streaming
+  int xa_mode = 0;
+  int xs_min_items = std::getenv("DM_XS_MIN_ITEMS") ? std::atoi(std::getenv("DM_XS_MIN_ITEMS"))
+                                                    : kXsMinItems;
+  bool use_xs(int n_active) const {
+    return xa_mode == 2 || (xa_mode == 0 && n_active * H >= xs_min_items);
+  }
   cudaGraph_t step_graph = nullptr;
   int gemv_counter_base = 0;
   std::vector<TcGemvMaps> maps;   // [Ld * 6 + 1]: per layer qkv,o,xq,xo,fc1,fc2; LM head
@@ -255,6 +264,11 @@ struct WhisperEngine {
     cudaEvent_t done = nullptr;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
+    // the same step with the streaming cross-attention (many active rows)
+    cudaGraph_t graph_xs = nullptr;
+    cudaGraphExec_t exec_xs = nullptr;
+    int n_active_host = 0;         // rows of the last set_active (picks the graph)
+    int* xs_ctr = nullptr;         // [Ld][2] ticket / finished-CTA counters
     // K-split partial sums of the linear projections (consumer-reduced)
     float *p_qkv = nullptr, *p_o = nullptr, *p_xq = nullptr, *p_xo = nullptr, *p_fc2 = nullptr;
   };
@@ -287,6 +301,8 @@ struct WhisperEngine {
     for (auto& g : groups) {
       if (g.exec) cudaGraphExecDestroy(g.exec);
       if (g.graph) cudaGraphDestroy(g.graph);
+      if (g.exec_xs) cudaGraphExecDestroy(g.exec_xs);
+      if (g.graph_xs) cudaGraphDestroy(g.graph_xs);
       if (g.stream) cudaStreamDestroy(g.stream);
       if (g.done) cudaEventDestroy(g.done);
     }
@@ -420,6 +436,7 @@ static int engine_init(WhisperEngine* e) {
                                                gemv_part_floats(c.vocab, d, GV_ARGMAX)));
     if (e->alloc_t(&gs.part, part)) return 2;
     if (e->alloc_t(&gs.counters, 4096)) return 2;
+    if (e->alloc_t(&gr.xs_ctr, size_t(e->Ld) * 2)) return 2;
     if (e->alloc_t(&gs.amax_val, size_t(tiles) * kRows)) return 2;
     if (e->alloc_t(&gs.amax_idx, size_t(tiles) * kRows)) return 2;
     gs.logits_dbg = nullptr;
@@ -467,7 +484,9 @@ static int encoder_forward(WhisperEngine* e, const int16_t* pcm, const int64_t* 
   const int d = e->d, H = e->H;
   const LogmelTables* tab = nullptr;
   if (int rc = get_logmel_tables(e->nm, &tab)) return rc;
-  if (int rc = launch_logmel(pcm, offsets, lengths, n, e->nm, tab, e->mel, e->mel_t, e->segmax, s))
+  // the fp32 feature contract is written only for the debug tap (dm_whisper_debug 15)
+  if (int rc = launch_logmel(pcm, offsets, lengths, n, e->nm, tab, e->mel_tap ? e->mel : nullptr,
+                             e->mel_t, e->segmax, s))
     return rc;
   // conv1 (implicit GEMM over the padded time-major mel), GELU
   {
@@ -556,7 +575,7 @@ static int launch_pdl_floor(cudaStream_t s) {
     ++st.trace_id;                    \
   } while (0)
 
-static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t s) {
+static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t s, bool xs) {
   DecodeState st = grp.st;        // local copy: trace_id numbers the step's kernels
   st.trace_id = 0;
   const int d = e->d;
@@ -586,8 +605,13 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
     DM_STEP(ln(2, b0 + 6, Partials{grp.p_o, go, d, e->W(b0 + 5)}));
     DM_STEP(gv(pi + 2, grp.p_xq, nullptr, nullptr, nullptr));
     // cross-attention with the cross-o projection in its tail (per-head partials)
-    DM_STEP(launch_cross_attn(st, e->xkv_map, l, Partials{grp.p_xq, gx, d, e->W(b0 + 9)}, 0.125f,
-                              e->xo_pack + size_t(l) * d * d, grp.p_xo, s));
+    if (xs)
+      DM_STEP(launch_cross_attn_stream(st, e->xkv_map, l, Partials{grp.p_xq, gx, d, e->W(b0 + 9)},
+                                       0.125f, e->xo_pack + size_t(l) * d * d, grp.p_xo,
+                                       grp.xs_ctr + 2 * l, s));
+    else
+      DM_STEP(launch_cross_attn(st, e->xkv_map, l, Partials{grp.p_xq, gx, d, e->W(b0 + 9)},
+                                0.125f, e->xo_pack + size_t(l) * d * d, grp.p_xo, s));
     DM_STEP(ln(2, b0 + 12, Partials{grp.p_xo, e->H, d, e->W(b0 + 11)}));
     DM_STEP(gv(pi + 4, nullptr, st.hh, st.hl, e->W(b0 + 15)));
     DM_STEP(gv(pi + 5, grp.p_fc2, nullptr, nullptr, nullptr));
@@ -603,25 +627,29 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
 
 static int build_step_graph(WhisperEngine* e) {
   for (auto& grp : e->groups) {
-    if (grp.exec) {
-      cudaGraphExecDestroy(grp.exec);
-      grp.exec = nullptr;
+    for (int xs = 0; xs < 2; ++xs) {
+      cudaGraphExec_t& ex = xs ? grp.exec_xs : grp.exec;
+      cudaGraph_t& gg = xs ? grp.graph_xs : grp.graph;
+      if (ex) {
+        cudaGraphExecDestroy(ex);
+        ex = nullptr;
+      }
+      if (gg) {
+        cudaGraphDestroy(gg);
+        gg = nullptr;
+      }
+      DM_CHECK_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
+      int rc = record_step(e, grp, e->cap_stream, xs != 0);
+      cudaGraph_t g = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &g);
+      if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+      }
+      DM_CHECK_CUDA(ce);
+      gg = g;
+      DM_CHECK_CUDA(cudaGraphInstantiate(&ex, g, 0));
     }
-    if (grp.graph) {
-      cudaGraphDestroy(grp.graph);
-      grp.graph = nullptr;
-    }
-    DM_CHECK_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
-    int rc = record_step(e, grp, e->cap_stream);
-    cudaGraph_t g = nullptr;
-    cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &g);
-    if (rc) {
-      if (g) cudaGraphDestroy(g);
-      return rc;
-    }
-    DM_CHECK_CUDA(ce);
-    grp.graph = g;
-    DM_CHECK_CUDA(cudaGraphInstantiate(&grp.exec, g, 0));
   }
   e->step_exec = e->groups[0].exec;     // marks "built"
   return 0;
@@ -674,6 +702,18 @@ int dm_logmel(const int16_t* pcm, const int64_t* offsets, const int32_t* lengths
   }
   uint32_t* segmax = sc.first;
   return launch_logmel(pcm, offsets, lengths, n, n_mels, tab, out, nullptr, segmax,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int dm_logmel_operand(const int16_t* pcm, const int64_t* offsets, const int32_t* lengths, int n,
+                      int n_mels, uint16_t* out, uint32_t* segmax, void* stream) {
+  DM_REQUIRE(n >= 0, "n < 0");
+  DM_REQUIRE(n_mels == 80 || n_mels == 128, "n_mels must be 80 or 128");
+  if (n == 0) return 0;
+  DM_REQUIRE(pcm && offsets && lengths && out && segmax, "null pointer");
+  const LogmelTables* tab = nullptr;
+  if (int rc = get_logmel_tables(n_mels, &tab)) return rc;
+  return launch_logmel(pcm, offsets, lengths, n, n_mels, tab, nullptr, out, segmax,
                        static_cast<cudaStream_t>(stream));
 }
 
@@ -827,6 +867,7 @@ int dm_whisper_set_active(void* handle, const int32_t* slot_ids, int n, void* st
   }
   for (int g = 0; g < G; ++g) {
     int32_t* row = rows.data() + g * (kRows + 1);
+    e->groups[g].n_active_host = row[0];
     if (int rc = e->ring.upload(e->groups[g].n_active_dev, row, sizeof(int32_t), s)) return rc;
     if (row[0])
       if (int rc = e->ring.upload(e->groups[g].active_dev, row + 1, sizeof(int32_t) * row[0], s))
@@ -842,13 +883,18 @@ int dm_whisper_step(void* handle, int n_steps, void* stream) {
   if (!e->step_exec)
     if (int rc = build_step_graph(e)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto exec_of = [&](const WhisperEngine::Group& grp) {
+    return e->use_xs(grp.n_active_host) ? grp.exec_xs : grp.exec;
+  };
   if (e->groups.size() == 1) {
-    for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(e->groups[0].exec, s));
+    cudaGraphExec_t ex = exec_of(e->groups[0]);
+    for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(ex, s));
   } else {
     DM_CHECK_CUDA(cudaEventRecord(e->step_start, s));
     for (auto& grp : e->groups) {
       DM_CHECK_CUDA(cudaStreamWaitEvent(grp.stream, e->step_start, 0));
-      for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(grp.exec, grp.stream));
+      cudaGraphExec_t ex = exec_of(grp);
+      for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(ex, grp.stream));
       DM_CHECK_CUDA(cudaEventRecord(grp.done, grp.stream));
     }
     for (auto& grp : e->groups) DM_CHECK_CUDA(cudaStreamWaitEvent(s, grp.done, 0));
@@ -909,6 +955,11 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
       case 6: return launch_pdl_floor(cs);
       case 7: return gv(pi + 4, nullptr, grp.st.hh, grp.st.hl, e->W(b0 + 15), cs);
       case 8: return gv(pi + 0, grp.p_qkv, nullptr, nullptr, nullptr, cs);
+      case 9:
+        return launch_cross_attn_stream(grp.st, e->xkv_map, layer,
+                                        Partials{grp.p_xq, e->plans[pi + 2].splits, d, e->W(b0 + 9)},
+                                        0.125f, e->xo_pack + size_t(layer) * d * d, grp.p_xo,
+                                        grp.xs_ctr + 2 * layer, cs);
       default: set_error("unknown kernel id"); return 1;
     }
   };
@@ -974,7 +1025,11 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
   size_t avail = 0;
   switch (which) {
     case 0: src = e->enc_out; avail = size_t(e->last_n) * 1500 * e->d * 2; break;
-    case 1: src = e->mel; avail = size_t(e->last_n) * e->nm * 3000 * 4; break;
+    case 1:
+      DM_REQUIRE(e->mel_tap, "log-mel tap not enabled (dm_whisper_debug 15 before the encode)");
+      src = e->mel; avail = size_t(e->last_n) * e->nm * 3000 * 4;
+      break;
+    case 15: e->mel_tap = bytes != 0; return 0;
     case 2:
       DM_REQUIRE(e->st.logits_dbg != nullptr, "logits tap not enabled");
       src = e->st.logits_dbg; avail = size_t(kRows) * e->cfg.vocab * 4;
@@ -989,10 +1044,14 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
     }
     case 4: e->enc_stop = int(bytes); return 0;
     case 7: e->enc_tap = bytes != 0; return 0;
+    case 14:         // cross-attention variant: 0 by active rows, 1 cluster, 2 streaming
+      DM_REQUIRE(bytes <= 2, "cross-attention mode must be 0, 1 or 2");
+      e->xa_mode = int(bytes);
+      return 0;
     case 10: {       // step timeline tap on (graph re-captured with per-kernel globaltimer marks)
       if (!e->groups[0].st.trace) {
         unsigned long long* t = nullptr;
-        if (e->alloc_t(&t, 128 * 8)) return 2;
+        if (e->alloc_t(&t, kTraceSlots * 8)) return 2;
         e->groups[0].st.trace = t;
         if (int rc = build_step_graph(e)) return rc;
       }
@@ -1000,8 +1059,8 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
     }
     case 11: {       // reset the timeline (entry/release minima to +inf, maxima to 0)
       DM_REQUIRE(e->groups[0].st.trace != nullptr, "timeline tap not enabled");
-      std::vector<unsigned long long> init(128 * 8, 0ull);
-      for (int k = 0; k < 128; ++k) init[k * 8] = init[k * 8 + 1] = ~0ull;
+      std::vector<unsigned long long> init(kTraceSlots * 8, 0ull);
+      for (int k = 0; k < kTraceSlots; ++k) init[k * 8] = init[k * 8 + 1] = ~0ull;
       DM_CHECK_CUDA(cudaMemcpyAsync(e->groups[0].st.trace, init.data(), init.size() * 8,
                                     cudaMemcpyHostToDevice, s));
       DM_CHECK_CUDA(cudaStreamSynchronize(s));
@@ -1009,7 +1068,7 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
     }
     case 12:
       DM_REQUIRE(e->groups[0].st.trace != nullptr, "timeline tap not enabled");
-      src = e->groups[0].st.trace; avail = 128 * 8 * 8;
+      src = e->groups[0].st.trace; avail = size_t(kTraceSlots) * 8 * 8;
       break;
     case 13: {       // guard check: host_dst int32[bytes/4] = {n_bad, (index, first bad offset, KB)...}
       DM_REQUIRE(e->guard, "engine created without DM_GUARD=1");

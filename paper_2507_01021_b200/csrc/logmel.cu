@@ -6,16 +6,24 @@
 // oracle/logmel.py (transformers 5.5.0 feature_extraction_whisper.py:140-164).
 //
 // Layout: segments are concatenated int16 PCM in HBM (offsets/lengths); the
-// 480,000-sample window is never materialised — samples past the true length
+// 480,000-sample window is never materialised -- samples past the true length
 // read as zero inside the loads. Per CTA: 32 consecutive frames of one
 // segment. The 400-point real DFT runs as a 200-point complex FFT
 // (even/odd packing), itself a 4-step 8 x 25 FFT staged through shared
 // memory; the 25-point DFTs are 5 x 5 radix-5 in registers. Power -> sparse
-// slaney mel (<= 2 taps per bin) -> log10(max(., 1e-10)) -> per-segment max
-// via an order-preserving atomicMax. A second pass clamps to max-8 and
-// normalises ((x+4)/4), writing both the fp32 [B, n_mels, 3000] feature
-// contract and a time-major bf16 copy (rows 1..3000 of a zero-padded
-// [B, 3002, n_mels] buffer) that feeds the conv1 implicit GEMM.
+// slaney mel -> log10(max(., 1e-10)) -> per-segment max via an
+// order-preserving atomicMax.
+//
+// Product path (encoder operand only): pass 1 writes bf16((x + 4) / 4) --
+// the normalisation WITHOUT the clamp -- straight into the time-major conv1
+// operand (rows 1..3000 of a zero-padded [B, 3002, ldt] bf16 buffer); pass 2
+// clamps that buffer in place to bf16((max - 8 + 4) / 4). Because
+// x -> bf16((x + 4) / 4) is monotonic, max(bf16(a), bf16(b)) = bf16(max(a, b)):
+// the result is bit for bit bf16((max(x, max - 8) + 4) / 4), the feature
+// extractor's clamp + normalise, with 2 bytes per value written once and
+// re-read once instead of an fp32 round trip. The fp32 [B, n_mels, 3000]
+// feature contract (dm_logmel, and the engine's debug tap) is a separate
+// output of the same passes.
 //
 // Frames whose 400-sample window lies entirely in the zero padding are
 // skipped (their power is exactly 0, so the result is log10(1e-10)).
@@ -122,10 +130,22 @@ struct LogmelSmem {
   float mw[1024];
 };
 
+__device__ __forceinline__ float fast_log10(float x) {
+  return __log2f(x) * 0.30102999566398120f;       // MUFU lg2 (abs err ~2^-22)
+}
+
+// bf16 bits of the normalised-but-unclamped value (x + 4) / 4
+__device__ __forceinline__ uint32_t norm_bf16_pair(float a, float b) {
+  return pack_bf16x2((a + 4.0f) / 4.0f, (b + 4.0f) / 4.0f);
+}
+
+// Pass 1. mel_t (nullable): the time-major bf16 operand, rows 1..3000 of
+// [B, 3002, ldt]; out32 (nullable): fp32 unnormalised log-mel [B, n_mels, 3000].
 __global__ void __launch_bounds__(kLogmelThreads)
 logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offsets,
               const int32_t* __restrict__ lengths, const LogmelTables* __restrict__ tab,
-              int n_mels, float* __restrict__ out, uint32_t* __restrict__ segmax) {
+              int n_mels, uint16_t* __restrict__ mel_t, int ldt, float* __restrict__ out32,
+              uint32_t* __restrict__ segmax) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   LogmelSmem& s = *reinterpret_cast<LogmelSmem*>(smem_raw);
   const int b = blockIdx.y;
@@ -135,16 +155,22 @@ logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offse
   int n = lengths[b];
   n = n < 0 ? 0 : (n > kWindow ? kWindow : n);
   const int16_t* x = pcm + offsets[b];
-  float* outb = out + size_t(b) * n_mels * kFrames;
+  uint16_t* tb = mel_t ? mel_t + (size_t(b) * (kFrames + 2) + f0 + 1) * ldt : nullptr;
+  float* ob = out32 ? out32 + size_t(b) * n_mels * kFrames : nullptr;
+  const int np = n_mels / 2;                        // mel pairs per frame (40 or 64)
 
   // Frames >= first_zero have all-zero windows: start index f*160-200 >= n.
   const int first_zero = n == 0 ? 0 : min(kFrames, (n + 200 + kHop - 1) / kHop);
   if (f0 >= first_zero) {
     const float v = log10f(1e-10f);
-    for (int i = tid; i < n_mels * nfr; i += kLogmelThreads) {
-      int m = i / nfr, f = i % nfr;
-      outb[size_t(m) * kFrames + f0 + f] = v;
+    if (tb) {
+      const uint32_t w = norm_bf16_pair(v, v);
+      for (int t = tid; t < np * nfr; t += kLogmelThreads)
+        reinterpret_cast<uint32_t*>(tb + size_t(t / np) * ldt)[t % np] = w;
     }
+    if (ob)
+      for (int i = tid; i < n_mels * nfr; i += kLogmelThreads)
+        ob[size_t(i / nfr) * kFrames + f0 + i % nfr] = v;
     if (tid == 0) atomicMax(segmax + b, float_to_ordered(v));
     return;
   }
@@ -193,8 +219,10 @@ logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offse
   __syncthreads();
 
   // Stage A: per (frame, q): 8-point DFT over p of z[25p+q], twiddle W200^{q k1}.
-  for (int t = tid; t < kFPB * 25; t += kLogmelThreads) {
-    int fr = t / 25, q = t % 25;
+  // (250 threads as q = tid % 25, frames tid / 25 + 10 i: one division per thread)
+  const int qa = tid % 25, fa = tid / 25;
+  for (int fr = fa; fr < kFPB && tid < 250; fr += 10) {
+    const int q = qa;
     float2 z[8];
     const float* src = s.samples + fr * kHop;
 #pragma unroll
@@ -238,33 +266,49 @@ logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offse
   }
   __syncthreads();
 
-  // Real-FFT post-processing + power.
+  // Real-FFT post-processing + power: thread = bin (201 of 256), loop over frames
   float* power = s.samples;
-  for (int t = tid; t < kFPB * kBins; t += kLogmelThreads) {
-    int fr = t / kBins, k = t % kBins;
-    const float2* Z = s.y + fr * 200;
-    float2 zk = Z[k % 200], zc = Z[(200 - k) % 200];
-    zc.y = -zc.y;                                        // conj(Z[200-k])
-    float2 E = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y + zc.y));
-    float2 D = make_float2(0.5f * (zk.x - zc.x), 0.5f * (zk.y - zc.y));
-    float2 O = make_float2(D.y, -D.x);                   // D / i
-    float2 X = cadd(E, cmul(s.tw400[k], O));
-    power[fr * kBins + k] = X.x * X.x + X.y * X.y;
+  if (tid < kBins) {
+    const int k = tid;
+    const float2 tw = s.tw400[k];
+    const int kz = k % 200, kc = (200 - k) % 200;
+#pragma unroll 4
+    for (int fr = 0; fr < kFPB; ++fr) {
+      const float2* Z = s.y + fr * 200;
+      float2 zk = Z[kz], zc = Z[kc];
+      zc.y = -zc.y;                                      // conj(Z[200-k])
+      float2 E = make_float2(0.5f * (zk.x + zc.x), 0.5f * (zk.y + zc.y));
+      float2 D = make_float2(0.5f * (zk.x - zc.x), 0.5f * (zk.y - zc.y));
+      float2 O = make_float2(D.y, -D.x);                 // D / i
+      float2 X = cadd(E, cmul(tw, O));
+      power[fr * kBins + k] = X.x * X.x + X.y * X.y;
+    }
   }
   __syncthreads();
 
-  // Sparse mel + log10; coalesced along frames.
+  // Sparse mel + log10: thread = (mel pair p, frame group g); the pair's bank
+  // rows stay in registers, frames g, g + 4, ... (bf16 pair stores run along
+  // the time-major row)
   float lmax = -INFINITY;
-  for (int t = tid; t < n_mels * kFPB; t += kLogmelThreads) {
-    int m = t / kFPB, fr = t % kFPB;
-    if (fr >= nfr) continue;
-    const int k0 = s.mstart[m], cnt = s.mcount[m], wo = s.mwoff[m];
-    const float* pw = power + fr * kBins + k0;
-    float acc = 0.f;
-    for (int i = 0; i < cnt; ++i) acc = fmaf(s.mw[wo + i], pw[i], acc);
-    float v = log10f(fmaxf(acc, 1e-10f));
-    outb[size_t(m) * kFrames + f0 + fr] = v;
-    lmax = fmaxf(lmax, v);
+  const int p = tid & 63, g = tid >> 6;
+  if (p < np) {
+    const int m0 = 2 * p;
+    const int st0 = s.mstart[m0], c0 = s.mcount[m0], w0 = s.mwoff[m0];
+    const int st1 = s.mstart[m0 + 1], c1 = s.mcount[m0 + 1], w1 = s.mwoff[m0 + 1];
+    for (int fr = g; fr < nfr; fr += kLogmelThreads / 64) {
+      const float* pw = power + fr * kBins;
+      float a0 = 0.f, a1 = 0.f;
+      for (int i = 0; i < c0; ++i) a0 = fmaf(s.mw[w0 + i], pw[st0 + i], a0);
+      for (int i = 0; i < c1; ++i) a1 = fmaf(s.mw[w1 + i], pw[st1 + i], a1);
+      const float v0 = fast_log10(fmaxf(a0, 1e-10f));
+      const float v1 = fast_log10(fmaxf(a1, 1e-10f));
+      if (tb) reinterpret_cast<uint32_t*>(tb + size_t(fr) * ldt)[p] = norm_bf16_pair(v0, v1);
+      if (ob) {
+        ob[size_t(m0) * kFrames + f0 + fr] = v0;
+        ob[size_t(m0 + 1) * kFrames + f0 + fr] = v1;
+      }
+      lmax = fmaxf(lmax, fmaxf(v0, v1));
+    }
   }
   // block max -> one atomic
 #pragma unroll
@@ -279,67 +323,76 @@ logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offse
   }
 }
 
-// Clamp to (segment max - 8), normalise, and emit the bf16 time-major copy.
+// Pass 2 (operand): clamp the bf16 operand in place to bf16((max - 8 + 4) / 4);
+// 8 channels per thread, written back only where a value rose.
 __global__ void __launch_bounds__(256)
-logmel_normalize_kernel(float* __restrict__ out, const uint32_t* __restrict__ segmax,
-                        int n_mels, uint16_t* __restrict__ mel_t /*[B,3002,ldt]*/, int ldt) {
-  __shared__ float tile[128][kFPB + 1];
+logmel_clamp_kernel(uint16_t* __restrict__ mel_t, const uint32_t* __restrict__ segmax,
+                    int n_mels, int ldt) {
   const int b = blockIdx.y;
-  const int f0 = blockIdx.x * kFPB;
-  const int nfr = min(kFPB, kFrames - f0);
+  const int vpr = n_mels / 8;                             // 16-byte vectors per frame row
+  const float fl = ordered_to_float(segmax[b]) - 8.0f;
+  const float floor_n = __uint_as_float(uint32_t(f32_to_bf16((fl + 4.0f) / 4.0f)) << 16);
+  uint16_t* base = mel_t + (size_t(b) * (kFrames + 2) + 1) * ldt;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < kFrames * vpr;
+       t += gridDim.x * blockDim.x) {
+    uint4* pv = reinterpret_cast<uint4*>(base + size_t(t / vpr) * ldt) + (t % vpr);
+    uint4 v = *pv;
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    bool changed = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float lo = __uint_as_float(w[u] << 16), hi = __uint_as_float(w[u] & 0xFFFF0000u);
+      const float nlo = fmaxf(lo, floor_n), nhi = fmaxf(hi, floor_n);
+      changed |= (nlo != lo) | (nhi != hi);
+      w[u] = (__float_as_uint(nlo) >> 16) | (__float_as_uint(nhi) & 0xFFFF0000u);
+    }
+    if (changed) *pv = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+}
+
+// Pass 2 (fp32 feature contract): clamp to (max - 8) and normalise in place.
+__global__ void __launch_bounds__(256)
+logmel_normalize_kernel(float* __restrict__ out, const uint32_t* __restrict__ segmax, int n_mels) {
+  const int b = blockIdx.y;
   const float floor_v = ordered_to_float(segmax[b]) - 8.0f;
-  float* outb = out + size_t(b) * n_mels * kFrames;
-  // 4 frames per float4 (rows of 3000 floats are 16-byte aligned, nfr % 4 == 0)
-  for (int t = threadIdx.x; t < n_mels * (kFPB / 4); t += blockDim.x) {
-    const int m = t / (kFPB / 4), fr = 4 * (t % (kFPB / 4));
-    if (fr >= nfr) continue;
-    float4* p = reinterpret_cast<float4*>(outb + size_t(m) * kFrames + f0 + fr);
-    float4 v = *p;
+  float4* o = reinterpret_cast<float4*>(out + size_t(b) * n_mels * kFrames);
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_mels * kFrames / 4;
+       t += gridDim.x * blockDim.x) {
+    float4 v = o[t];
     v.x = (fmaxf(v.x, floor_v) + 4.0f) / 4.0f;
     v.y = (fmaxf(v.y, floor_v) + 4.0f) / 4.0f;
     v.z = (fmaxf(v.z, floor_v) + 4.0f) / 4.0f;
     v.w = (fmaxf(v.w, floor_v) + 4.0f) / 4.0f;
-    *p = v;
-    tile[m][fr] = v.x;
-    tile[m][fr + 1] = v.y;
-    tile[m][fr + 2] = v.z;
-    tile[m][fr + 3] = v.w;
-  }
-  if (mel_t == nullptr) return;
-  __syncthreads();
-  // time-major bf16 rows: 8 mels per 16-byte store
-  uint16_t* dst = mel_t + (size_t(b) * (kFrames + 2) + f0 + 1) * ldt;
-  const int mc = n_mels / 8;
-  for (int t = threadIdx.x; t < mc * nfr; t += blockDim.x) {
-    const int fr = t / mc, m0 = 8 * (t % mc);
-    uint4 w;
-    w.x = pack_bf16x2(tile[m0][fr], tile[m0 + 1][fr]);
-    w.y = pack_bf16x2(tile[m0 + 2][fr], tile[m0 + 3][fr]);
-    w.z = pack_bf16x2(tile[m0 + 4][fr], tile[m0 + 5][fr]);
-    w.w = pack_bf16x2(tile[m0 + 6][fr], tile[m0 + 7][fr]);
-    *reinterpret_cast<uint4*>(dst + size_t(fr) * ldt + m0) = w;
+    o[t] = v;
   }
 }
 
 size_t logmel_smem_bytes() { return sizeof(LogmelSmem); }
 
 int launch_logmel(const int16_t* pcm, const int64_t* offsets, const int32_t* lengths,
-                  int n_segments, int n_mels, const LogmelTables* tables, float* out,
-                  uint16_t* mel_t, uint32_t* segmax, cudaStream_t stream) {
+                 int n_segments, int n_mels, const LogmelTables* tables, float* out32,
+                 uint16_t* mel_t, uint32_t* segmax, cudaStream_t stream) {
   DM_REQUIRE(n_mels == 80 || n_mels == 128, "n_mels must be 80 or 128");
   DM_REQUIRE(n_segments >= 0, "n_segments < 0");
+  DM_REQUIRE(out32 != nullptr || mel_t != nullptr, "no log-mel output");
   if (n_segments == 0) return 0;
   const size_t smem = logmel_smem_bytes();
   DM_SMEM_ATTR(logmel_kernel, int(smem));
   DM_CHECK_CUDA(cudaMemsetAsync(segmax, 0, sizeof(uint32_t) * n_segments, stream));
-  dim3 grid(ceil_div(kFrames, kFPB), n_segments);
-  logmel_kernel<<<grid, kLogmelThreads, smem, stream>>>(pcm, offsets, lengths, tables,
-                                                         n_mels, out, segmax);
-  DM_CHECK_LAUNCH();
-  // time-major copy rows are padded to 64 (n_mels <= 64) or 128 channels
+  // time-major operand rows are padded to 64 (n_mels <= 64) or 128 channels
   const int ldt = n_mels <= 64 ? 64 : 128;
-  logmel_normalize_kernel<<<grid, 256, 0, stream>>>(out, segmax, n_mels, mel_t, ldt);
+  dim3 grid(ceil_div(kFrames, kFPB), n_segments);
+  logmel_kernel<<<grid, kLogmelThreads, smem, stream>>>(pcm, offsets, lengths, tables, n_mels,
+                                                         mel_t, ldt, out32, segmax);
   DM_CHECK_LAUNCH();
+  if (mel_t) {
+    logmel_clamp_kernel<<<dim3(24, n_segments), 256, 0, stream>>>(mel_t, segmax, n_mels, ldt);
+    DM_CHECK_LAUNCH();
+  }
+  if (out32) {
+    logmel_normalize_kernel<<<dim3(48, n_segments), 256, 0, stream>>>(out32, segmax, n_mels);
+    DM_CHECK_LAUNCH();
+  }
   return 0;
 }
 

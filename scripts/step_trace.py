@@ -13,6 +13,8 @@ rows_list = [int(x) for x in sys.argv[2:]] or [64, 32, 8, 1]
 dims = get_model(name)
 S = 64
 eng = WhisperGPU(dims, max_slots=S, max_encode_batch=32)
+import os
+eng.set_cross_attn_mode(int(os.environ.get("XA_MODE", "0")))
 rng = np.random.default_rng(0)
 seg = rng.integers(-8000, 8000, size=160000, dtype=np.int16)
 slots = list(range(S))
@@ -40,7 +42,7 @@ for rows in rows_list:
         dbg(11)
         eng.step(1)
         torch.cuda.synchronize()
-        t = np.zeros((128, 8), np.uint64)
+        t = np.zeros((512, 8), np.uint64)
         dbg(12, t)
         t = t[:len(names)].astype(np.float64)
         t0 = t[0, 1]

@@ -113,3 +113,35 @@ def test_cta_pair_gemm_bitwise_equals_single_sm(native_lib, tmp_path):
                        timeout=300)
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("n_mels", [80, 128])
+def test_logmel_operand_is_bf16_of_features(native_lib, n_mels):
+    """The product path's bf16 operand (pass 1 writes bf16((x+4)/4) unclamped,
+    pass 2 clamps in place) is bit for bit the bf16 rounding of the fp32
+    feature contract (clamp to max-8, then normalise)."""
+    import ctypes as C
+    from paper_2507_01021_b200 import _native
+    lib = _native.load()
+    rng = np.random.default_rng(7 + n_mels)
+    segs = [rng.integers(-8000, 8000, size=n, dtype=np.int16) for n in (160_000, 48_000, 480_000, 1000)]
+    t = np.arange(200_000) / 16000.0
+    segs.append((3000 * np.sin(2 * np.pi * 440 * t)).astype(np.int16))
+    dev = torch.device("cuda", 0)
+    flat = torch.from_numpy(np.concatenate(segs)).to(dev)
+    offs = torch.tensor(np.cumsum([0] + [len(x) for x in segs[:-1]]), dtype=torch.int64, device=dev)
+    lens = torch.tensor([len(x) for x in segs], dtype=torch.int32, device=dev)
+    n = len(segs)
+    out = torch.empty(n, n_mels, 3000, dtype=torch.float32, device=dev)
+    ldt = 64 if n_mels <= 64 else 128
+    op = torch.zeros(n, 3002, ldt, dtype=torch.int16, device=dev)
+    segmax = torch.empty(n, dtype=torch.int32, device=dev)
+    P = lambda x: C.c_void_p(x.data_ptr())
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    _native.check(lib.dm_logmel(P(flat), P(offs), P(lens), n, n_mels, P(out), s))
+    _native.check(lib.dm_logmel_operand(P(flat), P(offs), P(lens), n, n_mels, P(op), P(segmax), s))
+    torch.cuda.synchronize()
+    want = out.to(torch.bfloat16).view(torch.int16).transpose(1, 2).cpu().numpy()
+    got = op.cpu().numpy()
+    assert np.array_equal(got[:, 1:3001, :n_mels], want)
+    assert not got[:, 0].any() and not got[:, 3001].any() and not got[:, :, n_mels:].any()

@@ -20,6 +20,7 @@ def test_large_v3_parity(native_lib):
     segs = [rng.integers(-8000, 8000, size=n, dtype=np.int16) for n in (160_000, 64_000)]
     gpu = WhisperGPU(WHISPER_LARGE_V3, seed=0, max_slots=4, max_encode_batch=2)
     got = gpu.transcribe_ids(segs, [8, 8])
+    gpu.enable_mel_tap()
     enc32 = gpu.encoder_output_f32(segs, [0, 1])
     mel = gpu.log_mel(2)
     gpu.encode(segs, [0, 1])
