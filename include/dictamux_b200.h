@@ -134,9 +134,7 @@ DM_API int dm_whisper_read_async(void* handle, int32_t* done, int32_t* n_gen, in
  *  which = 6: attention output of the last encoder layer run, [n, 1500, d] bf16
  *  which = 7: (bytes != 0) keep the fp32 encoder output; read it with which = 5
  *  which = 15: (bytes != 0) also write the fp32 features of later encodes (read with which = 1)
- *  which = 14: cross-attention kernel of later steps (bytes = 0: by active rows,
- *              1: always the cluster kernel, 2: always the streaming kernel;
- *              both compute the same values bit for bit) */
+ */
 DM_API int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void* stream);
 
 /* ------------------------------------------------------------ CTC engine (cfg5)
@@ -170,8 +168,7 @@ DM_API int dm_whisper_stats(void* handle, int64_t* out, int n);
  * `stream` (a probe: it may overwrite row-space activations): which =
  * 0 cross-attention(layer), 1 self-attention(layer), 2 LM head, 3 decoder LN
  * (+ residual partials), 4 cross-q projection, 5 fc2 projection,
- * 6 empty PDL kernel (launch floor), 7 fc1 projection (+GELU), 8 qkv projection,
- * 9 streaming cross-attention (+ cross-o).
+ * 6 empty PDL kernel (launch floor), 7 fc1 projection (+GELU), 8 qkv projection.
  * avg_ms = mean over iters back-to-back launches. layer < 0: launch i runs
  * decoder layer i % dec_layers (each launch streams a different layer's
  * cross-KV / weights, as inside a decode step). */

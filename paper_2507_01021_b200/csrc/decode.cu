@@ -136,13 +136,15 @@ static cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 
 constexpr int kGvThreads = 192;
 constexpr int kGvWBytes = 128 * 64 * 2;        // W block: 128 features x 64 k
 constexpr int kGvXBytes = kRows * 64 * 2;      // X block: 64 rows x 64 k (hi or lo)
+constexpr int kSmPerSm = 233472;               // shared memory per SM (228 KB)
 constexpr int kGvTr = kRows * 129 * 4;         // GV_ARGMAX transpose
 constexpr int kGvMaxStages = 8;
 constexpr int kGvMisc = 1024;
 constexpr int kSmemOptin = 232448;             // 227 KB per CTA (sm_100)
 
-__host__ __device__ constexpr int gemv_smem_bytes(int kb_per, int stages, int epi, int rgroups) {
-  return 1024 + kb_per * 2 * (kGvXBytes / rgroups) + stages * kGvWBytes +
+__host__ __device__ constexpr int gemv_smem_bytes(int kb_per, int stages, int epi, int rgroups,
+                                                  int xrows = kRows) {
+  return 1024 + kb_per * 2 * (xrows * 128 / rgroups) + stages * kGvWBytes +
          (epi != GV_PARTIAL ? kGvTr : 0) + kGvMisc;
 }
 
@@ -155,7 +157,8 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
   uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
   const int kb_per = a.kb_per, NS = a.stages;
   uint8_t* xs = smem;                                        // [kb][hi | lo], RG rows each
-  uint8_t* ws = xs + kb_per * 2 * (kRows / int(gridDim.z)) * 128;   // [stage] 16K
+  const int RG = a.xrows / int(gridDim.z);                  // rows per row group
+  uint8_t* ws = xs + kb_per * 2 * RG * 128;                  // [stage] 16K
   float* tr = reinterpret_cast<float*>(ws + NS * kGvWBytes); // GV_ARGMAX / GELU staging
   uint8_t* misc = reinterpret_cast<uint8_t*>(tr) + (EPI != GV_PARTIAL ? kGvTr : 0);
   uint64_t* wfull = reinterpret_cast<uint64_t*>(misc);
@@ -166,7 +169,6 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 2);
   int* is_last = reinterpret_cast<int*>(tmem_slot + 1);
   if (threadIdx.x == 0) trace_mark(st, 0);
-  pdl_trigger();          // dependents may launch now and prefetch their own inputs
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int split = blockIdx.y;
@@ -174,7 +176,6 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
   const int kb0 = split * kb_per;
   // rows of this CTA's row group: [r0, r0 + R); n_active is host-set before
   // the step graph runs, so it is safe to read before the wait
-  const int RG = kRows / int(gridDim.z);
   const int r0 = int(blockIdx.z) * RG;
   const int R = min(*st.n_active - r0, RG);
   if (R <= 0 && blockIdx.z > 0) return;                      // empty row group
@@ -202,6 +203,10 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // dependents may launch now and prefetch their own inputs. Not before the
+  // TMEM allocation: a dependent's CTAs that allocate TMEM and then wait for
+  // this grid must never hold the columns one of its CTAs still needs.
+  pdl_trigger();
 
   if (warp == 0) {
     if (elect_one()) {
@@ -367,9 +372,9 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
         float* part = st.part;
         const size_t base = (size_t(split) * tiles + tile) * kRows * 128;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          part[base + size_t(i) * 128 + f] = v0[i];
-          part[base + size_t(32 + i) * 128 + f] = v1[i];
+        for (int i = 0; i < 32; ++i) {                   // only the active rows travel
+          if (i < R) part[base + size_t(i) * 128 + f] = v0[i];
+          if (32 + i < R) part[base + size_t(32 + i) * 128 + f] = v1[i];
         }
         __threadfence();
         named_bar_sync(1, 128);
@@ -388,8 +393,8 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
           const float* ps = part + (size_t(s) * tiles + tile) * kRows * 128 + f;
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
-            v0[i] += __ldcg(ps + size_t(i) * 128);
-            v1[i] += __ldcg(ps + size_t(32 + i) * 128);
+            if (i < R) v0[i] += __ldcg(ps + size_t(i) * 128);
+            if (32 + i < R) v1[i] += __ldcg(ps + size_t(32 + i) * 128);
           }
         }
         if (et == 0) st.counters[a.counter_base + tile] = 0;
@@ -489,6 +494,33 @@ GemvArgs gemv_plan(int N, int K, int epi) {
   const int per_cta = ceil_div(tiles, gx) * a.kb_per;
   const int fixed = gemv_smem_bytes(a.kb_per, 0, epi, a.rgroups);
   a.stages = std::min({kGvMaxStages, (kSmemOptin - fixed) / kGvWBytes, per_cta});
+  a.xrows = kRows;
+  a.gx = gx;
+  return a;
+}
+
+GemvArgs gemv_plan_for_rows(const GemvArgs& base, int rows) {
+  GemvArgs a = base;
+  const int xr = std::min(kRows, std::max(kGvXBox, ceil_div(rows, kGvXBox) * kGvXBox));
+  int rg = a.rgroups;
+  while (rg > 1 && xr % (rg * kGvXBox) != 0) rg /= 2;
+  a.xrows = xr;
+  a.rgroups = rg;
+  const int tiles = ceil_div(a.N, 128);
+  // two CTAs per SM when the whole weight slice and the smaller activation
+  // buffer fit in half an SM: then every (tile, split) gets its own CTA
+  for (int cps = 2; cps >= 1; --cps) {
+    const int gx = std::max(1, std::min(tiles, cps * kNumSMs / a.splits));
+    const int per_cta = ceil_div(tiles, gx) * a.kb_per;
+    const int fixed = gemv_smem_bytes(a.kb_per, 0, a.epi, rg, xr);
+    const int stages = std::min({kGvMaxStages, (kSmemOptin - fixed) / kGvWBytes, per_cta});
+    const int smem = gemv_smem_bytes(a.kb_per, stages, a.epi, rg, xr);
+    if (cps == 1 || (stages == per_cta && cps * (smem + 1024) <= kSmPerSm)) {
+      a.gx = gx;
+      a.stages = stages;
+      break;
+    }
+  }
   return a;
 }
 
@@ -502,12 +534,10 @@ template <int EPI, bool SPLIT>
 static int launch_gv(const DecodeState& st, const TcGemvMaps& maps, const GemvArgs& a,
                      cudaStream_t stream) {
   DM_SMEM_ATTR((gemv_kernel<EPI, SPLIT>), kSmemOptin);
-  const int tiles = ceil_div(a.N, 128);
-  const int gx = std::max(1, std::min(tiles, kNumSMs / a.splits));
-  DM_CHECK_CUDA(launch_pdl(gemv_kernel<EPI, SPLIT>, dim3(gx, a.splits, a.rgroups),
+  DM_CHECK_CUDA(launch_pdl(gemv_kernel<EPI, SPLIT>, dim3(a.gx, a.splits, a.rgroups),
                            dim3(kGvThreads),
-                           size_t(gemv_smem_bytes(a.kb_per, a.stages, EPI, a.rgroups)), stream,
-                           maps.w, maps.xh, maps.xl, st, a));
+                           size_t(gemv_smem_bytes(a.kb_per, a.stages, EPI, a.rgroups, a.xrows)),
+                           stream, maps.w, maps.xh, maps.xl, st, a));
   return 0;
 }
 
@@ -517,8 +547,10 @@ int launch_gemv(const DecodeState& st, const TcGemvMaps& maps, const GemvArgs& a
   DM_REQUIRE(a.stages >= 1 && a.stages <= kGvMaxStages, "bad weight ring depth");
   DM_REQUIRE(a.rgroups == 1 || a.rgroups == 2 || a.rgroups == 4, "GEMV row groups: 1, 2 or 4");
   DM_REQUIRE(a.rgroups == 1 || (a.epi != GV_ARGMAX && a.splits == 1), "row groups: linear / fc1 only");
-  DM_REQUIRE(gemv_smem_bytes(a.kb_per, a.stages, a.epi, a.rgroups) <= kSmemOptin,
+  DM_REQUIRE(gemv_smem_bytes(a.kb_per, a.stages, a.epi, a.rgroups, a.xrows) <= kSmemOptin,
              "GEMV slice exceeds smem");
+  DM_REQUIRE(a.xrows % (16 * a.rgroups) == 0 && a.xrows <= kRows && a.gx >= 1,
+             "GEMV activation rows / grid");
   const bool sp = a.splits > 1;
   switch (a.epi) {
     case GV_PARTIAL:
@@ -651,7 +683,7 @@ int launch_ln(const DecodeState& st, const LnArgs& a, cudaStream_t stream) {
   DM_REQUIRE(a.mode != 2 || (a.res.p != nullptr && a.res.splits >= 1 &&
                              a.res.splits <= kMaxHeads && a.res.n == st.d),
              "LayerNorm: residual partials missing");
-  const dim3 grid(kRows), block(st.d / 4);
+  const dim3 grid(st.grid_rows), block(st.d / 4);
   switch (a.mode) {
     case 0: DM_CHECK_CUDA(launch_pdl(ln_kernel<0>, grid, block, 0, stream, st, a)); break;
     case 1: DM_CHECK_CUDA(launch_pdl(ln_kernel<1>, grid, block, 0, stream, st, a)); break;
@@ -877,14 +909,13 @@ int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, floa
   DM_REQUIRE(st.page_tokens == 64 && st.pages_per_slot * 64 <= kSaMaxKeys, "self-attn: page geometry");
   const int smem = kSaPrePages * 2 * kSaPageBytes + 16;
   DM_SMEM_ATTR(self_attn_kernel, smem);
-  DM_CHECK_CUDA(launch_pdl(self_attn_kernel, dim3(kRows, st.heads), dim3(kSaThreads), smem,
+  DM_CHECK_CUDA(launch_pdl(self_attn_kernel, dim3(st.grid_rows, st.heads), dim3(kSaThreads), smem,
                            stream, st, layer, qkv, q_scale));
   return 0;
 }
 
 constexpr int kXaThreads = 192;                               // one key per thread
 constexpr int kXaKeys = 192;                                  // ceil(1500 / 8 / 64) * 64
-constexpr int kXaSmem = 1024 + 2 * kXaKeys * 128 + 64;   // (align) K, V blocks + mbarriers
 constexpr int kXaPush = 64 + 4;                          // o[64], max, sum (+pad): floats per split
 static_assert(kXSplits * kXaKeys >= 1500 && (kXSplits - 1) * kXaKeys < 1500, "key splits");
 
@@ -902,31 +933,52 @@ __device__ __forceinline__ void st_async_v4(uint32_t addr, float4 v, uint32_t ba
 // (modeling_whisper.py:398-406, encoder_attn of the decoder layer; q·64^-½ at
 // :310). The split's K and V blocks (contiguous in the slot's cross-KV cache)
 // are TMA-loaded into shared memory before the dependency wait; after it only
-// q is read. The 8 key splits of a (row, head) form a cluster:
-//   1. scores (one key per thread), two-pass softmax, P.V over the split;
+// q is read. Scores and P.V run on the tensor cores (tcgen05, fp32 TMEM
+// accumulators) with fp32-equivalent operands split into bf16 hi/lo pairs:
+//   S^T[64 keys x 8] = K_box[64 x 64] . [q_hi; q_lo; 0]^T   (3 boxes, M = 64)
+//   s = S[:, 0] + S[:, 1]                                    (q = q_hi + q_lo)
+//   O^T[64 dims x 8] = V^T[64 x 192] . [p_hi; p_lo; 0]^T     (V as the MN-major
+//   A operand straight from the TMA box, M = 64)
+// so the CUDA cores only do the softmax, the split merge and the cross-o tail.
+// The 8 key splits of a (row, head) form a cluster:
+//   1. scores, two-pass softmax (exp kept unnormalised), P.V over the split;
 //   2. every split st.async's (o[64], max, sum) into every rank's shared
 //      memory (completion on that rank's mbarrier: no cluster-wide fence) and
 //      each rank merges the 8 splits in split order (identical on all ranks);
 //   3. rank s computes output features [s*d/8, +d/8) of Wo[:, h*64 .. +64].o_h
 //      -- its 16*d-byte weight slice is bulk-copied into the dead K buffer as
-//      soon as the scores are done -- and stores them as head h's partial.
-// The cross-o GEMV launch of the unfused chain disappears; every reduction
-// order depends only on d and key positions, never on the batch.
+//      soon as the score MMAs retired -- and stores them as head h's partial.
+// Every reduction order depends only on d and key positions, never on the batch.
+constexpr int kXaQOff = 2 * kXaKeys * 128;                // B operand [q_hi; q_lo; 0] (1 KB)
+constexpr int kXaPOff = kXaQOff + 1024;                   // B operand [p_hi; p_lo; 0] (3 x 1 KB)
+constexpr int kXaBarOff = kXaPOff + 3 * 1024;
+constexpr int kXaSmem = 1024 + kXaBarOff + 64;          // (align) K, V, q / p operands, mbarriers
+constexpr uint32_t kXaIdescS = umma_idesc_bf16(64, 8);                 // K-major A and B
+constexpr uint32_t kXaIdescO = umma_idesc_bf16(64, 8) | (1u << 15);    // A (V^T) MN-major
+
+__device__ __forceinline__ void tmem_ld2(uint32_t taddr, uint32_t& a, uint32_t& b) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
+               : "=r"(a), "=r"(b) : "r"(taddr));
+}
+// element (row n, k) of a K-major SW128 operand tile with 128-byte rows
+__device__ __forceinline__ int sw128_off(int n, int k) {
+  return n * 128 + ((((k >> 3) ^ n) & 7) << 4) + (k & 7) * 2;
+}
+
 __global__ void __launch_bounds__(kXaThreads, 4)
 cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, int layer,
                   const Partials xq, float q_scale, const uint16_t* __restrict__ wo_pack,
                   float* __restrict__ part_o) {
   extern __shared__ uint8_t xa_raw[];
-  uint8_t* xa_smem = xa_raw + ((1024 - (smem_u32(xa_raw) & 1023)) & 1023);   // TMA swizzle atoms
-  __shared__ __align__(16) float qs[64];
+  uint8_t* xa_smem = xa_raw + ((1024 - (smem_u32(xa_raw) & 1023)) & 1023);   // swizzle atoms
   __shared__ __align__(16) float oh[64];
+  __shared__ __align__(16) float ol[64];
   __shared__ __align__(16) float push[kXSplits][kXaPush];   // split results (pushed by every rank)
-  __shared__ float sc[kXaKeys], redm[8], reds[8];
-  __shared__ __align__(16) float op[kXaThreads / 32][64];
+  __shared__ float redm[4], reds[4];
+  __shared__ uint32_t tmem_slot;
   const int r = blockIdx.x, h = blockIdx.y, sp = blockIdx.z, tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
   if (tid == 0) trace_mark(st, 0);
-  pdl_trigger();
   if (r >= *st.n_active) return;                 // whole cluster (same row) leaves together
   const int slot = st.active[r];
   // (no done-slot early exit here: it would put a dependent load in front of
@@ -935,16 +987,22 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
   const int k0 = sp * kXaKeys, nk = min(1500, k0 + kXaKeys) - k0;
   uint8_t* Ks = xa_smem;
   uint8_t* Vs = xa_smem + kXaKeys * 128;
+  uint8_t* Qs = xa_smem + kXaQOff;
+  uint8_t* Ps = xa_smem + kXaPOff;
   const uint16_t* Wo = reinterpret_cast<const uint16_t*>(Ks);   // [d/8][64], after the scores
-  uint64_t* barK = reinterpret_cast<uint64_t*>(xa_smem + 2 * kXaKeys * 128);
+  uint64_t* barK = reinterpret_cast<uint64_t*>(xa_smem + kXaBarOff);
   uint64_t* barV = barK + 1;
   uint64_t* barW = barK + 2;
   uint64_t* barM = barK + 3;                     // the 8 split results landed (st.async)
+  uint64_t* barS = barK + 4;                     // score MMAs retired
+  uint64_t* barO = barK + 5;                     // P.V MMAs retired
   if (tid == 0) {
     mbar_init(barK, 1);
     mbar_init(barV, 1);
     mbar_init(barW, 1);
     mbar_init(barM, 1);
+    mbar_init(barS, 1);
+    mbar_init(barO, 1);
     fence_barrier_init();
     // K and V of the split: 3 TMA boxes of 64 keys each (128B-swizzled rows;
     // keys past the slot's 1500 are masked), cross-KV never depends on the
@@ -963,7 +1021,18 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
       tma_load_2d_hint(Vs + bx * 64 * 128, &tm, barV, 0, row_v + bx * 64, stream);
     mbar_arrive_expect_tx(barM, kXSplits * kXaPush * 4);
   }
+  if (warp == 1) tmem_alloc(&tmem_slot, 32);     // S: cols 0..23 (3 boxes x 8), O: 24..31
+  if (tid == 32) trace_mark(st, 4);
+  // rows 2..7 of the q / p operands stay zero (N = 8, only hi and lo are used)
+  for (int i = tid; i < 4 * 1024 / 16; i += kXaThreads) {
+    const int row = (i * 16 / 128) & 7;
+    if (row >= 2) reinterpret_cast<uint4*>(Qs)[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  tc_fence_before();
   __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+  pdl_trigger();                                 // (after the TMEM allocation, see gemv_kernel)
   cluster_arrive_relaxed();                      // every rank's barM is initialised
   const float bq = tid < 64 ? bf16_to_f32(xq.bias[h * 64 + tid]) : 0.f;
   pdl_wait();
@@ -971,98 +1040,124 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
   if (tid < 64) {
     const float* pp = xq.p + size_t(r) * xq.n + h * 64 + tid;
     const float a = sum_splits(pp, size_t(kRows) * xq.n, xq.splits);
-    qs[tid] = (a + bq) * q_scale;
+    const float qv = (a + bq) * q_scale;
+    uint16_t hi, lo;
+    split_hilo(qv, hi, lo);
+    *reinterpret_cast<uint16_t*>(Qs + sw128_off(0, tid)) = hi;
+    *reinterpret_cast<uint16_t*>(Qs + sw128_off(1, tid)) = lo;
   }
+  fence_proxy_async_smem();                      // generic smem writes -> tensor core
   __syncthreads();
-  float q[64];                                   // (broadcast reads)
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const float4 v = *reinterpret_cast<const float4*>(qs + 4 * j);
-    q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
-  }
-  mbar_wait(barK, 0);
-  float mloc = -INFINITY;
-  if (tid < nk) {
-    // key row tid, logical chunk j at physical chunk j ^ (tid & 7) (the TMA
-    // 128B swizzle): conflict-free, q in registers, dims summed in order
-    const uint8_t* kr = Ks + (tid >> 6) * 64 * 128 + (tid & 63) * 128;
-    const int sw = tid & 7;
-    float s = 0.f;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const uint4 w = *reinterpret_cast<const uint4*>(kr + ((j ^ sw) << 4));
-      s = fmaf(q[8 * j + 0], __uint_as_float(w.x << 16), s);
-      s = fmaf(q[8 * j + 1], __uint_as_float(w.x & 0xFFFF0000u), s);
-      s = fmaf(q[8 * j + 2], __uint_as_float(w.y << 16), s);
-      s = fmaf(q[8 * j + 3], __uint_as_float(w.y & 0xFFFF0000u), s);
-      s = fmaf(q[8 * j + 4], __uint_as_float(w.z << 16), s);
-      s = fmaf(q[8 * j + 5], __uint_as_float(w.z & 0xFFFF0000u), s);
-      s = fmaf(q[8 * j + 6], __uint_as_float(w.w << 16), s);
-      s = fmaf(q[8 * j + 7], __uint_as_float(w.w & 0xFFFF0000u), s);
-    }
-    sc[tid] = s;
-    mloc = s;
-  }
-  // block max and sum with one barrier each (separate per-warp slots, so no
-  // trailing barrier; same reduction order as block_max / block_sum_fixed)
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
-  if (lane == 0) redm[warp] = mloc;
-  __syncthreads();                               // (also retires every K read)
-  float m = -INFINITY;
-#pragma unroll
-  for (int w = 0; w < kXaThreads / 32; ++w) m = fmaxf(m, redm[w]);
   if (tid == 0) {
-    // the K buffer is dead: fetch this rank's cross-o slice into it
-    fence_proxy_async_smem();
+    mbar_wait(barK, 0);
+    trace_mark(st, 5);
+    tc_fence_after();
+    const uint64_t bq_desc = umma_desc_sw128(smem_u32(Qs));
+#pragma unroll
+    for (int bx = 0; bx < 3; ++bx) {
+      const uint64_t ak = umma_desc_sw128(smem_u32(Ks + bx * 64 * 128));
+#pragma unroll
+      for (int k = 0; k < 4; ++k)                // 16 dims per MMA: +32 B = +2 in the address
+        umma_bf16_ss(tmem + bx * 8, ak + 2 * k, bq_desc + 2 * k, kXaIdescS, k != 0);
+    }
+    umma_commit(barS);
+    trace_mark(st, 6);
+    // the K buffer is dead once the score MMAs retired: fetch this rank's
+    // cross-o slice into it
+    mbar_wait(barS, 0);
     mbar_arrive_expect_tx(barW, 16 * d);
     bulk_load(Ks, wo_pack + size_t(h * kXSplits + sp) * d8 * 64, 16 * d, barW);
   }
-  float e = 0.f;
-  if (tid < nk) {
-    e = exp2f((sc[tid] - m) * kLog2e);
-    sc[tid] = e;
-  }
-  float es = e;
+  // softmax over the split (warps 0..3; TMEM quadrant w holds accumulator rows
+  // 16w..16w+15 in its lanes 0..15 for M = 64): key of box j = 64 j + 16 w + lane
+  const bool sm = warp < 4;
+  const bool own = sm && lane < 16;
+  float s3[3], e3[3];
+  float m = -INFINITY, l = 0.f;
+  if (sm) {
+    mbar_wait(barS, 0);
+    tc_fence_after();
+    uint32_t a[3], b[3];
+    const uint32_t lane_base = uint32_t(warp * 32) << 16;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
-  if (lane == 0) reds[warp] = es;
-  __syncthreads();                               // (also publishes sc[])
-  float l = 0.f;
+    for (int j = 0; j < 3; ++j) tmem_ld2(tmem + lane_base + j * 8, a[j], b[j]);
+    tmem_wait_ld();
+    float mloc = -INFINITY;
 #pragma unroll
-  for (int w = 0; w < kXaThreads / 32; ++w) l += reds[w];
-  mbar_wait(barV, 0);
-  float o0 = 0.f, o1 = 0.f;
-  const int vch = lane >> 2, vwo = (lane & 3) * 4;     // dims (2 lane, 2 lane + 1)
-#pragma unroll 4
-  for (int t = warp; t < nk; t += kXaThreads / 32) {
-    const uint32_t w = *reinterpret_cast<const uint32_t*>(
-        Vs + (t >> 6) * 64 * 128 + (t & 63) * 128 + ((vch ^ (t & 7)) << 4) + vwo);
-    const float pe = sc[t];
-    o0 = fmaf(pe, __uint_as_float(w << 16), o0);
-    o1 = fmaf(pe, __uint_as_float(w & 0xFFFF0000u), o1);
+    for (int j = 0; j < 3; ++j) {
+      const int key = 64 * j + 16 * warp + lane;
+      s3[j] = (own && key < nk) ? __uint_as_float(a[j]) + __uint_as_float(b[j]) : -INFINITY;
+      mloc = fmaxf(mloc, s3[j]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
+    if (lane == 0) redm[warp] = mloc;
+    named_bar_sync(1, 128);
+    m = fmaxf(fmaxf(redm[0], redm[1]), fmaxf(redm[2], redm[3]));
+    float es = 0.f;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      e3[j] = s3[j] == -INFINITY ? 0.f : exp2f((s3[j] - m) * kLog2e);
+      es += e3[j];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
+    if (lane == 0) reds[warp] = es;
+    // p = e as a bf16 hi/lo pair: rows 0 and 1 of the K-major P operand (k-block j)
+    if (own) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        uint16_t hi, lo;
+        split_hilo(e3[j], hi, lo);
+        const int kk = 16 * warp + lane;
+        *reinterpret_cast<uint16_t*>(Ps + j * 1024 + sw128_off(0, kk)) = hi;
+        *reinterpret_cast<uint16_t*>(Ps + j * 1024 + sw128_off(1, kk)) = lo;
+      }
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(1, 128);
+    l = (reds[0] + reds[1]) + (reds[2] + reds[3]);
+    if (tid == 0) {
+      mbar_wait(barV, 0);
+      tc_fence_after();
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const uint64_t bp = umma_desc_sw128(smem_u32(Ps + j * 1024));
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {            // 16 keys per MMA: V^T rows 16k.. (2 atoms)
+          const uint64_t av = umma_desc_sw128(smem_u32(Vs + j * 64 * 128 + k * 2048));
+          umma_bf16_ss(tmem + 24, av, bp + 2 * k, kXaIdescO, (j | k) != 0);
+        }
+      }
+      umma_commit(barO);
+    }
+    mbar_wait(barO, 0);
+    tc_fence_after();
+    uint32_t oa, ob;
+    tmem_ld2(tmem + lane_base + 24, oa, ob);
+    tmem_wait_ld();
+    if (own) ol[16 * warp + lane] = __uint_as_float(oa) + __uint_as_float(ob);
   }
-  op[warp][2 * lane] = o0;
-  op[warp][2 * lane + 1] = o1;
+  tc_fence_before();
   __syncthreads();
+  if (warp == 1) tmem_dealloc(tmem, 32);
   // 2. push (o, max, sum) to every rank; merge the 8 splits in split order.
-  // Thread (rank dst, chunk ch) sums dims 4ch..4ch+3 over the warps itself
-  // and st.async's them (8 ranks x 16 chunks + 8 (max, sum) stores)
+  // Thread (rank dst, chunk ch) st.async's dims 4ch..4ch+3 (8 ranks x 16
+  // chunks + 8 (max, sum) stores)
+  if (tid == 0) { redm[0] = m; reds[0] = l; }
+  __syncthreads();
   cluster_wait();                                // (all ranks arrived long ago)
   if (tid < kXSplits * 16) {
     const int dst = tid >> 4, ch = tid & 15;
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int w = 0; w < kXaThreads / 32; ++w) {
-      const float4 v = *reinterpret_cast<const float4*>(&op[w][4 * ch]);
-      a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
-    }
+    const float4 a = *reinterpret_cast<const float4*>(&ol[4 * ch]);
     st_async_v4(dsmem_addr(&push[sp][4 * ch], dst), a, dsmem_addr(barM, dst));
   } else if (tid < kXSplits * 16 + kXSplits) {
     const int dst = tid - kXSplits * 16;
-    st_async_v4(dsmem_addr(&push[sp][64], dst), make_float4(m, l, 0.f, 0.f), dsmem_addr(barM, dst));
+    st_async_v4(dsmem_addr(&push[sp][64], dst), make_float4(redm[0], reds[0], 0.f, 0.f),
+                dsmem_addr(barM, dst));
   }
   mbar_wait(barM, 0);
+  if (tid == 0) trace_mark(st, 7);
   if (tid < 64) {
     float M = -INFINITY;
 #pragma unroll
@@ -1113,282 +1208,9 @@ int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int lay
   DM_REQUIRE(16 * st.d <= kXaKeys * 128 && st.heads <= kMaxHeads,
              "cross-attn: the cross-o slice must fit the K buffer");
   DM_SMEM_ATTR(cross_attn_kernel, kXaSmem);
-  DM_CHECK_CUDA(launch_pdl_cluster(cross_attn_kernel, dim3(kRows, st.heads, kXSplits),
+  DM_CHECK_CUDA(launch_pdl_cluster(cross_attn_kernel, dim3(st.grid_rows, st.heads, kXSplits),
                                    dim3(kXaThreads), dim3(1, 1, kXSplits), kXaSmem, stream,
                                    xkv_map, st, layer, xq, q_scale, wo_pack, part_o));
-  return 0;
-}
-
-// ------------------------------------------------------------ streaming cross-attention
-// The same arithmetic as cross_attn_kernel (bit for bit: every per-split
-// reduction, the split merge and the cross-o tail run in the same order), laid
-// out for many active rows: a persistent grid (2 CTAs per SM) pulls
-// (row, head) items from a global ticket counter; per CTA a producer warp
-// streams each item's 8 split K/V blocks (48 KB each) and then its cross-o
-// weight slice through a ring of kXsStages 48 KB stages while 6 consumer
-// warps compute split after split -- no cluster, no per-CTA prologue per
-// split, and the K/V stream never waits for a split's softmax / merge / tail.
-// The step graph uses it when the active rows give at least kXsMinItems
-// (row, head) items (the cluster kernel keeps low-row latency).
-constexpr int kXsStages = 2;
-constexpr int kXsStageBytes = 2 * kXaKeys * 128;                 // K + V of one split
-constexpr int kXsConsumers = kXaThreads;                         // 6 warps, one key per thread
-constexpr int kXsThreads = kXsConsumers + 32;                    // + producer warp
-constexpr int kXsSmem = 1024 + kXsStages * kXsStageBytes + 256;  // (align) ring + barriers
-constexpr int kXsCtasPerSm = 2;
-
-__device__ __forceinline__ int xs_wo_splits_per_stage(int d) {
-  int ws = kXSplits;
-  while (ws > 1 && ws * 16 * d > kXsStageBytes) ws >>= 1;
-  return ws;
-}
-
-__global__ void __launch_bounds__(kXsThreads, kXsCtasPerSm)
-cross_attn_stream_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, int layer,
-                         const Partials xq, float q_scale, const uint16_t* __restrict__ wo_pack,
-                         float* __restrict__ part_o, int* __restrict__ ctr) {
-  extern __shared__ uint8_t xs_raw[];
-  uint8_t* ring = xs_raw + ((1024 - (smem_u32(xs_raw) & 1023)) & 1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + kXsStages * kXsStageBytes);
-  uint64_t* empty = full + kXsStages;
-  int* stage_item = reinterpret_cast<int*>(empty + kXsStages);   // [kXsStages]
-  __shared__ __align__(16) float qs[64];
-  __shared__ __align__(16) float oh[64];
-  __shared__ __align__(16) float os[kXSplits][kXaPush];          // per-split (o[64], max, sum)
-  __shared__ float sc[kXaKeys], redm[8], reds[8];
-  __shared__ __align__(16) float op[kXsConsumers / 32][64];
-  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
-  const int d = st.d, H = st.heads, d8 = d / 8;
-  const int ws = xs_wo_splits_per_stage(d), wchunks = kXSplits / ws;
-  if (tid == 0) {
-    trace_mark(st, 0);
-    for (int i = 0; i < kXsStages; ++i) {
-      mbar_init(full + i, 1);
-      mbar_init(empty + i, 1);
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-  const int items = *st.n_active * H;            // host-set before the graph runs
-  if (warp == kXsConsumers / 32) {
-    // ---------------- producer (one lane): tickets -> TMA into the ring
-    if (lane == 0) {
-      tma_prefetch_desc(&tm);
-      const uint64_t stream = l2_policy_evict_first();
-      int stage = 0;
-      uint32_t ph = 0;
-      auto next_stage = [&](int item) {
-        mbar_wait(empty + stage, ph ^ 1);
-        stage_item[stage] = item;
-      };
-      auto advance = [&]() {
-        if (++stage == kXsStages) { stage = 0; ph ^= 1; }
-      };
-      for (;;) {
-        const int item = atomicAdd(ctr, 1);
-        if (item >= items) {
-          next_stage(-1);                          // end marker for the consumers
-          mbar_arrive(full + stage);
-          break;
-        }
-        const int r = item / H, h = item % H;
-        const int slot = st.active[r];
-        const int row_k0 = (((layer * st.max_slots + slot) * 2 + 0) * H + h) * 1500;
-        for (int sp = 0; sp < kXSplits; ++sp) {
-          next_stage(item);
-          uint8_t* Ks = ring + stage * kXsStageBytes;
-          const int row_k = row_k0 + sp * kXaKeys, row_v = row_k + H * 1500;
-          mbar_arrive_expect_tx(full + stage, kXsStageBytes);
-#pragma unroll
-          for (int bx = 0; bx < 3; ++bx)
-            tma_load_2d_hint(Ks + bx * 64 * 128, &tm, full + stage, 0, row_k + bx * 64, stream);
-#pragma unroll
-          for (int bx = 0; bx < 3; ++bx)
-            tma_load_2d_hint(Ks + kXaKeys * 128 + bx * 64 * 128, &tm, full + stage, 0,
-                             row_v + bx * 64, stream);
-          advance();
-        }
-        for (int c = 0; c < wchunks; ++c) {
-          next_stage(item);
-          mbar_arrive_expect_tx(full + stage, ws * 16 * d);
-          bulk_load(ring + stage * kXsStageBytes,
-                    wo_pack + size_t(h * kXSplits + c * ws) * d8 * 64, ws * 16 * d, full + stage);
-          advance();
-        }
-      }
-      // every ticket of this launch is taken once all CTAs got an out-of-range
-      // one: the last CTA resets the counter for the next launch of the layer
-      __threadfence();
-      if (atomicAdd(ctr + 1, 1) == int(gridDim.x) - 1) {
-        atomicExch(ctr + 1, 0);
-        atomicExch(ctr, 0);
-      }
-    }
-    __syncwarp();
-    pdl_trigger();
-    return;
-  }
-  // ---------------- consumers (6 warps)
-  pdl_wait();
-  if (tid == 0) trace_mark(st, 1);
-  int stage = 0;
-  uint32_t ph = 0;
-  auto advance = [&]() {
-    if (++stage == kXsStages) { stage = 0; ph ^= 1; }
-  };
-  for (;;) {
-    mbar_wait(full + stage, ph);
-    const int item = stage_item[stage];
-    if (item < 0) break;
-    const int r = item / H, h = item % H;
-    if (tid < 64) {
-      const float* pp = xq.p + size_t(r) * xq.n + h * 64 + tid;
-      const float a = sum_splits(pp, size_t(kRows) * xq.n, xq.splits);
-      qs[tid] = (a + bf16_to_f32(xq.bias[h * 64 + tid])) * q_scale;
-    }
-    named_bar_sync(1, kXsConsumers);
-    float q[64];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const float4 v = *reinterpret_cast<const float4*>(qs + 4 * j);
-      q[4 * j] = v.x; q[4 * j + 1] = v.y; q[4 * j + 2] = v.z; q[4 * j + 3] = v.w;
-    }
-    for (int sp = 0; sp < kXSplits; ++sp) {
-      if (sp) mbar_wait(full + stage, ph);
-      const uint8_t* Ks = ring + stage * kXsStageBytes;
-      const uint8_t* Vs = Ks + kXaKeys * 128;
-      const int k0 = sp * kXaKeys, nk = min(1500, k0 + kXaKeys) - k0;
-      float mloc = -INFINITY;
-      if (tid < nk) {
-        const uint8_t* kr = Ks + (tid >> 6) * 64 * 128 + (tid & 63) * 128;
-        const int sw = tid & 7;
-        float s = 0.f;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint4 w = *reinterpret_cast<const uint4*>(kr + ((j ^ sw) << 4));
-          s = fmaf(q[8 * j + 0], __uint_as_float(w.x << 16), s);
-          s = fmaf(q[8 * j + 1], __uint_as_float(w.x & 0xFFFF0000u), s);
-          s = fmaf(q[8 * j + 2], __uint_as_float(w.y << 16), s);
-          s = fmaf(q[8 * j + 3], __uint_as_float(w.y & 0xFFFF0000u), s);
-          s = fmaf(q[8 * j + 4], __uint_as_float(w.z << 16), s);
-          s = fmaf(q[8 * j + 5], __uint_as_float(w.z & 0xFFFF0000u), s);
-          s = fmaf(q[8 * j + 6], __uint_as_float(w.w << 16), s);
-          s = fmaf(q[8 * j + 7], __uint_as_float(w.w & 0xFFFF0000u), s);
-        }
-        sc[tid] = s;
-        mloc = s;
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
-      if (lane == 0) redm[warp] = mloc;
-      named_bar_sync(1, kXsConsumers);
-      float m = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < kXsConsumers / 32; ++w) m = fmaxf(m, redm[w]);
-      float e = 0.f;
-      if (tid < nk) {
-        e = exp2f((sc[tid] - m) * kLog2e);
-        sc[tid] = e;
-      }
-      float es = e;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
-      if (lane == 0) reds[warp] = es;
-      named_bar_sync(1, kXsConsumers);
-      float l = 0.f;
-#pragma unroll
-      for (int w = 0; w < kXsConsumers / 32; ++w) l += reds[w];
-      float o0 = 0.f, o1 = 0.f;
-      const int vch = lane >> 2, vwo = (lane & 3) * 4;
-#pragma unroll 4
-      for (int t = warp; t < nk; t += kXsConsumers / 32) {
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(
-            Vs + (t >> 6) * 64 * 128 + (t & 63) * 128 + ((vch ^ (t & 7)) << 4) + vwo);
-        const float pe = sc[t];
-        o0 = fmaf(pe, __uint_as_float(w << 16), o0);
-        o1 = fmaf(pe, __uint_as_float(w & 0xFFFF0000u), o1);
-      }
-      op[warp][2 * lane] = o0;
-      op[warp][2 * lane + 1] = o1;
-      named_bar_sync(1, kXsConsumers);           // every K/V read of the stage is done
-      if (tid == 0) mbar_arrive(empty + stage);
-      advance();
-      if (tid < 16) {
-        // the cluster kernel's push: float4 chunk sums over the warps in order
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int w = 0; w < kXsConsumers / 32; ++w) {
-          const float4 v = *reinterpret_cast<const float4*>(&op[w][4 * tid]);
-          a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
-        }
-        *reinterpret_cast<float4*>(&os[sp][4 * tid]) = a;
-      } else if (tid == 16) {
-        os[sp][64] = m;
-        os[sp][65] = l;
-      }
-    }
-    named_bar_sync(1, kXsConsumers);
-    if (tid < 64) {
-      float M = -INFINITY;
-#pragma unroll
-      for (int s = 0; s < kXSplits; ++s) M = fmaxf(M, os[s][64]);
-      float Ls = 0.f, O = 0.f;
-#pragma unroll
-      for (int s = 0; s < kXSplits; ++s) {
-        const float f = exp2f((os[s][64] - M) * kLog2e);
-        Ls += os[s][65] * f;
-        O += os[s][tid] * f;
-      }
-      oh[tid] = O / Ls;
-    }
-    named_bar_sync(1, kXsConsumers);
-    const int ch = tid & 7;
-    float ov[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) ov[j] = oh[ch * 8 + j];
-    for (int c = 0; c < wchunks; ++c) {
-      mbar_wait(full + stage, ph);
-      const uint16_t* Wc = reinterpret_cast<const uint16_t*>(ring + stage * kXsStageBytes);
-      for (int si = 0; si < ws; ++si) {
-        const int sp = c * ws + si;
-        const uint16_t* Wo = Wc + size_t(si) * d8 * 64;
-        float* dst = part_o + (size_t(h) * kRows + r) * d + sp * d8;
-        for (int n = tid >> 3; n < d8; n += kXsConsumers / 8) {
-          const uint4 w = *reinterpret_cast<const uint4*>(Wo + n * 64 + ch * 8);
-          float acc = ov[0] * __uint_as_float(w.x << 16);
-          acc = fmaf(ov[1], __uint_as_float(w.x & 0xFFFF0000u), acc);
-          acc = fmaf(ov[2], __uint_as_float(w.y << 16), acc);
-          acc = fmaf(ov[3], __uint_as_float(w.y & 0xFFFF0000u), acc);
-          acc = fmaf(ov[4], __uint_as_float(w.z << 16), acc);
-          acc = fmaf(ov[5], __uint_as_float(w.z & 0xFFFF0000u), acc);
-          acc = fmaf(ov[6], __uint_as_float(w.w << 16), acc);
-          acc = fmaf(ov[7], __uint_as_float(w.w & 0xFFFF0000u), acc);
-          acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-          acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-          acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-          if (ch == 0) dst[n] = acc;
-        }
-      }
-      named_bar_sync(1, kXsConsumers);
-      if (tid == 0) mbar_arrive(empty + stage);
-      advance();
-    }
-  }
-  if (tid == 0) trace_mark(st, 3);
-}
-
-int launch_cross_attn_stream(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
-                             const Partials& xq, float q_scale, const uint16_t* wo_pack,
-                             float* part_o, int* ctr, cudaStream_t stream) {
-  DM_REQUIRE(xq.p != nullptr && xq.n == st.d && xq.bias != nullptr && xq.splits >= 1 &&
-                 xq.splits <= kMaxSplits, "cross-attn: q partials");
-  DM_REQUIRE(wo_pack != nullptr && part_o != nullptr && ctr != nullptr, "cross-attn: operands");
-  DM_REQUIRE(st.d % 64 == 0 && 16 * st.d <= kXsStageBytes && st.heads <= kMaxHeads,
-             "cross-attn: shapes");
-  DM_SMEM_ATTR(cross_attn_stream_kernel, kXsSmem);
-  DM_CHECK_CUDA(launch_pdl(cross_attn_stream_kernel, dim3(kNumSMs * kXsCtasPerSm),
-                           dim3(kXsThreads), kXsSmem, stream, xkv_map, st, layer, xq, q_scale,
-                           wo_pack, part_o, ctr));
   return 0;
 }
 

@@ -43,6 +43,7 @@ struct DecodeState {
   int pages_per_slot;    // page-table width (7 -> 448 positions)
   int eot;
   int prompt_len;
+  int grid_rows;               // rows the step graph's per-row grids cover (>= n_active)
   const int32_t* prompt;       // [prompt_len]
   // slot bookkeeping
   const int32_t* active;       // [kRows] slot of row i (host-set before a step graph runs)
@@ -113,7 +114,9 @@ struct GemvArgs {
   int splits;              // K splits (fixed per shape; never depends on rows)
   int kb_per;              // 64-wide k-blocks per split
   int stages;              // weight ring depth (whole slice prefetched when it fits)
-  int rgroups;             // row groups (grid z): CTA z owns rows [z * 64 / rgroups, +64 / rgroups)
+  int rgroups;             // row groups (grid z): CTA z owns rows [z * xrows / rgroups, +xrows / rgroups)
+  int xrows;               // rows the activation buffer holds (multiple of 16, >= active rows)
+  int gx;                  // CTAs per K split (grid x); tiles c, c + gx, ... per CTA
   int counter_base;
   float* part;             // GV_PARTIAL output [splits][kRows][N]
   uint16_t *yh, *yl;       // GV_GELU_HILO targets [kRows, N]
@@ -131,6 +134,10 @@ int make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer
                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
 // Plan (splits, kb_per, stages) of a projection; depends only on (N, K, epilogue).
 GemvArgs gemv_plan(int N, int K, int epi);
+// The same plan for a step graph whose active rows are <= rows: the
+// activation buffer, row groups, ring depth and grid shrink with the rows
+// (two CTAs per SM when they fit); the K split -- hence every value -- stays.
+GemvArgs gemv_plan_for_rows(const GemvArgs& base, int rows);
 size_t gemv_part_floats(int N, int K, int epi);   // scratch for its partial sums
 int launch_gemv(const DecodeState& st, const TcGemvMaps& maps, const GemvArgs& a,
                 cudaStream_t stream);
@@ -161,14 +168,6 @@ constexpr int kMaxHeads = 20;   // per-head partial splits a LayerNorm may reduc
 int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
                       const Partials& xq, float q_scale, const uint16_t* wo_pack, float* part_o,
                       cudaStream_t stream);
-// The same computation for many active rows: persistent CTAs pull (row, head)
-// items from ctr[0] (ctr[1] counts finished CTAs; both reset by the last CTA,
-// so each layer needs its own zero-initialised pair) and stream K/V and the
-// cross-o slice through a TMA ring. Bitwise equal to launch_cross_attn.
-constexpr int kXsMinItems = 2 * 148;   // default: stream when rows x heads >= this
-int launch_cross_attn_stream(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
-                             const Partials& xq, float q_scale, const uint16_t* wo_pack,
-                             float* part_o, int* ctr, cudaStream_t stream);
 // [d, d] cross-o weight -> the per-(head, split) contiguous slices the cross-attention loads
 int repack_xo(const uint16_t* wo, uint16_t* out, int d, int H, cudaStream_t stream);
 int launch_finalize(const DecodeState& st, cudaStream_t stream);

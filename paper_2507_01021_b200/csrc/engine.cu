@@ -192,6 +192,9 @@ struct UploadRing {
 };
 
 // ------------------------------------------------------------ Whisper engine
+constexpr int kRowBuckets = 9;
+constexpr int kRowBucket[kRowBuckets] = {1, 2, 4, 8, 16, 24, 32, 48, kRows};
+
 struct WhisperEngine {
   int device = 0;                      // the CUDA device of every buffer/stream below
   UploadRing ring;
@@ -239,14 +242,6 @@ struct WhisperEngine {
   std::vector<void*> allocs;
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t step_exec = nullptr;
-  // cross-attention variant: 0 by active rows (streaming kernel when
-  // rows x heads >= xs_min_items), 1 always the cluster kernel, 2 always streaming
-  int xa_mode = 0;
-  int xs_min_items = std::getenv("DM_XS_MIN_ITEMS") ? std::atoi(std::getenv("DM_XS_MIN_ITEMS"))
-                                                    : kXsMinItems;
-  bool use_xs(int n_active) const {
-    return xa_mode == 2 || (xa_mode == 0 && n_active * H >= xs_min_items);
-  }
   cudaGraph_t step_graph = nullptr;
   int gemv_counter_base = 0;
   std::vector<TcGemvMaps> maps;   // [Ld * 6 + 1]: per layer qkv,o,xq,xo,fc1,fc2; LM head
@@ -262,13 +257,12 @@ struct WhisperEngine {
     int32_t* n_active_dev = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t done = nullptr;
-    cudaGraph_t graph = nullptr;
-    cudaGraphExec_t exec = nullptr;
-    // the same step with the streaming cross-attention (many active rows)
-    cudaGraph_t graph_xs = nullptr;
-    cudaGraphExec_t exec_xs = nullptr;
-    int n_active_host = 0;         // rows of the last set_active (picks the graph)
-    int* xs_ctr = nullptr;         // [Ld][2] ticket / finished-CTA counters
+    // one step graph per row bucket: per-row grids sized to the bucket, so a
+    // step with few active rows does not schedule thousands of empty CTAs
+    // (every kernel computes the same values whatever the grid)
+    cudaGraph_t graph[kRowBuckets] = {};
+    cudaGraphExec_t exec[kRowBuckets] = {};
+    int n_active_host = 0;
     // K-split partial sums of the linear projections (consumer-reduced)
     float *p_qkv = nullptr, *p_o = nullptr, *p_xq = nullptr, *p_xo = nullptr, *p_fc2 = nullptr;
   };
@@ -299,10 +293,10 @@ struct WhisperEngine {
 
   ~WhisperEngine() {
     for (auto& g : groups) {
-      if (g.exec) cudaGraphExecDestroy(g.exec);
-      if (g.graph) cudaGraphDestroy(g.graph);
-      if (g.exec_xs) cudaGraphExecDestroy(g.exec_xs);
-      if (g.graph_xs) cudaGraphDestroy(g.graph_xs);
+      for (int b = 0; b < kRowBuckets; ++b) {
+        if (g.exec[b]) cudaGraphExecDestroy(g.exec[b]);
+        if (g.graph[b]) cudaGraphDestroy(g.graph[b]);
+      }
       if (g.stream) cudaStreamDestroy(g.stream);
       if (g.done) cudaEventDestroy(g.done);
     }
@@ -372,6 +366,7 @@ static int engine_init(WhisperEngine* e) {
   st.max_slots = S; st.d = d; st.heads = e->H; st.layers = e->Ld; st.ffn = e->F;
   st.vocab = c.vocab; st.page_tokens = 64; st.pages_per_slot = 7; st.eot = c.eot;
   st.prompt_len = c.prompt_len;
+  st.grid_rows = kRows;            // debug / timing probes; step graphs use their bucket
   if (e->alloc_t(&e->prompt_dev, 8)) return 2;
   DM_CHECK_CUDA(cudaMemcpy(e->prompt_dev, c.prompt, sizeof(int32_t) * 8, cudaMemcpyHostToDevice));
   st.prompt = e->prompt_dev;
@@ -436,7 +431,6 @@ static int engine_init(WhisperEngine* e) {
                                                gemv_part_floats(c.vocab, d, GV_ARGMAX)));
     if (e->alloc_t(&gs.part, part)) return 2;
     if (e->alloc_t(&gs.counters, 4096)) return 2;
-    if (e->alloc_t(&gr.xs_ctr, size_t(e->Ld) * 2)) return 2;
     if (e->alloc_t(&gs.amax_val, size_t(tiles) * kRows)) return 2;
     if (e->alloc_t(&gs.amax_idx, size_t(tiles) * kRows)) return 2;
     gs.logits_dbg = nullptr;
@@ -575,13 +569,14 @@ static int launch_pdl_floor(cudaStream_t s) {
     ++st.trace_id;                    \
   } while (0)
 
-static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t s, bool xs) {
+static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t s, int rows) {
   DecodeState st = grp.st;        // local copy: trace_id numbers the step's kernels
   st.trace_id = 0;
+  st.grid_rows = rows;
   const int d = e->d;
   const int a = e->after_enc();
   auto gv = [&](int idx, float* part, uint16_t* yh, uint16_t* yl, const uint16_t* bias) {
-    GemvArgs g = e->plans[idx];
+    GemvArgs g = gemv_plan_for_rows(e->plans[idx], rows);
     g.bias = bias; g.part = part; g.yh = yh; g.yl = yl; g.counter_base = e->gemv_counter_base;
     return launch_gemv(st, grp.maps[idx], g, s);
   };
@@ -605,13 +600,8 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
     DM_STEP(ln(2, b0 + 6, Partials{grp.p_o, go, d, e->W(b0 + 5)}));
     DM_STEP(gv(pi + 2, grp.p_xq, nullptr, nullptr, nullptr));
     // cross-attention with the cross-o projection in its tail (per-head partials)
-    if (xs)
-      DM_STEP(launch_cross_attn_stream(st, e->xkv_map, l, Partials{grp.p_xq, gx, d, e->W(b0 + 9)},
-                                       0.125f, e->xo_pack + size_t(l) * d * d, grp.p_xo,
-                                       grp.xs_ctr + 2 * l, s));
-    else
-      DM_STEP(launch_cross_attn(st, e->xkv_map, l, Partials{grp.p_xq, gx, d, e->W(b0 + 9)},
-                                0.125f, e->xo_pack + size_t(l) * d * d, grp.p_xo, s));
+    DM_STEP(launch_cross_attn(st, e->xkv_map, l, Partials{grp.p_xq, gx, d, e->W(b0 + 9)}, 0.125f,
+                              e->xo_pack + size_t(l) * d * d, grp.p_xo, s));
     DM_STEP(ln(2, b0 + 12, Partials{grp.p_xo, e->H, d, e->W(b0 + 11)}));
     DM_STEP(gv(pi + 4, nullptr, st.hh, st.hl, e->W(b0 + 15)));
     DM_STEP(gv(pi + 5, grp.p_fc2, nullptr, nullptr, nullptr));
@@ -627,19 +617,17 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
 
 static int build_step_graph(WhisperEngine* e) {
   for (auto& grp : e->groups) {
-    for (int xs = 0; xs < 2; ++xs) {
-      cudaGraphExec_t& ex = xs ? grp.exec_xs : grp.exec;
-      cudaGraph_t& gg = xs ? grp.graph_xs : grp.graph;
-      if (ex) {
-        cudaGraphExecDestroy(ex);
-        ex = nullptr;
+    for (int b = 0; b < kRowBuckets; ++b) {
+      if (grp.exec[b]) {
+        cudaGraphExecDestroy(grp.exec[b]);
+        grp.exec[b] = nullptr;
       }
-      if (gg) {
-        cudaGraphDestroy(gg);
-        gg = nullptr;
+      if (grp.graph[b]) {
+        cudaGraphDestroy(grp.graph[b]);
+        grp.graph[b] = nullptr;
       }
       DM_CHECK_CUDA(cudaStreamBeginCapture(e->cap_stream, cudaStreamCaptureModeThreadLocal));
-      int rc = record_step(e, grp, e->cap_stream, xs != 0);
+      int rc = record_step(e, grp, e->cap_stream, kRowBucket[b]);
       cudaGraph_t g = nullptr;
       cudaError_t ce = cudaStreamEndCapture(e->cap_stream, &g);
       if (rc) {
@@ -647,11 +635,11 @@ static int build_step_graph(WhisperEngine* e) {
         return rc;
       }
       DM_CHECK_CUDA(ce);
-      gg = g;
-      DM_CHECK_CUDA(cudaGraphInstantiate(&ex, g, 0));
+      grp.graph[b] = g;
+      DM_CHECK_CUDA(cudaGraphInstantiate(&grp.exec[b], g, 0));
     }
   }
-  e->step_exec = e->groups[0].exec;     // marks "built"
+  e->step_exec = e->groups[0].exec[kRowBuckets - 1];     // marks "built"
   return 0;
 }
 
@@ -883,8 +871,10 @@ int dm_whisper_step(void* handle, int n_steps, void* stream) {
   if (!e->step_exec)
     if (int rc = build_step_graph(e)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  auto exec_of = [&](const WhisperEngine::Group& grp) {
-    return e->use_xs(grp.n_active_host) ? grp.exec_xs : grp.exec;
+  auto exec_of = [](const WhisperEngine::Group& grp) {
+    int b = 0;
+    while (b < kRowBuckets - 1 && kRowBucket[b] < grp.n_active_host) ++b;
+    return grp.exec[b];
   };
   if (e->groups.size() == 1) {
     cudaGraphExec_t ex = exec_of(e->groups[0]);
@@ -925,22 +915,28 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
   // GPU-side launch/complete latency, not host submission
   // probes run on decode group 0's state at its current active rows
   WhisperEngine::Group& grp = e->groups[0];
+  DecodeState pst = grp.st;    // per-row grids sized like the step graph's bucket
+  {
+    int b = 0;
+    while (b < kRowBuckets - 1 && kRowBucket[b] < grp.n_active_host) ++b;
+    pst.grid_rows = kRowBucket[b];
+  }
   const int d = e->d;
   auto gv = [&](int idx, float* part, uint16_t* yh, uint16_t* yl, const uint16_t* bias,
                 cudaStream_t cs) {
-    GemvArgs g = e->plans[idx];
+    GemvArgs g = gemv_plan_for_rows(e->plans[idx], pst.grid_rows);
     g.bias = bias; g.part = part; g.yh = yh; g.yl = yl; g.counter_base = e->gemv_counter_base;
-    return launch_gemv(grp.st, grp.maps[idx], g, cs);
+    return launch_gemv(pst, grp.maps[idx], g, cs);
   };
   auto launch_one = [&](int layer, cudaStream_t cs) -> int {
     const int b0 = e->dec_layer_base(layer), pi = layer * 6;
     switch (which) {
       case 0:
-        return launch_cross_attn(grp.st, e->xkv_map, layer,
+        return launch_cross_attn(pst, e->xkv_map, layer,
                                  Partials{grp.p_xq, e->plans[pi + 2].splits, d, e->W(b0 + 9)},
                                  0.125f, e->xo_pack + size_t(layer) * d * d, grp.p_xo, cs);
       case 1:
-        return launch_self_attn(grp.st, layer,
+        return launch_self_attn(pst, layer,
                                 Partials{grp.p_qkv, e->plans[pi].splits, 3 * d, e->W(b0 + 3)},
                                 0.125f, cs);
       case 2: return gv(e->Ld * 6, nullptr, nullptr, nullptr, nullptr, cs);
@@ -948,18 +944,13 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
         LnArgs la{};
         la.mode = 2; la.g = e->W(b0 + 6); la.b = e->W(b0 + 7);
         la.res = Partials{grp.p_o, e->plans[pi + 1].splits, d, e->W(b0 + 5)};
-        return launch_ln(grp.st, la, cs);
+        return launch_ln(pst, la, cs);
       }
       case 4: return gv(pi + 2, grp.p_xq, nullptr, nullptr, nullptr, cs);
       case 5: return gv(pi + 5, grp.p_fc2, nullptr, nullptr, nullptr, cs);
       case 6: return launch_pdl_floor(cs);
-      case 7: return gv(pi + 4, nullptr, grp.st.hh, grp.st.hl, e->W(b0 + 15), cs);
+      case 7: return gv(pi + 4, nullptr, pst.hh, pst.hl, e->W(b0 + 15), cs);
       case 8: return gv(pi + 0, grp.p_qkv, nullptr, nullptr, nullptr, cs);
-      case 9:
-        return launch_cross_attn_stream(grp.st, e->xkv_map, layer,
-                                        Partials{grp.p_xq, e->plans[pi + 2].splits, d, e->W(b0 + 9)},
-                                        0.125f, e->xo_pack + size_t(layer) * d * d, grp.p_xo,
-                                        grp.xs_ctr + 2 * layer, cs);
       default: set_error("unknown kernel id"); return 1;
     }
   };
@@ -1044,10 +1035,6 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
     }
     case 4: e->enc_stop = int(bytes); return 0;
     case 7: e->enc_tap = bytes != 0; return 0;
-    case 14:         // cross-attention variant: 0 by active rows, 1 cluster, 2 streaming
-      DM_REQUIRE(bytes <= 2, "cross-attention mode must be 0, 1 or 2");
-      e->xa_mode = int(bytes);
-      return 0;
     case 10: {       // step timeline tap on (graph re-captured with per-kernel globaltimer marks)
       if (!e->groups[0].st.trace) {
         unsigned long long* t = nullptr;

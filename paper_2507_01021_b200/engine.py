@@ -302,19 +302,13 @@ class WhisperGPU:
         return self._done, self._ngen, self._tokens.reshape(self.max_slots, MAX_TOKENS)
 
     def debug(self, which: int, out: np.ndarray | None = None) -> np.ndarray | None:
-        if which in (3, 8, 14, 15):
+        if which in (3, 8, 15):
             _native.check(self.lib.dm_whisper_debug(self.handle, which, None, 0, self._s))
             return None
         _native.check(self.lib.dm_whisper_debug(self.handle, which,
                                                 out.ctypes.data_as(C.c_void_p), out.nbytes,
                                                 self._s))
         return out
-
-    def set_cross_attn_mode(self, mode: int) -> None:
-        """Cross-attention kernel of later steps: 0 by active rows (streaming
-        kernel when rows x heads is large), 1 cluster kernel, 2 streaming kernel
-        (bitwise-identical results)."""
-        _native.check(self.lib.dm_whisper_debug(self.handle, 14, None, int(mode), self._s))
 
     def counters(self) -> dict:
         out = np.zeros(4, np.int64)

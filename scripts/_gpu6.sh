@@ -1,0 +1,12 @@
+python -m paper_2507_01021_b200.build > /dev/null
+timeout 300 python scripts/step_trace.py whisper-large-v3 64 32 8 1 > gpurun_out/trace_tc.json 2>&1
+python - <<'P'
+import json
+d=json.load(open("gpurun_out/trace_tc.json"))
+for rows,v in d.items():
+    print(rows, v["step_us"], {k:(x["gap_us"],x["span_us"]) for k,x in v["by_kind"].items()})
+    for r in v["layer0"]:
+        if r["k"].endswith("xattn"): print(r)
+P
+timeout 300 python scripts/xattn_compare.py whisper-large-v3 64 32 16 8 1 2>&1 | head -5
+timeout 600 python -m pytest tests/test_gpu_whisper.py -q -x -p no:cacheprovider 2>&1 | tail -2

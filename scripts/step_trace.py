@@ -13,8 +13,7 @@ rows_list = [int(x) for x in sys.argv[2:]] or [64, 32, 8, 1]
 dims = get_model(name)
 S = 64
 eng = WhisperGPU(dims, max_slots=S, max_encode_batch=32)
-import os
-eng.set_cross_attn_mode(int(os.environ.get("XA_MODE", "0")))
+
 rng = np.random.default_rng(0)
 seg = rng.integers(-8000, 8000, size=160000, dtype=np.int16)
 slots = list(range(S))
@@ -55,15 +54,16 @@ for rows in rows_list:
         entry, rel, rel_max, end = t[k][:4]
         rec = {"k": nm, "gap_us": round((rel - prev_end) / 1e3, 2),
                "span_us": round((end - rel) / 1e3, 2),
-               "early_us": round((rel - entry) / 1e3, 2)}
+               "early_us": round((rel - entry) / 1e3, 2),
+               "rel_spread_us": round((rel_max - rel) / 1e3, 2)}
         kind = nm.split(".")[-1]
         labs = {"self": ((4, "qkv_ready"), (5, "pages_landed"), (6, "softmax_done"), (7, "pv_done")),
                 "ln1": ((4, "loaded"), (5, "stats_done")), "ln2": ((4, "loaded"), (5, "stats_done")),
                 "ln3": ((4, "loaded"), (5, "stats_done")), "ln_f": ((4, "loaded"), (5, "stats_done")),
-                "xattn": (),
+                "xattn": ((4, "tmem_alloc"), (5, "k_landed"), (6, "s_issued"), (7, "merged")),
                 }.get(kind, ((4, "x_landed"), (7, "mma_issued"), (5, "mma_done"), (6, "stores")))
         for j, lab in labs:
-            if t[k][j] > 0 and t[k][j] >= rel:
+            if t[k][j] > 0:
                 rec[lab + "_us"] = round((t[k][j] - rel) / 1e3, 2)
         res.append(rec)
         prev_end = end
