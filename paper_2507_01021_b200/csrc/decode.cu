@@ -137,7 +137,8 @@ constexpr int kGvThreads = 192;
 constexpr int kGvWBytes = 128 * 64 * 2;        // W block: 128 features x 64 k
 constexpr int kGvXBytes = kRows * 64 * 2;      // X block: 64 rows x 64 k (hi or lo)
 constexpr int kSmPerSm = 233472;               // shared memory per SM (228 KB)
-constexpr int kGvTr = kRows * 129 * 4;         // GV_ARGMAX transpose
+constexpr int kGvTr = kRows * 129 * 4;         // GV_ARGMAX transpose / GELU staging (64 rows)
+__host__ __device__ constexpr int gemv_tr_bytes(int xrows) { return (xrows <= 16 ? 16 : kRows) * 129 * 4; }
 constexpr int kGvMaxStages = 8;
 constexpr int kGvMisc = 1024;
 constexpr int kSmemOptin = 232448;             // 227 KB per CTA (sm_100)
@@ -145,10 +146,12 @@ constexpr int kSmemOptin = 232448;             // 227 KB per CTA (sm_100)
 __host__ __device__ constexpr int gemv_smem_bytes(int kb_per, int stages, int epi, int rgroups,
                                                   int xrows = kRows) {
   return 1024 + kb_per * 2 * (xrows * 128 / rgroups) + stages * kGvWBytes +
-         (epi != GV_PARTIAL ? kGvTr : 0) + kGvMisc;
+         (epi != GV_PARTIAL ? gemv_tr_bytes(xrows) : 0) + kGvMisc;
 }
 
-template <int EPI, bool SPLIT>
+// XR: rows of the register / staging layout (16: step graphs of <= 16 active
+// rows, smaller shared memory; 64 otherwise)
+template <int EPI, bool SPLIT, int XR>
 __global__ void __launch_bounds__(kGvThreads, 1)
 gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap txh,
             const __grid_constant__ CUtensorMap txl, const DecodeState st, const GemvArgs a) {
@@ -160,7 +163,9 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
   const int RG = a.xrows / int(gridDim.z);                  // rows per row group
   uint8_t* ws = xs + kb_per * 2 * RG * 128;                  // [stage] 16K
   float* tr = reinterpret_cast<float*>(ws + NS * kGvWBytes); // GV_ARGMAX / GELU staging
-  uint8_t* misc = reinterpret_cast<uint8_t*>(tr) + (EPI != GV_PARTIAL ? kGvTr : 0);
+  uint8_t* misc = reinterpret_cast<uint8_t*>(tr) + (EPI != GV_PARTIAL ? gemv_tr_bytes(XR) : 0);
+  constexpr int V0N = XR < 32 ? XR : 32;           // rows held in v0 (v1: rows 32..63)
+  constexpr bool V1 = XR > 32;
   uint64_t* wfull = reinterpret_cast<uint64_t*>(misc);
   uint64_t* wempty = wfull + kGvMaxStages;
   uint64_t* xfull = wempty + kGvMaxStages;
@@ -372,9 +377,10 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
         float* part = st.part;
         const size_t base = (size_t(split) * tiles + tile) * kRows * 128;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {                   // only the active rows travel
-          if (i < R) part[base + size_t(i) * 128 + f] = v0[i];
-          if (32 + i < R) part[base + size_t(32 + i) * 128 + f] = v1[i];
+        for (int i = 0; i < V0N; ++i) part[base + size_t(i) * 128 + f] = v0[i];
+        if (V1) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) part[base + size_t(32 + i) * 128 + f] = v1[i];
         }
         __threadfence();
         named_bar_sync(1, 128);
@@ -392,9 +398,10 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
         for (int s = 0; s < a.splits; ++s) {
           const float* ps = part + (size_t(s) * tiles + tile) * kRows * 128 + f;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            if (i < R) v0[i] += __ldcg(ps + size_t(i) * 128);
-            if (32 + i < R) v1[i] += __ldcg(ps + size_t(32 + i) * 128);
+          for (int i = 0; i < V0N; ++i) v0[i] += __ldcg(ps + size_t(i) * 128);
+          if (V1) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v1[i] += __ldcg(ps + size_t(32 + i) * 128);
           }
         }
         if (et == 0) st.counters[a.counter_base + tile] = 0;
@@ -407,9 +414,10 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
           // one compact loop over the active rows (no unrolled erf copies)
           float* col = tr + f;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            col[i * 129] = v0[i];
-            col[(32 + i) * 129] = v1[i];
+          for (int i = 0; i < V0N; ++i) col[i * 129] = v0[i];
+          if (V1) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) col[(32 + i) * 129] = v1[i];
           }
 #pragma unroll 4
           for (int i = 0; i < R; ++i) {
@@ -422,9 +430,10 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
       }
       if (EPI == GV_ARGMAX) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          tr[i * 129 + f] = nvalid ? v0[i] : -INFINITY;
-          tr[(32 + i) * 129 + f] = nvalid ? v1[i] : -INFINITY;
+        for (int i = 0; i < V0N; ++i) tr[i * 129 + f] = nvalid ? v0[i] : -INFINITY;
+        if (V1) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) tr[(32 + i) * 129 + f] = nvalid ? v1[i] : -INFINITY;
         }
         if (st.logits_dbg && nvalid) {
 #pragma unroll
@@ -435,7 +444,7 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
         }
         // per row: max over this tile's 128 vocabulary ids, ties -> lowest id
         named_bar_sync(1, 128);
-        const int r = et >> 1, half = et & 1;
+        const int r = (et >> 1) % XR, half = et & 1;    // (rows >= XR repeat row r: unused)
         float best = -INFINITY;
         int bidx = 0x7FFFFFFF;
         const float* row = tr + r * 129 + half * 64;
@@ -446,7 +455,7 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
         const float ob = __shfl_xor_sync(0xffffffffu, best, 1);
         const int oi = __shfl_xor_sync(0xffffffffu, bidx, 1);
         if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
-        if (half == 0) {
+        if (half == 0 && (et >> 1) < XR) {
           st.amax_val[size_t(tile) * kRows + r] = best;
           st.amax_idx[size_t(tile) * kRows + r] = bidx;
         }
@@ -501,21 +510,26 @@ GemvArgs gemv_plan(int N, int K, int epi) {
 
 GemvArgs gemv_plan_for_rows(const GemvArgs& base, int rows) {
   GemvArgs a = base;
+  static const int mode = std::getenv("DM_GV_ROWPLAN") ? std::atoi(std::getenv("DM_GV_ROWPLAN")) : 1;
+  if (mode == 0) return a;
+  if (mode == 2 && a.epi != GV_PARTIAL) return a;
   const int xr = std::min(kRows, std::max(kGvXBox, ceil_div(rows, kGvXBox) * kGvXBox));
   int rg = a.rgroups;
   while (rg > 1 && xr % (rg * kGvXBox) != 0) rg /= 2;
   a.xrows = xr;
   a.rgroups = rg;
   const int tiles = ceil_div(a.N, 128);
-  // two CTAs per SM when the whole weight slice and the smaller activation
-  // buffer fit in half an SM: then every (tile, split) gets its own CTA
+  // two CTAs per SM when the activation buffer is small enough that half an
+  // SM still holds the whole weight slice (or a ring of >= 4 stages): more
+  // CTAs, fewer tiles each
   for (int cps = 2; cps >= 1; --cps) {
     const int gx = std::max(1, std::min(tiles, cps * kNumSMs / a.splits));
     const int per_cta = ceil_div(tiles, gx) * a.kb_per;
     const int fixed = gemv_smem_bytes(a.kb_per, 0, a.epi, rg, xr);
-    const int stages = std::min({kGvMaxStages, (kSmemOptin - fixed) / kGvWBytes, per_cta});
-    const int smem = gemv_smem_bytes(a.kb_per, stages, a.epi, rg, xr);
-    if (cps == 1 || (stages == per_cta && cps * (smem + 1024) <= kSmPerSm)) {
+    int room = (kSmemOptin - fixed) / kGvWBytes;
+    if (cps == 2) room = std::min(room, (kSmPerSm / 2 - 1024 - fixed) / kGvWBytes);
+    const int stages = std::min({kGvMaxStages, room, per_cta});
+    if (cps == 1 || stages >= std::min(per_cta, 4)) {
       a.gx = gx;
       a.stages = stages;
       break;
@@ -530,15 +544,22 @@ size_t gemv_part_floats(int N, int K, int epi) {
   return a.splits > 1 ? size_t(a.splits) * ceil_div(N, 128) * kRows * 128 : 0;
 }
 
-template <int EPI, bool SPLIT>
+template <int EPI, bool SPLIT, int XR>
 static int launch_gv(const DecodeState& st, const TcGemvMaps& maps, const GemvArgs& a,
                      cudaStream_t stream) {
-  DM_SMEM_ATTR((gemv_kernel<EPI, SPLIT>), kSmemOptin);
-  DM_CHECK_CUDA(launch_pdl(gemv_kernel<EPI, SPLIT>, dim3(a.gx, a.splits, a.rgroups),
+  DM_SMEM_ATTR((gemv_kernel<EPI, SPLIT, XR>), kSmemOptin);
+  DM_CHECK_CUDA(launch_pdl(gemv_kernel<EPI, SPLIT, XR>, dim3(a.gx, a.splits, a.rgroups),
                            dim3(kGvThreads),
                            size_t(gemv_smem_bytes(a.kb_per, a.stages, EPI, a.rgroups, a.xrows)),
                            stream, maps.w, maps.xh, maps.xl, st, a));
   return 0;
+}
+
+template <int EPI, bool SPLIT>
+static int launch_gv_rows(const DecodeState& st, const TcGemvMaps& maps, const GemvArgs& a,
+                          cudaStream_t stream) {
+  return a.xrows <= 16 ? launch_gv<EPI, SPLIT, 16>(st, maps, a, stream)
+                       : launch_gv<EPI, SPLIT, kRows>(st, maps, a, stream);
 }
 
 int launch_gemv(const DecodeState& st, const TcGemvMaps& maps, const GemvArgs& a,
@@ -555,11 +576,11 @@ int launch_gemv(const DecodeState& st, const TcGemvMaps& maps, const GemvArgs& a
   switch (a.epi) {
     case GV_PARTIAL:
       DM_REQUIRE(a.part != nullptr, "partial output missing");
-      return launch_gv<GV_PARTIAL, false>(st, maps, a, stream);
-    case GV_GELU_HILO: return sp ? launch_gv<GV_GELU_HILO, true>(st, maps, a, stream)
-                                 : launch_gv<GV_GELU_HILO, false>(st, maps, a, stream);
-    case GV_ARGMAX: return sp ? launch_gv<GV_ARGMAX, true>(st, maps, a, stream)
-                              : launch_gv<GV_ARGMAX, false>(st, maps, a, stream);
+      return launch_gv_rows<GV_PARTIAL, false>(st, maps, a, stream);
+    case GV_GELU_HILO: return sp ? launch_gv_rows<GV_GELU_HILO, true>(st, maps, a, stream)
+                                 : launch_gv_rows<GV_GELU_HILO, false>(st, maps, a, stream);
+    case GV_ARGMAX: return sp ? launch_gv_rows<GV_ARGMAX, true>(st, maps, a, stream)
+                              : launch_gv_rows<GV_ARGMAX, false>(st, maps, a, stream);
     default: DM_REQUIRE(false, "unknown epilogue");
   }
 }
