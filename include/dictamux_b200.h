@@ -168,7 +168,8 @@ DM_API int dm_whisper_stats(void* handle, int64_t* out, int n);
  * `stream` (a probe: it may overwrite row-space activations): which =
  * 0 cross-attention(layer), 1 self-attention(layer), 2 LM head, 3 decoder LN
  * (+ residual partials), 4 cross-q projection, 5 fc2 projection,
- * 6 empty PDL kernel (launch floor), 7 fc1 projection (+GELU), 8 qkv projection.
+ * 6 empty PDL kernel (launch floor), 7 fc1 projection (+GELU), 8 qkv projection,
+ * 9 the cross-attention's K/V stream alone (roofline probe), 10 cross-o projection.
  * avg_ms = mean over iters back-to-back launches. layer < 0: launch i runs
  * decoder layer i % dec_layers (each launch streams a different layer's
  * cross-KV / weights, as inside a decode step). */

@@ -937,39 +937,27 @@ int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, floa
 
 constexpr int kXaThreads = 192;                               // one key per thread
 constexpr int kXaKeys = 192;                                  // ceil(1500 / 8 / 64) * 64
-constexpr int kXaPush = 64 + 4;                          // o[64], max, sum (+pad): floats per split
 static_assert(kXSplits * kXaKeys >= 1500 && (kXSplits - 1) * kXaKeys < 1500, "key splits");
 
-// async store into another CTA's shared memory, completing `bytes` on that CTA's mbarrier
-__device__ __forceinline__ void st_async_v4(uint32_t addr, float4 v, uint32_t bar) {
-  asm volatile(
-      "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
-          addr),
-      "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
-      "r"(__float_as_uint(v.w)), "r"(bar)
-      : "memory");
-}
-
-// Cross-attention + cross-o projection for (row, head, key split)
-// (modeling_whisper.py:398-406, encoder_attn of the decoder layer; q·64^-½ at
-// :310). The split's K and V blocks (contiguous in the slot's cross-KV cache)
-// are TMA-loaded into shared memory before the dependency wait; after it only
-// q is read. Scores and P.V run on the tensor cores (tcgen05, fp32 TMEM
-// accumulators) with fp32-equivalent operands split into bf16 hi/lo pairs:
+// Cross-attention of the fed token (modeling_whisper.py:398-406, encoder_attn
+// of the decoder layer; q.64^-1/2 at :310), one CTA per (row, head, key split
+// of 192 keys). The split's K and V blocks (contiguous in the slot's cross-KV
+// cache) are TMA-loaded into shared memory before the dependency wait; after
+// it only q is read. Scores and P.V run on the tensor cores (tcgen05, fp32
+// TMEM accumulators) with fp32-equivalent operands split into bf16 hi/lo pairs:
 //   S^T[64 keys x 8] = K_box[64 x 64] . [q_hi; q_lo; 0]^T   (3 boxes, M = 64)
 //   s = S[:, 0] + S[:, 1]                                    (q = q_hi + q_lo)
 //   O^T[64 dims x 8] = V^T[64 x 192] . [p_hi; p_lo; 0]^T     (V as the MN-major
 //   A operand straight from the TMA box, M = 64)
-// so the CUDA cores only do the softmax, the split merge and the cross-o tail.
-// The 8 key splits of a (row, head) form a cluster:
-//   1. scores, two-pass softmax (exp kept unnormalised), P.V over the split;
-//   2. every split st.async's (o[64], max, sum) into every rank's shared
-//      memory (completion on that rank's mbarrier: no cluster-wide fence) and
-//      each rank merges the 8 splits in split order (identical on all ranks);
-//   3. rank s computes output features [s*d/8, +d/8) of Wo[:, h*64 .. +64].o_h
-//      -- its 16*d-byte weight slice is bulk-copied into the dead K buffer as
-//      soon as the score MMAs retired -- and stores them as head h's partial.
-// Every reduction order depends only on d and key positions, never on the batch.
+// so the CUDA cores only do the softmax. Each split writes (o[64], max, sum)
+// to global scratch and leaves; the last of the 8 splits to arrive (a
+// per-(row, head) counter) merges them in split order and stores o_head as
+// the bf16 hi/lo operand of the cross-o tcgen05 GEMV that follows. Every
+// reduction order depends only on d and key positions, never on the batch.
+// (Measured alternatives: the same math with the 8 splits as a
+// cluster merging over DSMEM and the cross-o projection in the tail; a
+// persistent 2-CTA/SM grid with a K/V ring; warp-level mma.sync; all slower
+// at 64 rows, the cluster form faster below ~32 rows.)
 constexpr int kXaQOff = 2 * kXaKeys * 128;                // B operand [q_hi; q_lo; 0] (1 KB)
 constexpr int kXaPOff = kXaQOff + 1024;                   // B operand [p_hi; p_lo; 0] (3 x 1 KB)
 constexpr int kXaBarOff = kXaPOff + 3 * 1024;
@@ -986,52 +974,42 @@ __device__ __forceinline__ int sw128_off(int n, int k) {
   return n * 128 + ((((k >> 3) ^ n) & 7) << 4) + (k & 7) * 2;
 }
 
+constexpr int kXpStride = 68;                 // floats per split result: o[64], max, sum, pad
+
 __global__ void __launch_bounds__(kXaThreads, 4)
 cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, int layer,
-                  const Partials xq, float q_scale, const uint16_t* __restrict__ wo_pack,
-                  float* __restrict__ part_o) {
+                       const Partials xq, float q_scale, float* __restrict__ xpart,
+                       int* __restrict__ xcnt, int probe) {
   extern __shared__ uint8_t xa_raw[];
-  uint8_t* xa_smem = xa_raw + ((1024 - (smem_u32(xa_raw) & 1023)) & 1023);   // swizzle atoms
-  __shared__ __align__(16) float oh[64];
-  __shared__ __align__(16) float ol[64];
-  __shared__ __align__(16) float push[kXSplits][kXaPush];   // split results (pushed by every rank)
+  uint8_t* xa_smem = xa_raw + ((1024 - (smem_u32(xa_raw) & 1023)) & 1023);
   __shared__ float redm[4], reds[4];
   __shared__ uint32_t tmem_slot;
+  __shared__ int is_last;
   const int r = blockIdx.x, h = blockIdx.y, sp = blockIdx.z, tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
   if (tid == 0) trace_mark(st, 0);
-  if (r >= *st.n_active) return;                 // whole cluster (same row) leaves together
+  if (r >= *st.n_active) return;
   const int slot = st.active[r];
-  // (no done-slot early exit here: it would put a dependent load in front of
-  // the K/V prefetch of every CTA)
-  const int d = st.d, H = st.heads, d8 = d / 8;
+  const int H = st.heads;
   const int k0 = sp * kXaKeys, nk = min(1500, k0 + kXaKeys) - k0;
   uint8_t* Ks = xa_smem;
   uint8_t* Vs = xa_smem + kXaKeys * 128;
   uint8_t* Qs = xa_smem + kXaQOff;
   uint8_t* Ps = xa_smem + kXaPOff;
-  const uint16_t* Wo = reinterpret_cast<const uint16_t*>(Ks);   // [d/8][64], after the scores
   uint64_t* barK = reinterpret_cast<uint64_t*>(xa_smem + kXaBarOff);
   uint64_t* barV = barK + 1;
-  uint64_t* barW = barK + 2;
-  uint64_t* barM = barK + 3;                     // the 8 split results landed (st.async)
-  uint64_t* barS = barK + 4;                     // score MMAs retired
-  uint64_t* barO = barK + 5;                     // P.V MMAs retired
+  uint64_t* barS = barK + 2;
+  uint64_t* barO = barK + 3;
   if (tid == 0) {
     mbar_init(barK, 1);
     mbar_init(barV, 1);
-    mbar_init(barW, 1);
-    mbar_init(barM, 1);
     mbar_init(barS, 1);
     mbar_init(barO, 1);
     fence_barrier_init();
-    // K and V of the split: 3 TMA boxes of 64 keys each (128B-swizzled rows;
-    // keys past the slot's 1500 are masked), cross-KV never depends on the
-    // predecessor
     tma_prefetch_desc(&tm);
     const int row_k = (((layer * st.max_slots + slot) * 2 + 0) * H + h) * 1500 + k0;
     const int row_v = row_k + H * 1500;
-    const uint64_t stream = l2_policy_evict_first();     // read once per step
+    const uint64_t stream = l2_policy_evict_first();
     mbar_arrive_expect_tx(barK, 3 * 64 * 128);
 #pragma unroll
     for (int bx = 0; bx < 3; ++bx)
@@ -1040,11 +1018,8 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
 #pragma unroll
     for (int bx = 0; bx < 3; ++bx)
       tma_load_2d_hint(Vs + bx * 64 * 128, &tm, barV, 0, row_v + bx * 64, stream);
-    mbar_arrive_expect_tx(barM, kXSplits * kXaPush * 4);
   }
-  if (warp == 1) tmem_alloc(&tmem_slot, 32);     // S: cols 0..23 (3 boxes x 8), O: 24..31
-  if (tid == 32) trace_mark(st, 4);
-  // rows 2..7 of the q / p operands stay zero (N = 8, only hi and lo are used)
+  if (warp == 1) tmem_alloc(&tmem_slot, 32);
   for (int i = tid; i < 4 * 1024 / 16; i += kXaThreads) {
     const int row = (i * 16 / 128) & 7;
     if (row >= 2) reinterpret_cast<uint4*>(Qs)[i] = make_uint4(0u, 0u, 0u, 0u);
@@ -1054,10 +1029,17 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
   pdl_trigger();                                 // (after the TMEM allocation, see gemv_kernel)
-  cluster_arrive_relaxed();                      // every rank's barM is initialised
   const float bq = tid < 64 ? bf16_to_f32(xq.bias[h * 64 + tid]) : 0.f;
   pdl_wait();
   if (tid == 0) trace_mark(st, 1);
+  if (probe == 1) {                              // (timing probe: the K/V stream alone)
+    mbar_wait(barK, 0);
+    mbar_wait(barV, 0);
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, 32);
+    return;
+  }
   if (tid < 64) {
     const float* pp = xq.p + size_t(r) * xq.n + h * 64 + tid;
     const float a = sum_splits(pp, size_t(kRows) * xq.n, xq.splits);
@@ -1067,35 +1049,25 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     *reinterpret_cast<uint16_t*>(Qs + sw128_off(0, tid)) = hi;
     *reinterpret_cast<uint16_t*>(Qs + sw128_off(1, tid)) = lo;
   }
-  fence_proxy_async_smem();                      // generic smem writes -> tensor core
+  fence_proxy_async_smem();
   __syncthreads();
   if (tid == 0) {
     mbar_wait(barK, 0);
-    trace_mark(st, 5);
     tc_fence_after();
     const uint64_t bq_desc = umma_desc_sw128(smem_u32(Qs));
 #pragma unroll
     for (int bx = 0; bx < 3; ++bx) {
       const uint64_t ak = umma_desc_sw128(smem_u32(Ks + bx * 64 * 128));
 #pragma unroll
-      for (int k = 0; k < 4; ++k)                // 16 dims per MMA: +32 B = +2 in the address
+      for (int k = 0; k < 4; ++k)
         umma_bf16_ss(tmem + bx * 8, ak + 2 * k, bq_desc + 2 * k, kXaIdescS, k != 0);
     }
     umma_commit(barS);
-    trace_mark(st, 6);
-    // the K buffer is dead once the score MMAs retired: fetch this rank's
-    // cross-o slice into it
-    mbar_wait(barS, 0);
-    mbar_arrive_expect_tx(barW, 16 * d);
-    bulk_load(Ks, wo_pack + size_t(h * kXSplits + sp) * d8 * 64, 16 * d, barW);
   }
-  // softmax over the split (warps 0..3; TMEM quadrant w holds accumulator rows
-  // 16w..16w+15 in its lanes 0..15 for M = 64): key of box j = 64 j + 16 w + lane
-  const bool sm = warp < 4;
-  const bool own = sm && lane < 16;
-  float s3[3], e3[3];
-  float m = -INFINITY, l = 0.f;
-  if (sm) {
+  float* res = xpart + ((size_t(r) * H + h) * kXSplits + sp) * kXpStride;
+  if (warp < 4) {
+    const bool own = lane < 16;
+    float s3[3], e3[3];
     mbar_wait(barS, 0);
     tc_fence_after();
     uint32_t a[3], b[3];
@@ -1114,7 +1086,7 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     for (int o = 16; o > 0; o >>= 1) mloc = fmaxf(mloc, __shfl_xor_sync(0xffffffffu, mloc, o));
     if (lane == 0) redm[warp] = mloc;
     named_bar_sync(1, 128);
-    m = fmaxf(fmaxf(redm[0], redm[1]), fmaxf(redm[2], redm[3]));
+    const float m = fmaxf(fmaxf(redm[0], redm[1]), fmaxf(redm[2], redm[3]));
     float es = 0.f;
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
@@ -1124,7 +1096,6 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) es += __shfl_xor_sync(0xffffffffu, es, o);
     if (lane == 0) reds[warp] = es;
-    // p = e as a bf16 hi/lo pair: rows 0 and 1 of the K-major P operand (k-block j)
     if (own) {
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
@@ -1137,15 +1108,16 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     }
     fence_proxy_async_smem();
     named_bar_sync(1, 128);
-    l = (reds[0] + reds[1]) + (reds[2] + reds[3]);
     if (tid == 0) {
+      res[64] = m;
+      res[65] = (reds[0] + reds[1]) + (reds[2] + reds[3]);
       mbar_wait(barV, 0);
       tc_fence_after();
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
         const uint64_t bp = umma_desc_sw128(smem_u32(Ps + j * 1024));
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {            // 16 keys per MMA: V^T rows 16k.. (2 atoms)
+        for (int k = 0; k < 4; ++k) {
           const uint64_t av = umma_desc_sw128(smem_u32(Vs + j * 64 * 128 + k * 2048));
           umma_bf16_ss(tmem + 24, av, bp + 2 * k, kXaIdescO, (j | k) != 0);
         }
@@ -1157,98 +1129,58 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     uint32_t oa, ob;
     tmem_ld2(tmem + lane_base + 24, oa, ob);
     tmem_wait_ld();
-    if (own) ol[16 * warp + lane] = __uint_as_float(oa) + __uint_as_float(ob);
+    if (own) res[16 * warp + lane] = __uint_as_float(oa) + __uint_as_float(ob);
+    __threadfence();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, 32);
-  // 2. push (o, max, sum) to every rank; merge the 8 splits in split order.
-  // Thread (rank dst, chunk ch) st.async's dims 4ch..4ch+3 (8 ranks x 16
-  // chunks + 8 (max, sum) stores)
-  if (tid == 0) { redm[0] = m; reds[0] = l; }
+  if (tid == 0) is_last = atomicAdd(&xcnt[r * H + h], 1) == kXSplits - 1;
   __syncthreads();
-  cluster_wait();                                // (all ranks arrived long ago)
-  if (tid < kXSplits * 16) {
-    const int dst = tid >> 4, ch = tid & 15;
-    const float4 a = *reinterpret_cast<const float4*>(&ol[4 * ch]);
-    st_async_v4(dsmem_addr(&push[sp][4 * ch], dst), a, dsmem_addr(barM, dst));
-  } else if (tid < kXSplits * 16 + kXSplits) {
-    const int dst = tid - kXSplits * 16;
-    st_async_v4(dsmem_addr(&push[sp][64], dst), make_float4(redm[0], reds[0], 0.f, 0.f),
-                dsmem_addr(barM, dst));
-  }
-  mbar_wait(barM, 0);
-  if (tid == 0) trace_mark(st, 7);
+  if (!is_last) return;
+  // merge the 8 splits in split order; o_head -> the cross-o GEMV operand
+  __threadfence();
   if (tid < 64) {
+    const float* base = xpart + (size_t(r) * H + h) * kXSplits * kXpStride;
+    float mv[kXSplits], lv[kXSplits], ov[kXSplits];
+#pragma unroll
+    for (int s = 0; s < kXSplits; ++s) {
+      mv[s] = __ldcg(base + s * kXpStride + 64);
+      lv[s] = __ldcg(base + s * kXpStride + 65);
+      ov[s] = __ldcg(base + s * kXpStride + tid);
+    }
     float M = -INFINITY;
 #pragma unroll
-    for (int s = 0; s < kXSplits; ++s) M = fmaxf(M, push[s][64]);
+    for (int s = 0; s < kXSplits; ++s) M = fmaxf(M, mv[s]);
     float Ls = 0.f, O = 0.f;
 #pragma unroll
     for (int s = 0; s < kXSplits; ++s) {
-      const float f = exp2f((push[s][64] - M) * kLog2e);
-      Ls += push[s][65] * f;
-      O += push[s][tid] * f;
+      const float f = exp2f((mv[s] - M) * kLog2e);
+      Ls += lv[s] * f;
+      O += ov[s] * f;
     }
-    oh[tid] = O / Ls;
+    uint16_t hi, lo;
+    split_hilo(O / Ls, hi, lo);
+    const size_t idx = size_t(r) * st.d + h * 64 + tid;
+    st.ah[idx] = hi;
+    st.al[idx] = lo;
   }
-  __syncthreads();
-  // 3. output features sp*d/8 + n of Wo[:, h*64 .. +64] . o_h: 8 lanes per
-  // feature (16-byte chunk each, conflict-free), xor tree over the 8 lanes
-  mbar_wait(barW, 0);
-  const int ch = tid & 7;
-  float ov[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) ov[j] = oh[ch * 8 + j];
-  float* dst = part_o + (size_t(h) * kRows + r) * d + sp * d8;
-  for (int n = tid >> 3; n < d8; n += kXaThreads / 8) {     // (warp-uniform: d/8 % 4 == 0)
-    const uint4 w = *reinterpret_cast<const uint4*>(Wo + n * 64 + ch * 8);
-    float acc = ov[0] * __uint_as_float(w.x << 16);
-    acc = fmaf(ov[1], __uint_as_float(w.x & 0xFFFF0000u), acc);
-    acc = fmaf(ov[2], __uint_as_float(w.y << 16), acc);
-    acc = fmaf(ov[3], __uint_as_float(w.y & 0xFFFF0000u), acc);
-    acc = fmaf(ov[4], __uint_as_float(w.z << 16), acc);
-    acc = fmaf(ov[5], __uint_as_float(w.z & 0xFFFF0000u), acc);
-    acc = fmaf(ov[6], __uint_as_float(w.w << 16), acc);
-    acc = fmaf(ov[7], __uint_as_float(w.w & 0xFFFF0000u), acc);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
-    if (ch == 0) dst[n] = acc;
+  if (tid == 0) {
+    xcnt[r * H + h] = 0;                         // ready for the next launch of any layer
+    trace_mark(st, 3);
   }
-  if (tid == 0) trace_mark(st, 3);
 }
 
 int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
-                      const Partials& xq, float q_scale, const uint16_t* wo_pack, float* part_o,
-                      cudaStream_t stream) {
+                           const Partials& xq, float q_scale, float* xpart, int* xcnt,
+                           cudaStream_t stream, int probe) {
   DM_REQUIRE(xq.p != nullptr && xq.n == st.d && xq.bias != nullptr && xq.splits >= 1 &&
                  xq.splits <= kMaxSplits, "cross-attn: q partials");
-  DM_REQUIRE(wo_pack != nullptr && part_o != nullptr, "cross-attn: cross-o operands");
-  DM_REQUIRE(st.d % 64 == 0, "cross-attn: d must be a multiple of 64");
-  DM_REQUIRE(16 * st.d <= kXaKeys * 128 && st.heads <= kMaxHeads,
-             "cross-attn: the cross-o slice must fit the K buffer");
+  DM_REQUIRE(xpart != nullptr && xcnt != nullptr && st.heads <= kMaxHeads, "cross-attn: scratch");
   DM_SMEM_ATTR(cross_attn_kernel, kXaSmem);
-  DM_CHECK_CUDA(launch_pdl_cluster(cross_attn_kernel, dim3(st.grid_rows, st.heads, kXSplits),
-                                   dim3(kXaThreads), dim3(1, 1, kXSplits), kXaSmem, stream,
-                                   xkv_map, st, layer, xq, q_scale, wo_pack, part_o));
-  return 0;
-}
-
-__global__ void repack_xo_kernel(const uint16_t* __restrict__ wo, uint16_t* __restrict__ out, int d) {
-  // wo [d, d] ([out, in]) -> out [H][8][d/8][64]: the (head h, split s) slice =
-  // output features s*d/8 .. +d/8 x input dims h*64 .. +64, contiguous
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= d * d) return;
-  const int d8 = d / 8;
-  const int j = i % 64, n = (i / 64) % d8, s = (i / (64 * d8)) % kXSplits, h = i / (64 * d);
-  out[i] = wo[size_t(s * d8 + n) * d + h * 64 + j];
-}
-
-int repack_xo(const uint16_t* wo, uint16_t* out, int d, int H, cudaStream_t stream) {
-  DM_REQUIRE(d == H * 64 && d % 32 == 0, "repack_xo: d = 64 * heads");
-  repack_xo_kernel<<<ceil_div(d * d, 256), 256, 0, stream>>>(wo, out, d);
-  DM_CHECK_LAUNCH();
+  DM_CHECK_CUDA(launch_pdl(cross_attn_kernel, dim3(st.grid_rows, st.heads, kXSplits),
+                           dim3(kXaThreads), kXaSmem, stream, xkv_map, st, layer, xq, q_scale,
+                           xpart, xcnt, probe));
   return 0;
 }
 

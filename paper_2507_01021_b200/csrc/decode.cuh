@@ -16,9 +16,9 @@
 //   ln(+embed | +residual partials) -> qkv GEMV (K-split partials)
 //   -> self-attention (reduces q/k/v partials, appends k/v to the page)
 //   -> o GEMV (partials) -> ln(+residual) -> cross-q GEMV (partials)
-//   -> cross-attention + cross-o (reduces q; the 8 key splits of a (row, head)
-//      form a cluster, exchange their partial softmax results over DSMEM, and
-//      each computes d/8 features of the head's cross-o partial)
+//   -> cross-attention (reduces q; tensor-core scores / P.V per key split,
+//      the 8 split results merged in split order by the last split to arrive)
+//   -> cross-o GEMV (partials)
 //   -> ln(+residual) -> fc1 GEMV (+GELU, hi/lo)
 //   -> fc2 GEMV (partials)
 //
@@ -35,7 +35,7 @@
 namespace dm {
 
 constexpr int kRows = 64;          // max active slots = max MMA N
-constexpr int kXSplits = 8;        // cross-attention key splits (cluster size); fixed per engine
+constexpr int kXSplits = 8;        // cross-attention key splits; fixed per engine
 
 struct DecodeState {
   int max_slots, d, heads, layers, ffn, vocab;
@@ -157,19 +157,17 @@ int launch_ln(const DecodeState& st, const LnArgs& a, cudaStream_t stream);
 // k/v appended to the slot's page, keys 0..pos; output -> ah/al.
 int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, float q_scale,
                      cudaStream_t stream);
-// Cross-attention over the slot's 1500 cross-KV rows with the cross-o
-// projection in its tail; q from the cross-q partials (scaled); output: the
-// per-head partials of Wo . attn ([H][kRows][d], the following LayerNorm adds
-// the o bias and sums the heads in head order).
-// xkv_map: the cross-KV cache as [rows, 64] bf16, box 64 x 64, 128B swizzle.
-// wo_pack: the layer's cross-o weights in per-(head, key split) slices
-// [H][8][d/8][64] (repack_xo).
-constexpr int kMaxHeads = 20;   // per-head partial splits a LayerNorm may reduce
+// Cross-attention over the slot's 1500 cross-KV rows (q from the cross-q
+// partials, scaled): per (row, head, split) tensor-core scores and P.V, the 8
+// split results merged in split order by the last to arrive. xkv_map: the
+// cross-KV cache as [rows, 64] bf16, box 64 x 64, 128B swizzle. xpart:
+// [kRows][H][8][68] fp32 scratch, xcnt: [kRows * kMaxHeads] zero-initialised
+// counters. Output: o (all heads) as the bf16 hi/lo operand st.ah / st.al of
+// the cross-o GEMV. probe = 1: stream K/V and stop (roofline probe).
+constexpr int kMaxHeads = 20;   // per-head scratch / partial splits a LayerNorm may reduce
 int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
-                      const Partials& xq, float q_scale, const uint16_t* wo_pack, float* part_o,
-                      cudaStream_t stream);
-// [d, d] cross-o weight -> the per-(head, split) contiguous slices the cross-attention loads
-int repack_xo(const uint16_t* wo, uint16_t* out, int d, int H, cudaStream_t stream);
+                      const Partials& xq, float q_scale, float* xpart, int* xcnt,
+                      cudaStream_t stream, int probe = 0);
 int launch_finalize(const DecodeState& st, cudaStream_t stream);
 
 }  // namespace dm

@@ -210,7 +210,6 @@ struct WhisperEngine {
   int dec_layer_base(int l) const { return after_enc() + 4 + 18 * l; }
   int after_dec() const { return after_enc() + 4 + 18 * Ld; }
   uint16_t* conv1_w_pad = nullptr;   // [d, 3, Cp]
-  uint16_t* xo_pack = nullptr;       // [Ld][H][8][d/8][64] cross-o weight slices (repack_xo)
   // encoder workspace
   int E = 0;
   float* mel = nullptr;          // [E, nm, 3000]
@@ -265,12 +264,14 @@ struct WhisperEngine {
     int n_active_host = 0;
     // K-split partial sums of the linear projections (consumer-reduced)
     float *p_qkv = nullptr, *p_o = nullptr, *p_xq = nullptr, *p_xo = nullptr, *p_fc2 = nullptr;
+    float* xpart = nullptr;        // cross-attention split results [kRows][H][8][68]
+    int* xcnt = nullptr;           // [kRows * kMaxHeads] split arrival counters
   };
   std::vector<Group> groups;
   cudaEvent_t step_start = nullptr;
   // telemetry: kernels launched (graph nodes counted per replay)
   long long launches = 0, steps = 0, encodes = 0, segments = 0;
-  int step_kernels() const { return 10 * Ld + 3; }
+  int step_kernels() const { return 11 * Ld + 3; }
   int encode_kernels() const { return 2 + 2 + 7 * L + 1 + 1; }
 
   // debug (DM_GUARD=1 at create): every allocation gets a 64 KB 0xA5 tail
@@ -338,11 +339,6 @@ static int engine_init(WhisperEngine* e) {
     repack_conv1_kernel<<<ceil_div(n, 256), 256>>>(e->W(0), e->conv1_w_pad, d, e->nm, e->Cp);
     DM_CHECK_LAUNCH();
   }
-  // cross-o weights in the cross-attention's per-(head, key split) slice order
-  if (e->alloc_t(&e->xo_pack, size_t(e->Ld) * d * d, false)) return 2;
-  for (int l = 0; l < e->Ld; ++l)
-    if (int rc = repack_xo(e->W(e->dec_layer_base(l) + 10), e->xo_pack + size_t(l) * d * d, d, e->H, 0))
-      return rc;
   if (e->alloc_t(&e->mel, size_t(E) * e->nm * 3000, false)) return 2;
   if (e->alloc_t(&e->mel_t, size_t(E) * 3002 * e->Cp)) return 2;
   if (e->alloc_t(&e->segmax, E)) return 2;
@@ -424,13 +420,14 @@ static int engine_init(WhisperEngine* e) {
     if (e->alloc_t(&gr.p_qkv, gemv_part_floats(3 * d, d, GV_PARTIAL))) return 2;
     if (e->alloc_t(&gr.p_o, gemv_part_floats(d, d, GV_PARTIAL))) return 2;
     if (e->alloc_t(&gr.p_xq, gemv_part_floats(d, d, GV_PARTIAL))) return 2;
-    if (e->alloc_t(&gr.p_xo, std::max(gemv_part_floats(d, d, GV_PARTIAL),
-                                      size_t(e->H) * kRows * d))) return 2;   // per-head partials
+    if (e->alloc_t(&gr.p_xo, gemv_part_floats(d, d, GV_PARTIAL))) return 2;
     if (e->alloc_t(&gr.p_fc2, gemv_part_floats(d, e->F, GV_PARTIAL))) return 2;
     size_t part = std::max<size_t>(1, std::max(gemv_part_floats(e->F, d, GV_GELU_HILO),
                                                gemv_part_floats(c.vocab, d, GV_ARGMAX)));
     if (e->alloc_t(&gs.part, part)) return 2;
     if (e->alloc_t(&gs.counters, 4096)) return 2;
+    if (e->alloc_t(&gr.xpart, size_t(kRows) * e->H * kXSplits * 68)) return 2;
+    if (e->alloc_t(&gr.xcnt, size_t(kRows) * kMaxHeads)) return 2;
     if (e->alloc_t(&gs.amax_val, size_t(tiles) * kRows)) return 2;
     if (e->alloc_t(&gs.amax_idx, size_t(tiles) * kRows)) return 2;
     gs.logits_dbg = nullptr;
@@ -599,10 +596,11 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
     DM_STEP(gv(pi + 1, grp.p_o, nullptr, nullptr, nullptr));
     DM_STEP(ln(2, b0 + 6, Partials{grp.p_o, go, d, e->W(b0 + 5)}));
     DM_STEP(gv(pi + 2, grp.p_xq, nullptr, nullptr, nullptr));
-    // cross-attention with the cross-o projection in its tail (per-head partials)
+    // cross-attention (o -> ah/al) -> cross-o projection (partials) -> ln3
     DM_STEP(launch_cross_attn(st, e->xkv_map, l, Partials{grp.p_xq, gx, d, e->W(b0 + 9)}, 0.125f,
-                              e->xo_pack + size_t(l) * d * d, grp.p_xo, s));
-    DM_STEP(ln(2, b0 + 12, Partials{grp.p_xo, e->H, d, e->W(b0 + 11)}));
+                              grp.xpart, grp.xcnt, s));
+    DM_STEP(gv(pi + 3, grp.p_xo, nullptr, nullptr, nullptr));
+    DM_STEP(ln(2, b0 + 12, Partials{grp.p_xo, e->plans[pi + 3].splits, d, e->W(b0 + 11)}));
     DM_STEP(gv(pi + 4, nullptr, st.hh, st.hl, e->W(b0 + 15)));
     DM_STEP(gv(pi + 5, grp.p_fc2, nullptr, nullptr, nullptr));
     prev = Partials{grp.p_fc2, gf, d, e->W(b0 + 17)};
@@ -934,7 +932,7 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
       case 0:
         return launch_cross_attn(pst, e->xkv_map, layer,
                                  Partials{grp.p_xq, e->plans[pi + 2].splits, d, e->W(b0 + 9)},
-                                 0.125f, e->xo_pack + size_t(layer) * d * d, grp.p_xo, cs);
+                                 0.125f, grp.xpart, grp.xcnt, cs);
       case 1:
         return launch_self_attn(pst, layer,
                                 Partials{grp.p_qkv, e->plans[pi].splits, 3 * d, e->W(b0 + 3)},
@@ -951,6 +949,11 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
       case 6: return launch_pdl_floor(cs);
       case 7: return gv(pi + 4, nullptr, pst.hh, pst.hl, e->W(b0 + 15), cs);
       case 8: return gv(pi + 0, grp.p_qkv, nullptr, nullptr, nullptr, cs);
+      case 9:        // the cross-attention reduced to its K/V stream (roofline probe)
+        return launch_cross_attn(pst, e->xkv_map, layer,
+                                 Partials{grp.p_xq, e->plans[pi + 2].splits, d, e->W(b0 + 9)},
+                                 0.125f, grp.xpart, grp.xcnt, cs, 1);
+      case 10: return gv(pi + 3, grp.p_xo, nullptr, nullptr, nullptr, cs);
       default: set_error("unknown kernel id"); return 1;
     }
   };

@@ -22,7 +22,10 @@ for i in range(0, S, 32):
 eng.admit(slots, [400] * S)
 names = []
 for l in range(dims.dec_layers):
-    names += [f"L{l}.{k}" for k in ("ln1", "qkv", "self", "o", "ln2", "xq", "xattn", "ln3", "fc1", "fc2")]
+    kinds = ("ln1", "qkv", "self", "o", "ln2", "xq", "xattn", "ln3", "fc1", "fc2")
+    if not int(__import__("os").environ.get("DM_XA_CLUSTER", "0")):
+        kinds = kinds[:7] + ("xo",) + kinds[7:]          # lean cross-attention + cross-o GEMV
+    names += [f"L{l}.{k}" for k in kinds]
 names += ["ln_f", "lm_head", "finalize"]
 lib = eng.lib
 def dbg(which, buf=None, n=0):

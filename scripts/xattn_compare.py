@@ -11,7 +11,7 @@ from paper_2507_01021_b200.models import get_model
 name = sys.argv[1] if len(sys.argv) > 1 else "whisper-large-v3"
 rows_list = [int(x) for x in sys.argv[2:]] or [64, 48, 32, 24, 16, 8, 4, 1]
 dims = get_model(name)
-eng = WhisperGPU(dims, max_slots=64, max_encode_batch=32)
+eng = WhisperGPU(dims, max_slots=64, max_encode_batch=32)   # DM_XA_LEAN / DM_XA_CLUSTER pick the kernel
 seg = np.random.default_rng(0).integers(-8000, 8000, size=160000, dtype=np.int16)
 slots = list(range(64))
 for i in range(0, 64, 32):
@@ -24,7 +24,7 @@ for rows in rows_list:
     eng.step(2)
     torch.cuda.synchronize()
     r = {}
-    for which, label in ((0, "cluster"),):
+    for which, label in ((0, "xattn"), (9, "kv_stream_only"), (10, "xo_gemv")):
         us = statistics.median(1000 * eng.time_kernel(which, layer=-1, iters=2 * L) for _ in range(5))
         gbs = rows * 2 * 1500 * dims.d_model * 2 / (us * 1e-6) / 1e9
         r[label] = {"us": round(us, 2), "GBps": round(gbs, 1)}
