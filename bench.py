@@ -533,14 +533,13 @@ def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
 
 
 def measure_roofline(eng, dims) -> dict:
-    """Cross-attention (decode, K6; cross-o projection fused in its tail) is
-    the dominant kernel: per launch it streams every active slot's K and V of
-    one layer, n_active * 2 * 1500 * d bf16 (SURVEY.md §8(d):
-    L*2*1500*d*2 B per segment per step; 491.5 MB per launch at 64 rows on
-    large-v3). Timed with CUDA events around a graph of one launch per decoder
-    layer (launch i runs layer i % L, so every launch reads a different
-    layer's cross-KV from HBM, PDL-chained as inside the step graph) at 64
-    active rows. The 2*d*d B cross-o weight slices (L2-resident) are not counted."""
+    """Cross-attention (decode, K6) is the dominant kernel: per launch it
+    streams every active slot's K and V of one layer, n_active * 2 * 1500 * d
+    bf16 (L*2*1500*d*2 B per segment per step; 491.5 MB per
+    launch at 64 rows on large-v3). Timed with CUDA events around a graph of
+    one launch per decoder layer (launch i runs layer i % L, so every launch
+    reads a different layer's cross-KV from HBM, PDL-chained as inside the
+    step graph) at 64 active rows."""
     import torch
     peaks = _peaks()
     peak = float(peaks.get("hbm_gbs", 6650.0))
@@ -556,6 +555,9 @@ def measure_roofline(eng, dims) -> dict:
     L = dims.dec_layers
     runs = [eng.time_kernel(0, layer=-1, iters=2 * L) for _ in range(5)]
     ms = statistics.median(runs)
+    # the same launches reduced to their K/V stream (what the CTA structure can
+    # move with no compute): the gap to `ms` is the kernel's own overhead
+    stream_ms = statistics.median(eng.time_kernel(9, layer=-1, iters=2 * L) for _ in range(5))
     eng.release(slots)
     eng.set_active([])
     torch.cuda.synchronize(eng.device)
@@ -566,7 +568,7 @@ def measure_roofline(eng, dims) -> dict:
     if tf.exists():     # dram read+write of one ncu --set full capture, scaled to rows
         t = json.loads(tf.read_text())
         traffic = (t["dram_bytes_read"] + t["dram_bytes_write"]) * S / t["rows"]
-    return {"kernel": "cross_attn_kernel (decode K6, + cross-o tail)", "bound": "hbm",
+    return {"kernel": "cross_attn_kernel (decode K6)", "bound": "hbm",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic,
             "traffic_unit": f"bytes per launch (ncu dram__bytes_read+write, {tf.name})",
@@ -574,6 +576,8 @@ def measure_roofline(eng, dims) -> dict:
                       f"launch i = decoder layer i % {L}, 64 active rows (median of 5)",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback",
             "bytes_per_launch": bytes_per_launch, "avg_launch_ms": ms,
+            "kv_stream_only_ms": stream_ms,
+            "kv_stream_only_frac": bytes_per_launch / (stream_ms / 1000.0) / 1e9 / peak,
             "per_unit": "2*1500*d*2 B per active slot per layer"}
 
 

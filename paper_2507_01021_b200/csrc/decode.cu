@@ -34,7 +34,7 @@ __device__ __forceinline__ void split_hilo(float v, uint16_t& hi, uint16_t& lo) 
 // Sum of up to kMaxSplits K-split partials p[s * stride] in split order. All
 // loads are issued before the first add (a runtime-trip loop would serialise
 // one L2 round trip per split on the consumer's critical path).
-constexpr int kMaxSplits = 8;
+constexpr int kMaxSplits = 10;
 __device__ __forceinline__ float sum_splits(const float* p, size_t stride, int splits) {
   float v[kMaxSplits];
 #pragma unroll
@@ -469,24 +469,28 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
   if (threadIdx.x == 0) trace_mark(st, 3);
 }
 
-GemvArgs gemv_plan(int N, int K, int epi) {
+GemvArgs gemv_plan(int N, int K, int epi, int max_splits) {
   GemvArgs a{};
   a.N = N;
   a.K = K;
   a.epi = epi;
   const int KB = K / 64;
   if (epi == GV_PARTIAL) {
-    // largest divisor of KB that is <= 2: the whole weight slice of a tile is
-    // prefetched before the dependency wait, and the per-CTA MMA time (bound
-    // by reading the weight tile from smem) stays short
-    a.kb_per = 1;
-    for (int k = 1; k <= 2 && k <= KB; ++k)
-      if (KB % k == 0) a.kb_per = k;
-    // ... but at most 8 partial sums for the consumer to reduce
-    while (KB / a.kb_per > 8 && a.kb_per < KB) {
-      int k = a.kb_per + 1;
-      while (KB % k) ++k;
-      a.kb_per = k;
+    // K split: as many CTAs as fill the GPU (several per SM at low rows, where
+    // the activation buffer is small) with the shortest weight slice each,
+    // each extra partial costing its consumer a little; at most max_splits
+    // partials (what the consumer reduces) and 8 k-blocks per CTA
+    const int tiles_n = ceil_div(N, 128);
+    float best = 1e30f;
+    a.kb_per = KB;
+    for (int kb = 1; kb <= 8 && kb <= KB; ++kb) {
+      if (KB % kb || KB / kb > max_splits) continue;
+      const int ctas = tiles_n * (KB / kb);
+      const int smem16 = gemv_smem_bytes(kb, kb, epi, 1, 16) + 1024;
+      const int cps = std::max(1, std::min(4, kSmPerSm / smem16));
+      const int waves = ceil_div(ctas, cps * kNumSMs);
+      const float cost = float(waves * kb) + 0.25f * float(KB / kb);
+      if (cost < best - 1e-6f) { best = cost; a.kb_per = kb; }
     }
   } else {
     // non-linear epilogue: as few K splits as fit (<= 8 k-blocks per CTA)
@@ -522,12 +526,12 @@ GemvArgs gemv_plan_for_rows(const GemvArgs& base, int rows) {
   // two CTAs per SM when the activation buffer is small enough that half an
   // SM still holds the whole weight slice (or a ring of >= 4 stages): more
   // CTAs, fewer tiles each
-  for (int cps = 2; cps >= 1; --cps) {
+  for (int cps = 4; cps >= 1; --cps) {
     const int gx = std::max(1, std::min(tiles, cps * kNumSMs / a.splits));
     const int per_cta = ceil_div(tiles, gx) * a.kb_per;
     const int fixed = gemv_smem_bytes(a.kb_per, 0, a.epi, rg, xr);
     int room = (kSmemOptin - fixed) / kGvWBytes;
-    if (cps == 2) room = std::min(room, (kSmPerSm / 2 - 1024 - fixed) / kGvWBytes);
+    if (cps > 1) room = std::min(room, (kSmPerSm / cps - 1024 - fixed) / kGvWBytes);
     const int stages = std::min({kGvMaxStages, room, per_cta});
     if (cps == 1 || stages >= std::min(per_cta, 4)) {
       a.gx = gx;
@@ -538,8 +542,8 @@ GemvArgs gemv_plan_for_rows(const GemvArgs& base, int rows) {
   return a;
 }
 
-size_t gemv_part_floats(int N, int K, int epi) {
-  const GemvArgs a = gemv_plan(N, K, epi);
+size_t gemv_part_floats(int N, int K, int epi, int max_splits) {
+  const GemvArgs a = gemv_plan(N, K, epi, max_splits);
   if (epi == GV_PARTIAL) return size_t(a.splits) * kRows * N;
   return a.splits > 1 ? size_t(a.splits) * ceil_div(N, 128) * kRows * 128 : 0;
 }
@@ -1181,6 +1185,46 @@ int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int lay
   DM_CHECK_CUDA(launch_pdl(cross_attn_kernel, dim3(st.grid_rows, st.heads, kXSplits),
                            dim3(kXaThreads), kXaSmem, stream, xkv_map, st, layer, xq, q_scale,
                            xpart, xcnt, probe));
+  return 0;
+}
+
+// ============================================================ split-K GELU
+// fc1 of the large models: the GEMV writes K-split partials like the linear
+// projections, and this kernel reduces them in split order, adds the bias,
+// applies the exact GELU and writes the bf16 hi/lo operand of fc2 -- the
+// epilogue spread over every SM instead of the last CTA of each tile.
+__global__ void __launch_bounds__(256)
+gelu_hilo_kernel(const DecodeState st, const Partials p, uint16_t* __restrict__ yh,
+                 uint16_t* __restrict__ yl) {
+  if (threadIdx.x == 0) trace_mark(st, 0);
+  pdl_trigger();
+  const int r = blockIdx.y;
+  const int n4 = blockIdx.x * blockDim.x + threadIdx.x;        // 4 features each
+  float4 b = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (4 * n4 < p.n) b = bf16x4_to_f32(__ldg(reinterpret_cast<const uint2*>(p.bias) + n4));
+  pdl_wait();
+  if (threadIdx.x == 0) trace_mark(st, 1);
+  if (r >= *st.n_active || 4 * n4 >= p.n) return;
+  const float4 a = sum_splits4<kMaxHeads>(p.p + size_t(r) * p.n + 4 * n4, size_t(kRows) * p.n,
+                                          p.splits);
+  const float v[4] = {a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w};
+  uint16_t h[4], l[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) split_hilo(gelu_erf(v[i]), h[i], l[i]);
+  const size_t o = size_t(r) * p.n + 4 * n4;
+  *reinterpret_cast<uint2*>(yh + o) = make_uint2(uint32_t(h[0]) | (uint32_t(h[1]) << 16),
+                                                 uint32_t(h[2]) | (uint32_t(h[3]) << 16));
+  *reinterpret_cast<uint2*>(yl + o) = make_uint2(uint32_t(l[0]) | (uint32_t(l[1]) << 16),
+                                                 uint32_t(l[2]) | (uint32_t(l[3]) << 16));
+  if (threadIdx.x == 0) trace_mark(st, 3);
+}
+
+int launch_gelu_hilo(const DecodeState& st, const Partials& p, uint16_t* yh, uint16_t* yl,
+                     cudaStream_t stream) {
+  DM_REQUIRE(p.p != nullptr && p.bias != nullptr && p.n % 4 == 0 && p.splits >= 1 &&
+                 p.splits <= kMaxHeads, "gelu: partials");
+  DM_CHECK_CUDA(launch_pdl(gelu_hilo_kernel, dim3(ceil_div(p.n / 4, 256), st.grid_rows), dim3(256),
+                           0, stream, st, p, yh, yl));
   return 0;
 }
 

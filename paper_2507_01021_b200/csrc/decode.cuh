@@ -132,13 +132,14 @@ constexpr int kGvXBox = 16;
 
 int make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
                  uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
-// Plan (splits, kb_per, stages) of a projection; depends only on (N, K, epilogue).
-GemvArgs gemv_plan(int N, int K, int epi);
+// Plan (splits, kb_per, stages) of a projection; depends only on (N, K,
+// epilogue, max_splits = the partials its consumer reduces).
+GemvArgs gemv_plan(int N, int K, int epi, int max_splits = 8);
 // The same plan for a step graph whose active rows are <= rows: the
 // activation buffer, row groups, ring depth and grid shrink with the rows
 // (two CTAs per SM when they fit); the K split -- hence every value -- stays.
 GemvArgs gemv_plan_for_rows(const GemvArgs& base, int rows);
-size_t gemv_part_floats(int N, int K, int epi);   // scratch for its partial sums
+size_t gemv_part_floats(int N, int K, int epi, int max_splits = 8);   // scratch for its partial sums
 int launch_gemv(const DecodeState& st, const TcGemvMaps& maps, const GemvArgs& a,
                 cudaStream_t stream);
 
@@ -165,9 +166,14 @@ int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, floa
 // counters. Output: o (all heads) as the bf16 hi/lo operand st.ah / st.al of
 // the cross-o GEMV. probe = 1: stream K/V and stop (roofline probe).
 constexpr int kMaxHeads = 20;   // per-head scratch / partial splits a LayerNorm may reduce
+constexpr int kAttnSplits = 10; // partial splits an attention kernel reduces (its q / k / v)
 int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
                       const Partials& xq, float q_scale, float* xpart, int* xcnt,
                       cudaStream_t stream, int probe = 0);
+// fc2's operand from fc1's K-split partials: split-order sum + bias, exact
+// GELU, bf16 hi/lo (the large models' fc1 needs a K split; see record_step).
+int launch_gelu_hilo(const DecodeState& st, const Partials& p, uint16_t* yh, uint16_t* yl,
+                     cudaStream_t stream);
 int launch_finalize(const DecodeState& st, cudaStream_t stream);
 
 }  // namespace dm

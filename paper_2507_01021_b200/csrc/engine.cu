@@ -264,6 +264,7 @@ struct WhisperEngine {
     int n_active_host = 0;
     // K-split partial sums of the linear projections (consumer-reduced)
     float *p_qkv = nullptr, *p_o = nullptr, *p_xq = nullptr, *p_xo = nullptr, *p_fc2 = nullptr;
+    float* p_fc1 = nullptr;        // fc1 K-split partials when fc1 is split (fc1_split)
     float* xpart = nullptr;        // cross-attention split results [kRows][H][8][68]
     int* xcnt = nullptr;           // [kRows * kMaxHeads] split arrival counters
   };
@@ -271,7 +272,12 @@ struct WhisperEngine {
   cudaEvent_t step_start = nullptr;
   // telemetry: kernels launched (graph nodes counted per replay)
   long long launches = 0, steps = 0, encodes = 0, segments = 0;
-  int step_kernels() const { return 11 * Ld + 3; }
+  int step_kernels() const { return (fc1_split() ? 12 : 11) * Ld + 3; }
+  bool fc1_split() const { return d / 64 > 8; }       // fc1's K does not fit one CTA
+  // fc1's K split (fixed per engine): steps of <= 16 rows reduce it in the
+  // GEMV's last CTA and apply GELU there; larger steps write partials and run
+  // gelu_hilo_kernel -- the same split-order sums, bit for bit
+  int fc1_splits = std::getenv("DM_FC1_SPLITS") ? std::atoi(std::getenv("DM_FC1_SPLITS")) : 4;
   int encode_kernels() const { return 2 + 2 + 7 * L + 1 + 1; }
 
   // debug (DM_GUARD=1 at create): every allocation gets a 64 KB 0xA5 tail
@@ -409,21 +415,30 @@ static int engine_init(WhisperEngine* e) {
     // launch plans (depend only on the projection shape) and their scratch
     e->plans.clear();
     for (int l = 0; l < e->Ld; ++l) {
-      e->plans.push_back(gemv_plan(3 * d, d, GV_PARTIAL));     // qkv
-      e->plans.push_back(gemv_plan(d, d, GV_PARTIAL));         // o
-      e->plans.push_back(gemv_plan(d, d, GV_PARTIAL));         // xq
-      e->plans.push_back(gemv_plan(d, d, GV_PARTIAL));         // xo
-      e->plans.push_back(gemv_plan(e->F, d, GV_GELU_HILO));    // fc1
-      e->plans.push_back(gemv_plan(d, e->F, GV_PARTIAL));      // fc2
+      // consumers: attention kernels reduce <= kAttnSplits partials, LayerNorms <= kMaxHeads
+      e->plans.push_back(gemv_plan(3 * d, d, GV_PARTIAL, 5));             // qkv (measured: <= 5)
+      e->plans.push_back(gemv_plan(d, d, GV_PARTIAL, kMaxHeads));         // o
+      e->plans.push_back(gemv_plan(d, d, GV_PARTIAL, kAttnSplits));       // xq
+      e->plans.push_back(gemv_plan(d, d, GV_PARTIAL, kMaxHeads));         // xo
+      // fc1: GELU in the GEMV epilogue when one CTA holds the whole K, else
+      // K-split partials + gelu_hilo_kernel
+      e->plans.push_back(e->fc1_split() ? gemv_plan(e->F, d, GV_PARTIAL, e->fc1_splits)
+                                        : gemv_plan(e->F, d, GV_GELU_HILO));          // fc1
+      e->plans.push_back(gemv_plan(d, e->F, GV_PARTIAL, kMaxHeads));      // fc2
     }
     e->plans.push_back(gemv_plan(c.vocab, d, GV_ARGMAX));      // LM head
-    if (e->alloc_t(&gr.p_qkv, gemv_part_floats(3 * d, d, GV_PARTIAL))) return 2;
-    if (e->alloc_t(&gr.p_o, gemv_part_floats(d, d, GV_PARTIAL))) return 2;
-    if (e->alloc_t(&gr.p_xq, gemv_part_floats(d, d, GV_PARTIAL))) return 2;
-    if (e->alloc_t(&gr.p_xo, gemv_part_floats(d, d, GV_PARTIAL))) return 2;
-    if (e->alloc_t(&gr.p_fc2, gemv_part_floats(d, e->F, GV_PARTIAL))) return 2;
+    if (e->alloc_t(&gr.p_qkv, gemv_part_floats(3 * d, d, GV_PARTIAL, 5))) return 2;
+    if (e->alloc_t(&gr.p_o, gemv_part_floats(d, d, GV_PARTIAL, kMaxHeads))) return 2;
+    if (e->alloc_t(&gr.p_xq, gemv_part_floats(d, d, GV_PARTIAL, kAttnSplits))) return 2;
+    if (e->alloc_t(&gr.p_xo, gemv_part_floats(d, d, GV_PARTIAL, kMaxHeads))) return 2;
+    if (e->alloc_t(&gr.p_fc2, gemv_part_floats(d, e->F, GV_PARTIAL, kMaxHeads))) return 2;
+    if (e->fc1_split() &&
+        e->alloc_t(&gr.p_fc1, gemv_part_floats(e->F, d, GV_PARTIAL, kMaxHeads))) return 2;
     size_t part = std::max<size_t>(1, std::max(gemv_part_floats(e->F, d, GV_GELU_HILO),
                                                gemv_part_floats(c.vocab, d, GV_ARGMAX)));
+    if (e->fc1_split())     // the fused split-GELU epilogue of few-row steps: fc1's own split
+      part = std::max(part, gemv_part_floats(e->F, d, GV_PARTIAL, e->fc1_splits) / kRows * 128 /
+                                ceil_div(e->F, 128) * ceil_div(e->F, 128));
     if (e->alloc_t(&gs.part, part)) return 2;
     if (e->alloc_t(&gs.counters, 4096)) return 2;
     if (e->alloc_t(&gr.xpart, size_t(kRows) * e->H * kXSplits * 68)) return 2;
@@ -601,7 +616,20 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
                               grp.xpart, grp.xcnt, s));
     DM_STEP(gv(pi + 3, grp.p_xo, nullptr, nullptr, nullptr));
     DM_STEP(ln(2, b0 + 12, Partials{grp.p_xo, e->plans[pi + 3].splits, d, e->W(b0 + 11)}));
-    DM_STEP(gv(pi + 4, nullptr, st.hh, st.hl, e->W(b0 + 15)));
+    if (e->fc1_split() && rows > 16) {
+      DM_STEP(gv(pi + 4, grp.p_fc1, nullptr, nullptr, nullptr));
+      DM_STEP(launch_gelu_hilo(st, Partials{grp.p_fc1, e->plans[pi + 4].splits, e->F, e->W(b0 + 15)},
+                               st.hh, st.hl, s));
+    } else if (e->fc1_split()) {
+      GemvArgs g = e->plans[pi + 4];
+      g.epi = GV_GELU_HILO;
+      g = gemv_plan_for_rows(g, rows);
+      g.bias = e->W(b0 + 15); g.part = nullptr; g.yh = st.hh; g.yl = st.hl;
+      g.counter_base = e->gemv_counter_base;
+      DM_STEP(launch_gemv(st, grp.maps[pi + 4], g, s));
+    } else {
+      DM_STEP(gv(pi + 4, nullptr, st.hh, st.hl, e->W(b0 + 15)));
+    }
     DM_STEP(gv(pi + 5, grp.p_fc2, nullptr, nullptr, nullptr));
     prev = Partials{grp.p_fc2, gf, d, e->W(b0 + 17)};
   }
@@ -947,7 +975,9 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
       case 4: return gv(pi + 2, grp.p_xq, nullptr, nullptr, nullptr, cs);
       case 5: return gv(pi + 5, grp.p_fc2, nullptr, nullptr, nullptr, cs);
       case 6: return launch_pdl_floor(cs);
-      case 7: return gv(pi + 4, nullptr, pst.hh, pst.hl, e->W(b0 + 15), cs);
+      case 7:
+        if (e->fc1_split()) return gv(pi + 4, grp.p_fc1, nullptr, nullptr, nullptr, cs);
+        return gv(pi + 4, nullptr, pst.hh, pst.hl, e->W(b0 + 15), cs);
       case 8: return gv(pi + 0, grp.p_qkv, nullptr, nullptr, nullptr, cs);
       case 9:        // the cross-attention reduced to its K/V stream (roofline probe)
         return launch_cross_attn(pst, e->xkv_map, layer,

@@ -20,13 +20,15 @@ slots = list(range(S))
 for i in range(0, S, 32):
     eng.encode([seg] * 32, slots[i:i + 32])
 eng.admit(slots, [400] * S)
-names = []
-for l in range(dims.dec_layers):
-    kinds = ("ln1", "qkv", "self", "o", "ln2", "xq", "xattn", "ln3", "fc1", "fc2")
-    if not int(__import__("os").environ.get("DM_XA_CLUSTER", "0")):
-        kinds = kinds[:7] + ("xo",) + kinds[7:]          # lean cross-attention + cross-o GEMV
-    names += [f"L{l}.{k}" for k in kinds]
-names += ["ln_f", "lm_head", "finalize"]
+def names_for(rows):
+    names = []
+    for l in range(dims.dec_layers):
+        kinds = ("ln1", "qkv", "self", "o", "ln2", "xq", "xattn", "ln3", "fc1", "fc2")
+        kinds = kinds[:7] + ("xo",) + kinds[7:]              # cross-attention, cross-o GEMV
+        if dims.d_model // 64 > 8 and rows > 16:             # split fc1 + GELU kernel
+            kinds = kinds[:10] + ("gelu",) + kinds[10:]
+        names += [f"L{l}.{k}" for k in kinds]
+    return names + ["ln_f", "lm_head", "finalize"]
 lib = eng.lib
 def dbg(which, buf=None, n=0):
     ptr = buf.ctypes.data_as(C.c_void_p) if buf is not None else None
@@ -35,6 +37,7 @@ def dbg(which, buf=None, n=0):
 dbg(10)
 out = {}
 for rows in rows_list:
+    names = names_for(rows)
     eng.set_active(slots[:rows])
     eng.step(6)
     torch.cuda.synchronize()

@@ -44,3 +44,20 @@ def test_large_v3_parity(native_lib):
     assert over.max() <= 0.0, over.max()
     want = [orc.greedy(enc[b], 8) for b in range(2)]
     assert got == want
+
+
+def test_large_v3_batch_invariance_across_fc1_paths(native_lib):
+    """large-v3's fc1 needs a K split: steps of <= 16 rows reduce it in the
+    GEMV's last CTA (+ GELU there), larger steps write partials and run the
+    GELU kernel; both use the same split-order sums, so a segment decodes to
+    the same tokens (and logits) alone and in a batch of 24."""
+    from paper_2507_01021_b200.engine import WhisperGPU
+    rng = np.random.default_rng(44)
+    segs = [rng.integers(-8000, 8000, size=int(rng.uniform(3, 30) * 16000), dtype=np.int16)
+            for _ in range(24)]
+    gpu = WhisperGPU(WHISPER_LARGE_V3, seed=0, init_std=0.05, max_slots=32, max_encode_batch=24)
+    caps = [6] * 24
+    together = gpu.transcribe_ids(segs, caps)
+    alone = [gpu.transcribe_ids([s], [6])[0] for s in segs[:3]]
+    assert together[:3] == alone
+    gpu.close()
