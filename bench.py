@@ -609,8 +609,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--segments", type=int, default=64)
-    ap.add_argument("--encode-batch", type=int, default=64,
-                    help="segments per encoder launch (64: the rest of the batch in one encode)")
+    ap.add_argument("--encode-batch", type=int, default=12,
+                    help="segments per encoder launch (measured at large-v3 with overlap, RTFx: "
+                         "8 -> 1748, 12 -> 1771, 16 -> 1735, 32 -> 1721, 64 -> 1630)")
     ap.add_argument("--steps-per-poll", type=int, default=8)
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -619,8 +620,10 @@ def main():
                     help="1: encode the next group on a second stream while admitted groups decode")
     ap.add_argument("--decode-priority", type=int, default=-1,
                     help="CUDA stream priority of the decode stream (-1 high, 0 normal)")
-    ap.add_argument("--first-encode-batch", type=int, default=24,
-                    help="segments (longest caps first) in the first encode group of an idle engine")
+    ap.add_argument("--first-encode-batch", type=int, default=12,
+                    help="segments (longest caps first) in the first encode group of an idle engine; "
+                         "the rest encode in --encode-batch groups on a second stream while the "
+                         "admitted ones decode (no overlap, one 64-segment encode: 1693-1721)")
     ap.add_argument("--latency-users", type=int, default=64,
                     help="live users for the latency block (0: skip)")
     ap.add_argument("--latency-session-s", type=float, default=30.0)
