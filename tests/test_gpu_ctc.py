@@ -52,7 +52,10 @@ def test_ctc_matches_oracle(ctc_pair):
         T = frames_for(len(x))
         h_ref = orc.hidden(x).numpy()
         err = float(np.abs(hid[b, :T] - h_ref).max())
-        assert err <= 5e-2, (b, err)
+        # 12 post-LN encoder layers on bf16 GEMM inputs: measured max-abs
+        # 0.019-0.022 on these segments (the 1-layer-deeper analogue of the
+        # Whisper encoder's 2e-2); asserted with a 25% margin
+        assert err <= 2.5e-2, (b, err)
         lg = h_ref @ head_w.T + orc.w["head.b"].numpy()
         ref_ids = lg.argmax(-1)
         top2 = np.sort(lg, axis=-1)[:, -2:]
@@ -65,9 +68,25 @@ def test_ctc_matches_oracle(ctc_pair):
         total += T
         want = orc.transcribe_ids(x)
         same += toks[b] == want
+        # the GPU's collapse (repeats merged, blanks dropped) of its own frame
+        # argmax is exact; vs the oracle, only flipped near-tie frames may differ
+        assert toks[b] == _collapse(ids[b, :T]), b
+        dist = _edit(toks[b], want)
+        assert dist <= 2 * len(bad), (b, dist, len(bad))
+        if not len(bad):
+            assert toks[b] == want, b
         print(f"seg {b}: T={T} hidden max|err|={err:.3g} frame flips={len(bad)} "
-              f"(near-tie margins <= {bound:.3g}) token edit distance={_edit(toks[b], want)}")
+              f"(near-tie margins <= {bound:.3g}) token edit distance={dist}")
     assert agree >= 0.99 * total, (agree, total)
+
+
+def _collapse(frame_ids, blank=0):
+    out, prev = [], None
+    for t in frame_ids.tolist():
+        if t != prev and t != blank:
+            out.append(t)
+        prev = t
+    return out
 
 
 def test_ctc_batch_invariance(ctc_pair):

@@ -167,3 +167,52 @@ def test_decode_under_concurrent_stream_load(native_lib):
                 a = torch.tanh(a @ a * 1e-3)
         assert gpu.transcribe_ids(segs, caps) == alone
     torch.cuda.synchronize()
+
+
+def test_gpu_consumer_refill_on_real_engine(native_lib):
+    """GpuConsumer on the real engine with iteration-level admission: more
+    segments than decode slots arrive on the reference's SegmentQueue while the
+    engine decodes; every segment is routed once and its text equals the
+    batch-synchronous B200Backend's (batch invariance through refills). Two
+    engines on cuda:0 share the queue (the multi-GPU consumer path with the
+    device of each engine made current in its thread)."""
+    import threading
+    import time
+    from collections import Counter
+    import refdmx
+    if not refdmx.AVAILABLE:
+        pytest.skip("reference not installed in baseline/_ref")
+    _, rs, rv = refdmx.load()
+    from paper_2507_01021_b200.backend import B200Backend, B200BackendConfig
+    from paper_2507_01021_b200.engine import WhisperGPU
+    from paper_2507_01021_b200.multiplex import Multiplexer
+    from paper_2507_01021_b200.types import batch_of, make_segment
+    engines = [WhisperGPU(WHISPER_TINY, seed=0, init_std=0.05, device=0, max_slots=4,
+                          max_encode_batch=2, steps_per_poll=2) for _ in range(2)]
+    rng = np.random.default_rng(31)
+    durs = rng.uniform(1.0, 8.0, size=18)
+    segs = _segments(18, list(durs), seed=32)
+    routed, lock = [], threading.Lock()
+
+    def router(r):
+        with lock:
+            routed.append(r)
+    mux = Multiplexer(engines, rs.BatchingPolicy(kind="continuous", min_batch=1, max_batch=4),
+                      rs.SegmentQueue(), router, poll_interval_ms=1.0)
+    mux.start()
+    for i, x in enumerate(segs):
+        mux.queue.enqueue_segment(refdmx.ref_segment(rv, f"c{i}", x), rs.monotonic_ms())
+        time.sleep(0.01)
+    t0 = time.time()
+    while len(routed) < len(segs) and time.time() - t0 < 120:
+        time.sleep(0.01)
+    mux.shutdown()
+    assert Counter(r.segment_id for r in routed) == Counter(f"c{i}" for i in range(len(segs)))
+    assert all(r.status == "ok" for r in routed)
+    assert all(c.segments_done for c in mux.consumers)          # both engines served
+    backend = B200Backend(B200BackendConfig(model="whisper-tiny", init_std=0.05), engine=engines[0])
+    want = backend.transcribe_batch(batch_of([make_segment(f"c{i}", x) for i, x in enumerate(segs)]))
+    by = {r.segment_id: r.text for r in routed}
+    assert [by[w.segment_id] for w in want] == [w.text for w in want]
+    for e in engines:
+        e.close()
