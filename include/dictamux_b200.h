@@ -113,6 +113,12 @@ DM_API int dm_whisper_admit(void* handle, const int32_t* slot_ids, const int32_t
                      void* stream);
 /* Free the pages of n slots (after their result was read). */
 DM_API int dm_whisper_release(void* handle, const int32_t* slot_ids, int n);
+/* The decoder prompt of later admissions (Listing 1's `prompt_tokens +
+ * [no_timestamps]`; the reference carries it as
+ * decode_options.prompt, backend.py:181-199): n <= 224 token ids, e.g.
+ * [<|startofprev|>, previous-text ids..., <|sot|>, lang, task, <|notimestamps|>].
+ * Only while no slot is admitted; the step graphs are re-captured. */
+DM_API int dm_whisper_set_prompt(void* handle, const int32_t* tokens, int n, void* stream);
 /* Decode slots set: slots[0..n) take part in subsequent steps. */
 DM_API int dm_whisper_set_active(void* handle, const int32_t* slot_ids, int n, void* stream);
 /* Run n_steps greedy decode steps for the active slots (CUDA graph). */

@@ -10,8 +10,9 @@ Follows transformers 5.5.0 `models/whisper/modeling_whisper.py`:
     self-attn (causal) / cross-attn / MLP, final LN; tied LM head
     (`:966,971,1081`).
 The greedy loop is hand-written (not `generate()`), so no logits processor
-applies: prompt [SOT, en, transcribe, notimestamps] (`PAPER.md:57-59`), then
-argmax (lowest index on ties) until EOT or the per-segment cap.
+applies: prompt [SOT, en, transcribe, notimestamps] (`PAPER.md:57-59`) or a
+given one (e.g. <|startofprev|> + context + that), then argmax (lowest index on
+ties) until EOT or the per-segment cap.
 
 Weights: the bf16-rounded values from the shared manifest, widened to fp32.
 All activations fp32 (the GPU path keeps bf16 GEMM inputs in the encoder and
@@ -136,7 +137,7 @@ class WhisperOracle:
 
     @torch.no_grad()
     def greedy(self, enc: torch.Tensor, cap: int, eot: int | None = None,
-               return_margins: bool = False):
+               return_margins: bool = False, prompt=None):
         """Greedy decode of ONE segment (enc [1500, d] or [1, 1500, d]) with a
         KV cache. Returns generated ids (EOT excluded) and optionally the
         top1-top2 logit margin of every step."""
@@ -147,7 +148,7 @@ class WhisperOracle:
         xkv = self.cross_kv(enc)
         scale = dims.head_dim ** -0.5
         cache = [[None, None] for _ in range(dims.dec_layers)]
-        prompt = list(dims.prompt)
+        prompt = list(dims.prompt if prompt is None else prompt)
         out: list[int] = []
         margins: list[float] = []
         pos = 0

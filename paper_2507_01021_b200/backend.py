@@ -27,7 +27,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .engine import SegmentJob, WhisperGPU
-from .models import SAMPLE_RATE, default_token_cap, get_model
+from .models import SAMPLE_RATE, byte_tokens, default_token_cap, get_model
 from .types import TranscriptResult
 
 _SYLLABLES = ("ka", "ri", "to", "ve", "na", "su", "mel", "or",
@@ -94,6 +94,12 @@ class B200BackendConfig:
     steps_per_poll: int = 8
     overlap_encode: bool = True         # next encode group on a second stream while others decode
     first_encode_batch: int = 8         # first group of an idle engine (longest caps first)
+    # previous-text conditioning (the reference's decode_options.prompt,
+    # backend.py:181-199): token ids, or a text turned into byte-level ids
+    # (no tokenizer files offline); the decoder prompt becomes
+    # <|startofprev|> + context + [SOT, lang, task, <|notimestamps|>]
+    prompt_tokens: tuple[int, ...] | None = None
+    prompt_text: str | None = None
 
     def __post_init__(self) -> None:
         get_model(self.model)
@@ -115,11 +121,16 @@ class B200Backend:
             steps_per_poll=self.cfg.steps_per_poll, overlap_encode=self.cfg.overlap_encode,
             first_encode_batch=self.cfg.first_encode_batch)
         self._device_lock = threading.Lock()
+        ctx = list(self.cfg.prompt_tokens or ())
+        if self.cfg.prompt_text:
+            ctx += byte_tokens(self.cfg.prompt_text)
+        if ctx:
+            self.engine.set_prompt(dims.prompt_with_context(ctx))
+        self._max_cap = 448 - len(getattr(self.engine, "prompt", dims.prompt))
 
     def cap_for(self, duration_s: float) -> int:
-        if self.cfg.cap_tokens is not None:
-            return self.cfg.cap_tokens
-        return default_token_cap(duration_s)
+        cap = self.cfg.cap_tokens if self.cfg.cap_tokens is not None else default_token_cap(duration_s)
+        return min(cap, self._max_cap)
 
     def transcribe_batch(self, batch) -> list[TranscriptResult]:
         entries = batch.entries

@@ -192,6 +192,7 @@ struct UploadRing {
 };
 
 // ------------------------------------------------------------ Whisper engine
+constexpr int kMaxPrompt = 224;     // Whisper: n_text_ctx / 2 (previous-text context + task tokens)
 constexpr int kRowBuckets = 9;
 constexpr int kRowBucket[kRowBuckets] = {1, 2, 4, 8, 16, 24, 32, 48, kRows};
 
@@ -369,8 +370,9 @@ static int engine_init(WhisperEngine* e) {
   st.vocab = c.vocab; st.page_tokens = 64; st.pages_per_slot = 7; st.eot = c.eot;
   st.prompt_len = c.prompt_len;
   st.grid_rows = kRows;            // debug / timing probes; step graphs use their bucket
-  if (e->alloc_t(&e->prompt_dev, 8)) return 2;
-  DM_CHECK_CUDA(cudaMemcpy(e->prompt_dev, c.prompt, sizeof(int32_t) * 8, cudaMemcpyHostToDevice));
+  if (e->alloc_t(&e->prompt_dev, kMaxPrompt)) return 2;
+  DM_CHECK_CUDA(cudaMemcpy(e->prompt_dev, c.prompt, sizeof(int32_t) * c.prompt_len,
+                           cudaMemcpyHostToDevice));
   st.prompt = e->prompt_dev;
   if (e->alloc_t(&e->active_dev, S)) return 2;
   if (e->alloc_t(&e->n_active_dev, 1)) return 2;
@@ -859,6 +861,25 @@ int dm_whisper_release(void* handle, const int32_t* slot_ids, int n) {
       e->free_pages.push_back(e->page_table_host[size_t(slot) * 7 + p]);
     e->slot_pages[slot] = 0;
   }
+  return 0;
+}
+
+int dm_whisper_set_prompt(void* handle, const int32_t* tokens, int n, void* stream) {
+  auto* e = static_cast<WhisperEngine*>(handle);
+  DM_REQUIRE(e != nullptr && tokens != nullptr, "null argument");
+  DM_ON_DEVICE(e->device);
+  DM_REQUIRE(n >= 1 && n <= kMaxPrompt, "prompt length in [1, 224]");
+  for (int s = 0; s < e->cfg.max_slots; ++s)
+    DM_REQUIRE(e->slot_pages[s] == 0, "set the prompt while no slot is admitted");
+  for (int i = 0; i < n; ++i)
+    DM_REQUIRE(tokens[i] >= 0 && tokens[i] < e->cfg.vocab, "prompt token out of the vocabulary");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  DM_CHECK_CUDA(cudaStreamSynchronize(s));
+  DM_CHECK_CUDA(cudaMemcpy(e->prompt_dev, tokens, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+  e->cfg.prompt_len = n;
+  e->st.prompt_len = n;
+  for (auto& g : e->groups) g.st.prompt_len = n;
+  e->step_exec = nullptr;              // step graphs bake the prompt length in: re-capture
   return 0;
 }
 

@@ -128,6 +128,7 @@ class WhisperGPU:
             for i, t in enumerate(dims.prompt):
                 cfg.prompt[i] = t
             cfg.prompt_len = len(dims.prompt)
+            self.prompt: tuple[int, ...] = tuple(dims.prompt)
             cfg.max_slots, cfg.max_encode_batch = max_slots, max_encode_batch
             cfg.num_pages = num_pages if num_pages is not None else max_slots * 7
             if decode_groups is None:
@@ -268,6 +269,15 @@ class WhisperGPU:
         self.stats.encode_calls += 1
         self.stats.segments_encoded += len(segs)
 
+    def set_prompt(self, tokens: Sequence[int]) -> None:
+        """Decoder prompt of later admissions (<= 224 ids; Listing 1's
+        `prompt_tokens + [no_timestamps]`), e.g. dims.prompt_with_context(ids).
+        Only while no slot is admitted; caps shrink to 448 - len(prompt)."""
+        tokens = [int(t) for t in tokens]
+        arr = (C.c_int32 * len(tokens))(*tokens)
+        _native.check(self.lib.dm_whisper_set_prompt(self.handle, arr, len(tokens), self._s))
+        self.prompt = tuple(tokens)
+
     def admit(self, slots: Sequence[int], caps: Sequence[int]) -> None:
         _native.check(self.lib.dm_whisper_admit(self.handle, self._i32(slots), self._i32(caps),
                                                 len(slots), self._s))
@@ -396,7 +406,7 @@ class WhisperGPU:
         left: dict[int, int] = {}              # slot -> steps to its cap
         waiting: list[tuple[int, SegmentJob]] = []   # finished, result in the next snapshot
         results: dict = {}
-        prompt_extra = len(self.dims.prompt) - 1
+        prompt_extra = len(self.prompt) - 1
         t0 = time.perf_counter()
         prev = None                            # (snapshot buffer, [(slot, job)], active slots)
         b = 0

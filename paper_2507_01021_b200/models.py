@@ -51,6 +51,18 @@ class WhisperDims:
         (`SPEC.md:261`)."""
         return (self.sot, self.lang_en, self.transcribe, self.no_timestamps)
 
+    @property
+    def start_of_prev(self) -> int:
+        """<|startofprev|> (two ids after <|transcribe|> in the OpenAI layout:
+        transcribe, startoflm, startofprev)."""
+        return self.transcribe + 2
+
+    def prompt_with_context(self, context: "list[int] | tuple[int, ...]") -> tuple[int, ...]:
+        """Whisper's conditioning prompt: <|startofprev|> + previous-text ids +
+        the task prompt; the context is cut from the left to fit 224 tokens."""
+        context = list(context)[-(224 - 1 - 4):]
+        return (self.start_of_prev, *context) + self.prompt if context else self.prompt
+
 
 WHISPER_TINY = WhisperDims("whisper-tiny", 384, 4, 4, 6, 1536, 80, 51865)
 WHISPER_BASE = WhisperDims("whisper-base", 512, 6, 6, 8, 2048, 80, 51865)
@@ -102,3 +114,16 @@ def default_token_cap(duration_s: float) -> int:
     the decoder's context (448 positions minus the 4-token prompt)."""
     import math
     return max(1, min(MAX_TARGET_POSITIONS - 4, math.ceil(3.75 * duration_s)))
+
+
+def byte_tokens(text: str) -> list[int]:
+    """Previous-text ids for a text prompt without tokenizer files (there is no
+    network for them): the UTF-8 bytes as the byte-level BPE's single-byte
+    tokens -- GPT-2's byte order (bytes_to_unicode: printable ranges first,
+    then the remaining bytes), which the Whisper vocabularies keep as ids
+    0..255. Unmerged, so longer than the real BPE, but within the vocabulary
+    and deterministic."""
+    bs = list(range(33, 127)) + list(range(161, 173)) + list(range(174, 256))
+    order = bs + [b for b in range(256) if b not in bs]
+    rank = {b: i for i, b in enumerate(order)}
+    return [rank[b] for b in text.encode("utf-8")]

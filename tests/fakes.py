@@ -22,6 +22,7 @@ class FakeEngine:
         self.admitted = []
         self.resets = 0
         self.held = set()          # slots holding self-KV pages, like WhisperGPU
+        self.prompt = (50258, 50259, 50359, 50363)
         self.max_active = 0
         self.lock = threading.Lock()
 
@@ -64,6 +65,9 @@ class FakeEngine:
                     if j.on_done:
                         j.on_done(key, ids)
         return results
+
+    def set_prompt(self, tokens):
+        self.prompt = tuple(tokens)
 
     def reset(self):
         self.resets += 1

@@ -57,11 +57,11 @@ def first_divergence(a, b):
     return None if len(a) == len(b) else min(len(a), len(b))
 
 
-def audit(orc, enc, got, want, eot, tol, label):
+def audit(orc, enc, got, want, eot, tol, label, prompt=None):
     """Classify each segment: identical, or diverging at step k with the
     oracle's teacher-forced gap (top-1 logit minus the logit of the GPU's
     token) at that step. Returns (n_identical, divergences)."""
-    prompt = list(orc.dims.prompt)
+    prompt = list(orc.dims.prompt if prompt is None else prompt)
     same, divs = 0, []
     for b, (g, w) in enumerate(zip(got, want)):
         k = first_divergence(g, w)
@@ -263,3 +263,34 @@ def test_weight_fill_bit_exact_large_v3(native_lib):
     for n in names:
         t = man[n]
         assert np.array_equal(bits[t.offset:t.offset + t.numel], tensor_bits(man, t)), n
+
+
+def test_prompt_tokens_with_context(tiny):
+    """Listing 1's `prompt_tokens + [no_timestamps]` with previous-text
+    context: <|startofprev|> + context ids + [SOT, en, transcribe,
+    notimestamps] (the reference's decode_options.prompt as byte-level ids);
+    decode-only parity with the oracle's greedy loop on the same prompt, and
+    the backend's prompt_text wiring produces that prompt."""
+    from paper_2507_01021_b200.backend import B200Backend, B200BackendConfig
+    from paper_2507_01021_b200.models import byte_tokens
+    orc, gpu = tiny
+    prompt = WHISPER_TINY.prompt_with_context(byte_tokens("courtroom dictation"))
+    assert len(prompt) == 1 + 19 + 4
+    segs = _segments([9.0, 22.0, 4.0], seed=106)
+    caps = [40, 60, 25]
+    gpu.set_prompt(prompt)
+    try:
+        enc = gpu_encoder_out(gpu, segs)
+        got = gpu.transcribe_ids(segs, caps)
+        want = [orc.greedy(enc[b], caps[b], prompt=prompt) for b in range(3)]
+        same, divs = audit(orc, enc, got, want, WHISPER_TINY.eot, TIE_TOL_DECODE,
+                           "tiny prompt with context", prompt=prompt)
+        assert all(d["near_tie"] for d in divs), divs
+        plain = [orc.greedy(enc[b], caps[b]) for b in range(3)]
+        assert want != plain                          # the context changes the decode
+    finally:
+        gpu.set_prompt(WHISPER_TINY.prompt)
+    be = B200Backend(B200BackendConfig(model="whisper-tiny", init_std=STD, max_slots=8,
+                                       max_encode_batch=4, prompt_text="courtroom dictation"))
+    assert be.engine.prompt == prompt
+    be.close()
