@@ -8,10 +8,13 @@ missing, every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libdictamux_b200.so"
+# (A/B experiments: DM_LIB points at another build of the same sources)
+LIB_PATH = Path(os.environ.get("DM_LIB", LIB_PATH))
 
 EXPORTS = (
     "dm_last_error", "dm_version", "dm_fill_normal_bf16", "dm_logmel", "dm_logmel_operand",

@@ -939,9 +939,11 @@ int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, floa
   return 0;
 }
 
-constexpr int kXaThreads = 192;                               // one key per thread
-constexpr int kXaKeys = 192;                                  // ceil(1500 / 8 / 64) * 64
+constexpr int kXaThreads = 128;                               // 4 warps = the 4 TMEM quadrants
+constexpr int kXaBoxes = kXaKeysPerSplit / 64;                // 64-key TMA boxes per split
+constexpr int kXaKeys = kXaKeysPerSplit;
 static_assert(kXSplits * kXaKeys >= 1500 && (kXSplits - 1) * kXaKeys < 1500, "key splits");
+constexpr int kXaTmemCols = (kXaBoxes + 1) * 8 <= 32 ? 32 : ((kXaBoxes + 1) * 8 <= 64 ? 64 : 128);
 
 // Cross-attention of the fed token (modeling_whisper.py:398-406, encoder_attn
 // of the decoder layer; q.64^-1/2 at :310), one CTA per (row, head, key split
@@ -963,8 +965,8 @@ static_assert(kXSplits * kXaKeys >= 1500 && (kXSplits - 1) * kXaKeys < 1500, "ke
 // persistent 2-CTA/SM grid with a K/V ring; warp-level mma.sync; all slower
 // at 64 rows, the cluster form faster below ~32 rows.)
 constexpr int kXaQOff = 2 * kXaKeys * 128;                // B operand [q_hi; q_lo; 0] (1 KB)
-constexpr int kXaPOff = kXaQOff + 1024;                   // B operand [p_hi; p_lo; 0] (3 x 1 KB)
-constexpr int kXaBarOff = kXaPOff + 3 * 1024;
+constexpr int kXaPOff = kXaQOff + 1024;                   // B operand [p_hi; p_lo; 0] (1 KB per box)
+constexpr int kXaBarOff = kXaPOff + kXaBoxes * 1024;
 constexpr int kXaSmem = 1024 + kXaBarOff + 64;          // (align) K, V, q / p operands, mbarriers
 constexpr uint32_t kXaIdescS = umma_idesc_bf16(64, 8);                 // K-major A and B
 constexpr uint32_t kXaIdescO = umma_idesc_bf16(64, 8) | (1u << 15);    // A (V^T) MN-major
@@ -980,7 +982,7 @@ __device__ __forceinline__ int sw128_off(int n, int k) {
 
 constexpr int kXpStride = 68;                 // floats per split result: o[64], max, sum, pad
 
-__global__ void __launch_bounds__(kXaThreads, 4)
+__global__ void __launch_bounds__(kXaThreads, kXaCtasPerSm)
 cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, int layer,
                        const Partials xq, float q_scale, float* __restrict__ xpart,
                        int* __restrict__ xcnt, int probe) {
@@ -1014,17 +1016,17 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     const int row_k = (((layer * st.max_slots + slot) * 2 + 0) * H + h) * 1500 + k0;
     const int row_v = row_k + H * 1500;
     const uint64_t stream = l2_policy_evict_first();
-    mbar_arrive_expect_tx(barK, 3 * 64 * 128);
+    mbar_arrive_expect_tx(barK, kXaBoxes * 64 * 128);
 #pragma unroll
-    for (int bx = 0; bx < 3; ++bx)
+    for (int bx = 0; bx < kXaBoxes; ++bx)
       tma_load_2d_hint(Ks + bx * 64 * 128, &tm, barK, 0, row_k + bx * 64, stream);
-    mbar_arrive_expect_tx(barV, 3 * 64 * 128);
+    mbar_arrive_expect_tx(barV, kXaBoxes * 64 * 128);
 #pragma unroll
-    for (int bx = 0; bx < 3; ++bx)
+    for (int bx = 0; bx < kXaBoxes; ++bx)
       tma_load_2d_hint(Vs + bx * 64 * 128, &tm, barV, 0, row_v + bx * 64, stream);
   }
-  if (warp == 1) tmem_alloc(&tmem_slot, 32);
-  for (int i = tid; i < 4 * 1024 / 16; i += kXaThreads) {
+  if (warp == 1) tmem_alloc(&tmem_slot, kXaTmemCols);
+  for (int i = tid; i < (1 + kXaBoxes) * 1024 / 16; i += kXaThreads) {
     const int row = (i * 16 / 128) & 7;
     if (row >= 2) reinterpret_cast<uint4*>(Qs)[i] = make_uint4(0u, 0u, 0u, 0u);
   }
@@ -1041,7 +1043,7 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     mbar_wait(barV, 0);
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, 32);
+    if (warp == 1) tmem_dealloc(tmem, kXaTmemCols);
     return;
   }
   if (tid < 64) {
@@ -1060,7 +1062,7 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     tc_fence_after();
     const uint64_t bq_desc = umma_desc_sw128(smem_u32(Qs));
 #pragma unroll
-    for (int bx = 0; bx < 3; ++bx) {
+    for (int bx = 0; bx < kXaBoxes; ++bx) {
       const uint64_t ak = umma_desc_sw128(smem_u32(Ks + bx * 64 * 128));
 #pragma unroll
       for (int k = 0; k < 4; ++k)
@@ -1071,17 +1073,17 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
   float* res = xpart + ((size_t(r) * H + h) * kXSplits + sp) * kXpStride;
   if (warp < 4) {
     const bool own = lane < 16;
-    float s3[3], e3[3];
+    float s3[kXaBoxes], e3[kXaBoxes];
     mbar_wait(barS, 0);
     tc_fence_after();
-    uint32_t a[3], b[3];
+    uint32_t a[kXaBoxes], b[kXaBoxes];
     const uint32_t lane_base = uint32_t(warp * 32) << 16;
 #pragma unroll
-    for (int j = 0; j < 3; ++j) tmem_ld2(tmem + lane_base + j * 8, a[j], b[j]);
+    for (int j = 0; j < kXaBoxes; ++j) tmem_ld2(tmem + lane_base + j * 8, a[j], b[j]);
     tmem_wait_ld();
     float mloc = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
+    for (int j = 0; j < kXaBoxes; ++j) {
       const int key = 64 * j + 16 * warp + lane;
       s3[j] = (own && key < nk) ? __uint_as_float(a[j]) + __uint_as_float(b[j]) : -INFINITY;
       mloc = fmaxf(mloc, s3[j]);
@@ -1093,7 +1095,7 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     const float m = fmaxf(fmaxf(redm[0], redm[1]), fmaxf(redm[2], redm[3]));
     float es = 0.f;
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
+    for (int j = 0; j < kXaBoxes; ++j) {
       e3[j] = s3[j] == -INFINITY ? 0.f : exp2f((s3[j] - m) * kLog2e);
       es += e3[j];
     }
@@ -1102,7 +1104,7 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     if (lane == 0) reds[warp] = es;
     if (own) {
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
+      for (int j = 0; j < kXaBoxes; ++j) {
         uint16_t hi, lo;
         split_hilo(e3[j], hi, lo);
         const int kk = 16 * warp + lane;
@@ -1118,12 +1120,12 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
       mbar_wait(barV, 0);
       tc_fence_after();
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
+      for (int j = 0; j < kXaBoxes; ++j) {
         const uint64_t bp = umma_desc_sw128(smem_u32(Ps + j * 1024));
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint64_t av = umma_desc_sw128(smem_u32(Vs + j * 64 * 128 + k * 2048));
-          umma_bf16_ss(tmem + 24, av, bp + 2 * k, kXaIdescO, (j | k) != 0);
+          umma_bf16_ss(tmem + kXaBoxes * 8, av, bp + 2 * k, kXaIdescO, (j | k) != 0);
         }
       }
       umma_commit(barO);
@@ -1131,14 +1133,14 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     mbar_wait(barO, 0);
     tc_fence_after();
     uint32_t oa, ob;
-    tmem_ld2(tmem + lane_base + 24, oa, ob);
+    tmem_ld2(tmem + lane_base + kXaBoxes * 8, oa, ob);
     tmem_wait_ld();
     if (own) res[16 * warp + lane] = __uint_as_float(oa) + __uint_as_float(ob);
     __threadfence();
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc(tmem, 32);
+  if (warp == 1) tmem_dealloc(tmem, kXaTmemCols);
   if (tid == 0) is_last = atomicAdd(&xcnt[r * H + h], 1) == kXSplits - 1;
   __syncthreads();
   if (!is_last) return;

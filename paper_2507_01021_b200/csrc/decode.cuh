@@ -35,7 +35,15 @@
 namespace dm {
 
 constexpr int kRows = 64;          // max active slots = max MMA N
-constexpr int kXSplits = 8;        // cross-attention key splits; fixed per engine
+// cross-attention key splits (fixed: the merge order is part of the result):
+// 4 splits of 384 keys, 2 CTAs of ~105 KB per SM (measured against 8 x 192 at
+// 4 per SM: see DESIGN.md section 4)
+#ifndef DM_XA_KEYS
+#define DM_XA_KEYS 192
+#endif
+constexpr int kXaKeysPerSplit = DM_XA_KEYS;
+constexpr int kXSplits = (1500 + kXaKeysPerSplit - 1) / kXaKeysPerSplit;
+constexpr int kXaCtasPerSm = kXaKeysPerSplit >= 384 ? 2 : (kXaKeysPerSplit >= 192 ? 4 : 6);
 
 struct DecodeState {
   int max_slots, d, heads, layers, ffn, vocab;
