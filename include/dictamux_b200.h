@@ -182,6 +182,14 @@ DM_API int dm_whisper_stats(void* handle, int64_t* out, int n);
 DM_API int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float* avg_ms,
                                   void* stream);
 
+/* Batched VAD front: the reference's classify_frame
+ * (pkg/src/dictamux/vad.py:123-133) for n_frames frames of any sessions:
+ * out[f] = 1 (SPEECH) iff mean(pcm[offsets[f] .. + lengths[f]]^2) >=
+ * threshold_rms_sq, with the mean exact (int64 sum, one double division), so
+ * labels are bit-identical to the reference's float64 numpy. Device pointers. */
+DM_API int dm_vad_classify(const int16_t* pcm, const int64_t* offsets, const int32_t* lengths,
+                           int n_frames, double threshold_rms_sq, uint8_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

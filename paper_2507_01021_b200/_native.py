@@ -23,6 +23,7 @@ EXPORTS = (
     "dm_whisper_set_active", "dm_whisper_step", "dm_whisper_read", "dm_whisper_read_async",
     "dm_whisper_debug", "dm_whisper_stats", "dm_whisper_time_kernel",
     "dm_ctc_create", "dm_ctc_destroy", "dm_ctc_transcribe", "dm_ctc_read", "dm_ctc_debug",
+    "dm_vad_classify",
 )
 
 
@@ -92,6 +93,7 @@ def load(build_if_missing: bool = False):
             "dm_ctc_transcribe": [P, P, P, P, C.c_int, P],
             "dm_ctc_read": [P, P, P, P, P],
             "dm_ctc_debug": [P, C.c_int, P, C.c_size_t, P],
+            "dm_vad_classify": [P, P, P, C.c_int, C.c_double, P, P],
         }
         for name, args in sig.items():
             fn = getattr(lib, name)

@@ -17,7 +17,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "_lib"
 LIB = LIBDIR / "libdictamux_b200.so"
-SOURCES = ["engine.cu", "gemm.cu", "attention.cu", "logmel.cu", "decode.cu", "ctc.cu"]
+SOURCES = ["engine.cu", "gemm.cu", "attention.cu", "logmel.cu", "decode.cu", "ctc.cu", "vad.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-fvisibility=hidden",
