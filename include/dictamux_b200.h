@@ -106,6 +106,16 @@ DM_API int dm_whisper_destroy(void* handle);
  * dm_logmel (device). */
 DM_API int dm_whisper_encode(void* handle, const int16_t* pcm, const int64_t* offsets,
                       const int32_t* lengths, int n, const int32_t* slot_ids, void* stream);
+/* Length-aware encode (opt-in): as dm_whisper_encode, but
+ * each segment's encoder runs on its own window of ceil(n / 320) positions
+ * (<= 1500) instead of the 30 s pad_or_trim window: the log-mel frames past
+ * the window are the conv's zero padding, attention is masked to the window,
+ * and decode cross-attends only to it (fewer FLOPs and cross-KV bytes; the
+ * result differs from the padded path). host_lengths: the same lengths as
+ * `lengths`, on the host (they size the batch's window). */
+DM_API int dm_whisper_encode_lengths(void* handle, const int16_t* pcm, const int64_t* offsets,
+                                     const int32_t* lengths, const int32_t* host_lengths, int n,
+                                     const int32_t* slot_ids, void* stream);
 /* Reset n slots for a new segment: greedy cap per slot (tokens, <= 444);
  * allocates the slot's self-KV pages. Returns DM_ERR_RESOURCE if the page
  * pool is exhausted. */

@@ -83,7 +83,8 @@ class WhisperOracle:
         x = F.gelu(F.conv1d(x, w1, self.w["enc.conv1.b"], padding=1))
         x = F.gelu(F.conv1d(x, w2, self.w["enc.conv2.b"], stride=2,
                             padding=1))
-        x = x.permute(0, 2, 1) + self.w["enc.pos"]
+        x = x.permute(0, 2, 1)
+        x = x + self.w["enc.pos"][:x.shape[1]]
         scale = self.dims.head_dim ** -0.5
         for i in range(self.dims.enc_layers):
             p = f"enc.l{i}"
@@ -95,6 +96,17 @@ class WhisperOracle:
             h = self._ln(x, f"{p}.ln2")
             x = x + self._lin(F.gelu(self._lin(h, f"{p}.fc1")), f"{p}.fc2")
         return self._ln(x, "enc.ln")
+
+    @torch.no_grad()
+    def encode_length_aware(self, mel: np.ndarray | torch.Tensor, n_samples: int) -> torch.Tensor:
+        """The opt-in length-aware encoder's definition: the feature
+        extractor's frames of the padded window (same values and clamp), cut to
+        the segment's own window of ceil(n / 320) positions (2 frames each; the
+        conv sees zero padding after it) -> [len, d]."""
+        n = min(int(n_samples), 480000)
+        ln = max(1, min(1500, (n + 319) // 320))
+        m = torch.as_tensor(mel, dtype=torch.float32).reshape(1, self.dims.n_mels, -1)
+        return self.encode(m[:, :, :2 * ln])[0]
 
     # -------------------------------------------------------------- decoder
     def cross_kv(self, enc: torch.Tensor):

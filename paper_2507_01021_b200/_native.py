@@ -19,7 +19,7 @@ LIB_PATH = Path(os.environ.get("DM_LIB", LIB_PATH))
 EXPORTS = (
     "dm_last_error", "dm_version", "dm_fill_normal_bf16", "dm_logmel", "dm_logmel_operand",
     "dm_gemm_bf16_f32", "dm_whisper_create", "dm_whisper_destroy",
-    "dm_whisper_encode", "dm_whisper_admit", "dm_whisper_release", "dm_whisper_set_prompt",
+    "dm_whisper_encode", "dm_whisper_encode_lengths", "dm_whisper_admit", "dm_whisper_release", "dm_whisper_set_prompt",
     "dm_whisper_set_active", "dm_whisper_step", "dm_whisper_read", "dm_whisper_read_async",
     "dm_whisper_debug", "dm_whisper_stats", "dm_whisper_time_kernel",
     "dm_ctc_create", "dm_ctc_destroy", "dm_ctc_transcribe", "dm_ctc_read", "dm_ctc_debug",
@@ -78,6 +78,7 @@ def load(build_if_missing: bool = False):
                                   C.POINTER(C.c_void_p)],
             "dm_whisper_destroy": [P],
             "dm_whisper_encode": [P, P, P, P, C.c_int, P, P],
+            "dm_whisper_encode_lengths": [P, P, P, P, P, C.c_int, P, P],
             "dm_whisper_admit": [P, P, P, C.c_int, P],
             "dm_whisper_release": [P, P, C.c_int],
             "dm_whisper_set_prompt": [P, P, C.c_int, P],

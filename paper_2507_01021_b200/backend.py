@@ -100,6 +100,9 @@ class B200BackendConfig:
     # <|startofprev|> + context + [SOT, lang, task, <|notimestamps|>]
     prompt_tokens: tuple[int, ...] | None = None
     prompt_text: str | None = None
+    # opt-in length-aware encoder: skips the 30 s window's
+    # zero padding; changes results vs the pad_or_trim contract
+    length_aware: bool = False
 
     def __post_init__(self) -> None:
         get_model(self.model)
@@ -119,7 +122,7 @@ class B200Backend:
             dims, seed=self.cfg.seed, init_std=self.cfg.init_std, device=self.cfg.device,
             max_slots=self.cfg.max_slots, max_encode_batch=self.cfg.max_encode_batch,
             steps_per_poll=self.cfg.steps_per_poll, overlap_encode=self.cfg.overlap_encode,
-            first_encode_batch=self.cfg.first_encode_batch)
+            first_encode_batch=self.cfg.first_encode_batch, length_aware=self.cfg.length_aware)
         self._device_lock = threading.Lock()
         ctx = list(self.cfg.prompt_tokens or ())
         if self.cfg.prompt_text:

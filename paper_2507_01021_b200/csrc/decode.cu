@@ -982,6 +982,48 @@ __device__ __forceinline__ int sw128_off(int n, int k) {
 
 constexpr int kXpStride = 68;                 // floats per split result: o[64], max, sum, pad
 
+// After a split's (o, max, sum) is in `xpart`: count it; the last of the 8
+// splits of (row, head) merges them in split order into the cross-o operand.
+__device__ __forceinline__ void xattn_finish(const DecodeState& st, const float* xpart, int* xcnt,
+                                             int r, int h, int tid, int* is_last) {
+  const int H = st.heads;
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) *is_last = atomicAdd(&xcnt[r * H + h], 1) == kXSplits - 1;
+  __syncthreads();
+  if (!*is_last) return;
+  __threadfence();
+  if (tid < 64) {
+    const float* base = xpart + (size_t(r) * H + h) * kXSplits * kXpStride;
+    float mv[kXSplits], lv[kXSplits], ov[kXSplits];
+#pragma unroll
+    for (int s = 0; s < kXSplits; ++s) {
+      mv[s] = __ldcg(base + s * kXpStride + 64);
+      lv[s] = __ldcg(base + s * kXpStride + 65);
+      ov[s] = __ldcg(base + s * kXpStride + tid);
+    }
+    float M = -INFINITY;
+#pragma unroll
+    for (int s = 0; s < kXSplits; ++s) M = fmaxf(M, mv[s]);
+    float Ls = 0.f, O = 0.f;
+#pragma unroll
+    for (int s = 0; s < kXSplits; ++s) {
+      const float f = exp2f((mv[s] - M) * kLog2e);
+      Ls += lv[s] * f;
+      O += ov[s] * f;
+    }
+    uint16_t hi, lo;
+    split_hilo(O / Ls, hi, lo);
+    const size_t idx = size_t(r) * st.d + h * 64 + tid;
+    st.ah[idx] = hi;
+    st.al[idx] = lo;
+  }
+  if (tid == 0) {
+    xcnt[r * H + h] = 0;                         // ready for the next launch of any layer
+    trace_mark(st, 3);
+  }
+}
+
 __global__ void __launch_bounds__(kXaThreads, kXaCtasPerSm)
 cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, int layer,
                        const Partials xq, float q_scale, float* __restrict__ xpart,
@@ -997,7 +1039,16 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
   if (r >= *st.n_active) return;
   const int slot = st.active[r];
   const int H = st.heads;
-  const int k0 = sp * kXaKeys, nk = min(1500, k0 + kXaKeys) - k0;
+  const int k0 = sp * kXaKeys, nk = min(st.enc_len[slot], k0 + kXaKeys) - k0;
+  float* res = xpart + ((size_t(r) * H + h) * kXSplits + sp) * kXpStride;
+  if (nk <= 0) {
+    // a split past a length-aware segment's window: no stream, an empty result
+    pdl_wait();
+    if (tid < 64) res[tid] = 0.f;
+    if (tid == 64) { res[64] = -INFINITY; res[65] = 0.f; }
+    xattn_finish(st, xpart, xcnt, r, h, tid, &is_last);
+    return;
+  }
   uint8_t* Ks = xa_smem;
   uint8_t* Vs = xa_smem + kXaKeys * 128;
   uint8_t* Qs = xa_smem + kXaQOff;
@@ -1070,7 +1121,6 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     }
     umma_commit(barS);
   }
-  float* res = xpart + ((size_t(r) * H + h) * kXSplits + sp) * kXpStride;
   if (warp < 4) {
     const bool own = lane < 16;
     float s3[kXaBoxes], e3[kXaBoxes];
@@ -1141,40 +1191,7 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, kXaTmemCols);
-  if (tid == 0) is_last = atomicAdd(&xcnt[r * H + h], 1) == kXSplits - 1;
-  __syncthreads();
-  if (!is_last) return;
-  // merge the 8 splits in split order; o_head -> the cross-o GEMV operand
-  __threadfence();
-  if (tid < 64) {
-    const float* base = xpart + (size_t(r) * H + h) * kXSplits * kXpStride;
-    float mv[kXSplits], lv[kXSplits], ov[kXSplits];
-#pragma unroll
-    for (int s = 0; s < kXSplits; ++s) {
-      mv[s] = __ldcg(base + s * kXpStride + 64);
-      lv[s] = __ldcg(base + s * kXpStride + 65);
-      ov[s] = __ldcg(base + s * kXpStride + tid);
-    }
-    float M = -INFINITY;
-#pragma unroll
-    for (int s = 0; s < kXSplits; ++s) M = fmaxf(M, mv[s]);
-    float Ls = 0.f, O = 0.f;
-#pragma unroll
-    for (int s = 0; s < kXSplits; ++s) {
-      const float f = exp2f((mv[s] - M) * kLog2e);
-      Ls += lv[s] * f;
-      O += ov[s] * f;
-    }
-    uint16_t hi, lo;
-    split_hilo(O / Ls, hi, lo);
-    const size_t idx = size_t(r) * st.d + h * 64 + tid;
-    st.ah[idx] = hi;
-    st.al[idx] = lo;
-  }
-  if (tid == 0) {
-    xcnt[r * H + h] = 0;                         // ready for the next launch of any layer
-    trace_mark(st, 3);
-  }
+  xattn_finish(st, xpart, xcnt, r, h, tid, &is_last);
 }
 
 int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,

@@ -65,6 +65,8 @@ struct DecodeState {
   const int32_t* page_table;   // [S, pages_per_slot] (host-set at admission)
   uint16_t* kv_pool;           // [pages][L][2][H][page_tokens][64] bf16
   const uint16_t* xkv;         // [L][S][2][H][1500][64] bf16
+  const int32_t* enc_len;      // [S] encoder positions of the slot's segment (1500, or fewer
+                               // after a length-aware encode); cross-attention keys < enc_len
   // row-space activations
   float* x;                    // [kRows, d] residual stream (fp32)
   uint16_t *xh, *xl;           // [kRows, d]   LN output, bf16 hi/lo

@@ -40,7 +40,8 @@ cudaError_t set_max_smem(const void* fn, int bytes) {
 // forward decls (logmel.cu / attention.cu)
 struct LogmelTables;
 int launch_logmel(const int16_t*, const int64_t*, const int32_t*, int, int,
-                  const LogmelTables*, float*, uint16_t*, uint32_t*, cudaStream_t);
+                  const LogmelTables*, float*, uint16_t*, uint32_t*, cudaStream_t,
+                  int frames = 3000);
 int launch_layernorm_bf16(const float*, const uint16_t*, const uint16_t*, uint16_t*, int, int,
                           cudaStream_t, float* y32 = nullptr);
 int launch_attention(const uint16_t*, const uint16_t*, const uint16_t*, int, int, int, int,
@@ -224,8 +225,11 @@ struct WhisperEngine {
   uint16_t* fc1_out = nullptr;   // [E*1500, F]
   uint16_t* enc_out = nullptr;   // [E*1500, d]
   int32_t* slot_dev = nullptr;   // [E]
+  int32_t* seg_len_dev = nullptr;  // [E] encoder positions per segment of the last encode
+  int32_t* enc_len_dev = nullptr;  // [max_slots] encoder positions per slot (st.enc_len)
   int32_t* slot_host = nullptr;  // pinned [E]
   int last_n = 0;
+  int last_rows = 1500;          // encoder positions per segment of the last encode
   int enc_stop = 1 << 30;        // debug: run only the first enc_stop layers
   bool enc_tap = false;          // debug: keep the fp32 encoder output (in resid)
   bool mel_tap = false;          // debug: also write the fp32 [n, n_mels, 3000] features
@@ -279,7 +283,7 @@ struct WhisperEngine {
   // GEMV's last CTA and apply GELU there; larger steps write partials and run
   // gelu_hilo_kernel -- the same split-order sums, bit for bit
   int fc1_splits = std::getenv("DM_FC1_SPLITS") ? std::atoi(std::getenv("DM_FC1_SPLITS")) : 4;
-  int encode_kernels() const { return 2 + 2 + 7 * L + 1 + 1; }
+  int encode_kernels() const { return 2 + 1 + 2 + 7 * L + 1 + 1; }
 
   // debug (DM_GUARD=1 at create): every allocation gets a 64 KB 0xA5 tail
   // guard; dm_whisper_debug(13) reports the allocations whose guard changed
@@ -359,6 +363,7 @@ static int engine_init(WhisperEngine* e) {
   if (e->alloc_t(&e->fc1_out, rows * e->F, false)) return 2;
   if (e->alloc_t(&e->enc_out, rows * d, false)) return 2;
   if (e->alloc_t(&e->slot_dev, E)) return 2;
+  if (e->alloc_t(&e->seg_len_dev, E)) return 2;
   DM_CHECK_CUDA(cudaMallocHost(&e->slot_host, sizeof(int32_t) * E));
   if (int rc = e->ring.init()) return rc;
   if (e->alloc_t(&e->admit_args_dev, size_t(2) * S)) return 2;
@@ -397,6 +402,12 @@ static int engine_init(WhisperEngine* e) {
   uint16_t* xkv = nullptr;
   if (e->alloc_t(&xkv, size_t(e->Ld) * S * 2 * e->H * 1500 * 64)) return 2;
   st.xkv = xkv;
+  if (e->alloc_t(&e->enc_len_dev, S)) return 2;
+  {
+    std::vector<int32_t> full(S, 1500);
+    DM_CHECK_CUDA(cudaMemcpy(e->enc_len_dev, full.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice));
+  }
+  st.enc_len = e->enc_len_dev;
   const int G = std::max(1, std::min(c.decode_groups > 0 ? c.decode_groups : 1, S));
   e->groups.resize(G);
   const int tiles = ceil_div(c.vocab, 128);
@@ -487,19 +498,57 @@ static int engine_init(WhisperEngine* e) {
   return 0;
 }
 
+// Per encode: encoder positions per segment (1500, or ceil(n / 320) for a
+// length-aware encode), the slots' enc_len, the conv1 input's zero frame right
+// after each segment's window (length-aware), and the conv1 output's two zero
+// pad rows (its row stride follows the window).
+__global__ void encode_prep_kernel(const int32_t* __restrict__ lengths, int n, int length_aware,
+                                   const int32_t* __restrict__ slot_ids, int32_t* __restrict__ seg_len,
+                                   int32_t* __restrict__ enc_len, uint16_t* __restrict__ mel_t, int ldt,
+                                   uint16_t* __restrict__ conv1_out, int c1_rows, int d) {
+  const int b = blockIdx.x;
+  if (b >= n) return;
+  int len = 1500;
+  if (length_aware) {
+    const int ns = min(max(lengths[b], 0), 480000);
+    len = max(1, min(1500, (ns + 319) / 320));
+  }
+  if (threadIdx.x == 0) {
+    seg_len[b] = len;
+    enc_len[slot_ids[b]] = len;
+  }
+  if (length_aware)          // frame 2 len (row 2 len + 1) of the conv1 input: zero padding
+    for (int c = threadIdx.x; c < ldt; c += blockDim.x)
+      mel_t[(size_t(b) * 3002 + 2 * len + 1) * ldt + c] = 0;
+  uint16_t* c1 = conv1_out + size_t(b) * c1_rows * d;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    c1[c] = 0;
+    c1[size_t(c1_rows - 1) * d + c] = 0;
+  }
+}
+
+// rows: encoder positions computed per segment (1500, or the batch's longest
+// length-aware window); length_aware: mask each segment to its own window.
 static int encoder_forward(WhisperEngine* e, const int16_t* pcm, const int64_t* offsets,
-                           const int32_t* lengths, int n, cudaStream_t s) {
+                           const int32_t* lengths, int n, cudaStream_t s, int rows,
+                           bool length_aware) {
   const int d = e->d, H = e->H;
+  const int frames = 2 * rows, t_pad = ceil_div(rows, 128) * 128;
   const LogmelTables* tab = nullptr;
   if (int rc = get_logmel_tables(e->nm, &tab)) return rc;
   // the fp32 feature contract is written only for the debug tap (dm_whisper_debug 15)
   if (int rc = launch_logmel(pcm, offsets, lengths, n, e->nm, tab, e->mel_tap ? e->mel : nullptr,
-                             e->mel_t, e->segmax, s))
+                             e->mel_t, e->segmax, s, e->mel_tap ? 3000 : frames))
     return rc;
+  encode_prep_kernel<<<n, 128, 0, s>>>(lengths, n, length_aware ? 1 : 0, e->slot_dev,
+                                       e->seg_len_dev, e->enc_len_dev, e->mel_t, e->Cp,
+                                       e->conv1_out, frames + 2, d);
+  DM_CHECK_LAUNCH();
   // conv1 (implicit GEMM over the padded time-major mel), GELU
   {
     GemmArgs g;
-    g.A = e->mel_t; g.a_mode = A_CONV_S1; g.C = e->Cp; g.K = 3 * e->Cp; g.T = 3000; g.Bt = n;
+    g.A = e->mel_t; g.a_mode = A_CONV_S1; g.C = e->Cp; g.K = 3 * e->Cp; g.T = frames; g.Bt = n;
+    g.a_rows = 3002;
     g.W = e->conv1_w_pad; g.N = d;
     g.epi.mode = EPI_CONV1; g.epi.bias = e->W(1); g.epi.out = e->conv1_out; g.epi.ldo = d;
     if (int rc = launch_gemm(g, s)) return rc;
@@ -507,13 +556,13 @@ static int encoder_forward(WhisperEngine* e, const int16_t* pcm, const int64_t* 
   // conv2 (stride 2), GELU, + sinusoid positions -> fp32 residual stream
   {
     GemmArgs g;
-    g.A = e->conv1_out; g.a_mode = A_CONV_S2; g.C = d; g.K = 3 * d; g.T = 1500; g.Bt = n;
+    g.A = e->conv1_out; g.a_mode = A_CONV_S2; g.C = d; g.K = 3 * d; g.T = rows; g.Bt = n;
     g.W = e->W(2); g.N = d;
     g.epi.mode = EPI_CONV2_POS; g.epi.bias = e->W(3); g.epi.out = e->resid; g.epi.ldo = d;
     g.epi.pos = e->W(4);
     if (int rc = launch_gemm(g, s)) return rc;
   }
-  const int M = n * 1500;
+  const int M = n * rows;
   auto flat = [&](const uint16_t* A, int K, const uint16_t* Wt, int N) {
     GemmArgs g;
     g.A = A; g.a_mode = A_FLAT; g.K = K; g.T = M; g.Bt = 1; g.lda = K; g.a_bstride = 0;
@@ -527,11 +576,13 @@ static int encoder_forward(WhisperEngine* e, const int16_t* pcm, const int64_t* 
     {
       GemmArgs g = flat(e->lnb, d, e->W(b0 + 2), 3 * d);
       g.epi.mode = EPI_QKV; g.epi.bias = e->W(b0 + 3);
-      g.epi.q = e->qb; g.epi.k = e->kb; g.epi.vt = e->vtb; g.epi.heads = H; g.epi.t_pad = 1536;
+      g.epi.q = e->qb; g.epi.k = e->kb; g.epi.vt = e->vtb; g.epi.heads = H; g.epi.t_pad = t_pad;
+      g.epi.seg_rows = rows;
       g.epi.q_scale = 0.125f;
       if (int rc = launch_gemm(g, s)) return rc;
     }
-    if (int rc = launch_attention(e->qb, e->kb, e->vtb, n, H, 1500, 1536, e->attn_out, d, s))
+    if (int rc = launch_attention(e->qb, e->kb, e->vtb, n, H, rows, t_pad, e->attn_out, d, s,
+                                  length_aware ? e->seg_len_dev : nullptr))
       return rc;
     {
       GemmArgs g = flat(e->attn_out, d, e->W(b0 + 4), d);
@@ -562,7 +613,7 @@ static int encoder_forward(WhisperEngine* e, const int16_t* pcm, const int64_t* 
     GemmArgs g = flat(e->enc_out, d, e->W(x), 2 * d * e->Ld);
     g.epi.mode = EPI_XKV; g.epi.bias = e->W(x + 1); g.epi.out = const_cast<uint16_t*>(e->st.xkv);
     g.epi.slot_ids = e->slot_dev; g.epi.n_slots = e->cfg.max_slots; g.epi.layers = e->Ld;
-    g.epi.heads = H;
+    g.epi.heads = H; g.epi.seg_rows = rows;
     if (int rc = launch_gemm(g, s)) return rc;
   }
   return 0;
@@ -775,21 +826,36 @@ int dm_whisper_destroy(void* handle) {
   return 0;
 }
 
-int dm_whisper_encode(void* handle, const int16_t* pcm, const int64_t* offsets,
-                      const int32_t* lengths, int n, const int32_t* slot_ids, void* stream) {
+int dm_whisper_encode_lengths(void* handle, const int16_t* pcm, const int64_t* offsets,
+                              const int32_t* lengths, const int32_t* host_lengths, int n,
+                              const int32_t* slot_ids, void* stream) {
   auto* e = static_cast<WhisperEngine*>(handle);
   DM_REQUIRE(e != nullptr, "null handle");
   DM_ON_DEVICE(e->device);
   DM_REQUIRE(n >= 1 && n <= e->E, "n must be in [1, max_encode_batch]");
   for (int i = 0; i < n; ++i)
     DM_REQUIRE(slot_ids[i] >= 0 && slot_ids[i] < e->cfg.max_slots, "slot id out of range");
+  int rows = 1500;
+  if (host_lengths) {            // length-aware: the longest window of the batch
+    rows = 1;
+    for (int i = 0; i < n; ++i) {
+      const int ns = std::min(std::max(host_lengths[i], 0), 480000);
+      rows = std::max(rows, std::min(1500, (ns + 319) / 320));
+    }
+  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (int rc = e->ring.upload(e->slot_dev, slot_ids, sizeof(int32_t) * n, s)) return rc;
   e->last_n = n;
+  e->last_rows = rows;
   e->encodes += 1;
   e->segments += n;
   e->launches += e->encode_kernels();
-  return encoder_forward(e, pcm, offsets, lengths, n, s);
+  return encoder_forward(e, pcm, offsets, lengths, n, s, rows, host_lengths != nullptr);
+}
+
+int dm_whisper_encode(void* handle, const int16_t* pcm, const int64_t* offsets,
+                      const int32_t* lengths, int n, const int32_t* slot_ids, void* stream) {
+  return dm_whisper_encode_lengths(handle, pcm, offsets, lengths, nullptr, n, slot_ids, stream);
 }
 
 __global__ void admit_kernel(DecodeState st, const int32_t* args, int n) {
@@ -1069,7 +1135,7 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
   const void* src = nullptr;
   size_t avail = 0;
   switch (which) {
-    case 0: src = e->enc_out; avail = size_t(e->last_n) * 1500 * e->d * 2; break;
+    case 0: src = e->enc_out; avail = size_t(e->last_n) * e->last_rows * e->d * 2; break;
     case 1:
       DM_REQUIRE(e->mel_tap, "log-mel tap not enabled (dm_whisper_debug 15 before the encode)");
       src = e->mel; avail = size_t(e->last_n) * e->nm * 3000 * 4;
@@ -1135,8 +1201,8 @@ int dm_whisper_debug(void* handle, int which, void* host_dst, size_t bytes, void
       if (cap > 0) out[0] = nbad;
       return 0;
     }
-    case 5: src = e->resid; avail = size_t(e->last_n) * 1500 * e->d * 4; break;
-    case 6: src = e->attn_out; avail = size_t(e->last_n) * 1500 * e->d * 2; break;
+    case 5: src = e->resid; avail = size_t(e->last_n) * e->last_rows * e->d * 4; break;
+    case 6: src = e->attn_out; avail = size_t(e->last_n) * e->last_rows * e->d * 2; break;
     default: DM_REQUIRE(false, "unknown debug tap");
   }
   DM_REQUIRE(bytes <= avail, "debug copy larger than the tapped buffer");

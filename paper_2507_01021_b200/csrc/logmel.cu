@@ -327,13 +327,13 @@ logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offse
 // 8 channels per thread, written back only where a value rose.
 __global__ void __launch_bounds__(256)
 logmel_clamp_kernel(uint16_t* __restrict__ mel_t, const uint32_t* __restrict__ segmax,
-                    int n_mels, int ldt) {
+                    int n_mels, int ldt, int frames) {
   const int b = blockIdx.y;
   const int vpr = n_mels / 8;                             // 16-byte vectors per frame row
   const float fl = ordered_to_float(segmax[b]) - 8.0f;
   const float floor_n = __uint_as_float(uint32_t(f32_to_bf16((fl + 4.0f) / 4.0f)) << 16);
   uint16_t* base = mel_t + (size_t(b) * (kFrames + 2) + 1) * ldt;
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < kFrames * vpr;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < frames * vpr;
        t += gridDim.x * blockDim.x) {
     uint4* pv = reinterpret_cast<uint4*>(base + size_t(t / vpr) * ldt) + (t % vpr);
     uint4 v = *pv;
@@ -371,7 +371,7 @@ size_t logmel_smem_bytes() { return sizeof(LogmelSmem); }
 
 int launch_logmel(const int16_t* pcm, const int64_t* offsets, const int32_t* lengths,
                  int n_segments, int n_mels, const LogmelTables* tables, float* out32,
-                 uint16_t* mel_t, uint32_t* segmax, cudaStream_t stream) {
+                 uint16_t* mel_t, uint32_t* segmax, cudaStream_t stream, int frames) {
   DM_REQUIRE(n_mels == 80 || n_mels == 128, "n_mels must be 80 or 128");
   DM_REQUIRE(n_segments >= 0, "n_segments < 0");
   DM_REQUIRE(out32 != nullptr || mel_t != nullptr, "no log-mel output");
@@ -381,12 +381,18 @@ int launch_logmel(const int16_t* pcm, const int64_t* offsets, const int32_t* len
   DM_CHECK_CUDA(cudaMemsetAsync(segmax, 0, sizeof(uint32_t) * n_segments, stream));
   // time-major operand rows are padded to 64 (n_mels <= 64) or 128 channels
   const int ldt = n_mels <= 64 ? 64 : 128;
-  dim3 grid(ceil_div(kFrames, kFPB), n_segments);
+  // frames < 3000: only the first `frames` (the length-aware encoder's
+  // window; the per-segment max is unchanged: every later frame of a shorter
+  // segment is zero padding)
+  DM_REQUIRE(frames >= 1 && frames <= kFrames && (out32 == nullptr || frames == kFrames),
+             "log-mel frames");
+  dim3 grid(ceil_div(frames, kFPB), n_segments);
   logmel_kernel<<<grid, kLogmelThreads, smem, stream>>>(pcm, offsets, lengths, tables, n_mels,
                                                          mel_t, ldt, out32, segmax);
   DM_CHECK_LAUNCH();
   if (mel_t) {
-    logmel_clamp_kernel<<<dim3(24, n_segments), 256, 0, stream>>>(mel_t, segmax, n_mels, ldt);
+    logmel_clamp_kernel<<<dim3(24, n_segments), 256, 0, stream>>>(mel_t, segmax, n_mels, ldt,
+                                                                  frames);
     DM_CHECK_LAUNCH();
   }
   if (out32) {

@@ -101,7 +101,8 @@ class WhisperGPU:
                  max_encode_batch: int = 32, num_pages: int | None = None,
                  eot: int | None = None, steps_per_poll: int = 8,
                  decode_groups: int | None = None, first_encode_batch: int = 8,
-                 overlap_encode: bool = True, decode_priority: int = -1):
+                 overlap_encode: bool = True, decode_priority: int = -1,
+                 length_aware: bool = False):
         if not torch.cuda.is_available():
             raise _native.DmError("no CUDA device: the B200 engine has no CPU fallback")
         self.dims = dims
@@ -112,6 +113,9 @@ class WhisperGPU:
         self.steps_per_poll = steps_per_poll
         self.first_encode_batch = first_encode_batch
         self.overlap_encode = overlap_encode
+        # opt-in: each segment encodes its own ceil(n / 320)
+        # positions instead of the 30 s window; results differ from pad_or_trim
+        self.length_aware = length_aware
         self.eot = dims.eot if eot is None else eot
         with torch.cuda.device(self.device):
             # run_jobs(overlap_encode) encodes on enc_stream so a new group's
@@ -261,8 +265,16 @@ class WhisperGPU:
         decode stream, so a following admit/step/debug is ordered after it)."""
         stream = self.stream if stream is None else stream
         pcm, offp, lenp = self.upload_segments(segs, stream)
-        _native.check(self.lib.dm_whisper_encode(self.handle, pcm, offp, lenp, len(segs),
-                                                 self._i32(slots), C.c_void_p(stream.cuda_stream)))
+        if self.length_aware:
+            host_lens = self._i32([min(s.length if isinstance(s, ResidentPCM) else len(s), N_SAMPLES)
+                                   for s in segs])
+            _native.check(self.lib.dm_whisper_encode_lengths(
+                self.handle, pcm, offp, lenp, host_lens, len(segs), self._i32(slots),
+                C.c_void_p(stream.cuda_stream)))
+        else:
+            _native.check(self.lib.dm_whisper_encode(self.handle, pcm, offp, lenp, len(segs),
+                                                     self._i32(slots),
+                                                     C.c_void_p(stream.cuda_stream)))
         b = self._last_buf
         self._enc_done[b].record(stream)          # buffer b free for the upload after next
         self._enc_used[b] = True
@@ -332,8 +344,10 @@ class WhisperGPU:
                                                       C.byref(ms), self._s))
         return ms.value
 
-    def encoder_output(self, n: int) -> np.ndarray:
-        bits = np.empty((n, 1500, self.dims.d_model), np.uint16)
+    def encoder_output(self, n: int, rows: int = 1500) -> np.ndarray:
+        """bf16 encoder output of the last encode, [n, rows, d] (rows: the
+        batch's window after a length-aware encode)."""
+        bits = np.empty((n, rows, self.dims.d_model), np.uint16)
         self.debug(0, bits)
         return (bits.astype(np.uint32) << 16).view(np.float32)
 

@@ -69,7 +69,8 @@ def audit(orc, enc, got, want, eot, tol, label, prompt=None):
             same += 1
             continue
         fed = torch.tensor([prompt + list(g[:k])])
-        logits = orc.decoder_logits(fed, enc[b:b + 1])[0, -1]
+        eb = enc[b]                                # [T, d] (a batch row or a list item)
+        logits = orc.decoder_logits(fed, eb.reshape(1, -1, eb.shape[-1]))[0, -1]
         tok = g[k] if k < len(g) else eot
         gap = float(logits.max() - logits[tok])
         top2 = torch.topk(logits, 2).values
