@@ -985,11 +985,11 @@ constexpr int kXpStride = 68;                 // floats per split result: o[64],
 // After a split's (o, max, sum) is in `xpart`: count it; the last of the 8
 // splits of (row, head) merges them in split order into the cross-o operand.
 __device__ __forceinline__ void xattn_finish(const DecodeState& st, const float* xpart, int* xcnt,
-                                             int r, int h, int tid, int* is_last) {
+                                             int r, int h, int nsplit, int tid, int* is_last) {
   const int H = st.heads;
   __threadfence();
   __syncthreads();
-  if (tid == 0) *is_last = atomicAdd(&xcnt[r * H + h], 1) == kXSplits - 1;
+  if (tid == 0) *is_last = atomicAdd(&xcnt[r * H + h], 1) == nsplit - 1;
   __syncthreads();
   if (!*is_last) return;
   __threadfence();
@@ -997,10 +997,10 @@ __device__ __forceinline__ void xattn_finish(const DecodeState& st, const float*
     const float* base = xpart + (size_t(r) * H + h) * kXSplits * kXpStride;
     float mv[kXSplits], lv[kXSplits], ov[kXSplits];
 #pragma unroll
-    for (int s = 0; s < kXSplits; ++s) {
-      mv[s] = __ldcg(base + s * kXpStride + 64);
-      lv[s] = __ldcg(base + s * kXpStride + 65);
-      ov[s] = __ldcg(base + s * kXpStride + tid);
+    for (int s = 0; s < kXSplits; ++s) {      // splits past the window: empty
+      mv[s] = s < nsplit ? __ldcg(base + s * kXpStride + 64) : -INFINITY;
+      lv[s] = s < nsplit ? __ldcg(base + s * kXpStride + 65) : 0.f;
+      ov[s] = s < nsplit ? __ldcg(base + s * kXpStride + tid) : 0.f;
     }
     float M = -INFINITY;
 #pragma unroll
@@ -1033,22 +1033,20 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
   __shared__ float redm[4], reds[4];
   __shared__ uint32_t tmem_slot;
   __shared__ int is_last;
-  const int r = blockIdx.x, h = blockIdx.y, sp = blockIdx.z, tid = threadIdx.x;
+  // grid (split, head, row): a row's splits are adjacent in launch order, so the
+  // splits past a short window (which leave at once) interleave with real ones
+  const int sp = blockIdx.x, h = blockIdx.y, r = blockIdx.z, tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
   if (tid == 0) trace_mark(st, 0);
   if (r >= *st.n_active) return;
   const int slot = st.active[r];
   const int H = st.heads;
-  const int k0 = sp * kXaKeys, nk = min(st.enc_len[slot], k0 + kXaKeys) - k0;
+  // splits past a (length-aware) segment's window do not exist for it: the
+  // CTA leaves at once and the merge counts only the slot's own splits
+  const int len = st.enc_len[slot], nsplit = ceil_div(len, kXaKeys);
+  if (sp >= nsplit) return;
+  const int k0 = sp * kXaKeys, nk = min(len, k0 + kXaKeys) - k0;
   float* res = xpart + ((size_t(r) * H + h) * kXSplits + sp) * kXpStride;
-  if (nk <= 0) {
-    // a split past a length-aware segment's window: no stream, an empty result
-    pdl_wait();
-    if (tid < 64) res[tid] = 0.f;
-    if (tid == 64) { res[64] = -INFINITY; res[65] = 0.f; }
-    xattn_finish(st, xpart, xcnt, r, h, tid, &is_last);
-    return;
-  }
   uint8_t* Ks = xa_smem;
   uint8_t* Vs = xa_smem + kXaKeys * 128;
   uint8_t* Qs = xa_smem + kXaQOff;
@@ -1191,7 +1189,7 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, kXaTmemCols);
-  xattn_finish(st, xpart, xcnt, r, h, tid, &is_last);
+  xattn_finish(st, xpart, xcnt, r, h, nsplit, tid, &is_last);
 }
 
 int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
@@ -1201,7 +1199,7 @@ int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int lay
                  xq.splits <= kMaxSplits, "cross-attn: q partials");
   DM_REQUIRE(xpart != nullptr && xcnt != nullptr && st.heads <= kMaxHeads, "cross-attn: scratch");
   DM_SMEM_ATTR(cross_attn_kernel, kXaSmem);
-  DM_CHECK_CUDA(launch_pdl(cross_attn_kernel, dim3(st.grid_rows, st.heads, kXSplits),
+  DM_CHECK_CUDA(launch_pdl(cross_attn_kernel, dim3(kXSplits, st.heads, st.grid_rows),
                            dim3(kXaThreads), kXaSmem, stream, xkv_map, st, layer, xq, q_scale,
                            xpart, xcnt, probe));
   return 0;

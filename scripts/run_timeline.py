@@ -13,7 +13,9 @@ fe = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 eb = int(sys.argv[2]) if len(sys.argv) > 2 else 64
 dims = get_model(bench.MODEL)
 segs = bench.make_workload(64, 0)
-eng = WhisperGPU(dims, max_slots=64, max_encode_batch=eb, first_encode_batch=fe)
+import os
+eng = WhisperGPU(dims, max_slots=64, max_encode_batch=eb, first_encode_batch=fe,
+                 length_aware=bool(int(os.environ.get("LA", "0"))))
 flat = np.concatenate([x for _, x in segs])
 pcm = torch.from_numpy(flat).cuda()
 eng.set_resident(pcm)

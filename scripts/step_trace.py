@@ -12,7 +12,9 @@ name = sys.argv[1] if len(sys.argv) > 1 else "whisper-base"
 rows_list = [int(x) for x in sys.argv[2:]] or [64, 32, 8, 1]
 dims = get_model(name)
 S = 64
-eng = WhisperGPU(dims, max_slots=S, max_encode_batch=32)
+import os
+eng = WhisperGPU(dims, max_slots=S, max_encode_batch=32,
+                 length_aware=bool(int(os.environ.get("LA", "0"))))
 
 rng = np.random.default_rng(0)
 seg = rng.integers(-8000, 8000, size=160000, dtype=np.int16)

@@ -11,7 +11,9 @@ from paper_2507_01021_b200.models import get_model
 name = sys.argv[1] if len(sys.argv) > 1 else "whisper-large-v3"
 rows_list = [int(x) for x in sys.argv[2:]] or [64, 48, 32, 24, 16, 8, 4, 1]
 dims = get_model(name)
-eng = WhisperGPU(dims, max_slots=64, max_encode_batch=32)   # DM_XA_LEAN / DM_XA_CLUSTER pick the kernel
+import os
+eng = WhisperGPU(dims, max_slots=64, max_encode_batch=32,
+                 length_aware=bool(int(os.environ.get("LA", "0"))))
 seg = np.random.default_rng(0).integers(-8000, 8000, size=160000, dtype=np.int16)
 slots = list(range(64))
 for i in range(0, 64, 32):
