@@ -382,17 +382,17 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
 #pragma unroll
           for (int i = 0; i < 32; ++i) part[base + size_t(32 + i) * 128 + f] = v1[i];
         }
-        __threadfence();
         named_bar_sync(1, 128);
-        if (et == 0) {
+        if (et == 0) {                 // one release (cumulative over the barrier)
+          __threadfence();
           const int prev = atomicAdd(&st.counters[a.counter_base + tile], 1);
           *is_last = (prev == a.splits - 1);
+          if (*is_last) __threadfence();
         }
         named_bar_sync(1, 128);
         const int last = *is_last;
         named_bar_sync(1, 128);
         if (!last) continue;
-        __threadfence();
 #pragma unroll
         for (int i = 0; i < 32; ++i) { v0[i] = 0.f; v1[i] = 0.f; }
         for (int s = 0; s < a.splits; ++s) {
@@ -987,12 +987,16 @@ constexpr int kXpStride = 68;                 // floats per split result: o[64],
 __device__ __forceinline__ void xattn_finish(const DecodeState& st, const float* xpart, int* xcnt,
                                              int r, int h, int nsplit, int tid, int* is_last) {
   const int H = st.heads;
-  __threadfence();
+  // the CTA's result stores, then one release by thread 0 (cumulative over
+  // the barrier), and the last arriver's acquire before it reads the others
   __syncthreads();
-  if (tid == 0) *is_last = atomicAdd(&xcnt[r * H + h], 1) == nsplit - 1;
+  if (tid == 0) {
+    __threadfence();
+    *is_last = atomicAdd(&xcnt[r * H + h], 1) == nsplit - 1;
+    if (*is_last) __threadfence();
+  }
   __syncthreads();
   if (!*is_last) return;
-  __threadfence();
   if (tid < 64) {
     const float* base = xpart + (size_t(r) * H + h) * kXSplits * kXpStride;
     float mv[kXSplits], lv[kXSplits], ov[kXSplits];
@@ -1184,7 +1188,6 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
     tmem_ld2(tmem + lane_base + kXaBoxes * 8, oa, ob);
     tmem_wait_ld();
     if (own) res[16 * warp + lane] = __uint_as_float(oa) + __uint_as_float(ob);
-    __threadfence();
   }
   tc_fence_before();
   __syncthreads();
