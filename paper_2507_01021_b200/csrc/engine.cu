@@ -233,6 +233,9 @@ struct WhisperEngine {
   int enc_stop = 1 << 30;        // debug: run only the first enc_stop layers
   bool enc_tap = false;          // debug: keep the fp32 encoder output (in resid)
   bool mel_tap = false;          // debug: also write the fp32 [n, n_mels, 3000] features
+  // encoder GEMM grid cap (experiment knob, DM_ENC_MAX_CTAS): SMs left free
+  // for the decode stream while a group encodes beside it
+  int enc_max_ctas = std::getenv("DM_ENC_MAX_CTAS") ? std::atoi(std::getenv("DM_ENC_MAX_CTAS")) : 0;
   // decode
   DecodeState st{};
   int32_t* prompt_dev = nullptr;
@@ -547,6 +550,7 @@ static int encoder_forward(WhisperEngine* e, const int16_t* pcm, const int64_t* 
   // conv1 (implicit GEMM over the padded time-major mel), GELU
   {
     GemmArgs g;
+    g.max_ctas = e->enc_max_ctas;
     g.A = e->mel_t; g.a_mode = A_CONV_S1; g.C = e->Cp; g.K = 3 * e->Cp; g.T = frames; g.Bt = n;
     g.a_rows = 3002;
     g.W = e->conv1_w_pad; g.N = d;
@@ -556,6 +560,7 @@ static int encoder_forward(WhisperEngine* e, const int16_t* pcm, const int64_t* 
   // conv2 (stride 2), GELU, + sinusoid positions -> fp32 residual stream
   {
     GemmArgs g;
+    g.max_ctas = e->enc_max_ctas;
     g.A = e->conv1_out; g.a_mode = A_CONV_S2; g.C = d; g.K = 3 * d; g.T = rows; g.Bt = n;
     g.W = e->W(2); g.N = d;
     g.epi.mode = EPI_CONV2_POS; g.epi.bias = e->W(3); g.epi.out = e->resid; g.epi.ldo = d;
@@ -565,6 +570,7 @@ static int encoder_forward(WhisperEngine* e, const int16_t* pcm, const int64_t* 
   const int M = n * rows;
   auto flat = [&](const uint16_t* A, int K, const uint16_t* Wt, int N) {
     GemmArgs g;
+    g.max_ctas = e->enc_max_ctas;
     g.A = A; g.a_mode = A_FLAT; g.K = K; g.T = M; g.Bt = 1; g.lda = K; g.a_bstride = 0;
     g.W = Wt; g.N = N;
     return g;

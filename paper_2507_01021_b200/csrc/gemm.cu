@@ -767,7 +767,8 @@ static int launch_bn_mode(const GemmArgs& g, cudaStream_t stream) {
   geo.cpb = g.grouped ? 1 : (g.C > 0 ? g.C / kBK : 1);
   const int smem = GemmSmem<BN, STAGES, MODE>::kBytes;
   DM_SMEM_ATTR((gemm_tcgen05_kernel<BN, STAGES, MODE>), smem);
-  int grid = geo.tiles < kNumSMs ? geo.tiles : kNumSMs;
+  const int sms = g.max_ctas > 0 ? std::min(g.max_ctas, kNumSMs) : kNumSMs;
+  int grid = geo.tiles < sms ? geo.tiles : sms;
   gemm_tcgen05_kernel<BN, STAGES, MODE><<<grid, kGemmThreads, smem, stream>>>(ma, mb, mr, g, geo);
   DM_CHECK_LAUNCH();
   return 0;
@@ -809,7 +810,7 @@ static int launch_pair_mode(const GemmArgs& g, cudaStream_t stream) {
   geo.cpb = g.C > 0 ? g.C / kBK : 1;
   const int smem = PairSmem<STAGES>::kBytes;
   DM_SMEM_ATTR((gemm_pair_kernel<STAGES, MODE>), smem);
-  const int pairs = std::min(geo.tiles, kNumSMs / 2);
+  const int pairs = std::min(geo.tiles, (g.max_ctas > 0 ? std::min(g.max_ctas, kNumSMs) : kNumSMs) / 2);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(kGemmThreads);

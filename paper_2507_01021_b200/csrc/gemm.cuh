@@ -70,6 +70,7 @@ struct GemmArgs {
   int grouped = 0;        // conv modes: grouped conv, one 64-channel group per N tile
   const uint16_t* W = nullptr;   // [N, K] bf16 (K contiguous)
   int N = 0;
+  int max_ctas = 0;       // persistent grid size cap (0: one CTA per SM); SMs left to other streams
   Epilogue epi;
 };
 
