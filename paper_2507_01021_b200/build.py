@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import hashlib
 import os
+import shlex
 import subprocess
 import sys
 from pathlib import Path
@@ -22,6 +23,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC,-fvisibility=hidden",
          "-Xptxas", "-v"]
+# experiment builds only (e.g. -DDM_ATTN_TRACE, -DDM_XA_KEYS=128): scripts/build_variant.sh
+FLAGS += shlex.split(os.environ.get("DM_NVCC_EXTRA", ""))
 
 
 def _fingerprint() -> str:

@@ -6,9 +6,10 @@
 //   w2..9: softmax, two warpgroups (one per query tile), one query row per
 //       thread (TMEM lane = row): row max (3-input FMNMX) /
 //       exp2 / row sum entirely in registers (no shuffles), P_j written as
-//       bf16 straight into the 128B-swizzled K-major smem layout the next MMA
-//       reads, PV_j folded into a register accumulator with the online-softmax
-//       rescale.
+//       packed bf16 into TMEM, where the P.V MMA reads it as its A operand
+//       (shared memory then only carries Q, K and V: a P round trip through
+//       smem cost 128 KB of smem bandwidth per key block pair, the kernel's
+//       bound), O accumulated in TMEM with a lazy rescale.
 // Q arrives pre-scaled by head_dim^-0.5 (modeling_whisper.py:310) from the
 // QKV GEMM epilogue; V arrives transposed ([dims, positions]) so both MMAs
 // are K-major. Keys >= 1500 (the 1536-padded tail) are masked to -inf.
@@ -17,19 +18,28 @@
 
 namespace dm {
 
+#ifdef DM_ATTN_TRACE
+// phase timeline of one CTA (clock64): [tile][j][sfull, ld, off, emit] and
+// MMA warp [tile][j][S issue, PV issue]
+__device__ unsigned long long g_attn_trace[2 * 16 * 4 + 2 * 16 * 2 + 1];
+#define ATRACE(idx) do { if (traced && lane == 0) g_attn_trace[idx] = clock64(); } while (0)
+#define ATRACE_E(idx) do { if (traced) g_attn_trace[idx] = clock64(); } while (0)
+#else
+#define ATRACE(idx) do {} while (0)
+#define ATRACE_E(idx) do {} while (0)
+#endif
+
 constexpr int kAttnThreads = 320;    // w0 TMA, w1 MMA, w2..5 softmax tile A, w6..9 tile B
 constexpr int kAttnKS = 4;           // K/V ring depth (TMA lookahead of 3 key blocks)
 constexpr int kQBytes = 128 * 128;   // 128 rows x 64 bf16
 constexpr int kKBytes = 128 * 128;
 constexpr int kVBytes = 2 * 64 * 128;  // two 64-key boxes of [64 dims x 64 keys]
-constexpr int kPBytes = 2 * 128 * 128; // two 64-key column blocks of [128 rows x 64 keys]
 
 struct AttnSmemLayout {
   static constexpr int q = 0;                          // [2 tiles]
   static constexpr int k = q + 2 * kQBytes;
   static constexpr int v = k + kAttnKS * kKBytes;
-  static constexpr int p = v + kAttnKS * kVBytes;      // [2 tiles]
-  static constexpr int bars = p + 2 * kPBytes;
+  static constexpr int bars = v + kAttnKS * kVBytes;
   static constexpr int total = bars + 256 + 1024;
 };
 
@@ -45,7 +55,7 @@ __device__ __forceinline__ float ex2(float x) {
 }
 
 // One CTA per (pair of 128-query tiles, segment*head). The two tiles share
-// every K/V tile; each has its own S (128 TMEM cols), O (64 cols) and P (smem)
+// every K/V tile; each has its own S (128 TMEM cols), O (64 cols), P (64 cols)
 // and its own softmax warpgroup, so the tensor core works on one tile while
 // the other tile's softmax runs.
 __global__ void __launch_bounds__(kAttnThreads, 1)
@@ -74,6 +84,10 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
   const int T = seg_len ? seg_len[bh / heads] : T_rows;
   if (qp * 256 >= T) return;
   const int nb = ceil_div(T, 128);
+#ifdef DM_ATTN_TRACE
+  const bool traced = qp == 2 && bh == 5 && nb <= 16;
+  if (traced && threadIdx.x == 0) g_attn_trace[192] = clock64();
+#endif
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_q);
@@ -95,7 +109,7 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM columns: S tile t at 128 t, O tile t at 256 + 64 t
+  // TMEM columns: S tile t at 128 t, O tile t at 256 + 64 t, P tile t at 384 + 64 t
 
   if (warp == 0) {
     if (elect_one()) {
@@ -134,7 +148,9 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
       __syncwarp();
     };
     mbar_wait(&kv_full[0], 0);
+    if (lane == 0) ATRACE_E(128 + 0);
     issue_s(0, 0);
+    if (lane == 0) ATRACE_E(128 + 32);
     issue_s(1, 0);
     for (int j = 0; j < nb; ++j) {
       const int st = j % kAttnKS;
@@ -147,19 +163,19 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
         if (j + 1 < nb) {
           if (t == 0) mbar_wait(&kv_full[(j + 1) % kAttnKS], ((j + 1) / kAttnKS) & 1);
           mbar_wait(&s_empty[t], ph);
+          if (lane == 0) ATRACE_E(128 + (t * 16 + j + 1) * 2);
           issue_s(t, j + 1);
         }
         // softmax_t(j) done: P_t(j) written and O_t rescaled if its max moved
         mbar_wait(&p_full[t], ph);
+        if (lane == 0) ATRACE_E(128 + (t * 16 + j) * 2 + 1);
         tc_fence_after();
-        if (elect_one()) {                   // O_t += P_t V_j (accumulated in TMEM)
-          const uint32_t sp = smem_u32(smem + AttnSmemLayout::p + t * kPBytes);
+        if (elect_one()) {                   // O_t += P_t V_j (P from TMEM, O in TMEM)
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t a = sp + (kk >> 2) * (128 * 128) + (kk & 3) * 32;
             const uint32_t bb = sv + (kk >> 2) * (64 * 128) + (kk & 3) * 32;
-            umma_bf16_ss(tmem + 256 + t * 64, umma_desc_sw128(a), umma_desc_sw128(bb), idesc_o,
-                         (j | kk) != 0);
+            umma_bf16_ts(tmem + 256 + t * 64, tmem + 384 + t * 64 + kk * 8, umma_desc_sw128(bb),
+                         idesc_o, (j | kk) != 0);
           }
           umma_commit(&o_full[t]);
           if (t == 1) umma_commit(&kv_empty[st]);
@@ -172,16 +188,16 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
     const int quad = warp & 3;
     const int r = quad * 32 + lane;                       // query row in tile
     const uint32_t lane_off = uint32_t(quad * 32) << 16;
-    const uint32_t s_col = t * 128, o_col = 256 + t * 64;
+    const uint32_t s_col = t * 128, o_col = 256 + t * 64, p_col = 384 + t * 64;
     constexpr float kLog2e = 1.4426950408889634f;
     // O_t accumulates in TMEM across key blocks. The exponent offset m_run
     // only moves when the block max exceeds it by more than 2^8 (then O_t's
     // row is rescaled in TMEM before the next P.V accumulates): P <= 256 fits
     // bf16, and numerator and row sum share the same offset.
     float m_run = -INFINITY, l_run = 0.f;
-    uint8_t* prow = smem + AttnSmemLayout::p + t * kPBytes + r * 128;
     for (int j = 0; j < nb; ++j) {
       mbar_wait(&s_full[t], j & 1);
+      if (quad == 0) ATRACE((t * 16 + j) * 4 + 0);
       tc_fence_after();
       const int kvalid = T - j * 128;                     // < 128 only on the tail block
       float alpha = 1.f, m_use = m_run, mscaled = 0.f;
@@ -214,7 +230,7 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
           }
         }
       };
-      // p = exp2(s log2e - m log2e), row sum, bf16 P into swizzled smem
+      // p = exp2(s log2e - m log2e), row sum, bf16 P into TMEM
       float rs0 = 0.f, rs1 = 0.f, rs2 = 0.f, rs3 = 0.f;
       auto emit = [&](int c, const uint32_t (&v)[32], bool full) {
         uint32_t pk[16];
@@ -232,14 +248,7 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
           if (i & 1) { rs2 += p0; rs3 += p1; } else { rs0 += p0; rs1 += p1; }
           pk[i] = pack_bf16x2(p0, p1);
         }
-        // 32 keys = 4 chunks of 16 B; block = c / 2, chunk-in-row = (c % 2) * 4 + u
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int chunk = (c & 1) * 4 + u;
-          uint4* dst = reinterpret_cast<uint4*>(prow + (c >> 1) * (128 * 128) +
-                                                ((chunk ^ (r & 7)) << 4));
-          *dst = make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
-        }
+        tmem_st16(tmem + lane_off + p_col + c * 16, pk);   // keys 32c..32c+31
       };
       auto release_s = [&]() {                   // the MMA warp may issue S_t(j + 1)
         tc_fence_before();
@@ -255,6 +264,7 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
         tmem_ld32(tmem + lane_off + s_col + 96, s3);
         tmem_wait_ld();
         release_s();
+        if (quad == 0) ATRACE((t * 16 + j) * 4 + 1);
         float m0 = m_run, m1 = m_run, m2 = m_run, m3 = m_run;
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
@@ -264,6 +274,7 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
           m3 = fmax3(m3, __uint_as_float(s3[i]), __uint_as_float(s3[i + 1]));
         }
         offset(fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)));
+        if (quad == 0) ATRACE((t * 16 + j) * 4 + 2);
         emit(0, s0, true);
         emit(1, s1, true);
         emit(2, s2, true);
@@ -289,8 +300,9 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
         }
       }
       const float rs = (rs0 + rs1) + (rs2 + rs3);
-      tc_fence_before();                      // (orders an O_t rescale before the next P.V)
-      fence_proxy_async_smem();
+      if (quad == 0) ATRACE((t * 16 + j) * 4 + 3);
+      tmem_wait_st();
+      tc_fence_before();                      // P_t (and an O_t rescale) before the next P.V
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
       l_run = l_run * alpha + rs;
@@ -412,5 +424,11 @@ int launch_attention(const uint16_t* q, const uint16_t* k, const uint16_t* vt, i
   DM_CHECK_LAUNCH();
   return 0;
 }
+
+#ifdef DM_ATTN_TRACE
+extern "C" __attribute__((visibility("default"))) int dm_attn_trace_read(unsigned long long* host) {
+  return (int)cudaMemcpyFromSymbol(host, g_attn_trace, sizeof(g_attn_trace));
+}
+#endif
 
 }  // namespace dm

@@ -110,3 +110,43 @@ def test_reference_dispatch_loop_drives_b200backend_gpu(dmx, native_lib):
                      formed_at=0.0, total_audio_s=s.duration_s)
     assert backend.transcribe_batch(batch)[0].text == by[s.segment_id]
     backend.close()
+
+
+@pytest.mark.gpu
+def test_failure_mid_run_then_next_batch_served_gpu(dmx, native_lib):
+    """A failure after admission (slots hold self-KV pages, encodes may still
+    be in flight) must not wedge the real engine: transcribe_batch resets it
+    and re-raises (the reference loop turns that into error rows,
+    scheduler.py:258-275), and the next batch is served with the same text a
+    fresh run gives."""
+    from paper_2507_01021_b200.backend import B200Backend, B200BackendConfig
+    rb, rs, rv = dmx
+    rng = np.random.default_rng(5)
+    segs = [ref_segment(rv, f"f{i}", rng.integers(-3000, 3000, size=16000 * (2 + i), dtype=np.int16))
+            for i in range(6)]
+
+    def batch(ss, name):
+        return rs.Batch(batch_id=name, entries=[rs.QueueEntry(segment=s, enqueue_time=0.0) for s in ss],
+                        formed_at=0.0, total_audio_s=sum(s.duration_s for s in ss))
+    cfg = B200BackendConfig(model="whisper-tiny", cap_tokens=8, max_slots=4, max_encode_batch=2,
+                            init_std=0.05)
+    backend = B200Backend(cfg)
+    eng = backend.engine
+    real_step, calls = eng.step, []
+
+    def failing_step(n):
+        calls.append(n)
+        if len(calls) == 2:
+            raise RuntimeError("injected failure")
+        return real_step(n)
+    eng.step = failing_step
+    with pytest.raises(RuntimeError, match="injected"):
+        backend.transcribe_batch(batch(segs, "doomed"))
+    eng.step = real_step
+    got = [r.text for r in backend.transcribe_batch(batch(segs[:5], "after"))]
+    assert all(got)
+    fresh = B200Backend(cfg)
+    want = [r.text for r in fresh.transcribe_batch(batch(segs[:5], "fresh"))]
+    assert got == want
+    fresh.close()
+    backend.close()
