@@ -581,15 +581,17 @@ def measure_roofline(eng, dims) -> dict:
     bytes_per_launch = S * 2 * 1500 * dims.d_model * 2
     achieved = bytes_per_launch / (ms / 1000.0) / 1e9
     traffic = None
-    tf = ROOT / "profiles" / "r02_xattn_traffic_large_v3.json"
+    tf = ROOT / "profiles" / "r02_xattn_traffic_large_v3_v11.json"
     if tf.exists():     # dram read+write of one ncu --set full capture, scaled to rows
         t = json.loads(tf.read_text())
         traffic = (t["dram_bytes_read"] + t["dram_bytes_write"]) * S / t["rows"]
-    return {"kernel": "cross_attn_kernel (decode K6)", "bound": "hbm",
+    return {"kernel": "cross_attn_kernel + xattn_merge_kernel (decode K6 cross-attention)",
+            "bound": "hbm",
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic,
             "traffic_unit": f"bytes per launch (ncu dram__bytes_read+write, {tf.name})",
-            "timing": f"CUDA events on the engine stream around a graph of {2 * L} launches, "
+            "timing": f"CUDA events on the engine stream around a graph of {2 * L} launches "
+                      f"(each the cross-attention + its split-merge kernel, as in the step), "
                       f"launch i = decoder layer i % {L}, 64 active rows (median of 5)",
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)" if peaks else "fallback",
             "bytes_per_launch": bytes_per_launch, "avg_launch_ms": ms,

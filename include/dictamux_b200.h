@@ -182,10 +182,12 @@ DM_API int dm_ctc_debug(void* handle, int which, void* host_dst, size_t bytes, v
 DM_API int dm_whisper_stats(void* handle, int64_t* out, int n);
 /* Time one decode kernel over the current active slots with CUDA events on
  * `stream` (a probe: it may overwrite row-space activations): which =
- * 0 cross-attention(layer), 1 self-attention(layer), 2 LM head, 3 decoder LN
+ * 0 cross-attention(layer) (+ its split-merge kernel above kXaTailMergeRows
+ * rows, as in the step), 1 self-attention(layer), 2 LM head, 3 decoder LN
  * (+ residual partials), 4 cross-q projection, 5 fc2 projection,
  * 6 empty PDL kernel (launch floor), 7 fc1 projection (+GELU), 8 qkv projection,
- * 9 the cross-attention's K/V stream alone (roofline probe), 10 cross-o projection.
+ * 9 the cross-attention's K/V stream alone (roofline probe), 10 cross-o projection,
+ * 11 the cross-attention without its split merge (timing probe).
  * avg_ms = mean over iters back-to-back launches. layer < 0: launch i runs
  * decoder layer i % dec_layers (each launch streams a different layer's
  * cross-KV / weights, as inside a decode step). */

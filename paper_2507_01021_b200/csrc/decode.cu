@@ -982,8 +982,42 @@ __device__ __forceinline__ int sw128_off(int n, int k) {
 
 constexpr int kXpStride = 68;                 // floats per split result: o[64], max, sum, pad
 
+// Merge of the (o, max, sum) results of a (row, head)'s splits, in split
+// order, into the cross-o operand; thread `c` < 64 does head dimension c. The
+// same arithmetic in the last-arriver tail and in xattn_merge_kernel, so both
+// paths give the same bits.
+__device__ __forceinline__ void xattn_merge_head(const DecodeState& st, const float* xpart, int r,
+                                                 int h, int nsplit, int c) {
+  const float* base = xpart + (size_t(r) * st.heads + h) * kXSplits * kXpStride;
+  float mv[kXSplits], lv[kXSplits], ov[kXSplits];
+#pragma unroll
+  for (int s = 0; s < kXSplits; ++s) {        // splits past the window: empty
+    mv[s] = s < nsplit ? __ldcg(base + s * kXpStride + 64) : -INFINITY;
+    lv[s] = s < nsplit ? __ldcg(base + s * kXpStride + 65) : 0.f;
+    ov[s] = s < nsplit ? __ldcg(base + s * kXpStride + c) : 0.f;
+  }
+  float M = -INFINITY;
+#pragma unroll
+  for (int s = 0; s < kXSplits; ++s) M = fmaxf(M, mv[s]);
+  float Ls = 0.f, O = 0.f;
+#pragma unroll
+  for (int s = 0; s < kXSplits; ++s) {
+    const float f = exp2f((mv[s] - M) * kLog2e);
+    Ls += lv[s] * f;
+    O += ov[s] * f;
+  }
+  uint16_t hi, lo;
+  split_hilo(O / Ls, hi, lo);
+  const size_t idx = size_t(r) * st.d + h * 64 + c;
+  st.ah[idx] = hi;
+  st.al[idx] = lo;
+}
+
 // After a split's (o, max, sum) is in `xpart`: count it; the last of the 8
 // splits of (row, head) merges them in split order into the cross-o operand.
+// (Few-row steps only: the release fence and the counter round trip keep every
+// CTA -- and its 52 KB of K/V staging -- alive ~2 us longer, 29 of 101 us per
+// layer at 64 rows; many-row steps merge in xattn_merge_kernel instead.)
 __device__ __forceinline__ void xattn_finish(const DecodeState& st, const float* xpart, int* xcnt,
                                              int r, int h, int nsplit, int tid, int* is_last) {
   const int H = st.heads;
@@ -997,41 +1031,40 @@ __device__ __forceinline__ void xattn_finish(const DecodeState& st, const float*
   }
   __syncthreads();
   if (!*is_last) return;
-  if (tid < 64) {
-    const float* base = xpart + (size_t(r) * H + h) * kXSplits * kXpStride;
-    float mv[kXSplits], lv[kXSplits], ov[kXSplits];
-#pragma unroll
-    for (int s = 0; s < kXSplits; ++s) {      // splits past the window: empty
-      mv[s] = s < nsplit ? __ldcg(base + s * kXpStride + 64) : -INFINITY;
-      lv[s] = s < nsplit ? __ldcg(base + s * kXpStride + 65) : 0.f;
-      ov[s] = s < nsplit ? __ldcg(base + s * kXpStride + tid) : 0.f;
-    }
-    float M = -INFINITY;
-#pragma unroll
-    for (int s = 0; s < kXSplits; ++s) M = fmaxf(M, mv[s]);
-    float Ls = 0.f, O = 0.f;
-#pragma unroll
-    for (int s = 0; s < kXSplits; ++s) {
-      const float f = exp2f((mv[s] - M) * kLog2e);
-      Ls += lv[s] * f;
-      O += ov[s] * f;
-    }
-    uint16_t hi, lo;
-    split_hilo(O / Ls, hi, lo);
-    const size_t idx = size_t(r) * st.d + h * 64 + tid;
-    st.ah[idx] = hi;
-    st.al[idx] = lo;
-  }
+  if (tid < 64) xattn_merge_head(st, xpart, r, h, nsplit, tid);
   if (tid == 0) {
     xcnt[r * H + h] = 0;                         // ready for the next launch of any layer
     trace_mark(st, 3);
   }
 }
 
+// The split merge as its own kernel (steps with more than kXaTailMergeRows
+// rows): one thread per (row, head, dimension); the cross-attention CTAs
+// store their split results and leave.
+__global__ void __launch_bounds__(256)
+xattn_merge_kernel(const DecodeState st, const float* __restrict__ xpart) {
+  if (threadIdx.x == 0) trace_mark(st, 0);
+  pdl_trigger();
+  const int r = blockIdx.y, h = blockIdx.x * 4 + threadIdx.x / 64;
+  pdl_wait();
+  if (threadIdx.x == 0) trace_mark(st, 1);
+  if (r >= *st.n_active || h >= st.heads) return;
+  const int nsplit = ceil_div(st.enc_len[st.active[r]], kXaKeys);
+  xattn_merge_head(st, xpart, r, h, nsplit, threadIdx.x % 64);
+  if (threadIdx.x == 0) trace_mark(st, 3);
+}
+
+int launch_xattn_merge(const DecodeState& st, const float* xpart, cudaStream_t stream) {
+  DM_REQUIRE(xpart != nullptr && st.heads <= kMaxHeads, "cross-attn merge: scratch");
+  DM_CHECK_CUDA(launch_pdl(xattn_merge_kernel, dim3(ceil_div(st.heads, 4), st.grid_rows),
+                           dim3(256), 0, stream, st, xpart));
+  return 0;
+}
+
 __global__ void __launch_bounds__(kXaThreads, kXaCtasPerSm)
 cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, int layer,
                        const Partials xq, float q_scale, float* __restrict__ xpart,
-                       int* __restrict__ xcnt, int probe) {
+                       int* __restrict__ xcnt, int probe, int tail_merge) {
   extern __shared__ uint8_t xa_raw[];
   uint8_t* xa_smem = xa_raw + ((1024 - (smem_u32(xa_raw) & 1023)) & 1023);
   __shared__ float redm[4], reds[4];
@@ -1192,19 +1225,20 @@ cross_attn_kernel(const __grid_constant__ CUtensorMap tm, const DecodeState st, 
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tmem, kXaTmemCols);
+  if (!tail_merge) return;                       // xattn_merge_kernel follows
   xattn_finish(st, xpart, xcnt, r, h, nsplit, tid, &is_last);
 }
 
 int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
                            const Partials& xq, float q_scale, float* xpart, int* xcnt,
-                           cudaStream_t stream, int probe) {
+                           cudaStream_t stream, int probe, bool tail_merge) {
   DM_REQUIRE(xq.p != nullptr && xq.n == st.d && xq.bias != nullptr && xq.splits >= 1 &&
                  xq.splits <= kMaxSplits, "cross-attn: q partials");
   DM_REQUIRE(xpart != nullptr && xcnt != nullptr && st.heads <= kMaxHeads, "cross-attn: scratch");
   DM_SMEM_ATTR(cross_attn_kernel, kXaSmem);
   DM_CHECK_CUDA(launch_pdl(cross_attn_kernel, dim3(kXSplits, st.heads, st.grid_rows),
                            dim3(kXaThreads), kXaSmem, stream, xkv_map, st, layer, xq, q_scale,
-                           xpart, xcnt, probe));
+                           xpart, xcnt, probe, int(tail_merge && probe != 2)));
   return 0;
 }
 

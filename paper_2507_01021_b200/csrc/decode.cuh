@@ -174,12 +174,19 @@ int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, floa
 // cross-KV cache as [rows, 64] bf16, box 64 x 64, 128B swizzle. xpart:
 // [kRows][H][8][68] fp32 scratch, xcnt: [kRows * kMaxHeads] zero-initialised
 // counters. Output: o (all heads) as the bf16 hi/lo operand st.ah / st.al of
-// the cross-o GEMV. probe = 1: stream K/V and stop (roofline probe).
+// the cross-o GEMV. probe = 1: stream K/V and stop (roofline probe); probe = 2:
+// no merge (timing probe). tail_merge = false: the splits only store their
+// results and launch_xattn_merge (same arithmetic) must follow.
 constexpr int kMaxHeads = 20;   // per-head scratch / partial splits a LayerNorm may reduce
 constexpr int kAttnSplits = 10; // partial splits an attention kernel reduces (its q / k / v)
+// Steps with at most this many active rows merge the cross-attention splits in
+// the last-arriving CTA (saves a kernel on the latency-bound chain); above it,
+// in xattn_merge_kernel (measured: scripts/xattn_compare.py).
+constexpr int kXaTailMergeRows = 1;
 int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
                       const Partials& xq, float q_scale, float* xpart, int* xcnt,
-                      cudaStream_t stream, int probe = 0);
+                      cudaStream_t stream, int probe = 0, bool tail_merge = true);
+int launch_xattn_merge(const DecodeState& st, const float* xpart, cudaStream_t stream);
 // fc2's operand from fc1's K-split partials: split-order sum + bias, exact
 // GELU, bf16 hi/lo (the large models' fc1 needs a K split; see record_step).
 int launch_gelu_hilo(const DecodeState& st, const Partials& p, uint16_t* yh, uint16_t* yl,

@@ -269,6 +269,7 @@ struct WhisperEngine {
     // (every kernel computes the same values whatever the grid)
     cudaGraph_t graph[kRowBuckets] = {};
     cudaGraphExec_t exec[kRowBuckets] = {};
+    size_t nodes[kRowBuckets] = {};  // kernels per step graph (launch telemetry)
     int n_active_host = 0;
     // K-split partial sums of the linear projections (consumer-reduced)
     float *p_qkv = nullptr, *p_o = nullptr, *p_xq = nullptr, *p_xo = nullptr, *p_fc2 = nullptr;
@@ -280,12 +281,16 @@ struct WhisperEngine {
   cudaEvent_t step_start = nullptr;
   // telemetry: kernels launched (graph nodes counted per replay)
   long long launches = 0, steps = 0, encodes = 0, segments = 0;
-  int step_kernels() const { return (fc1_split() ? 12 : 11) * Ld + 3; }
   bool fc1_split() const { return d / 64 > 8; }       // fc1's K does not fit one CTA
   // fc1's K split (fixed per engine): steps of <= 16 rows reduce it in the
   // GEMV's last CTA and apply GELU there; larger steps write partials and run
   // gelu_hilo_kernel -- the same split-order sums, bit for bit
   int fc1_splits = std::getenv("DM_FC1_SPLITS") ? std::atoi(std::getenv("DM_FC1_SPLITS")) : 4;
+  // cross-attention split merge in the last CTA up to this many rows, else
+  // xattn_merge_kernel (DM_XA_TAIL_MERGE_ROWS: experiments)
+  int xa_tail_merge_rows = std::getenv("DM_XA_TAIL_MERGE_ROWS")
+                               ? std::atoi(std::getenv("DM_XA_TAIL_MERGE_ROWS"))
+                               : kXaTailMergeRows;
   int encode_kernels() const { return 2 + 1 + 2 + 7 * L + 1 + 1; }
 
   // debug (DM_GUARD=1 at create): every allocation gets a 64 KB 0xA5 tail
@@ -671,8 +676,10 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
     DM_STEP(ln(2, b0 + 6, Partials{grp.p_o, go, d, e->W(b0 + 5)}));
     DM_STEP(gv(pi + 2, grp.p_xq, nullptr, nullptr, nullptr));
     // cross-attention (o -> ah/al) -> cross-o projection (partials) -> ln3
+    const bool tail_merge = rows <= e->xa_tail_merge_rows;
     DM_STEP(launch_cross_attn(st, e->xkv_map, l, Partials{grp.p_xq, gx, d, e->W(b0 + 9)}, 0.125f,
-                              grp.xpart, grp.xcnt, s));
+                              grp.xpart, grp.xcnt, s, 0, tail_merge));
+    if (!tail_merge) DM_STEP(launch_xattn_merge(st, grp.xpart, s));
     DM_STEP(gv(pi + 3, grp.p_xo, nullptr, nullptr, nullptr));
     DM_STEP(ln(2, b0 + 12, Partials{grp.p_xo, e->plans[pi + 3].splits, d, e->W(b0 + 11)}));
     if (e->fc1_split() && rows > 16) {
@@ -721,6 +728,7 @@ static int build_step_graph(WhisperEngine* e) {
       }
       DM_CHECK_CUDA(ce);
       grp.graph[b] = g;
+      DM_CHECK_CUDA(cudaGraphGetNodes(g, nullptr, &grp.nodes[b]));
       DM_CHECK_CUDA(cudaGraphInstantiate(&grp.exec[b], g, 0));
     }
   }
@@ -990,26 +998,27 @@ int dm_whisper_step(void* handle, int n_steps, void* stream) {
   if (!e->step_exec)
     if (int rc = build_step_graph(e)) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  auto exec_of = [](const WhisperEngine::Group& grp) {
+  auto bucket_of = [](const WhisperEngine::Group& grp) {
     int b = 0;
     while (b < kRowBuckets - 1 && kRowBucket[b] < grp.n_active_host) ++b;
-    return grp.exec[b];
+    return b;
   };
   if (e->groups.size() == 1) {
-    cudaGraphExec_t ex = exec_of(e->groups[0]);
-    for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(ex, s));
+    const int b = bucket_of(e->groups[0]);
+    for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(e->groups[0].exec[b], s));
+    e->launches += (long long)n_steps * e->groups[0].nodes[b];
   } else {
     DM_CHECK_CUDA(cudaEventRecord(e->step_start, s));
     for (auto& grp : e->groups) {
       DM_CHECK_CUDA(cudaStreamWaitEvent(grp.stream, e->step_start, 0));
-      cudaGraphExec_t ex = exec_of(grp);
-      for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(ex, grp.stream));
+      const int b = bucket_of(grp);
+      for (int i = 0; i < n_steps; ++i) DM_CHECK_CUDA(cudaGraphLaunch(grp.exec[b], grp.stream));
+      e->launches += (long long)n_steps * grp.nodes[b];
       DM_CHECK_CUDA(cudaEventRecord(grp.done, grp.stream));
     }
     for (auto& grp : e->groups) DM_CHECK_CUDA(cudaStreamWaitEvent(s, grp.done, 0));
   }
   e->steps += n_steps;
-  e->launches += (long long)n_steps * e->step_kernels();
   return 0;
 }
 
@@ -1050,10 +1059,14 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
   auto launch_one = [&](int layer, cudaStream_t cs) -> int {
     const int b0 = e->dec_layer_base(layer), pi = layer * 6;
     switch (which) {
-      case 0:
-        return launch_cross_attn(pst, e->xkv_map, layer,
-                                 Partials{grp.p_xq, e->plans[pi + 2].splits, d, e->W(b0 + 9)},
-                                 0.125f, grp.xpart, grp.xcnt, cs);
+      case 0: {      // as in the step: split merge in the tail or its own kernel
+        const bool tail = pst.grid_rows <= e->xa_tail_merge_rows;
+        if (int rc = launch_cross_attn(pst, e->xkv_map, layer,
+                                       Partials{grp.p_xq, e->plans[pi + 2].splits, d, e->W(b0 + 9)},
+                                       0.125f, grp.xpart, grp.xcnt, cs, 0, tail))
+          return rc;
+        return tail ? 0 : launch_xattn_merge(pst, grp.xpart, cs);
+      }
       case 1:
         return launch_self_attn(pst, layer,
                                 Partials{grp.p_qkv, e->plans[pi].splits, 3 * d, e->W(b0 + 3)},
@@ -1077,6 +1090,10 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
                                  Partials{grp.p_xq, e->plans[pi + 2].splits, d, e->W(b0 + 9)},
                                  0.125f, grp.xpart, grp.xcnt, cs, 1);
       case 10: return gv(pi + 3, grp.p_xo, nullptr, nullptr, nullptr, cs);
+      case 11:       // the cross-attention without its split merge (timing probe)
+        return launch_cross_attn(pst, e->xkv_map, layer,
+                                 Partials{grp.p_xq, e->plans[pi + 2].splits, d, e->W(b0 + 9)},
+                                 0.125f, grp.xpart, grp.xcnt, cs, 2);
       default: set_error("unknown kernel id"); return 1;
     }
   };

@@ -22,13 +22,18 @@ slots = list(range(S))
 for i in range(0, S, 32):
     eng.encode([seg] * 32, slots[i:i + 32])
 eng.admit(slots, [400] * S)
+XA_TAIL_MERGE_ROWS = int(os.environ.get("DM_XA_TAIL_MERGE_ROWS", "1"))  # kXaTailMergeRows
+
+
 def names_for(rows):
     names = []
     for l in range(dims.dec_layers):
         kinds = ("ln1", "qkv", "self", "o", "ln2", "xq", "xattn", "ln3", "fc1", "fc2")
         kinds = kinds[:7] + ("xo",) + kinds[7:]              # cross-attention, cross-o GEMV
+        if rows > XA_TAIL_MERGE_ROWS:                        # split merge kernel
+            kinds = kinds[:7] + ("xmerge",) + kinds[7:]
         if dims.d_model // 64 > 8 and rows > 16:             # split fc1 + GELU kernel
-            kinds = kinds[:10] + ("gelu",) + kinds[10:]
+            kinds = kinds[:-1] + ("gelu",) + kinds[-1:]
         names += [f"L{l}.{k}" for k in kinds]
     return names + ["ln_f", "lm_head", "finalize"]
 lib = eng.lib

@@ -26,7 +26,7 @@ for rows in rows_list:
     eng.step(2)
     torch.cuda.synchronize()
     r = {}
-    for which, label in ((0, "xattn"), (9, "kv_stream_only"), (10, "xo_gemv")):
+    for which, label in ((0, "xattn"), (9, "kv_stream_only"), (11, "no_merge"), (10, "xo_gemv")):
         us = statistics.median(1000 * eng.time_kernel(which, layer=-1, iters=2 * L) for _ in range(5))
         gbs = rows * 2 * 1500 * dims.d_model * 2 / (us * 1e-6) / 1e9
         r[label] = {"us": round(us, 2), "GBps": round(gbs, 1)}
