@@ -104,6 +104,13 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint
       : "memory");
 }
 
+// 1-D bulk prefetch global -> L2 (no completion; the later loads hit L2)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gsrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(gsrc)),
+               "r"(bytes)
+               : "memory");
+}
+
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block,
                                       dim3 cluster, size_t smem, cudaStream_t stream,
@@ -748,10 +755,17 @@ __device__ __forceinline__ void store_hilo1(const DecodeState& st, int r, int c,
   st.al[size_t(r) * st.d + c] = lo;
 }
 
-constexpr int kSaThreads = 256;
+#ifndef DM_SA_THREADS
+#define DM_SA_THREADS 256
+#endif
+#ifndef DM_SA_PREPAGES
+#define DM_SA_PREPAGES 2
+#endif
+constexpr int kSaThreads = DM_SA_THREADS;
+constexpr int kSaWarps = kSaThreads / 32;
 constexpr int kSaMaxKeys = 448;
 constexpr int kSaPageBytes = 64 * 128;                         // one page block: 64 keys x 64 dims
-constexpr int kSaPrePages = 2;                                 // pages staged in shared memory
+constexpr int kSaPrePages = DM_SA_PREPAGES;                    // pages staged in shared memory
 
 // Self-attention for (row, head). The fed token's position and the slot's
 // earlier keys/values do not depend on this step's predecessors (positions
@@ -766,8 +780,8 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
   __shared__ __align__(16) float qs[64];
   __shared__ float kc[64], vc[64];
   __shared__ float sc[kSaMaxKeys];
-  __shared__ float redm[8], reds[8];
-  __shared__ float op[8][64];
+  __shared__ float redm[kSaWarps], reds[kSaWarps];
+  __shared__ float op[kSaWarps][64];
   const int r = blockIdx.x, h = blockIdx.y, tid = threadIdx.x;
   const int warp = tid / 32, lane = tid % 32;
   if (tid == 0) trace_mark(st, 0);
@@ -793,6 +807,14 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
         bulk_load(sa_smem + g * 2 * kSaPageBytes, kb, kSaPageBytes, bar);
         bulk_load(sa_smem + g * 2 * kSaPageBytes + kSaPageBytes, kb + kv_off, kSaPageBytes, bar);
       }
+    }
+  } else if (tid < 32) {
+    // later pages (positions >= 64 * kSaPrePages) are read from global memory
+    // after the wait: pull them into L2 now (one lane per K or V page block)
+    const int g = kSaPrePages + (tid >> 1);
+    if (g < ceil_div(p, 64)) {
+      const uint16_t* kb = st.kv_pool + ((size_t(pt[g]) * L + layer) * 2 * H + h) * 64 * 64;
+      bulk_prefetch_l2((tid & 1) ? kb + kv_off : kb, kSaPageBytes);
     }
   }
   float bq = 0.f, bk = 0.f, bv = 0.f;
@@ -893,8 +915,8 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
   for (int w = 0; w < kSaThreads / 32; ++w) l += reds[w];
   if (tid == 0) trace_mark(st, 6);
   float o0 = 0.f, o1 = 0.f;
-#pragma unroll 4
-  for (int t = warp; t < nk; t += 8) {
+#pragma unroll 8
+  for (int t = warp; t < nk; t += kSaWarps) {
     float v0, v1;
     if (t < p) {
       const uint32_t w =
@@ -921,7 +943,7 @@ self_attn_kernel(const DecodeState st, int layer, const Partials qkv, float q_sc
   if (tid < 64) {
     float a = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) a += op[w][tid];
+    for (int w = 0; w < kSaWarps; ++w) a += op[w][tid];
     store_hilo1(st, r, h * 64 + tid, a / l);
   }
   if (tid == 0) trace_mark(st, 3);
