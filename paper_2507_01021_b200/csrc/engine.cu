@@ -282,10 +282,13 @@ struct WhisperEngine {
   // telemetry: kernels launched (graph nodes counted per replay)
   long long launches = 0, steps = 0, encodes = 0, segments = 0;
   bool fc1_split() const { return d / 64 > 8; }       // fc1's K does not fit one CTA
-  // fc1's K split (fixed per engine): steps of <= 16 rows reduce it in the
-  // GEMV's last CTA and apply GELU there; larger steps write partials and run
-  // gelu_hilo_kernel -- the same split-order sums, bit for bit
+  // fc1's K split (fixed per engine): the GEMV writes partials and
+  // gelu_hilo_kernel reduces them in split order, adds the bias, applies GELU
   int fc1_splits = std::getenv("DM_FC1_SPLITS") ? std::atoi(std::getenv("DM_FC1_SPLITS")) : 4;
+  // fc1 split merge + GELU in the GEMV's last CTA per tile up to this many
+  // rows, else gelu_hilo_kernel: the kernel measured faster at every row
+  // count (1 row 1.37 -> 1.34 ms per step), so 0 (DM_FC1_TAIL_ROWS: experiments)
+  int fc1_tail_rows = std::getenv("DM_FC1_TAIL_ROWS") ? std::atoi(std::getenv("DM_FC1_TAIL_ROWS")) : 0;
   // cross-attention split merge in the last CTA up to this many rows, else
   // xattn_merge_kernel (DM_XA_TAIL_MERGE_ROWS: experiments)
   int xa_tail_merge_rows = std::getenv("DM_XA_TAIL_MERGE_ROWS")
@@ -682,7 +685,7 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
     if (!tail_merge) DM_STEP(launch_xattn_merge(st, grp.xpart, s));
     DM_STEP(gv(pi + 3, grp.p_xo, nullptr, nullptr, nullptr));
     DM_STEP(ln(2, b0 + 12, Partials{grp.p_xo, e->plans[pi + 3].splits, d, e->W(b0 + 11)}));
-    if (e->fc1_split() && rows > 16) {
+    if (e->fc1_split() && rows > e->fc1_tail_rows) {
       DM_STEP(gv(pi + 4, grp.p_fc1, nullptr, nullptr, nullptr));
       DM_STEP(launch_gelu_hilo(st, Partials{grp.p_fc1, e->plans[pi + 4].splits, e->F, e->W(b0 + 15)},
                                st.hh, st.hl, s));

@@ -25,6 +25,9 @@ eng.admit(slots, [400] * S)
 XA_TAIL_MERGE_ROWS = int(os.environ.get("DM_XA_TAIL_MERGE_ROWS", "1"))  # kXaTailMergeRows
 
 
+FC1_TAIL_ROWS = int(os.environ.get("DM_FC1_TAIL_ROWS", "0"))
+
+
 def names_for(rows):
     names = []
     for l in range(dims.dec_layers):
@@ -32,7 +35,7 @@ def names_for(rows):
         kinds = kinds[:7] + ("xo",) + kinds[7:]              # cross-attention, cross-o GEMV
         if rows > XA_TAIL_MERGE_ROWS:                        # split merge kernel
             kinds = kinds[:7] + ("xmerge",) + kinds[7:]
-        if dims.d_model // 64 > 8 and rows > 16:             # split fc1 + GELU kernel
+        if dims.d_model // 64 > 8 and rows > FC1_TAIL_ROWS:   # split fc1 + GELU kernel
             kinds = kinds[:-1] + ("gelu",) + kinds[-1:]
         names += [f"L{l}.{k}" for k in kinds]
     return names + ["ln_f", "lm_head", "finalize"]

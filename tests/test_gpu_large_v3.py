@@ -47,10 +47,10 @@ def test_large_v3_parity(native_lib):
 
 
 def test_large_v3_batch_invariance_across_fc1_paths(native_lib):
-    """large-v3's fc1 needs a K split: steps of <= 16 rows reduce it in the
-    GEMV's last CTA (+ GELU there), larger steps write partials and run the
-    GELU kernel; both use the same split-order sums, so a segment decodes to
-    the same tokens (and logits) alone and in a batch of 24."""
+    """large-v3's fc1 needs a K split (partials reduced in split order by the
+    GELU kernel; DM_FC1_TAIL_ROWS can move few-row steps to the GEMV's
+    last-CTA merge, the same sums), and every row bucket has its own grids:
+    a segment decodes to the same tokens alone and in a batch of 24."""
     from paper_2507_01021_b200.engine import WhisperGPU
     rng = np.random.default_rng(44)
     segs = [rng.integers(-8000, 8000, size=int(rng.uniform(3, 30) * 16000), dtype=np.int16)
