@@ -905,19 +905,28 @@ int launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   // wide N, or long K (fc2, the stride-2 conv): 128 x 256 tiles cut the per-SM
   // operand stream (bytes per FLOP (128 + BN) / (128 BN)); with a long K the
   // epilogue's global traffic overlaps the next tile's mainloop
-  if (g.N % 256 == 0 && (g.N >= 1024 || g.K >= 1536)) {
-    // long K (stride-2 conv, fc2): the mainloop's L2 -> SMEM operand stream
-    // bounds the 1-SM kernel, so 256 x 256 tiles run on CTA pairs
-    // (cta_group::2; measured conv2 99 -> 95 us, fc2 118 -> 112 us). The
+  // (experiments: DM_GEMM_PAIR_MIN_K moves the CTA-pair threshold,
+  // DM_GEMM_RESID128=1 sends wide residual GEMMs to the 128-wide residual path)
+  static const int pair_min_k =
+      std::getenv("DM_GEMM_PAIR_MIN_K") ? std::atoi(std::getenv("DM_GEMM_PAIR_MIN_K")) : 1024;
+  static const bool resid128 = std::getenv("DM_GEMM_RESID128") != nullptr;
+  const bool resid_path = g.epi.mode == EPI_RESID_F32 && g.a_mode == A_FLAT && g.Bt == 1;
+  if (g.N % 256 == 0 && (g.N >= 1024 || g.K >= 1536) && !(resid128 && resid_path)) {
+    // K >= 1024 (large-v3's projections, fc2, the stride-2 conv): the
+    // mainloop's L2 -> SMEM operand stream bounds the 1-SM kernel, so 256 x 256
+    // tiles run on CTA pairs (cta_group::2; measured at large-v3, 12
+    // segments: cross-KV 4.64 -> 3.64 ms, qkv 144 -> 131 us, o 86 -> 81 us,
+    // fc1 unchanged; whisper-base conv2 99 -> 95 us, fc2 118 -> 112 us). The
     // K = 512 GEMMs are bound by their epilogues (GELU, Q/K/V scatter) and
     // stay on the 1-SM kernel (pairs measured slower: fc1 163 -> 176 us).
-    // DM_GEMM_NO_PAIR=1 forces the 1-SM kernel (same per-element MMA sequence).
+    // The 128-wide TMA-prefetched residual path measured slower for the wide
+    // o-projection (86 -> 166 us). DM_GEMM_NO_PAIR=1 forces the 1-SM kernel
+    // (same per-element MMA sequence).
     static const bool no_pair = std::getenv("DM_GEMM_NO_PAIR") != nullptr;
-    if (g.K >= 1536 && !no_pair) return launch_pair<6>(g, stream);
+    if (g.K >= pair_min_k && !no_pair) return launch_pair<6>(g, stream);
     return launch_bn<256, 4>(g, stream);
   }
-  if (g.epi.mode == EPI_RESID_F32 && g.a_mode == A_FLAT && g.Bt == 1)
-    return launch_bn_mode<128, 5, EPI_RESID_F32>(g, stream);     // + 64 KB residual buffer
+  if (resid_path) return launch_bn_mode<128, 5, EPI_RESID_F32>(g, stream);  // + 64 KB residual buffer
   return launch_bn<128, 6>(g, stream);
 }
 
