@@ -121,7 +121,7 @@ __device__ __forceinline__ float ordered_to_float(uint32_t k) {
 struct LogmelSmem {
   float samples[kSpan];           // also reused as power[kFPB][kBins]
   float pad_[kFPB * kBins - kSpan > 0 ? kFPB * kBins - kSpan : 1];
-  float2 y[kFPB * 200];           // stage A out / stage B out (Z)
+  float2 y[kFPB * 200];           // stage A out ([frame][k1][q]) / stage B out (Z, natural order)
   float2 tw200[200];
   float2 tw25[25];
   float2 tw400[kBins];
@@ -175,7 +175,8 @@ logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offse
     return;
   }
 
-  for (int i = tid; i < 200; i += kLogmelThreads) s.tw200[i] = tab->tw200[i];
+  // twiddles as [k1][q] (the table is [q][k1]): stage A's lanes run along q
+  for (int i = tid; i < 200; i += kLogmelThreads) s.tw200[(i % 8) * 25 + i / 8] = tab->tw200[i];
   for (int i = tid; i < 25; i += kLogmelThreads) s.tw25[i] = tab->tw25[i];
   for (int i = tid; i < kBins; i += kLogmelThreads) s.tw400[i] = tab->tw400[i];
   for (int i = tid; i < kFFT; i += kLogmelThreads) s.window[i] = tab->window[i];
@@ -232,9 +233,10 @@ logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offse
                          src[2 * m + 1] * s.window[2 * m + 1]);
     }
     dft8(z);
-    float2* dst = s.y + fr * 200 + q * 8;
+    // Y[k1][q] (k1-major: a warp's lanes store consecutive q, conflict-free)
+    float2* dst = s.y + fr * 200 + q;
 #pragma unroll
-    for (int k1 = 0; k1 < 8; ++k1) dst[k1] = cmul(z[k1], s.tw200[q * 8 + k1]);
+    for (int k1 = 0; k1 < 8; ++k1) dst[k1 * 25] = cmul(z[k1], s.tw200[k1 * 25 + q]);
   }
   __syncthreads();
 
@@ -242,9 +244,9 @@ logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offse
   {
     const int fr = tid / 8, k1 = tid % 8;               // 256 tasks exactly
     float2 v[25];
-    const float2* src = s.y + fr * 200 + k1;
+    const float2* src = s.y + fr * 200 + k1 * 25;
 #pragma unroll
-    for (int q = 0; q < 25; ++q) v[q] = src[q * 8];
+    for (int q = 0; q < 25; ++q) v[q] = src[q];
     // q = 5a + c: DFT over a for each c, twiddle W25^{c e}
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
