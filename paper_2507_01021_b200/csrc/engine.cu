@@ -106,6 +106,7 @@ static int build_logmel_tables(int n_mels, LogmelTablesHost* t) {
       }
     }
     if (start < 0) start = 0;
+    if (count > 16) return 1;        // logmel.cu kMelMaxBins: filter weights held in registers
     t->mel_start[m] = start;
     t->mel_count[m] = count;
     t->mel_woff[m] = woff;

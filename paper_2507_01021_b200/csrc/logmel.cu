@@ -41,6 +41,7 @@ constexpr int kFPB = 32;                               // frames per CTA
 static_assert(kFrames % 4 == 0 && kFPB % 4 == 0, "float4 frame groups");
 constexpr int kSpan = (kFPB - 1) * kHop + kFFT;        // 5360 samples
 constexpr int kLogmelThreads = 256;
+constexpr int kMelMaxBins = 16;                        // bins of the widest mel filter (host-checked)
 
 // Twiddles / window / sparse mel bank, prepared on the host (float64 -> fp32).
 struct LogmelTables {
@@ -297,11 +298,23 @@ logmel_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offse
     const int m0 = 2 * p;
     const int st0 = s.mstart[m0], c0 = s.mcount[m0], w0 = s.mwoff[m0];
     const int st1 = s.mstart[m0 + 1], c1 = s.mcount[m0 + 1], w1 = s.mwoff[m0 + 1];
+    // the pair's filter weights in registers for all its frames (<= kMelMaxBins
+    // bins per filter: 14 at 80 mels, 9 at 128; same summation order)
+    float r0[kMelMaxBins], r1[kMelMaxBins];
+#pragma unroll
+    for (int i = 0; i < kMelMaxBins; ++i) {
+      r0[i] = i < c0 ? s.mw[w0 + i] : 0.f;
+      r1[i] = i < c1 ? s.mw[w1 + i] : 0.f;
+    }
     for (int fr = g; fr < nfr; fr += kLogmelThreads / 64) {
       const float* pw = power + fr * kBins;
       float a0 = 0.f, a1 = 0.f;
-      for (int i = 0; i < c0; ++i) a0 = fmaf(s.mw[w0 + i], pw[st0 + i], a0);
-      for (int i = 0; i < c1; ++i) a1 = fmaf(s.mw[w1 + i], pw[st1 + i], a1);
+#pragma unroll
+      for (int i = 0; i < kMelMaxBins; ++i)
+        if (i < c0) a0 = fmaf(r0[i], pw[st0 + i], a0);
+#pragma unroll
+      for (int i = 0; i < kMelMaxBins; ++i)
+        if (i < c1) a1 = fmaf(r1[i], pw[st1 + i], a1);
       const float v0 = fast_log10(fmaxf(a0, 1e-10f));
       const float v1 = fast_log10(fmaxf(a1, 1e-10f));
       if (tb) reinterpret_cast<uint32_t*>(tb + size_t(fr) * ldt)[p] = norm_bf16_pair(v0, v1);
