@@ -132,6 +132,76 @@ static cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+constexpr int kXpStride = 68;                 // floats per split result: o[64], max, sum, pad
+
+__device__ __forceinline__ float4 bf16x4_to_f32(uint2 w) {
+  return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
+                     __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
+}
+
+// Cross-attention output of (row r, head h, dimension c): the split-order
+// merge of its splits' (o, max, sum) in `xpart` (the last-arriver tail, the
+// merge kernel and the cross-o GEMV's operand builder all use this).
+__device__ __forceinline__ float xattn_merged(const DecodeState& st, const float* xpart, int r,
+                                              int h, int nsplit, int c) {
+  const float* base = xpart + (size_t(r) * st.heads + h) * kXSplits * kXpStride;
+  float mv[kXSplits], lv[kXSplits], ov[kXSplits];
+#pragma unroll
+  for (int s = 0; s < kXSplits; ++s) {        // splits past the window: empty
+    mv[s] = s < nsplit ? __ldcg(base + s * kXpStride + 64) : -INFINITY;
+    lv[s] = s < nsplit ? __ldcg(base + s * kXpStride + 65) : 0.f;
+    ov[s] = s < nsplit ? __ldcg(base + s * kXpStride + c) : 0.f;
+  }
+  float M = -INFINITY;
+#pragma unroll
+  for (int s = 0; s < kXSplits; ++s) M = fmaxf(M, mv[s]);
+  float Ls = 0.f, O = 0.f;
+#pragma unroll
+  for (int s = 0; s < kXSplits; ++s) {
+    const float f = exp2f((mv[s] - M) * kLog2e);
+    Ls += lv[s] * f;
+    O += ov[s] * f;
+  }
+  return O / Ls;
+}
+
+// xattn_merged for dimensions c .. c + 3 (c % 4 == 0): each lane of the result
+// is computed exactly as xattn_merged computes it (same operations, same
+// order); the max / sum loads are shared and o is read as float4.
+__device__ __forceinline__ float4 xattn_merged4(const DecodeState& st, const float* xpart, int r,
+                                                int h, int nsplit, int c) {
+  const float* base = xpart + (size_t(r) * st.heads + h) * kXSplits * kXpStride;
+  float mv[kXSplits], lv[kXSplits];
+  float4 ov[kXSplits];
+#pragma unroll
+  for (int s = 0; s < kXSplits; ++s) {
+    mv[s] = s < nsplit ? __ldcg(base + s * kXpStride + 64) : -INFINITY;
+    lv[s] = s < nsplit ? __ldcg(base + s * kXpStride + 65) : 0.f;
+    ov[s] = s < nsplit ? __ldcg(reinterpret_cast<const float4*>(base + s * kXpStride + c))
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  float M = -INFINITY;
+#pragma unroll
+  for (int s = 0; s < kXSplits; ++s) M = fmaxf(M, mv[s]);
+  float Ls = 0.f;
+  float4 O = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int s = 0; s < kXSplits; ++s) {
+    const float f = exp2f((mv[s] - M) * kLog2e);
+    Ls += lv[s] * f;
+    O.x += ov[s].x * f;
+    O.y += ov[s].y * f;
+    O.z += ov[s].z * f;
+    O.w += ov[s].w * f;
+  }
+  return make_float4(O.x / Ls, O.y / Ls, O.z / Ls, O.w / Ls);
+}
+
+// element (row n, k) of a K-major SW128 operand tile with 128-byte rows
+__device__ __forceinline__ int sw128_off(int n, int k) {
+  return n * 128 + ((((k >> 3) ^ n) & 7) << 4) + (k & 7) * 2;
+}
+
 // ============================================================ tcgen05 GEMV
 // CTA (c, split) owns N tiles c, c + gridDim.x, ... for one K split. Warp
 // roles: w0 TMA, w1 MMA (+ TMEM alloc), w2..5 epilogue (thread = output
@@ -248,12 +318,14 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
       }
       pdl_wait();
       trace_mark(st, 1);
-      mbar_arrive_expect_tx(xfull, kb_per * 2 * G * kGvXBox * 128);
-      for (int i = 0; i < kb_per; ++i) {
-        uint8_t* xb = xs + i * 2 * XB;          // [hi: Np rows | lo: Np rows], 128 B rows
-        for (int g = 0; g < G; ++g) {
-          tma_load_2d(xb + g * kGvXBox * 128, &txh, xfull, (kb0 + i) * 64, r0 + g * kGvXBox);
-          tma_load_2d(xb + (Np + g * kGvXBox) * 128, &txl, xfull, (kb0 + i) * 64, r0 + g * kGvXBox);
+      if (a.xsrc == GV_X_TMA) {                 // (else the epilogue warps build it)
+        mbar_arrive_expect_tx(xfull, kb_per * 2 * G * kGvXBox * 128);
+        for (int i = 0; i < kb_per; ++i) {
+          uint8_t* xb = xs + i * 2 * XB;        // [hi: Np rows | lo: Np rows], 128 B rows
+          for (int g = 0; g < G; ++g) {
+            tma_load_2d(xb + g * kGvXBox * 128, &txh, xfull, (kb0 + i) * 64, r0 + g * kGvXBox);
+            tma_load_2d(xb + (Np + g * kGvXBox) * 128, &txl, xfull, (kb0 + i) * 64, r0 + g * kGvXBox);
+          }
         }
       }
       for (int q = pre; q < total; ++q) issue_w(q);
@@ -329,6 +401,42 @@ gemv_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUte
     if (EPI != GV_PARTIAL && a.bias != nullptr && int(blockIdx.x) * 128 + f < a.N)
       bcur = bf16_to_f32(a.bias[blockIdx.x * 128 + f]);
     pdl_wait();
+    if (a.xsrc != GV_X_TMA) {
+      // build this CTA's activation slice (rows [r0, r0 + Np), k-blocks kb0..)
+      // in the SW128 layout the TMA would have produced, 4 k per item
+      const int kq = kb_per * 16;
+#pragma unroll 2
+      for (int e = et; e < Np * kq; e += 128) {
+        const int row = e / kq, kk = (e % kq) * 4;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (row < R) {
+          const int gr = r0 + row, gk = kb0 * 64 + kk;
+          float4 y;
+          if (a.xsrc == GV_X_GELU) {       // gelu_hilo_kernel's arithmetic
+            const float4 sa = sum_splits4<8>(a.xp + size_t(gr) * a.K + gk, size_t(kRows) * a.K,
+                                             a.xs_splits);
+            const float4 bb = bf16x4_to_f32(*reinterpret_cast<const uint2*>(a.xbias + gk));
+            y = make_float4(gelu_erf(sa.x + bb.x), gelu_erf(sa.y + bb.y), gelu_erf(sa.z + bb.z),
+                            gelu_erf(sa.w + bb.w));
+          } else {                         // xattn_merge_kernel's arithmetic
+            const int nsplit = ceil_div(st.enc_len[st.active[gr]], kXaKeysPerSplit);
+            y = xattn_merged4(st, a.xp, gr, gk >> 6, nsplit, gk & 63);
+          }
+          v[0] = y.x; v[1] = y.y; v[2] = y.z; v[3] = y.w;
+        }
+        uint16_t h[4], l[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) split_hilo(v[u], h[u], l[u]);
+        uint8_t* xb = xs + (kk >> 6) * 2 * XB;
+        *reinterpret_cast<uint2*>(xb + sw128_off(row, kk & 63)) =
+            make_uint2(uint32_t(h[0]) | (uint32_t(h[1]) << 16), uint32_t(h[2]) | (uint32_t(h[3]) << 16));
+        *reinterpret_cast<uint2*>(xb + sw128_off(Np + row, kk & 63)) =
+            make_uint2(uint32_t(l[0]) | (uint32_t(l[1]) << 16), uint32_t(l[2]) | (uint32_t(l[3]) << 16));
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (et == 0) mbar_arrive(xfull);
+    }
     int it = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x, ++it) {
       const int n = tile * 128 + f;
@@ -583,6 +691,10 @@ int launch_gemv(const DecodeState& st, const TcGemvMaps& maps, const GemvArgs& a
              "GEMV slice exceeds smem");
   DM_REQUIRE(a.xrows % (16 * a.rgroups) == 0 && a.xrows <= kRows && a.gx >= 1,
              "GEMV activation rows / grid");
+  DM_REQUIRE(a.xsrc == GV_X_TMA ||
+                 (a.xrows <= 16 && a.rgroups == 1 && a.xp != nullptr &&
+                  (a.xsrc == GV_X_XMERGE || (a.xbias != nullptr && a.xs_splits >= 1 && a.xs_splits <= 8))),
+             "GEMV operand builder: <= 16 rows, one row group, source set");
   const bool sp = a.splits > 1;
   switch (a.epi) {
     case GV_PARTIAL:
@@ -601,10 +713,6 @@ int launch_gemv(const DecodeState& st, const TcGemvMaps& maps, const GemvArgs& a
 // are fetched before the dependency wait; after it, one round of loads (x and
 // the residual partials, or the embedding rows), two block reductions (mean,
 // then the centred second moment), and the hi/lo operand stores.
-__device__ __forceinline__ float4 bf16x4_to_f32(uint2 w) {
-  return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u),
-                     __uint_as_float(w.y << 16), __uint_as_float(w.y & 0xFFFF0000u));
-}
 
 __device__ __forceinline__ float block_sum_fixed(float v, float* red) {
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
@@ -997,12 +1105,7 @@ __device__ __forceinline__ void tmem_ld2(uint32_t taddr, uint32_t& a, uint32_t& 
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];"
                : "=r"(a), "=r"(b) : "r"(taddr));
 }
-// element (row n, k) of a K-major SW128 operand tile with 128-byte rows
-__device__ __forceinline__ int sw128_off(int n, int k) {
-  return n * 128 + ((((k >> 3) ^ n) & 7) << 4) + (k & 7) * 2;
-}
 
-constexpr int kXpStride = 68;                 // floats per split result: o[64], max, sum, pad
 
 // Merge of the (o, max, sum) results of a (row, head)'s splits, in split
 // order, into the cross-o operand; thread `c` < 64 does head dimension c. The
@@ -1010,26 +1113,8 @@ constexpr int kXpStride = 68;                 // floats per split result: o[64],
 // paths give the same bits.
 __device__ __forceinline__ void xattn_merge_head(const DecodeState& st, const float* xpart, int r,
                                                  int h, int nsplit, int c) {
-  const float* base = xpart + (size_t(r) * st.heads + h) * kXSplits * kXpStride;
-  float mv[kXSplits], lv[kXSplits], ov[kXSplits];
-#pragma unroll
-  for (int s = 0; s < kXSplits; ++s) {        // splits past the window: empty
-    mv[s] = s < nsplit ? __ldcg(base + s * kXpStride + 64) : -INFINITY;
-    lv[s] = s < nsplit ? __ldcg(base + s * kXpStride + 65) : 0.f;
-    ov[s] = s < nsplit ? __ldcg(base + s * kXpStride + c) : 0.f;
-  }
-  float M = -INFINITY;
-#pragma unroll
-  for (int s = 0; s < kXSplits; ++s) M = fmaxf(M, mv[s]);
-  float Ls = 0.f, O = 0.f;
-#pragma unroll
-  for (int s = 0; s < kXSplits; ++s) {
-    const float f = exp2f((mv[s] - M) * kLog2e);
-    Ls += lv[s] * f;
-    O += ov[s] * f;
-  }
   uint16_t hi, lo;
-  split_hilo(O / Ls, hi, lo);
+  split_hilo(xattn_merged(st, xpart, r, h, nsplit, c), hi, lo);
   const size_t idx = size_t(r) * st.d + h * 64 + c;
   st.ah[idx] = hi;
   st.al[idx] = lo;

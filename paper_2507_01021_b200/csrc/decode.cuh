@@ -130,7 +130,20 @@ struct GemvArgs {
   int counter_base;
   float* part;             // GV_PARTIAL output [splits][kRows][N]
   uint16_t *yh, *yl;       // GV_GELU_HILO targets [kRows, N]
+  // Activation source. GV_X_TMA: the hi/lo operand in global memory (TMA).
+  // Steps of <= 16 rows may instead build it in shared memory from the
+  // producer's raw output, saving the producer's finishing kernel:
+  //   GV_X_GELU:  gelu(sum of xs_splits K-split partials xp[s][kRows][K] + xbias)
+  //               (fc2 after a split fc1: what gelu_hilo_kernel computes)
+  //   GV_X_XMERGE: the split-order merge of the cross-attention results xp
+  //               (cross-o: what xattn_merge_kernel computes)
+  // -- the same arithmetic, so every row bucket gives the same bits.
+  int xsrc;
+  const float* xp;
+  int xs_splits;
+  const uint16_t* xbias;
 };
+enum GemvXSrc : int { GV_X_TMA = 0, GV_X_GELU = 1, GV_X_XMERGE = 2 };
 
 // Pre-encoded TMA maps of one projection: weights [N, K] (box 128 x 64) and the
 // hi/lo activation input [kRows, K] (box 16 rows x 64, loads scale with rows).
@@ -180,9 +193,12 @@ int launch_self_attn(const DecodeState& st, int layer, const Partials& qkv, floa
 constexpr int kMaxHeads = 20;   // per-head scratch / partial splits a LayerNorm may reduce
 constexpr int kAttnSplits = 10; // partial splits an attention kernel reduces (its q / k / v)
 // Steps with at most this many active rows merge the cross-attention splits in
-// the last-arriving CTA (saves a kernel on the latency-bound chain); above it,
-// in xattn_merge_kernel (measured: scripts/xattn_compare.py).
-constexpr int kXaTailMergeRows = 1;
+// the last-arriving CTA (0: never; the cross-o GEMV's operand builder does it
+// for few-row steps, xattn_merge_kernel above kGvFuseRows).
+constexpr int kXaTailMergeRows = 0;
+// Steps with at most this many rows build the cross-o / fc2 GEMV operands in
+// the GEMV (GemvArgs::xsrc) instead of running the merge / GELU kernels.
+constexpr int kGvFuseRows = 8;
 int launch_cross_attn(const DecodeState& st, const CUtensorMap& xkv_map, int layer,
                       const Partials& xq, float q_scale, float* xpart, int* xcnt,
                       cudaStream_t stream, int probe = 0, bool tail_merge = true);

@@ -295,6 +295,11 @@ struct WhisperEngine {
   int xa_tail_merge_rows = std::getenv("DM_XA_TAIL_MERGE_ROWS")
                                ? std::atoi(std::getenv("DM_XA_TAIL_MERGE_ROWS"))
                                : kXaTailMergeRows;
+  // steps of <= gv_fuse_rows rows (at most 16) skip the split-merge and GELU
+  // kernels: the cross-o and fc2 GEMVs build their operands from the raw
+  // results (DM_GV_FUSE_ROWS: experiments; 0 disables)
+  int gv_fuse_rows = std::min(16, std::getenv("DM_GV_FUSE_ROWS") ? std::atoi(std::getenv("DM_GV_FUSE_ROWS"))
+                                                                 : kGvFuseRows);
   int encode_kernels() const { return 2 + 1 + 2 + 7 * L + 1 + 1; }
 
   // debug (DM_GUARD=1 at create): every allocation gets a 64 KB 0xA5 tail
@@ -680,16 +685,29 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
     DM_STEP(ln(2, b0 + 6, Partials{grp.p_o, go, d, e->W(b0 + 5)}));
     DM_STEP(gv(pi + 2, grp.p_xq, nullptr, nullptr, nullptr));
     // cross-attention (o -> ah/al) -> cross-o projection (partials) -> ln3
+    // the 8 split results of the cross-attention are merged by the last split
+    // (<= xa_tail_merge_rows rows), by the cross-o GEMV while it builds its
+    // operand (<= gv_fuse_rows), or by xattn_merge_kernel
     const bool tail_merge = rows <= e->xa_tail_merge_rows;
+    const bool fuse = rows <= e->gv_fuse_rows;
     DM_STEP(launch_cross_attn(st, e->xkv_map, l, Partials{grp.p_xq, gx, d, e->W(b0 + 9)}, 0.125f,
                               grp.xpart, grp.xcnt, s, 0, tail_merge));
-    if (!tail_merge) DM_STEP(launch_xattn_merge(st, grp.xpart, s));
-    DM_STEP(gv(pi + 3, grp.p_xo, nullptr, nullptr, nullptr));
+    if (!tail_merge && !fuse) DM_STEP(launch_xattn_merge(st, grp.xpart, s));
+    {
+      GemvArgs g = gemv_plan_for_rows(e->plans[pi + 3], rows);
+      g.part = grp.p_xo; g.counter_base = e->gemv_counter_base;
+      if (!tail_merge && fuse) { g.xsrc = GV_X_XMERGE; g.xp = grp.xpart; }
+      DM_STEP(launch_gemv(st, grp.maps[pi + 3], g, s));
+    }
     DM_STEP(ln(2, b0 + 12, Partials{grp.p_xo, e->plans[pi + 3].splits, d, e->W(b0 + 11)}));
+    bool fc2_builds = false;     // fc2 computes GELU(fc1 partials) into its own operand
     if (e->fc1_split() && rows > e->fc1_tail_rows) {
       DM_STEP(gv(pi + 4, grp.p_fc1, nullptr, nullptr, nullptr));
-      DM_STEP(launch_gelu_hilo(st, Partials{grp.p_fc1, e->plans[pi + 4].splits, e->F, e->W(b0 + 15)},
-                               st.hh, st.hl, s));
+      if (fuse)
+        fc2_builds = true;
+      else
+        DM_STEP(launch_gelu_hilo(st, Partials{grp.p_fc1, e->plans[pi + 4].splits, e->F, e->W(b0 + 15)},
+                                 st.hh, st.hl, s));
     } else if (e->fc1_split()) {
       GemvArgs g = e->plans[pi + 4];
       g.epi = GV_GELU_HILO;
@@ -700,7 +718,15 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
     } else {
       DM_STEP(gv(pi + 4, nullptr, st.hh, st.hl, e->W(b0 + 15)));
     }
-    DM_STEP(gv(pi + 5, grp.p_fc2, nullptr, nullptr, nullptr));
+    {
+      GemvArgs g = gemv_plan_for_rows(e->plans[pi + 5], rows);
+      g.part = grp.p_fc2; g.counter_base = e->gemv_counter_base;
+      if (fc2_builds) {
+        g.xsrc = GV_X_GELU; g.xp = grp.p_fc1; g.xs_splits = e->plans[pi + 4].splits;
+        g.xbias = e->W(b0 + 15);
+      }
+      DM_STEP(launch_gemv(st, grp.maps[pi + 5], g, s));
+    }
     prev = Partials{grp.p_fc2, gf, d, e->W(b0 + 17)};
   }
   const int x = e->after_dec();

@@ -22,21 +22,22 @@ slots = list(range(S))
 for i in range(0, S, 32):
     eng.encode([seg] * 32, slots[i:i + 32])
 eng.admit(slots, [400] * S)
-XA_TAIL_MERGE_ROWS = int(os.environ.get("DM_XA_TAIL_MERGE_ROWS", "1"))  # kXaTailMergeRows
-
-
+XA_TAIL_MERGE_ROWS = int(os.environ.get("DM_XA_TAIL_MERGE_ROWS", "0"))  # kXaTailMergeRows
 FC1_TAIL_ROWS = int(os.environ.get("DM_FC1_TAIL_ROWS", "0"))
+GV_FUSE_ROWS = min(16, int(os.environ.get("DM_GV_FUSE_ROWS", "8")))     # kGvFuseRows
 
 
 def names_for(rows):
     names = []
+    fuse = rows <= GV_FUSE_ROWS
     for l in range(dims.dec_layers):
-        kinds = ("ln1", "qkv", "self", "o", "ln2", "xq", "xattn", "ln3", "fc1", "fc2")
-        kinds = kinds[:7] + ("xo",) + kinds[7:]              # cross-attention, cross-o GEMV
-        if rows > XA_TAIL_MERGE_ROWS:                        # split merge kernel
-            kinds = kinds[:7] + ("xmerge",) + kinds[7:]
-        if dims.d_model // 64 > 8 and rows > FC1_TAIL_ROWS:   # split fc1 + GELU kernel
-            kinds = kinds[:-1] + ("gelu",) + kinds[-1:]
+        kinds = ["ln1", "qkv", "self", "o", "ln2", "xq", "xattn"]
+        if rows > XA_TAIL_MERGE_ROWS and not fuse:           # split merge kernel
+            kinds.append("xmerge")
+        kinds += ["xo", "ln3", "fc1"]
+        if dims.d_model // 64 > 8 and rows > FC1_TAIL_ROWS and not fuse:   # GELU kernel
+            kinds.append("gelu")
+        kinds.append("fc2")
         names += [f"L{l}.{k}" for k in kinds]
     return names + ["ln_f", "lm_head", "finalize"]
 lib = eng.lib
