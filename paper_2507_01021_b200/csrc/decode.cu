@@ -1392,6 +1392,65 @@ int launch_gelu_hilo(const DecodeState& st, const Partials& p, uint16_t* yh, uin
 // ============================================================ finalize
 // One warp per active row: argmax over the vocab-tile partials (ties -> lowest
 // id), then the greedy state machine (prompt forcing, EOT, per-slot cap).
+// LM head tail: logits = the K-split partials summed in split order, then per
+// (128-id vocabulary tile, row) the argmax (ties -> lowest id) into
+// amax_val / amax_idx for finalize_kernel -- the values and ties of the GEMV's
+// last-CTA ARGMAX merge, without its per-tile release fence and counter.
+// One warp per (tile, row), lane l covers ids 4l .. 4l + 3 of the tile (each
+// lane scans its ids in increasing order, so a tie keeps the lowest id).
+__global__ void __launch_bounds__(256)
+lm_argmax_kernel(const DecodeState st, const Partials p) {
+  if (threadIdx.x == 0) trace_mark(st, 0);
+  pdl_trigger();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int tiles = ceil_div(st.vocab, 128);
+  const int tile = blockIdx.x, r = blockIdx.y * 8 + warp;
+  pdl_wait();
+  if (threadIdx.x == 0) trace_mark(st, 1);
+  if (r >= *st.n_active || tile >= tiles) return;
+  const size_t stride = size_t(kRows) * p.n;
+  float best = -INFINITY;
+  int bidx = 0x7FFFFFFF;
+  float v[4][kMaxSplits];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {                 // all loads first
+    const int n = tile * 128 + 4 * lane + u;
+    const float* q = p.p + size_t(r) * p.n + n;
+#pragma unroll
+    for (int s = 0; s < kMaxSplits; ++s) v[u][s] = (s < p.splits && n < st.vocab) ? __ldcg(q + s * stride) : 0.f;
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int n = tile * 128 + 4 * lane + u;
+    if (n >= st.vocab) break;
+    float a = v[u][0];
+#pragma unroll
+    for (int s = 1; s < kMaxSplits; ++s)
+      if (s < p.splits) a += v[u][s];
+    if (st.logits_dbg) st.logits_dbg[size_t(r) * st.vocab + n] = a;
+    if (a > best) { best = a; bidx = n; }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+    if (ob > best || (ob == best && oi < bidx)) { best = ob; bidx = oi; }
+  }
+  if (lane == 0) {
+    st.amax_val[size_t(tile) * kRows + r] = best;
+    st.amax_idx[size_t(tile) * kRows + r] = bidx;
+  }
+  if (threadIdx.x == 0) trace_mark(st, 3);
+}
+
+int launch_lm_argmax(const DecodeState& st, const Partials& p, cudaStream_t stream) {
+  DM_REQUIRE(p.p != nullptr && p.n == st.vocab && p.splits >= 1 &&
+                 p.splits <= kMaxSplits, "LM head argmax: partials");
+  DM_CHECK_CUDA(launch_pdl(lm_argmax_kernel, dim3(ceil_div(st.vocab, 128), ceil_div(st.grid_rows, 8)),
+                           dim3(256), 0, stream, st, p));
+  return 0;
+}
+
 __global__ void finalize_kernel(const DecodeState st) {
   const int r = blockIdx.x * 4 + threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) trace_mark(st, 0);

@@ -207,6 +207,9 @@ int launch_xattn_merge(const DecodeState& st, const float* xpart, cudaStream_t s
 // GELU, bf16 hi/lo (the large models' fc1 needs a K split; see record_step).
 int launch_gelu_hilo(const DecodeState& st, const Partials& p, uint16_t* yh, uint16_t* yl,
                      cudaStream_t stream);
+// LM head from K-split partials: split-order sum + per-tile argmax (ties ->
+// lowest id) into st.amax_val / amax_idx (what the GV_ARGMAX epilogue writes).
+int launch_lm_argmax(const DecodeState& st, const Partials& p, cudaStream_t stream);
 int launch_finalize(const DecodeState& st, cudaStream_t stream);
 
 }  // namespace dm

@@ -275,6 +275,7 @@ struct WhisperEngine {
     // K-split partial sums of the linear projections (consumer-reduced)
     float *p_qkv = nullptr, *p_o = nullptr, *p_xq = nullptr, *p_xo = nullptr, *p_fc2 = nullptr;
     float* p_fc1 = nullptr;        // fc1 K-split partials when fc1 is split (fc1_split)
+    float* p_lm = nullptr;         // LM-head K-split partials [splits][kRows][vocab]
     float* xpart = nullptr;        // cross-attention split results [kRows][H][8][68]
     int* xcnt = nullptr;           // [kRows * kMaxHeads] split arrival counters
   };
@@ -298,6 +299,7 @@ struct WhisperEngine {
   // steps of <= gv_fuse_rows rows (at most 16) skip the split-merge and GELU
   // kernels: the cross-o and fc2 GEMVs build their operands from the raw
   // results (DM_GV_FUSE_ROWS: experiments; 0 disables)
+  bool lm_argmax_epi = std::getenv("DM_LM_ARGMAX_EPI") != nullptr;   // (A/B: last-CTA merge)
   int gv_fuse_rows = std::min(16, std::getenv("DM_GV_FUSE_ROWS") ? std::atoi(std::getenv("DM_GV_FUSE_ROWS"))
                                                                  : kGvFuseRows);
   int encode_kernels() const { return 2 + 1 + 2 + 7 * L + 1 + 1; }
@@ -456,7 +458,13 @@ static int engine_init(WhisperEngine* e) {
                                         : gemv_plan(e->F, d, GV_GELU_HILO));          // fc1
       e->plans.push_back(gemv_plan(d, e->F, GV_PARTIAL, kMaxHeads));      // fc2
     }
-    e->plans.push_back(gemv_plan(c.vocab, d, GV_ARGMAX));      // LM head
+    {
+      // LM head: the K split of the last-CTA ARGMAX plan (<= 8 k-blocks per
+      // CTA); partials + lm_argmax_kernel unless DM_LM_ARGMAX_EPI=1
+      GemvArgs lm = gemv_plan(c.vocab, d, GV_ARGMAX);
+      if (!e->lm_argmax_epi) lm.epi = GV_PARTIAL;
+      e->plans.push_back(lm);
+    }
     if (e->alloc_t(&gr.p_qkv, gemv_part_floats(3 * d, d, GV_PARTIAL, 5))) return 2;
     if (e->alloc_t(&gr.p_o, gemv_part_floats(d, d, GV_PARTIAL, kMaxHeads))) return 2;
     if (e->alloc_t(&gr.p_xq, gemv_part_floats(d, d, GV_PARTIAL, kAttnSplits))) return 2;
@@ -470,6 +478,8 @@ static int engine_init(WhisperEngine* e) {
       part = std::max(part, gemv_part_floats(e->F, d, GV_PARTIAL, e->fc1_splits) / kRows * 128 /
                                 ceil_div(e->F, 128) * ceil_div(e->F, 128));
     if (e->alloc_t(&gs.part, part)) return 2;
+    if (!e->lm_argmax_epi &&
+        e->alloc_t(&gr.p_lm, size_t(e->plans.back().splits) * kRows * c.vocab)) return 2;
     if (e->alloc_t(&gs.counters, 4096)) return 2;
     if (e->alloc_t(&gr.xpart, size_t(kRows) * e->H * kXSplits * 68)) return 2;
     if (e->alloc_t(&gr.xcnt, size_t(kRows) * kMaxHeads)) return 2;
@@ -731,7 +741,12 @@ static int record_step(WhisperEngine* e, WhisperEngine::Group& grp, cudaStream_t
   }
   const int x = e->after_dec();
   DM_STEP(ln(2, x + 2, prev));                                   // final LayerNorm
-  DM_STEP(gv(e->Ld * 6, nullptr, nullptr, nullptr, nullptr));    // tied LM head + tile argmax
+  if (e->lm_argmax_epi) {
+    DM_STEP(gv(e->Ld * 6, nullptr, nullptr, nullptr, nullptr));  // tied LM head + tile argmax
+  } else {
+    DM_STEP(gv(e->Ld * 6, grp.p_lm, nullptr, nullptr, nullptr));  // tied LM head partials
+    DM_STEP(launch_lm_argmax(st, Partials{grp.p_lm, e->plans[e->Ld * 6].splits, e->cfg.vocab, nullptr}, s));
+  }
   DM_STEP(launch_finalize(st, s));
   return 0;
 }
@@ -1101,7 +1116,10 @@ int dm_whisper_time_kernel(void* handle, int which, int layer, int iters, float*
         return launch_self_attn(pst, layer,
                                 Partials{grp.p_qkv, e->plans[pi].splits, 3 * d, e->W(b0 + 3)},
                                 0.125f, cs);
-      case 2: return gv(e->Ld * 6, nullptr, nullptr, nullptr, nullptr, cs);
+      case 2:        // LM head (+ its argmax kernel, as in the step)
+        if (e->lm_argmax_epi) return gv(e->Ld * 6, nullptr, nullptr, nullptr, nullptr, cs);
+        if (int rc = gv(e->Ld * 6, grp.p_lm, nullptr, nullptr, nullptr, cs)) return rc;
+        return launch_lm_argmax(pst, Partials{grp.p_lm, e->plans[e->Ld * 6].splits, e->cfg.vocab, nullptr}, cs);
       case 3: {
         LnArgs la{};
         la.mode = 2; la.g = e->W(b0 + 6); la.b = e->W(b0 + 7);

@@ -39,7 +39,8 @@ def names_for(rows):
             kinds.append("gelu")
         kinds.append("fc2")
         names += [f"L{l}.{k}" for k in kinds]
-    return names + ["ln_f", "lm_head", "finalize"]
+    lm = ["lm_head"] if os.environ.get("DM_LM_ARGMAX_EPI") else ["lm_head", "lm_argmax"]
+    return names + ["ln_f"] + lm + ["finalize"]
 lib = eng.lib
 def dbg(which, buf=None, n=0):
     ptr = buf.ctypes.data_as(C.c_void_p) if buf is not None else None
