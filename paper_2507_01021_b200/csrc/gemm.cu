@@ -905,13 +905,11 @@ int launch_gemm(const GemmArgs& g, cudaStream_t stream) {
   // wide N, or long K (fc2, the stride-2 conv): 128 x 256 tiles cut the per-SM
   // operand stream (bytes per FLOP (128 + BN) / (128 BN)); with a long K the
   // epilogue's global traffic overlaps the next tile's mainloop
-  // (experiments: DM_GEMM_PAIR_MIN_K moves the CTA-pair threshold,
-  // DM_GEMM_RESID128=1 sends wide residual GEMMs to the 128-wide residual path)
+  // (experiments: DM_GEMM_PAIR_MIN_K moves the CTA-pair threshold)
   static const int pair_min_k =
       std::getenv("DM_GEMM_PAIR_MIN_K") ? std::atoi(std::getenv("DM_GEMM_PAIR_MIN_K")) : 1024;
-  static const bool resid128 = std::getenv("DM_GEMM_RESID128") != nullptr;
   const bool resid_path = g.epi.mode == EPI_RESID_F32 && g.a_mode == A_FLAT && g.Bt == 1;
-  if (g.N % 256 == 0 && (g.N >= 1024 || g.K >= 1536) && !(resid128 && resid_path)) {
+  if (g.N % 256 == 0 && (g.N >= 1024 || g.K >= 1536)) {
     // K >= 1024 (large-v3's projections, fc2, the stride-2 conv): the
     // mainloop's L2 -> SMEM operand stream bounds the 1-SM kernel, so 256 x 256
     // tiles run on CTA pairs (cta_group::2; measured at large-v3, 12
