@@ -611,11 +611,12 @@ def measure_latency(eng, dims, args, rs) -> dict | None:
              for i in range(args.latency_users)}
     policy = rs.BatchingPolicy(kind="continuous", min_batch=32, max_batch=64,
                                starvation_flush_ms=args.starvation_ms)
-    mux = lb.run_multiplexed([eng], users, policy, rs)
+    mux = lb.run_multiplexed([eng], users, policy, rs, eager_start=bool(args.latency_eager))
     seq = lb.run_sequential_reference([eng], users["u000"], 64, MODEL)
     return {"users": args.latency_users, "session_s": args.latency_session_s,
             "policy": {"kind": "continuous", "min_batch": 32, "max_batch": 64,
                        "starvation_flush_ms": args.starvation_ms},
+            "eager_start": bool(args.latency_eager),
             "multiplexed": mux, "sequential_single_user": seq,
             "p95_below_sequential": mux["p95_ms"] < seq["p95_ms"],
             "percentile": "nearest rank (report.py:17-26)"}
@@ -646,6 +647,9 @@ def main():
     ap.add_argument("--latency-users", type=int, default=64,
                     help="live users for the latency block (0: skip)")
     ap.add_argument("--latency-session-s", type=float, default=30.0)
+    ap.add_argument("--latency-eager", type=int, default=1,
+                    help="1 (GpuConsumer default): an idle consumer starts on whatever is queued; "
+                         "0: it waits for the policy's batch (min_batch / starvation flush)")
     ap.add_argument("--starvation-ms", type=float, default=100.0)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--share-devices", action="store_true",

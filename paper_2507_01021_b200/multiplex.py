@@ -51,9 +51,16 @@ class GpuConsumer(threading.Thread):
                  result_router: Callable[[TranscriptResult], None], *,
                  cap_fn: Callable[[float], int] = default_token_cap,
                  silence_is_empty: bool = True, poll_interval_ms: float = 10.0,
-                 clock: Callable[[], float] = monotonic_ms, name: str = "gpu-consumer"):
+                 clock: Callable[[], float] = monotonic_ms, name: str = "gpu-consumer",
+                 eager_start: bool = True):
         super().__init__(name=name, daemon=True)
         self.queue, self.policy, self.engine = queue, policy, engine
+        # eager_start: an idle engine takes whatever is queued (the policy with
+        # min_batch 1) instead of waiting for the policy's batch to form; a
+        # running engine admits at every step batch either way (_refill)
+        self.eager_start = eager_start
+        self._idle_policy = (dataclasses.replace(policy, kind=CONTINUOUS, min_batch=1)
+                             if eager_start else policy)
         self.result_router, self.cap_fn = result_router, cap_fn
         self.silence_is_empty = silence_is_empty
         self.poll_interval_ms, self.clock = poll_interval_ms, clock
@@ -122,7 +129,7 @@ class GpuConsumer(threading.Thread):
             self.queue.wait_for_work(self.poll_interval_ms / 1000.0)
             if self._stop_requested.is_set() or self.queue.closed:
                 break
-            jobs = self._jobs_for(self.queue.try_form_batch(self.policy, self.clock()))
+            jobs = self._jobs_for(self.queue.try_form_batch(self._idle_policy, self.clock()))
             if jobs:
                 self._serve(jobs)
         while True:   # drain: every accepted segment is routed exactly once

@@ -65,14 +65,15 @@ def user_session(seed, uid, session_s):
     return segs
 
 
-def run_multiplexed(engines, users, policy, rs):
+def run_multiplexed(engines, users, policy, rs, eager_start=True):
     lock = threading.Lock()
     delivered = {}
 
     def router(r):
         with lock:
             delivered[r.segment_id] = (time.monotonic(), r)
-    mux = Multiplexer(engines, policy, rs.SegmentQueue(), router, poll_interval_ms=2.0)
+    mux = Multiplexer(engines, policy, rs.SegmentQueue(), router, poll_interval_ms=2.0,
+                      eager_start=eager_start)
     mux.start()
     t0 = time.monotonic() + 0.5
     endpoints = {}

@@ -144,3 +144,24 @@ def test_refill_policy_keeps_reference_policy_fields():
         q.enqueue_segment(seg(f"p{i}", 2.0), 0.0)
     jobs = c._refill(4)         # continuous: no target_audio cut at 3 s
     assert len(jobs) == 4
+
+
+@pytest.mark.parametrize("eager", [True, False])
+def test_idle_consumer_eager_start(eager):
+    """An idle consumer with eager_start (the default) serves a lone segment at
+    once; with eager_start=False it honours the policy (min_batch 8, long
+    starvation flush) and keeps waiting."""
+    q = rs.SegmentQueue()
+    routed = []
+    pol = rs.BatchingPolicy(kind="continuous", max_batch=8, min_batch=8, starvation_flush_ms=60000.0)
+    c = GpuConsumer(q, pol, FakeEngine(), routed.append, cap_fn=lambda d: 1, poll_interval_ms=1.0,
+                    eager_start=eager)
+    c.start()
+    q.enqueue_segment(seg("lone", 0.5), time.monotonic() * 1000.0)
+    t0 = time.time()
+    while not routed and time.time() - t0 < 1.0:
+        time.sleep(0.01)
+    got = [r.segment_id for r in routed]
+    c.shutdown()                    # the drain serves it in any case
+    assert got == (["lone"] if eager else [])
+    assert [r.segment_id for r in routed] == ["lone"]
