@@ -461,6 +461,7 @@ def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
     peaks = _peaks()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     tc = float(peaks.get("bf16_tflops", 2250.0))
+    tc_sus = float(peaks.get("bf16_tflops_sustained", tc))
     dev = pcm_dev.device
     E = eng.max_encode_batch
     sub = [(uid, x, int(o)) for (uid, x), o in zip(segs[:E], offs[:E])]
@@ -540,7 +541,12 @@ def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
         "encoder": {"bound": "tensor", "achieved": E * enc_flop / (en_ms / 1e3) / 1e12, "peak": tc,
                     "unit": "TFLOP/s", "frac": E * enc_flop / (en_ms / 1e3) / 1e12 / tc,
                     "ms": en_ms, "flop": E * enc_flop, "segments": E,
-                    "note": "whole dm_whisper_encode (log-mel + conv stem + layers + LN + cross-KV)"},
+                    "peak_sustained": tc_sus,
+                    "frac_vs_sustained": E * enc_flop / (en_ms / 1e3) / 1e12 / tc_sus,
+                    "note": "whole dm_whisper_encode (log-mel + conv stem + layers + LN + cross-KV); "
+                            "frac vs the burst bf16 peak (one 8192^3 matmul), frac_vs_sustained vs "
+                            "MEASURED_PEAKS' sustained figure (back-to-back matmuls: the power-capped "
+                            "clocks a ~37 ms multi-kernel encode runs at)"},
         "decode_step": {"bound": "hbm", "achieved": st_bytes / (st_ms / 1e3) / 1e9, "peak": hbm,
                         "unit": "GB/s", "frac": st_bytes / (st_ms / 1e3) / 1e9 / hbm,
                         "ms": st_ms, "bytes": st_bytes, "rows": S,
