@@ -97,6 +97,22 @@ ctc_conv0_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ of
   const int b = blockIdx.y, f0 = blockIdx.x * kF0;
   const int n = lens[b];
   const int T0 = n >= 10 ? (n - 10) / 5 + 1 : 0;
+  if (f0 >= T0) {
+    // frames past this segment's end (the batch is padded to its longest
+    // segment): no statistics, zero operand rows -- no convolution work
+    if (PASS == 0) {
+      for (int c = threadIdx.x; c < kC; c += blockDim.x) {
+        gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c) * 2] = 0.f;
+        gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c) * 2 + 1] = 0.f;
+      }
+    } else {
+      const int nf = min(kF0, R0 - f0);
+      uint32_t* o32 = reinterpret_cast<uint32_t*>(out + (size_t(b) * R0 + f0) * kC);
+      for (int i = threadIdx.x; i < nf * kC / 2; i += blockDim.x) o32[i] = 0u;
+    }
+    return;
+  }
+  const int nvalid = min(kF0, T0 - f0);        // frames of this CTA inside the segment
   float mean, rstd;
   norm_stats(npart, b, n, mean, rstd);
   const int16_t* x = pcm + offs[b];
@@ -122,14 +138,17 @@ ctc_conv0_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ of
     }
     for (int f = 0; f < kF0; ++f) {
       const int t = f0 + f;
+      if (f >= nvalid) {                       // past the segment: zero rows (pass 1)
+        if (PASS == 1 && t < R0) out[(size_t(b) * R0 + t) * kC + c] = 0;
+        continue;
+      }
       float y = 0.f;
 #pragma unroll
       for (int k = 0; k < 10; ++k) y = fmaf(w[k], xs[f * 5 + k], y);
       if (PASS == 0) {
-        if (t < T0) { s += y; q += y * y; }
+        s += y; q += y * y;
       } else if (t < R0) {
-        const float v = t < T0 ? gelu_erf((y - m) * r * gg + gb) : 0.f;
-        out[(size_t(b) * R0 + t) * kC + c] = f32_to_bf16(v);
+        out[(size_t(b) * R0 + t) * kC + c] = f32_to_bf16(gelu_erf((y - m) * r * gg + gb));
       }
     }
     if (PASS == 0) {
