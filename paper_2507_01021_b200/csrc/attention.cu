@@ -346,10 +346,12 @@ template <int V4>  // float4 per lane
 __global__ void __launch_bounds__(256)
 layernorm_bf16_kernel(const float* __restrict__ x, const uint16_t* __restrict__ g,
                       const uint16_t* __restrict__ bta, uint16_t* __restrict__ y, int rows,
-                      int d, float* __restrict__ y32) {
+                      int d, float* __restrict__ y32, const int32_t* __restrict__ seg_len,
+                      int seg_rows) {
   const int row = blockIdx.x * 8 + threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
   if (row >= rows) return;
+  if (seg_len && row % seg_rows >= seg_len[row / seg_rows]) return;   // padding row: skipped
   const float4* xr = reinterpret_cast<const float4*>(x + size_t(row) * d);
   const int n4 = d / 4;
   float4 v[V4];
@@ -391,13 +393,14 @@ layernorm_bf16_kernel(const float* __restrict__ x, const uint16_t* __restrict__ 
 }
 
 int launch_layernorm_bf16(const float* x, const uint16_t* g, const uint16_t* b, uint16_t* y,
-                          int rows, int d, cudaStream_t stream, float* y32) {
+                          int rows, int d, cudaStream_t stream, float* y32,
+                          const int32_t* seg_len, int seg_rows) {
   DM_REQUIRE(d % 128 == 0 && d <= 1280, "layernorm d must be a multiple of 128, <= 1280");
   dim3 grid(ceil_div(rows, 8));
   const int v4 = d / 128;
   switch (v4) {
 #define DM_LN_CASE(n) \
-  case n: layernorm_bf16_kernel<n><<<grid, 256, 0, stream>>>(x, g, b, y, rows, d, y32); break;
+  case n: layernorm_bf16_kernel<n><<<grid, 256, 0, stream>>>(x, g, b, y, rows, d, y32, seg_len, seg_rows); break;
     DM_LN_CASE(1) DM_LN_CASE(2) DM_LN_CASE(3) DM_LN_CASE(4) DM_LN_CASE(5)
     DM_LN_CASE(6) DM_LN_CASE(7) DM_LN_CASE(8) DM_LN_CASE(9) DM_LN_CASE(10)
 #undef DM_LN_CASE

@@ -28,7 +28,8 @@
 namespace dm {
 
 int launch_layernorm_bf16(const float*, const uint16_t*, const uint16_t*, uint16_t*, int, int,
-                          cudaStream_t, float* y32);
+                          cudaStream_t, float* y32, const int32_t* seg_len = nullptr,
+                          int seg_rows = 0);
 int launch_attention(const uint16_t*, const uint16_t*, const uint16_t*, int, int, int, int,
                      uint16_t*, int, cudaStream_t, const int32_t* seg_len);
 int make_tmap_2d(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer,
@@ -246,6 +247,10 @@ struct CtcEngine {
   int32_t* tokens = nullptr;
   int32_t* counts = nullptr;
   int64_t* host_stage = nullptr;  // pinned
+  // live GEMM row-block lists of the current batch (GemmArgs::mblocks)
+  static constexpr size_t kMbCap = 1 << 18;
+  int32_t* mb_host = nullptr;     // pinned
+  int32_t* mb_dev = nullptr;
   std::vector<void*> allocs;
   int last_n = 0, last_R6 = 0;
   std::vector<int> last_tlen;
@@ -262,6 +267,7 @@ struct CtcEngine {
   ~CtcEngine() {
     for (void* p : allocs) cudaFree(p);
     if (host_stage) cudaFreeHost(host_stage);
+    if (mb_host) cudaFreeHost(mb_host);
   }
 };
 
@@ -307,6 +313,8 @@ static int ctc_init(CtcEngine* e) {
   if (e->alloc_t(&e->tokens, rows)) return 2;
   if (e->alloc_t(&e->counts, B)) return 2;
   DM_CHECK_CUDA(cudaMallocHost(&e->host_stage, sizeof(int64_t) * 4 * B));
+  DM_CHECK_CUDA(cudaMallocHost(&e->mb_host, sizeof(int32_t) * CtcEngine::kMbCap));
+  if (e->alloc_t(&e->mb_dev, CtcEngine::kMbCap)) return 2;
   DM_CHECK_CUDA(cudaDeviceSynchronize());
   return 0;
 }
@@ -338,6 +346,63 @@ static int ctc_forward(CtcEngine* e, const int16_t* pcm, int n, const std::vecto
   int32_t* hs = reinterpret_cast<int32_t*>(e->host_stage);
   for (int b = 0; b < n; ++b) hs[b] = tlen[b];
   DM_CHECK_CUDA(cudaMemcpyAsync(e->tlen_dev, hs, sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
+  // Live row blocks: the batch is padded to its longest segment, and a row
+  // block wholly past every segment's end in it is never computed (its rows
+  // feed only other padding rows: the stride-2 convs read rows < 2T + k - 1,
+  // the projection zeroes rows >= T, attention masks keys >= T, the collapse
+  // reads frames < T). Per conv layer i: rows t < T_i[b] of item b; the flat
+  // transformer rows b * R6 + t are live for t < T_6[b].
+  std::vector<std::vector<int>> Ti(7, std::vector<int>(n));
+  for (int b = 0; b < n; ++b) {
+    int T = lens[b];
+    for (int i = 0; i < 7; ++i) Ti[i][b] = T = conv_out(T, ks[i], i == 0 ? 5 : 2);
+  }
+  size_t mb_used = 0;
+  auto add_list = [&](GemmArgs& g, int k, const std::vector<int>& live_mb) -> int {
+    DM_REQUIRE(mb_used + live_mb.size() <= CtcEngine::kMbCap, "CTC live-block list overflow");
+    std::copy(live_mb.begin(), live_mb.end(), e->mb_host + mb_used);
+    g.mblocks[k] = e->mb_dev + mb_used;
+    g.mblock_count[k] = int(live_mb.size());
+    mb_used += live_mb.size();
+    return 0;
+  };
+  // per-item blocks (conv modes): mb = b * MT + mt, mt * BM < valid[b]
+  auto per_item = [&](int T, int BM, const std::vector<int>& valid) {
+    std::vector<int> v;
+    const int MT = ceil_div(T, BM);
+    for (int b = 0; b < n; ++b)
+      for (int mt = 0; mt < MT && mt * BM < valid[b]; ++mt) v.push_back(b * MT + mt);
+    return v;
+  };
+  // flat rows b * R6 + t: block mt live if any of its rows has t < T6[b]
+  auto flat_rows = [&](int BM) {
+    std::vector<int> v;
+    const int M = n * R6, MT = ceil_div(M, BM);
+    for (int mt = 0; mt < MT; ++mt) {
+      const int r0 = mt * BM, r1 = std::min(M, r0 + BM) - 1;
+      bool live = r0 % R6 < Ti[6][r0 / R6];
+      for (int b = r0 / R6 + 1; !live && b <= r1 / R6; ++b) live = Ti[6][b] > 0;
+      if (live) v.push_back(mt);
+    }
+    return v;
+  };
+  GemmArgs conv_g[7], flat_g, pos_g;
+  for (int i = 1; i < 7; ++i) {
+    if (add_list(conv_g[i], 0, per_item(R[i], 128, Ti[i]))) return 2;
+    if (add_list(conv_g[i], 1, per_item(R[i], 256, Ti[i]))) return 2;
+  }
+  if (add_list(flat_g, 0, flat_rows(128))) return 2;
+  if (add_list(flat_g, 1, flat_rows(256))) return 2;
+  if (add_list(pos_g, 0, per_item(R6, 128, Ti[6]))) return 2;
+  if (add_list(pos_g, 1, per_item(R6, 256, Ti[6]))) return 2;
+  DM_CHECK_CUDA(cudaMemcpyAsync(e->mb_dev, e->mb_host, sizeof(int32_t) * mb_used,
+                                cudaMemcpyHostToDevice, s));
+  auto live = [](GemmArgs& g, const GemmArgs& lists) {
+    for (int k = 0; k < 2; ++k) {
+      g.mblocks[k] = lists.mblocks[k];
+      g.mblock_count[k] = lists.mblock_count[k];
+    }
+  };
   // input normalisation stats, conv0 stats, GroupNorm stats, conv0 apply
   ctc_norm_partials<<<dim3(kNormBlocks, n), 256, 0, s>>>(pcm, e->offs_dev, e->lens_dev, e->npart);
   DM_CHECK_LAUNCH();
@@ -357,6 +422,7 @@ static int ctc_forward(CtcEngine* e, const int16_t* pcm, int n, const std::vecto
   uint16_t* dst = e->act_b;
   for (int i = 1; i < 7; ++i) {
     GemmArgs g;
+    live(g, conv_g[i]);
     g.A = src; g.a_mode = A_CONV_S2; g.C = kC; g.K = ks[i] * kC; g.T = R[i]; g.Bt = n;
     g.a_rows = R[i - 1]; g.W = e->W(i); g.N = kC;
     if (i < 6) {
@@ -369,12 +435,14 @@ static int ctc_forward(CtcEngine* e, const int16_t* pcm, int n, const std::vecto
   }
   const int M = n * R6;
   // feature projection: LN(512) -> Linear(512 -> 768); fp32 h + zero-padded grouped copy
-  if (int rc = launch_layernorm_bf16(e->f32buf, e->W(9), e->W(10), e->lnb, M, kC, s, nullptr))
+  if (int rc = launch_layernorm_bf16(e->f32buf, e->W(9), e->W(10), e->lnb, M, kC, s, nullptr,
+                                     e->tlen_dev, R6))
     return rc;
   DM_CHECK_CUDA(cudaMemsetAsync(e->grp, 0, size_t(n) * (R6 + 128) * 1024 * 2, s));
   float* x = e->f32buf;                            // hidden states [M, 768] fp32
   {
     GemmArgs g;
+    live(g, flat_g);
     g.A = e->lnb; g.a_mode = A_FLAT; g.K = kC; g.T = M; g.Bt = 1; g.lda = kC;
     g.W = e->W(11); g.N = 768;
     g.epi.mode = EPI_W2V_PROJ; g.epi.bias = e->W(12); g.epi.out = x; g.epi.ldo = 768;
@@ -385,15 +453,18 @@ static int ctc_forward(CtcEngine* e, const int16_t* pcm, int n, const std::vecto
   // positional conv (grouped, k128) + GELU added into x
   {
     GemmArgs g;
+    live(g, pos_g);
     g.A = e->grp; g.a_mode = A_CONV_S1; g.grouped = 1; g.C = 1024; g.K = 128 * 64; g.T = R6;
     g.Bt = n; g.a_rows = R6 + 128; g.W = e->posw; g.N = 1024;
     g.epi.mode = EPI_W2V_POS; g.epi.bias = nullptr; g.epi.pos = e->W(14); g.epi.out = x;
     g.epi.ldo = 768; g.epi.grp_cpg = 48;
     if (int rc = launch_gemm(g, s)) return rc;
   }
-  if (int rc = launch_layernorm_bf16(x, e->W(15), e->W(16), e->lnb, M, 768, s, x)) return rc;
+  if (int rc = launch_layernorm_bf16(x, e->W(15), e->W(16), e->lnb, M, 768, s, x, e->tlen_dev, R6))
+    return rc;
   auto flat = [&](const uint16_t* A, int K, const uint16_t* Wt, int N) {
     GemmArgs g;
+    live(g, flat_g);
     g.A = A; g.a_mode = A_FLAT; g.K = K; g.T = M; g.Bt = 1; g.lda = K; g.W = Wt; g.N = N;
     return g;
   };
@@ -413,7 +484,7 @@ static int ctc_forward(CtcEngine* e, const int16_t* pcm, int n, const std::vecto
       if (int rc = launch_gemm(g, s)) return rc;
     }
     if (int rc = launch_layernorm_bf16(x, e->W(e->layer(l, 4)), e->W(e->layer(l, 5)), e->lnb, M,
-                                       768, s, x))
+                                       768, s, x, e->tlen_dev, R6))
       return rc;
     {
       GemmArgs g = flat(e->lnb, 768, e->W(e->layer(l, 6)), 3072);
@@ -427,7 +498,7 @@ static int ctc_forward(CtcEngine* e, const int16_t* pcm, int n, const std::vecto
       if (int rc = launch_gemm(g, s)) return rc;
     }
     if (int rc = launch_layernorm_bf16(x, e->W(e->layer(l, 10)), e->W(e->layer(l, 11)), e->lnb,
-                                       M, 768, s, x))
+                                       M, 768, s, x, e->tlen_dev, R6))
       return rc;
   }
   {

@@ -43,7 +43,8 @@ int launch_logmel(const int16_t*, const int64_t*, const int32_t*, int, int,
                   const LogmelTables*, float*, uint16_t*, uint32_t*, cudaStream_t,
                   int frames = 3000);
 int launch_layernorm_bf16(const float*, const uint16_t*, const uint16_t*, uint16_t*, int, int,
-                          cudaStream_t, float* y32 = nullptr);
+                          cudaStream_t, float* y32 = nullptr, const int32_t* seg_len = nullptr,
+                          int seg_rows = 0);
 int launch_attention(const uint16_t*, const uint16_t*, const uint16_t*, int, int, int, int,
                      uint16_t*, int, cudaStream_t, const int32_t* seg_len = nullptr);
 

@@ -283,7 +283,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
       int it = 0;
       for (int tile = blockIdx.x; tile < geo.tiles; tile += gridDim.x, ++it) {
         const int nt = tile % geo.NT;
-        const int mb = tile / geo.NT;
+        const int mb = g.mblocks[0] ? g.mblocks[0][tile / geo.NT] : tile / geo.NT;
         const int b = mb / geo.MT, mt = mb % geo.MT;
         if (RT) {
           // this tile's residual, once the epilogue holds the previous one in registers
@@ -352,7 +352,7 @@ gemm_tcgen05_kernel(const __grid_constant__ CUtensorMap tmap_a,
     int it = 0;
     for (int tile = blockIdx.x; tile < geo.tiles; tile += gridDim.x, ++it) {
       const int nt = tile % geo.NT;
-      const int mb = tile / geo.NT;
+      const int mb = g.mblocks[0] ? g.mblocks[0][tile / geo.NT] : tile / geo.NT;
       const int b = mb / geo.MT, mt = mb % geo.MT;
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
@@ -571,7 +571,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a,
       uint32_t phase = 0;
       for (int tile = pair; tile < geo.tiles; tile += npairs) {
         const int nt = tile % geo.NT;
-        const int mb = tile / geo.NT;
+        const int mb = g.mblocks[1] ? g.mblocks[1][tile / geo.NT] : tile / geo.NT;
         const int b = mb / geo.MT, mt = mb % geo.MT;
         const int row0 = mt * (2 * kBM) + int(rank) * kBM;
         for (int kb = 0; kb < geo.KB; ++kb) {
@@ -637,7 +637,7 @@ gemm_pair_kernel(const __grid_constant__ CUtensorMap tmap_a,
     int it = 0;
     for (int tile = pair; tile < geo.tiles; tile += npairs, ++it) {
       const int nt = tile % geo.NT;
-      const int mb = tile / geo.NT;
+      const int mb = g.mblocks[1] ? g.mblocks[1][tile / geo.NT] : tile / geo.NT;
       const int b = mb / geo.MT, mt = mb % geo.MT;
       const int as = it & 1;
       const uint32_t aphase = (it >> 1) & 1;
@@ -762,7 +762,8 @@ static int launch_bn_mode(const GemmArgs& g, cudaStream_t stream) {
   TileGeom geo;
   geo.MT = ceil_div(g.T, kBM);
   geo.NT = ceil_div(g.N, BN);
-  geo.tiles = g.Bt * geo.MT * geo.NT;
+  geo.tiles = (g.mblocks[0] ? g.mblock_count[0] : g.Bt * geo.MT) * geo.NT;
+  if (geo.tiles == 0) return 0;
   geo.KB = ceil_div(g.K, kBK);
   geo.cpb = g.grouped ? 1 : (g.C > 0 ? g.C / kBK : 1);
   const int smem = GemmSmem<BN, STAGES, MODE>::kBytes;
@@ -805,7 +806,8 @@ static int launch_pair_mode(const GemmArgs& g, cudaStream_t stream) {
   TileGeom geo;
   geo.MT = ceil_div(g.T, 2 * kBM);
   geo.NT = ceil_div(g.N, BN);
-  geo.tiles = g.Bt * geo.MT * geo.NT;
+  geo.tiles = (g.mblocks[1] ? g.mblock_count[1] : g.Bt * geo.MT) * geo.NT;
+  if (geo.tiles == 0) return 0;
   geo.KB = ceil_div(g.K, kBK);
   geo.cpb = g.C > 0 ? g.C / kBK : 1;
   const int smem = PairSmem<STAGES>::kBytes;

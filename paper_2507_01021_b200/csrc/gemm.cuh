@@ -71,6 +71,12 @@ struct GemmArgs {
   const uint16_t* W = nullptr;   // [N, K] bf16 (K contiguous)
   int N = 0;
   int max_ctas = 0;       // persistent grid size cap (0: one CTA per SM); SMs left to other streams
+  // Live M blocks (device lists of mb = b * MT + mt): only these row blocks
+  // are computed (variable-length batches skip blocks wholly past every
+  // segment's end). [0]: 128-row blocks (1-SM kernel), [1]: 256-row blocks
+  // (CTA pairs); null: every block.
+  const int32_t* mblocks[2] = {nullptr, nullptr};
+  int mblock_count[2] = {0, 0};
   Epilogue epi;
 };
 
