@@ -123,39 +123,64 @@ ctc_conv0_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ of
   }
   for (int i = threadIdx.x; i < kC * 10; i += blockDim.x) ws[i] = bf16_to_f32(w0[i]);
   __syncthreads();
-#pragma unroll 1
-  for (int half = 0; half < 2; ++half) {
-    const int c = threadIdx.x + half * 256;
-    float w[10];
+  // both of this thread's channels (c, c + 256) per frame, two frames per
+  // step from one 15-sample window: each shared-memory sample read feeds 4
+  // convolution taps (same per-output tap order and per-channel frame order)
+  const int c0 = threadIdx.x, c1 = threadIdx.x + 256;
+  float wa[10], wb[10];
 #pragma unroll
-    for (int k = 0; k < 10; ++k) w[k] = ws[c * 10 + k];
-    float s = 0.f, q = 0.f;
-    float m = 0.f, r = 0.f, gg = 0.f, gb = 0.f;
-    if (PASS == 1) {
-      m = gstat[(b * kC + c) * 2];
-      r = gstat[(b * kC + c) * 2 + 1];
-      gg = bf16_to_f32(gn_g[c]);
-      gb = bf16_to_f32(gn_b[c]);
-    }
-    for (int f = 0; f < kF0; ++f) {
-      const int t = f0 + f;
-      if (f >= nvalid) {                       // past the segment: zero rows (pass 1)
-        if (PASS == 1 && t < R0) out[(size_t(b) * R0 + t) * kC + c] = 0;
+  for (int k = 0; k < 10; ++k) {
+    wa[k] = ws[c0 * 10 + k];
+    wb[k] = ws[c1 * 10 + k];
+  }
+  float sa = 0.f, qa = 0.f, sb = 0.f, qb = 0.f;
+  float ma = 0.f, ra = 0.f, ga = 0.f, ba = 0.f, mb = 0.f, rb = 0.f, gb2 = 0.f, bb = 0.f;
+  if (PASS == 1) {
+    ma = gstat[(b * kC + c0) * 2];
+    ra = gstat[(b * kC + c0) * 2 + 1];
+    ga = bf16_to_f32(gn_g[c0]);
+    ba = bf16_to_f32(gn_b[c0]);
+    mb = gstat[(b * kC + c1) * 2];
+    rb = gstat[(b * kC + c1) * 2 + 1];
+    gb2 = bf16_to_f32(gn_g[c1]);
+    bb = bf16_to_f32(gn_b[c1]);
+  }
+  static_assert(kF0 % 2 == 0 && (kF0 - 2) * 5 + 14 < kF0 * 5 + 5, "conv0 window");
+#pragma unroll 1
+  for (int f = 0; f < kF0; f += 2) {
+    float xw[15];
+#pragma unroll
+    for (int k = 0; k < 15; ++k) xw[k] = xs[f * 5 + k];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int ff = f + h, t = f0 + ff;
+      if (ff >= nvalid) {                      // past the segment: zero rows (pass 1)
+        if (PASS == 1 && t < R0) {
+          out[(size_t(b) * R0 + t) * kC + c0] = 0;
+          out[(size_t(b) * R0 + t) * kC + c1] = 0;
+        }
         continue;
       }
-      float y = 0.f;
+      float ya = 0.f, yb = 0.f;
 #pragma unroll
-      for (int k = 0; k < 10; ++k) y = fmaf(w[k], xs[f * 5 + k], y);
+      for (int k = 0; k < 10; ++k) {
+        ya = fmaf(wa[k], xw[5 * h + k], ya);
+        yb = fmaf(wb[k], xw[5 * h + k], yb);
+      }
       if (PASS == 0) {
-        s += y; q += y * y;
+        sa += ya; qa += ya * ya;
+        sb += yb; qb += yb * yb;
       } else if (t < R0) {
-        out[(size_t(b) * R0 + t) * kC + c] = f32_to_bf16(gelu_erf((y - m) * r * gg + gb));
+        out[(size_t(b) * R0 + t) * kC + c0] = f32_to_bf16(gelu_erf((ya - ma) * ra * ga + ba));
+        out[(size_t(b) * R0 + t) * kC + c1] = f32_to_bf16(gelu_erf((yb - mb) * rb * gb2 + bb));
       }
     }
-    if (PASS == 0) {
-      gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c) * 2] = s;
-      gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c) * 2 + 1] = q;
-    }
+  }
+  if (PASS == 0) {
+    gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c0) * 2] = sa;
+    gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c0) * 2 + 1] = qa;
+    gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c1) * 2] = sb;
+    gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c1) * 2 + 1] = qb;
   }
 }
 
