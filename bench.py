@@ -519,14 +519,17 @@ def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
     eng.set_active(allslots)
     eng.step(8)                       # past the prompt: positions 7..
     torch.cuda.synchronize(dev)
-    pos = 8
-    st_ms = ev_ms(lambda: eng.step(1), reps=9)
+    # 8 back-to-back step graphs per timed call (as in the bench step; one
+    # step streams ~17 GB, far more than L2), median of 5 calls: positions
+    # 8..47, mean self-KV length ~28
+    st_ms = ev_ms(lambda: eng.step(8), reps=5) / 8
+    pos = 28
     eng.release(allslots)
     eng.set_active([])
     torch.cuda.synchronize(dev)
     w_bytes = 2 * (Ld * (4 * d * d + 2 * d * d + 2 * d * F) + dims.vocab * d)
     x_bytes = S * Ld * 2 * 1500 * d * 2
-    kv_bytes = S * Ld * 2 * d * 2 * (pos + 5)
+    kv_bytes = S * Ld * 2 * d * 2 * (pos + 1)   # keys 0..pos per slot and layer
     st_bytes = w_bytes + x_bytes + kv_bytes
     return {
         "logmel": {"bound": "hbm", "achieved": lm_bytes / (lm_ms / 1e3) / 1e9, "peak": hbm,
@@ -550,7 +553,7 @@ def measure_stages(eng, dims, segs, offs, pcm_dev) -> dict:
         "decode_step": {"bound": "hbm", "achieved": st_bytes / (st_ms / 1e3) / 1e9, "peak": hbm,
                         "unit": "GB/s", "frac": st_bytes / (st_ms / 1e3) / 1e9 / hbm,
                         "ms": st_ms, "bytes": st_bytes, "rows": S,
-                        "note": "one CUDA-graph step: weights + cross-KV + self-KV, 64 active slots"},
+                        "note": "CUDA-graph step (8 back to back per timed call, median of 5): weights + cross-KV + self-KV, 64 active slots"},
         "peak_source": "MEASURED_PEAKS.json (hbm_gbs burst copy, bf16_tflops burst)" if peaks else "fallback",
     }
 
