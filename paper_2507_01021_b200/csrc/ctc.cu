@@ -83,13 +83,98 @@ __device__ __forceinline__ void norm_stats(const double* part, int b, int n, flo
 }
 
 // ------------------------------------------------------------ conv0 (+ GroupNorm + GELU)
-// Pass 0: per-channel partial sum / sum-of-squares over this CTA's valid frames.
-// Pass 1: recompute, normalise per channel, GELU, write the bf16 conv1 operand.
-template <int PASS>
+constexpr int kGramBlocks = 16;   // Gram partials per segment
+constexpr int kGram = 65;         // 10 tap sums + 55 upper-triangle tap products
+
+// GroupNorm (512 groups = channels) statistics of conv0 without running the
+// convolution: for channel c, sum_t y_c(t) = w_c . A and sum_t y_c(t)^2 =
+// w_c^T G w_c with A_k = sum_t x(5t + k), G_kj = sum_t x(5t + k) x(5t + j) over
+// the segment's frames (x = the normalised input exactly as conv0 forms it):
+// 65 double sums per segment instead of a second pass of 512-channel
+// convolutions. Fixed-order reductions throughout.
+__global__ void __launch_bounds__(256)
+ctc_gram_partials(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offs,
+                  const int32_t* __restrict__ lens, const double* __restrict__ npart,
+                  double* __restrict__ gram_part) {
+  const int b = blockIdx.y, blk = blockIdx.x;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int n = lens[b];
+  const int T0 = n >= 10 ? (n - 10) / 5 + 1 : 0;
+  float mean, rstd;
+  norm_stats(npart, b, n, mean, rstd);
+  const int16_t* x = pcm + offs[b];
+  double acc[kGram];
+#pragma unroll
+  for (int i = 0; i < kGram; ++i) acc[i] = 0.0;
+  for (int t = blk * blockDim.x + threadIdx.x; t < T0; t += kGramBlocks * blockDim.x) {
+    float xv[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+      const int j = 5 * t + k;
+      xv[k] = j < n ? (float(x[j]) * (1.0f / 32768.0f) - mean) * rstd : 0.f;
+    }
+    int idx = 10;
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+      acc[k] += double(xv[k]);
+#pragma unroll
+      for (int j = k; j < 10; ++j) acc[idx++] += double(xv[k]) * double(xv[j]);
+    }
+  }
+  __shared__ double red[8][kGram];
+#pragma unroll
+  for (int i = 0; i < kGram; ++i) {
+    double v = acc[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kGram) {
+    double v = 0.0;
+    for (int w = 0; w < int(blockDim.x) / 32; ++w) v += red[w][threadIdx.x];
+    gram_part[(size_t(b) * kGramBlocks + blk) * kGram + threadIdx.x] = v;
+  }
+}
+
+// Per (segment, channel) mean / rstd of conv0's output from the Gram sums.
+__global__ void __launch_bounds__(kC)
+ctc_gn_finalize(const double* __restrict__ gram_part, const uint16_t* __restrict__ w0,
+                const int32_t* __restrict__ lens, float* __restrict__ gstat) {
+  const int b = blockIdx.x, c = threadIdx.x;
+  __shared__ double g[kGram];
+  if (c < kGram) {
+    double v = 0.0;
+    for (int i = 0; i < kGramBlocks; ++i) v += gram_part[(size_t(b) * kGramBlocks + i) * kGram + c];
+    g[c] = v;
+  }
+  __syncthreads();
+  const int n = lens[b];
+  const int T0 = n >= 10 ? (n - 10) / 5 + 1 : 0;
+  double w[10];
+#pragma unroll
+  for (int k = 0; k < 10; ++k) w[k] = double(bf16_to_f32(w0[c * 10 + k]));
+  double s = 0.0, q = 0.0;
+  int idx = 10;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    s += w[k] * g[k];
+#pragma unroll
+    for (int j = k; j < 10; ++j, ++idx) q += (j == k ? 1.0 : 2.0) * w[k] * w[j] * g[idx];
+  }
+  const double m = T0 > 0 ? s / T0 : 0.0;
+  double var = T0 > 0 ? q / T0 - m * m : 0.0;
+  var = var > 0 ? var : 0.0;
+  gstat[(b * kC + c) * 2] = float(m);
+  gstat[(b * kC + c) * 2 + 1] = float(1.0 / sqrt(var + 1e-5));
+}
+
+// conv0 -> GroupNorm -> GELU -> the bf16 conv1 operand. Frames past the
+// segment (the batch is padded to its longest) get zero rows and no work.
 __global__ void __launch_bounds__(256)
 ctc_conv0_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ offs,
                  const int32_t* __restrict__ lens, const double* __restrict__ npart,
-                 const uint16_t* __restrict__ w0 /*[512][10]*/, float* __restrict__ gpart,
+                 const uint16_t* __restrict__ w0 /*[512][10]*/,
                  const float* __restrict__ gstat /*[B][512][2] mean, rstd*/,
                  const uint16_t* __restrict__ gn_g, const uint16_t* __restrict__ gn_b,
                  uint16_t* __restrict__ out, int R0) {
@@ -99,18 +184,9 @@ ctc_conv0_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ of
   const int n = lens[b];
   const int T0 = n >= 10 ? (n - 10) / 5 + 1 : 0;
   if (f0 >= T0) {
-    // frames past this segment's end (the batch is padded to its longest
-    // segment): no statistics, zero operand rows -- no convolution work
-    if (PASS == 0) {
-      for (int c = threadIdx.x; c < kC; c += blockDim.x) {
-        gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c) * 2] = 0.f;
-        gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c) * 2 + 1] = 0.f;
-      }
-    } else {
-      const int nf = min(kF0, R0 - f0);
-      uint32_t* o32 = reinterpret_cast<uint32_t*>(out + (size_t(b) * R0 + f0) * kC);
-      for (int i = threadIdx.x; i < nf * kC / 2; i += blockDim.x) o32[i] = 0u;
-    }
+    const int nf = min(kF0, R0 - f0);
+    uint32_t* o32 = reinterpret_cast<uint32_t*>(out + (size_t(b) * R0 + f0) * kC);
+    for (int i = threadIdx.x; i < nf * kC / 2; i += blockDim.x) o32[i] = 0u;
     return;
   }
   const int nvalid = min(kF0, T0 - f0);        // frames of this CTA inside the segment
@@ -125,7 +201,7 @@ ctc_conv0_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ of
   __syncthreads();
   // both of this thread's channels (c, c + 256) per frame, two frames per
   // step from one 15-sample window: each shared-memory sample read feeds 4
-  // convolution taps (same per-output tap order and per-channel frame order)
+  // convolution taps
   const int c0 = threadIdx.x, c1 = threadIdx.x + 256;
   float wa[10], wb[10];
 #pragma unroll
@@ -133,18 +209,10 @@ ctc_conv0_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ of
     wa[k] = ws[c0 * 10 + k];
     wb[k] = ws[c1 * 10 + k];
   }
-  float sa = 0.f, qa = 0.f, sb = 0.f, qb = 0.f;
-  float ma = 0.f, ra = 0.f, ga = 0.f, ba = 0.f, mb = 0.f, rb = 0.f, gb2 = 0.f, bb = 0.f;
-  if (PASS == 1) {
-    ma = gstat[(b * kC + c0) * 2];
-    ra = gstat[(b * kC + c0) * 2 + 1];
-    ga = bf16_to_f32(gn_g[c0]);
-    ba = bf16_to_f32(gn_b[c0]);
-    mb = gstat[(b * kC + c1) * 2];
-    rb = gstat[(b * kC + c1) * 2 + 1];
-    gb2 = bf16_to_f32(gn_g[c1]);
-    bb = bf16_to_f32(gn_b[c1]);
-  }
+  const float ma = gstat[(b * kC + c0) * 2], ra = gstat[(b * kC + c0) * 2 + 1];
+  const float ga = bf16_to_f32(gn_g[c0]), ba = bf16_to_f32(gn_b[c0]);
+  const float mb = gstat[(b * kC + c1) * 2], rb = gstat[(b * kC + c1) * 2 + 1];
+  const float gb2 = bf16_to_f32(gn_g[c1]), bb = bf16_to_f32(gn_b[c1]);
   static_assert(kF0 % 2 == 0 && (kF0 - 2) * 5 + 14 < kF0 * 5 + 5, "conv0 window");
 #pragma unroll 1
   for (int f = 0; f < kF0; f += 2) {
@@ -154,11 +222,10 @@ ctc_conv0_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ of
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int ff = f + h, t = f0 + ff;
-      if (ff >= nvalid) {                      // past the segment: zero rows (pass 1)
-        if (PASS == 1 && t < R0) {
-          out[(size_t(b) * R0 + t) * kC + c0] = 0;
-          out[(size_t(b) * R0 + t) * kC + c1] = 0;
-        }
+      if (t >= R0) continue;
+      if (ff >= nvalid) {                      // past the segment: zero rows
+        out[(size_t(b) * R0 + t) * kC + c0] = 0;
+        out[(size_t(b) * R0 + t) * kC + c1] = 0;
         continue;
       }
       float ya = 0.f, yb = 0.f;
@@ -167,40 +234,10 @@ ctc_conv0_kernel(const int16_t* __restrict__ pcm, const int64_t* __restrict__ of
         ya = fmaf(wa[k], xw[5 * h + k], ya);
         yb = fmaf(wb[k], xw[5 * h + k], yb);
       }
-      if (PASS == 0) {
-        sa += ya; qa += ya * ya;
-        sb += yb; qb += yb * yb;
-      } else if (t < R0) {
-        out[(size_t(b) * R0 + t) * kC + c0] = f32_to_bf16(gelu_erf((ya - ma) * ra * ga + ba));
-        out[(size_t(b) * R0 + t) * kC + c1] = f32_to_bf16(gelu_erf((yb - mb) * rb * gb2 + bb));
-      }
+      out[(size_t(b) * R0 + t) * kC + c0] = f32_to_bf16(gelu_erf((ya - ma) * ra * ga + ba));
+      out[(size_t(b) * R0 + t) * kC + c1] = f32_to_bf16(gelu_erf((yb - mb) * rb * gb2 + bb));
     }
   }
-  if (PASS == 0) {
-    gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c0) * 2] = sa;
-    gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c0) * 2 + 1] = qa;
-    gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c1) * 2] = sb;
-    gpart[((size_t(b) * gridDim.x + blockIdx.x) * kC + c1) * 2 + 1] = qb;
-  }
-}
-
-// GroupNorm(512 groups = channels) statistics: fixed-order reduction.
-__global__ void ctc_gn_finalize(const float* __restrict__ gpart, int nblk,
-                                const int32_t* __restrict__ lens, float* __restrict__ gstat) {
-  const int b = blockIdx.x, c = threadIdx.x + blockIdx.y * blockDim.x;
-  if (c >= kC) return;
-  const int n = lens[b];
-  const int T0 = n >= 10 ? (n - 10) / 5 + 1 : 0;
-  double s = 0.0, q = 0.0;
-  for (int i = 0; i < nblk; ++i) {
-    s += gpart[((size_t(b) * nblk + i) * kC + c) * 2];
-    q += gpart[((size_t(b) * nblk + i) * kC + c) * 2 + 1];
-  }
-  const double m = T0 > 0 ? s / T0 : 0.0;
-  double var = T0 > 0 ? q / T0 - m * m : 0.0;
-  var = var > 0 ? var : 0.0;
-  gstat[(b * kC + c) * 2] = float(m);
-  gstat[(b * kC + c) * 2 + 1] = float(1.0 / sqrt(var + 1e-5));
 }
 
 // ------------------------------------------------------------ CTC collapse
@@ -259,7 +296,7 @@ struct CtcEngine {
   int32_t* lens_dev = nullptr;    // [B] samples
   int32_t* tlen_dev = nullptr;    // [B] output frames
   double* npart = nullptr;
-  float* gpart = nullptr;
+  double* gram_part = nullptr;   // [B][kGramBlocks][65] conv0 GroupNorm Gram partials
   float* gstat = nullptr;
   uint16_t *act_a = nullptr, *act_b = nullptr;   // conv ping-pong [B, R, 512]
   float* f32buf = nullptr;        // conv6 out / hidden x [B*R6, 768] fp32
@@ -321,7 +358,7 @@ static int ctc_init(CtcEngine* e) {
   if (e->alloc_t(&e->lens_dev, B)) return 2;
   if (e->alloc_t(&e->tlen_dev, B)) return 2;
   if (e->alloc_t(&e->npart, size_t(B) * kNormBlocks * 2)) return 2;
-  if (e->alloc_t(&e->gpart, size_t(B) * ceil_div(int(R0), kF0) * kC * 2)) return 2;
+  if (e->alloc_t(&e->gram_part, size_t(B) * kGramBlocks * kGram)) return 2;
   if (e->alloc_t(&e->gstat, size_t(B) * kC * 2)) return 2;
   if (e->alloc_t(&e->act_a, size_t(B) * R0 * kC)) return 2;
   if (e->alloc_t(&e->act_b, size_t(B) * e->max_R1 * kC)) return 2;
@@ -432,15 +469,13 @@ static int ctc_forward(CtcEngine* e, const int16_t* pcm, int n, const std::vecto
   ctc_norm_partials<<<dim3(kNormBlocks, n), 256, 0, s>>>(pcm, e->offs_dev, e->lens_dev, e->npart);
   DM_CHECK_LAUNCH();
   const int nblk = ceil_div(std::max(R[0], 1), kF0);
-  ctc_conv0_kernel<0><<<dim3(nblk, n), 256, 0, s>>>(pcm, e->offs_dev, e->lens_dev, e->npart,
-                                                     e->W(0), e->gpart, nullptr, nullptr, nullptr,
-                                                     nullptr, R[0]);
+  ctc_gram_partials<<<dim3(kGramBlocks, n), 256, 0, s>>>(pcm, e->offs_dev, e->lens_dev, e->npart,
+                                                         e->gram_part);
   DM_CHECK_LAUNCH();
-  ctc_gn_finalize<<<dim3(n, 2), 256, 0, s>>>(e->gpart, nblk, e->lens_dev, e->gstat);
+  ctc_gn_finalize<<<n, kC, 0, s>>>(e->gram_part, e->W(0), e->lens_dev, e->gstat);
   DM_CHECK_LAUNCH();
-  ctc_conv0_kernel<1><<<dim3(nblk, n), 256, 0, s>>>(pcm, e->offs_dev, e->lens_dev, e->npart,
-                                                     e->W(0), nullptr, e->gstat, e->W(7), e->W(8),
-                                                     e->act_a, R[0]);
+  ctc_conv0_kernel<<<dim3(nblk, n), 256, 0, s>>>(pcm, e->offs_dev, e->lens_dev, e->npart, e->W(0),
+                                                 e->gstat, e->W(7), e->W(8), e->act_a, R[0]);
   DM_CHECK_LAUNCH();
   // conv1..6: stride-2 implicit GEMMs, GELU (conv6 -> fp32 for the projection LN)
   uint16_t* src = e->act_a;
