@@ -29,17 +29,25 @@ __device__ unsigned long long g_attn_trace[2 * 16 * 4 + 2 * 16 * 2 + 1];
 #define ATRACE_E(idx) do {} while (0)
 #endif
 
-constexpr int kAttnThreads = 320;    // w0 TMA, w1 MMA, w2..5 softmax tile A, w6..9 tile B
-constexpr int kAttnKS = 4;           // K/V ring depth (TMA lookahead of 3 key blocks)
 constexpr int kQBytes = 128 * 128;   // 128 rows x 64 bf16
 constexpr int kKBytes = 128 * 128;
 constexpr int kVBytes = 2 * 64 * 128;  // two 64-key boxes of [64 dims x 64 keys]
 
-struct AttnSmemLayout {
-  static constexpr int q = 0;                          // [2 tiles]
-  static constexpr int k = q + 2 * kQBytes;
-  static constexpr int v = k + kAttnKS * kKBytes;
-  static constexpr int bars = v + kAttnKS * kVBytes;
+// NT query tiles per CTA (w0 TMA, w1 MMA, one softmax warpgroup per tile) and
+// a KS-deep K/V ring. NT = 1 (default): 256 TMEM columns and a 2-deep ring, so
+// two independent CTAs share an SM -- their exponential phases drift apart
+// instead of running in lockstep, and short sequences hide each other's
+// setup (whisper-large-v3 layer, 12 segments: 253 -> 239 µs; CTC 78 -> 72 µs).
+// NT = 2: two tiles share every K/V tile, one CTA per SM (512 columns).
+template <int NT>
+struct AttnCfg {
+  static constexpr int kThreads = (2 + 4 * NT) * 32;
+  static constexpr int kKS = NT == 2 ? 4 : 2;
+  static constexpr int kTmemCols = 256 * NT;        // S NT x 128, O NT x 64, P NT x 64
+  static constexpr int q = 0;                       // [NT tiles]
+  static constexpr int k = q + NT * kQBytes;
+  static constexpr int v = k + kKS * kKBytes;
+  static constexpr int bars = v + kKS * kVBytes;
   static constexpr int total = bars + 256 + 1024;
 };
 
@@ -58,7 +66,8 @@ __device__ __forceinline__ float ex2(float x) {
 // every K/V tile; each has its own S (128 TMEM cols), O (64 cols), P (64 cols)
 // and its own softmax warpgroup, so the tensor core works on one tile while
 // the other tile's softmax runs.
-__global__ void __launch_bounds__(kAttnThreads, 1)
+template <int NT>
+__global__ void __launch_bounds__(AttnCfg<NT>::kThreads, 3 - NT)
 attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
                     const __grid_constant__ CUtensorMap tm_k,
                     const __grid_constant__ CUtensorMap tm_vt, int T_rows, int t_pad,
@@ -67,7 +76,9 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024 - (raw_addr & 1023)) & 1023);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + AttnSmemLayout::bars);
+  using L = AttnCfg<NT>;
+  constexpr int kAttnKS = L::kKS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::bars);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;            // [KS]
   uint64_t* kv_empty = kv_full + kAttnKS;  // [KS]
@@ -82,7 +93,7 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
   const int qp = blockIdx.x, bh = blockIdx.y;
   // per-segment valid length (variable-length CTC batches); whisper: all 1500
   const int T = seg_len ? seg_len[bh / heads] : T_rows;
-  if (qp * 256 >= T) return;
+  if (qp * 128 * NT >= T) return;
   const int nb = ceil_div(T, 128);
 #ifdef DM_ATTN_TRACE
   const bool traced = qp == 2 && bh == 5 && nb <= 16;
@@ -95,7 +106,7 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
     tma_prefetch_desc(&tm_vt);
     mbar_init(q_full, 1);
     for (int i = 0; i < kAttnKS; ++i) { mbar_init(&kv_full[i], 1); mbar_init(&kv_empty[i], 1); }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NT; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 4);
       mbar_init(&p_full[i], 4);
@@ -104,25 +115,26 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 1) tmem_alloc(tmem_slot, L::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // TMEM columns: S tile t at 128 t, O tile t at 256 + 64 t, P tile t at 384 + 64 t
+  // TMEM columns: S tile t at 128 t, O tile t at kO + 64 t, P tile t at kP + 64 t
+  constexpr uint32_t kO = 128 * NT, kP = 192 * NT;
 
   if (warp == 0) {
     if (elect_one()) {
-      mbar_arrive_expect_tx(q_full, 2 * kQBytes);
-      tma_load_2d(smem + AttnSmemLayout::q, &tm_q, q_full, 0, bh * t_pad + qp * 256);
-      tma_load_2d(smem + AttnSmemLayout::q + kQBytes, &tm_q, q_full, 0, bh * t_pad + qp * 256 + 128);
+      mbar_arrive_expect_tx(q_full, NT * kQBytes);
+      for (int t = 0; t < NT; ++t)
+        tma_load_2d(smem + L::q + t * kQBytes, &tm_q, q_full, 0, bh * t_pad + qp * 128 * NT + 128 * t);
       for (int j = 0; j < nb; ++j) {
         const int st = j % kAttnKS;
         mbar_wait(&kv_empty[st], ((j / kAttnKS) & 1) ^ 1);
         mbar_arrive_expect_tx(&kv_full[st], kKBytes + kVBytes);
-        tma_load_2d(smem + AttnSmemLayout::k + st * kKBytes, &tm_k, &kv_full[st], 0,
+        tma_load_2d(smem + L::k + st * kKBytes, &tm_k, &kv_full[st], 0,
                     bh * t_pad + j * 128);
-        uint8_t* sv = smem + AttnSmemLayout::v + st * kVBytes;
+        uint8_t* sv = smem + L::v + st * kVBytes;
         tma_load_2d(sv, &tm_vt, &kv_full[st], j * 128, bh * 64);
         tma_load_2d(sv + 64 * 128, &tm_vt, &kv_full[st], j * 128 + 64, bh * 64);
       }
@@ -135,10 +147,10 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
     constexpr uint32_t idesc_o = umma_idesc_bf16(128, 64);
     mbar_wait(q_full, 0);
     auto issue_s = [&](int t, int j) {           // S_t = Q_t K_j^T
-      const uint32_t sk = smem_u32(smem + AttnSmemLayout::k + (j % kAttnKS) * kKBytes);
+      const uint32_t sk = smem_u32(smem + L::k + (j % kAttnKS) * kKBytes);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t sq = smem_u32(smem + AttnSmemLayout::q + t * kQBytes);
+        const uint32_t sq = smem_u32(smem + L::q + t * kQBytes);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           umma_bf16_ss(tmem + t * 128, umma_desc_sw128(sq + kk * 32),
@@ -151,13 +163,13 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
     if (lane == 0) ATRACE_E(128 + 0);
     issue_s(0, 0);
     if (lane == 0) ATRACE_E(128 + 32);
-    issue_s(1, 0);
+    if (NT == 2) issue_s(1, 0);
     for (int j = 0; j < nb; ++j) {
       const int st = j % kAttnKS;
       const uint32_t ph = j & 1;
-      const uint32_t sv = smem_u32(smem + AttnSmemLayout::v + st * kVBytes);
+      const uint32_t sv = smem_u32(smem + L::v + st * kVBytes);
 #pragma unroll
-      for (int t = 0; t < 2; ++t) {
+      for (int t = 0; t < NT; ++t) {
         // S_t(j + 1) as soon as softmax_t(j) has read S_t(j) out of TMEM (before
         // it finishes P_t(j)): the tile's next scores overlap its own exp/pack
         if (j + 1 < nb) {
@@ -174,11 +186,11 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint32_t bb = sv + (kk >> 2) * (64 * 128) + (kk & 3) * 32;
-            umma_bf16_ts(tmem + 256 + t * 64, tmem + 384 + t * 64 + kk * 8, umma_desc_sw128(bb),
+            umma_bf16_ts(tmem + kO + t * 64, tmem + kP + t * 64 + kk * 8, umma_desc_sw128(bb),
                          idesc_o, (j | kk) != 0);
           }
           umma_commit(&o_full[t]);
-          if (t == 1) umma_commit(&kv_empty[st]);
+          if (t == NT - 1) umma_commit(&kv_empty[st]);
         }
         __syncwarp();
       }
@@ -188,7 +200,7 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
     const int quad = warp & 3;
     const int r = quad * 32 + lane;                       // query row in tile
     const uint32_t lane_off = uint32_t(quad * 32) << 16;
-    const uint32_t s_col = t * 128, o_col = 256 + t * 64, p_col = 384 + t * 64;
+    const uint32_t s_col = t * 128, o_col = kO + t * 64, p_col = kP + t * 64;
     constexpr float kLog2e = 1.4426950408889634f;
     // O_t accumulates in TMEM across key blocks. The exponent offset m_run
     // only moves when the block max exceeds it by more than 2^8 (then O_t's
@@ -311,7 +323,7 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
     mbar_wait(&o_full[t], (nb - 1) & 1);
     tc_fence_after();
     // normalise and store this query row
-    const int tq = qp * 256 + t * 128 + r;
+    const int tq = qp * 128 * NT + t * 128 + r;
     const float inv = 1.0f / l_run;
     const int b = bh / heads, h = bh % heads;
 #pragma unroll 1
@@ -335,7 +347,7 @@ attn_tcgen05_kernel(const __grid_constant__ CUtensorMap tm_q,
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, 512);
+    tmem_dealloc(tmem, L::kTmemCols);
   }
 }
 
@@ -420,10 +432,21 @@ int launch_attention(const uint16_t* q, const uint16_t* k, const uint16_t* vt, i
   DM_REQUIRE(t_pad % 128 == 0 && t_pad >= T, "t_pad must be a multiple of 128 >= T");
   CUtensorMap mq, mk, mv;
   if (make_attn_maps(q, k, vt, n_seg * heads, t_pad, &mq, &mk, &mv)) return 2;
-  DM_SMEM_ATTR(attn_tcgen05_kernel, AttnSmemLayout::total);
-  dim3 grid(ceil_div(T, 256), n_seg * heads);
-  attn_tcgen05_kernel<<<grid, kAttnThreads, AttnSmemLayout::total, stream>>>(
-      mq, mk, mv, T, t_pad, heads, out, ldo, seg_len);
+  // one query tile per CTA, two CTAs per SM (DM_ATTN_NT1_MAX_T: longest T that
+  // uses it; experiments)
+  static const int nt1_max = std::getenv("DM_ATTN_NT1_MAX_T") ? std::atoi(std::getenv("DM_ATTN_NT1_MAX_T"))
+                                                               : 1 << 30;
+  if (T <= nt1_max) {
+    using L = AttnCfg<1>;
+    DM_SMEM_ATTR(attn_tcgen05_kernel<1>, L::total);
+    attn_tcgen05_kernel<1><<<dim3(ceil_div(T, 128), n_seg * heads), L::kThreads, L::total, stream>>>(
+        mq, mk, mv, T, t_pad, heads, out, ldo, seg_len);
+  } else {
+    using L = AttnCfg<2>;
+    DM_SMEM_ATTR(attn_tcgen05_kernel<2>, L::total);
+    attn_tcgen05_kernel<2><<<dim3(ceil_div(T, 256), n_seg * heads), L::kThreads, L::total, stream>>>(
+        mq, mk, mv, T, t_pad, heads, out, ldo, seg_len);
+  }
   DM_CHECK_LAUNCH();
   return 0;
 }
