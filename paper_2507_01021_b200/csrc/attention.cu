@@ -394,10 +394,12 @@ layernorm_bf16_kernel(const float* __restrict__ x, const uint16_t* __restrict__ 
   for (int i = 0; i < V4; ++i) {
     int c = lane + 32 * i;
     if (c < n4) {
-      float o0 = (v[i].x - mean) * rstd * bf16_to_f32(g[4 * c]) + bf16_to_f32(bta[4 * c]);
-      float o1 = (v[i].y - mean) * rstd * bf16_to_f32(g[4 * c + 1]) + bf16_to_f32(bta[4 * c + 1]);
-      float o2 = (v[i].z - mean) * rstd * bf16_to_f32(g[4 * c + 2]) + bf16_to_f32(bta[4 * c + 2]);
-      float o3 = (v[i].w - mean) * rstd * bf16_to_f32(g[4 * c + 3]) + bf16_to_f32(bta[4 * c + 3]);
+      const uint2 gw = __ldg(reinterpret_cast<const uint2*>(g) + c);     // 4 bf16 each
+      const uint2 bw = __ldg(reinterpret_cast<const uint2*>(bta) + c);
+      float o0 = (v[i].x - mean) * rstd * __uint_as_float(gw.x << 16) + __uint_as_float(bw.x << 16);
+      float o1 = (v[i].y - mean) * rstd * __uint_as_float(gw.x & 0xFFFF0000u) + __uint_as_float(bw.x & 0xFFFF0000u);
+      float o2 = (v[i].z - mean) * rstd * __uint_as_float(gw.y << 16) + __uint_as_float(bw.y << 16);
+      float o3 = (v[i].w - mean) * rstd * __uint_as_float(gw.y & 0xFFFF0000u) + __uint_as_float(bw.y & 0xFFFF0000u);
       yr[c] = make_uint2(pack_bf16x2(o0, o1), pack_bf16x2(o2, o3));
       if (y32) reinterpret_cast<float4*>(y32 + size_t(row) * d)[c] = make_float4(o0, o1, o2, o3);
     }
