@@ -241,7 +241,8 @@ def cpu_model() -> str:
 
 
 def workload_name(segments: int) -> str:
-    return (f"cfg3: {MODEL} random-init bf16 (seed 0), {segments} segments/GPU x U[3,30] s "
+    cfg = "cfg3" if MODEL == "whisper-large-v3" else ("cfg2" if MODEL == "whisper-base" else "side run")
+    return (f"{cfg}: {MODEL} random-init bf16 (seed 0), {segments} segments/GPU x U[3,30] s "
             f"synthetic speech, continuous batching (min_batch 32, max_batch 64) over 64 decode "
             f"slots, greedy cap ceil(3.75*dur)")
 
@@ -634,6 +635,8 @@ def measure_latency(eng, dims, args, rs) -> dict | None:
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--model", default=None,
+                    help="side runs on another model (e.g. whisper-base for cfg2); default large-v3 (cfg3)")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
@@ -666,6 +669,9 @@ def main():
     ap.add_argument("--profile", action="store_true",
                     help="run exactly one resident-input step and exit (ncu)")
     args = ap.parse_args()
+    global MODEL
+    if args.model:                       # side runs only; the headline is cfg3 (large-v3)
+        MODEL = args.model
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(relaunch_under_torchrun(args.gpus))
     rank, world, local = dist_env()
