@@ -1366,8 +1366,12 @@ gelu_hilo_kernel(const DecodeState st, const Partials p, uint16_t* __restrict__ 
   pdl_wait();
   if (threadIdx.x == 0) trace_mark(st, 1);
   if (r >= *st.n_active || 4 * n4 >= p.n) return;
-  const float4 a = sum_splits4<kMaxHeads>(p.p + size_t(r) * p.n + 4 * n4, size_t(kRows) * p.n,
-                                          p.splits);
+  // (fc1's split is 4 by default: a 4-wide load set keeps the registers and
+  // the loads in flight small; same split-order sums either way)
+  const float4 a = p.splits <= 4
+                       ? sum_splits4<4>(p.p + size_t(r) * p.n + 4 * n4, size_t(kRows) * p.n, p.splits)
+                       : sum_splits4<kMaxHeads>(p.p + size_t(r) * p.n + 4 * n4, size_t(kRows) * p.n,
+                                                p.splits);
   const float v[4] = {a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w};
   uint16_t h[4], l[4];
 #pragma unroll
